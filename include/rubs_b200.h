@@ -1,0 +1,152 @@
+/*
+ * rubs_b200.h -- C ABI of the B200-native space-variant box-spline filter.
+ *
+ * The reference (arxiv/paper_1003_2022, package "rubs") is pure Python; its
+ * drop-in boundary is the public Python API (pkg/src/rubs/__init__.py:46-53).
+ * Each entry point below replaces one reference function; the reference
+ * file:line it replaces is given with it.  The Python host layer
+ * (paper_1003_2022_b200/) binds these with ctypes and keeps the reference
+ * signatures, argument meaning and exceptions.
+ *
+ * Conventions
+ *   - Images are row-major; element (r, c) sits at lattice point
+ *     (n1, n2) = (c, r): x = column, y = row (reference zp.py:56-66).
+ *   - ld_* are row strides in ELEMENTS (not bytes).
+ *   - "Device" entry points take device pointers and enqueue on `stream`
+ *     (a cudaStream_t, NULL = legacy default stream); they synchronise the
+ *     stream before returning so that the status is final.
+ *   - "_host" entry points take host pointers (pageable or pinned), stage
+ *     the copies themselves and return when the result is in `out`.
+ *   - Outputs are always float64, like the reference (engine.py:285).
+ *   - No torch types cross this boundary.
+ *
+ * Status codes (mapped by the Python layer to the reference's exceptions):
+ *   RUBS_OK           0
+ *   RUBS_EVALUE       1  -> ValueError      (engine.py:286-289, 210-215)
+ *   RUBS_EOVERFLOW    2  -> OverflowError   (engine.py:195-200)
+ *   RUBS_EOUTOFGRID   3  -> OutOfGrid       (solver.py:304-307)
+ *   RUBS_ECUDA        4  -> RuntimeError    (CUDA error / OOM)
+ *   RUBS_EUNSUPPORTED 5  -> RuntimeError    (configuration not handled)
+ */
+#ifndef RUBS_B200_H
+#define RUBS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RUBS_OK 0
+#define RUBS_EVALUE 1
+#define RUBS_EOVERFLOW 2
+#define RUBS_EOUTOFGRID 3
+#define RUBS_ECUDA 4
+#define RUBS_EUNSUPPORTED 5
+
+#define RUBS_F32 0
+#define RUBS_F64 1
+
+/* Library version string and the last error message of this thread. */
+const char *rubs_b200_version(void);
+const char *rubs_b200_last_error(void);
+
+/* Number of kernel launches issued by this thread since the last reset
+ * (bench.py reports it as gpu_launches). */
+int64_t rubs_b200_launch_count(void);
+void rubs_b200_reset_launch_count(void);
+
+/*
+ * Space-variant filter, per-pixel scale field.
+ * Replaces engine.filter_space_variant (pkg/src/rubs/engine.py:265-324).
+ *   f        device image, H x W, dtype RUBS_F32 | RUBS_F64, row stride ld_f
+ *   field    device (H, W, 4) float64 scale-vectors, row stride ld_field
+ *            (in pixels, i.e. the (r, c, k) element is at
+ *            field[(r * ld_field + c) * 4 + k]);
+ *            or, when field_is_uniform != 0, a HOST pointer to 4 doubles
+ *            (the reference's (4,) broadcast, engine.py:208-209)
+ *   iterations  >= 1 (engine.py:288-289, 292-323)
+ *   out      device H x W float64, row stride ld_out
+ * Entries below SCALE_FLOOR = 0.05 are clamped (engine.py:58, 292);
+ * non-finite entries give RUBS_EVALUE (engine.py:214-215).
+ */
+int rubs_b200_filter(const void *f, int f_dtype, int64_t H, int64_t W, int64_t ld_f,
+                     const double *field, int field_is_uniform, int64_t ld_field,
+                     int iterations, double *out, int64_t ld_out, void *stream);
+
+/* Same, host buffers (timed by bench.py as the end-to-end call). */
+int rubs_b200_filter_host(const void *f, int f_dtype, int64_t H, int64_t W,
+                          const double *field, int field_is_uniform, int iterations,
+                          double *out);
+
+/*
+ * Device-resident scale lookup table (the reference's ScaleLut,
+ * solver.py:232-247).  Built on the host by build_lut (solver.py:250-281)
+ * and uploaded once.
+ */
+typedef struct rubs_lut rubs_lut;
+int rubs_b200_lut_create(const double *rho_grid, const double *phi_grid,
+                         const double *entries /* n_rho*n_phi*4 */, int n_rho, int n_phi,
+                         rubs_lut **out);
+void rubs_b200_lut_destroy(rubs_lut *lut);
+
+/*
+ * Vectorised LUT lookup on the device.
+ * Replaces solver.lookup_many (pkg/src/rubs/solver.py:289-335).
+ *   size, elong, orient   device arrays of n values, dtype p_dtype
+ *   out                   device n x 4 float64
+ */
+int rubs_b200_lookup(const rubs_lut *lut, const void *size, const void *elong,
+                     const void *orient, int p_dtype, int64_t n, double *out, void *stream);
+
+/*
+ * Fused mapping + filter: per-pixel (size, elongation, orientation) ->
+ * scale-vector through the LUT (solver.py:289-335), then the space-variant
+ * filter (engine.py:265-324).  Equivalent to
+ *   filter_space_variant(f, lookup_many(lut, size, elong, orient), iterations)
+ * without materialising the (H, W, 4) field.
+ *   size/elong/orient   device H x W arrays, dtype p_dtype, row stride ld_p
+ */
+int rubs_b200_filter_params(const void *f, int f_dtype, int64_t H, int64_t W, int64_t ld_f,
+                            const void *size, const void *elong, const void *orient,
+                            int p_dtype, int64_t ld_p, const rubs_lut *lut, int iterations,
+                            double *out, int64_t ld_out, void *stream);
+
+/* Same, host buffers. */
+int rubs_b200_filter_params_host(const void *f, int f_dtype, int64_t H, int64_t W,
+                                 const void *size, const void *elong, const void *orient,
+                                 int p_dtype, const rubs_lut *lut, int iterations,
+                                 double *out);
+
+/*
+ * Global pre-integration with the reference's canvas semantics.
+ * Replaces engine.preintegrate (pkg/src/rubs/engine.py:145-201).
+ * rubs_b200_preintegrate_shape returns the canvas geometry for the given
+ * image placement and requested lattice ranges (engine.py:169-177):
+ *   rows, cols   plane shape;  c_lo, r_lo  lattice of plane[0, 0]
+ * rubs_b200_preintegrate then fills `plane` (device, rows x cols float64,
+ * row stride ld_plane) and applies the 2^53 guard (RUBS_EOVERFLOW).
+ */
+int rubs_b200_preintegrate_shape(int64_t h, int64_t w, int64_t col0, int64_t row0,
+                                 int64_t need_c0, int64_t need_c1, int64_t need_r0,
+                                 int64_t need_r1, int64_t *rows, int64_t *cols,
+                                 int64_t *c_lo, int64_t *r_lo);
+int rubs_b200_preintegrate(const void *f, int f_dtype, int64_t h, int64_t w, int64_t ld_f,
+                           int64_t col0, int64_t row0, int64_t need_c0, int64_t need_c1,
+                           int64_t need_r0, int64_t need_r1, double *plane, int64_t ld_plane,
+                           void *stream);
+
+/*
+ * Seven-tap ZP interpolation of a pre-integrated plane at n points.
+ * Replaces zp.interpolate (pkg/src/rubs/zp.py:186-228); reads outside the
+ * plane clamp to its edge like the reference.
+ */
+int rubs_b200_interpolate(const double *plane, int64_t rows, int64_t cols, int64_t ld_plane,
+                          int64_t col0, int64_t row0, const double *x1, const double *x2,
+                          int64_t n, double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RUBS_B200_H */

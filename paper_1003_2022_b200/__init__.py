@@ -1,0 +1,68 @@
+"""B200-native drop-in for the reference's space-variant filtering path.
+
+The reference (arxiv/paper_1003_2022, Python package ``rubs``) filters an
+image with a per-pixel four-direction box-spline kernel in O(1) per pixel:
+four directional running sums, then a 16-vertex finite difference read
+through a 7-tap Zwart-Powell interpolant.  This package keeps that API
+(pkg/src/rubs/__init__.py:46-53) and runs the path in hand-written sm_100a
+kernels (csrc/) behind a C ABI (include/rubs_b200.h).
+
+There is no CPU fallback: without the native library (or without a CUDA
+device) every filtering call raises.
+"""
+
+from .engine import (
+    SCALE_FLOOR,
+    DeviceLut,
+    FdMesh,
+    IntegratedImage,
+    ScaleField,
+    device_lut,
+    fd_mesh,
+    filter_space_invariant,
+    filter_space_variant,
+    filter_space_variant_params,
+    interpolate,
+    lookup_many,
+    preintegrate,
+)
+from .geometry import (
+    MIN_ELONGATION_BOUND,
+    as_scale_vector,
+    covariance_from_params,
+    covariance_of,
+    elongation_bound,
+    sigma_to_size,
+)
+from .solver import Infeasible, OutOfGrid, ScaleLut, build_lut, default_lut, optimize_scale_vector
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "SCALE_FLOOR",
+    "DeviceLut",
+    "FdMesh",
+    "IntegratedImage",
+    "ScaleField",
+    "ScaleLut",
+    "Infeasible",
+    "OutOfGrid",
+    "MIN_ELONGATION_BOUND",
+    "as_scale_vector",
+    "build_lut",
+    "covariance_from_params",
+    "covariance_of",
+    "default_lut",
+    "device_lut",
+    "elongation_bound",
+    "fd_mesh",
+    "filter_space_invariant",
+    "filter_space_variant",
+    "filter_space_variant_params",
+    "interpolate",
+    "lookup_many",
+    "optimize_scale_vector",
+    "preintegrate",
+    "sigma_to_size",
+    "__version__",
+]

@@ -1,0 +1,111 @@
+"""ctypes binding of the C ABI in include/rubs_b200.h.
+
+The shared library is built in-tree (``build_native``) as
+``paper_1003_2022_b200/_lib/librubs_b200.so`` for sm_100a.  There is no CPU
+fallback: if the library is missing or CUDA is unavailable every entry point
+raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_REPO = os.path.dirname(_PKG)
+LIB_DIR = os.path.join(_PKG, "_lib")
+LIB_PATH = os.path.join(LIB_DIR, "librubs_b200.so")
+CSRC = os.path.join(_PKG, "csrc")
+INCLUDE = os.path.join(_REPO, "include")
+
+NVCC_FLAGS = [
+    "-gencode", "arch=compute_100a,code=sm_100a",
+    "-O3", "-lineinfo", "-std=c++17",
+    "-Xcompiler", "-fPIC", "-shared",
+]
+
+RUBS_OK, RUBS_EVALUE, RUBS_EOVERFLOW, RUBS_EOUTOFGRID, RUBS_ECUDA, RUBS_EUNSUPPORTED = range(6)
+RUBS_F32, RUBS_F64 = 0, 1
+
+
+def build_native(verbose: bool = False) -> str:
+    """Compile csrc/*.cu into the in-tree shared library (sm_100a)."""
+    os.makedirs(LIB_DIR, exist_ok=True)
+    srcs = [os.path.join(CSRC, "rubs_b200.cu")]
+    cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-o", LIB_PATH + ".tmp", *srcs]
+    if verbose:
+        cmd.insert(1, "-Xptxas=-v")
+    subprocess.run(cmd, check=True)
+    os.replace(LIB_PATH + ".tmp", LIB_PATH)
+    return LIB_PATH
+
+
+_lib = None
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_int = ctypes.c_int
+_dp = ctypes.POINTER(ctypes.c_double)
+_lp = ctypes.POINTER(ctypes.c_int64)
+
+# name -> (restype, argtypes); kept identical to include/rubs_b200.h
+SIGNATURES = {
+    "rubs_b200_version": (ctypes.c_char_p, []),
+    "rubs_b200_last_error": (ctypes.c_char_p, []),
+    "rubs_b200_launch_count": (_i64, []),
+    "rubs_b200_reset_launch_count": (None, []),
+    "rubs_b200_filter": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _int, _i64, _int, _vp, _i64, _vp]),
+    "rubs_b200_filter_host": (_int, [_vp, _int, _i64, _i64, _vp, _int, _int, _vp]),
+    "rubs_b200_lut_create": (_int, [_vp, _vp, _vp, _int, _int, ctypes.POINTER(_vp)]),
+    "rubs_b200_lut_destroy": (None, [_vp]),
+    "rubs_b200_lookup": (_int, [_vp, _vp, _vp, _vp, _int, _i64, _vp, _vp]),
+    "rubs_b200_filter_params": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp, _int, _i64, _vp,
+                                       _int, _vp, _i64, _vp]),
+    "rubs_b200_filter_params_host": (_int, [_vp, _int, _i64, _i64, _vp, _vp, _vp, _int, _vp, _int,
+                                            _vp]),
+    "rubs_b200_preintegrate_shape": (_int, [_i64, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _lp,
+                                            _lp, _lp, _lp]),
+    "rubs_b200_preintegrate": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _i64,
+                                      _i64, _vp, _i64, _vp]),
+    "rubs_b200_interpolate": (_int, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp]),
+}
+
+
+def load(path: str | None = None):
+    """Load the shared library (CPU-safe: loading needs no GPU)."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = path or LIB_PATH
+    if not os.path.exists(p):
+        raise RuntimeError(
+            f"native library {p} is missing; build it with "
+            "paper_1003_2022_b200._native.build_native() (no CPU fallback exists)")
+    L = ctypes.CDLL(p)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = L
+    return L
+
+
+class OutOfGridError(ValueError):
+    pass
+
+
+def check(rc: int) -> None:
+    """Map a C status to the reference's exception classes."""
+    if rc == RUBS_OK:
+        return
+    msg = load().rubs_b200_last_error().decode(errors="replace")
+    if rc == RUBS_EVALUE:
+        raise ValueError(msg)
+    if rc == RUBS_EOVERFLOW:
+        raise OverflowError(msg)
+    if rc == RUBS_EOUTOFGRID:
+        from .solver import OutOfGrid
+        raise OutOfGrid(msg)
+    raise RuntimeError(f"rubs_b200 error {rc}: {msg}")
