@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 space-variant filter path (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 2|1|4]
+
+One step = one filter pass over one synthetic image of the chosen
+BASELINE.json config (default: config 2, 2048^2 fp64 image, LUT-mapped
+smooth (size, elongation, orientation) fields in float32, one pass; the
+fused params path, i.e. rubs_b200_filter_params).  With N GPUs (torchrun)
+every rank filters its own image per step (weak scaling, no collective on
+the data path); value = all pixels / max-over-ranks device time.
+
+Printed JSON (rank 0, one line) carries the driver's keys plus
+  e2e          the same metric through the public API with HOST buffers
+               (H2D of image + params and D2H of the result inside the
+               timed region; wall clock around calls that return only when
+               the result is on the host)
+  roofline     dominant kernel (tile_filter_kernel): algorithmic bytes per
+               launch / CUDA-event kernel time, against MEASURED_PEAKS.json
+  fp64         the same kernel against the fp64 issue rate (the bound that
+               binds)
+  cpu_baseline the reference algorithm (oracle/port.py, numpy) on a bounded
+               sample of the same workload, all host cores, rank 0 at N=1
+`--impl reference` prints the same line for the CPU port alone.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "Gpixel/s filtered"
+UNIT = "Gpixel/s"
+# Algorithmic bytes per output pixel for the fused path: f64 image (8) +
+# three f32 params (12) + f64 output (8) = 28.
+BYTES_PER_PX = {"2": 28, "1": 48, "4": 52}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="2", choices=["1", "2", "4"])
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d.get("hbm_gbs", 6650.0)), float(d.get("sm_max_mhz", 1965.0)), "measured"
+    return 6650.0, 1965.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.thread.join(timeout=1)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def make_inputs(cfg: str, torch, device, copies: int, rank: int):
+    """Device-resident inputs (rotating copies so the working set of
+    consecutive steps exceeds L2) plus one host copy for the e2e leg."""
+    from paper_1003_2022_b200 import workloads
+    if cfg == "2":
+        w = workloads.config2(device=device, param_dtype=torch.float32)
+    elif cfg == "1":
+        w = workloads.config1()
+    else:
+        w = workloads.config4_image(rank, device=device, param_dtype=torch.float32)
+    f = torch.as_tensor(w["f"]).to(device)
+    sets = []
+    for _ in range(copies):
+        if "field" in w:
+            fld = torch.as_tensor(w["field"]).to(device)
+            sets.append({"f": f.clone(), "field": fld.clone()})
+        else:
+            sets.append({"f": f.clone(), "p": [v.clone() for v in (w["size"], w["elong"], w["orient"])]})
+    return w, sets
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    import torch.distributed as dist
+    import paper_1003_2022_b200 as rb
+    from paper_1003_2022_b200 import _native
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+    L = _native.load()
+    w, sets = make_inputs(args.config, torch, device, 4, rank)
+    iters = int(w["iterations"])
+    H, W = w["f"].shape
+    outs = [torch.empty((H, W), dtype=torch.float64, device=device) for _ in sets]
+
+    def step(i):
+        s = sets[i % len(sets)]
+        if "p" in s:
+            return rb.filter_space_variant_params(s["f"], *s["p"], iterations=iters)
+        return rb.filter_space_variant(s["f"], s["field"], iters)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    if rank == 0:
+        clocks.start()
+    L.rubs_b200_reset_launch_count()
+    L.rubs_b200_reset_kernel_time()
+    L.rubs_b200_set_profiling(1)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for i in range(args.steps):
+        step(i)
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    L.rubs_b200_set_profiling(0)
+    ms_total = ev0.elapsed_time(ev1)
+    launches = int(L.rubs_b200_launch_count())
+    import ctypes
+    tile_ms, tile_n = ctypes.c_double(), ctypes.c_int64()
+    L.rubs_b200_kernel_time(0, ctypes.byref(tile_ms), ctypes.byref(tile_n))
+    all_ms, all_n = ctypes.c_double(), ctypes.c_int64()
+    L.rubs_b200_kernel_time(2, ctypes.byref(all_ms), ctypes.byref(all_n))
+    clk = clocks.stop() if rank == 0 else None
+
+    t = torch.tensor([ms_total], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    px_total = float(H * W) * args.steps * world
+    value = px_total / (ms_max * 1e-3) / 1e9
+
+    # ---- end to end through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        if "p" in sets[0]:
+            hf = torch.empty((H, W), dtype=sets[0]["f"].dtype, pin_memory=True)
+            hf.copy_(sets[0]["f"].cpu())
+            hp = []
+            for v in sets[0]["p"]:
+                t_ = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                t_.copy_(v.cpu())
+                hp.append(t_.numpy())
+            hfn = hf.numpy()
+            lut = rb.default_lut()
+
+            def e2e_step():
+                return rb.filter_space_variant_params(hfn, *hp, lut=lut, iterations=iters)
+            h2d = hf.numel() * hf.element_size() + sum(p.nbytes for p in hp)
+        else:
+            hf = torch.empty((H, W), dtype=sets[0]["f"].dtype, pin_memory=True)
+            hf.copy_(sets[0]["f"].cpu())
+            hfl = torch.empty(sets[0]["field"].shape, dtype=torch.float64, pin_memory=True)
+            hfl.copy_(sets[0]["field"].cpu())
+            hfn, hfln = hf.numpy(), hfl.numpy()
+
+            def e2e_step():
+                return rb.filter_space_variant(hfn, hfln, iters)
+            h2d = hfn.nbytes + hfln.nbytes
+        for _ in range(max(2, args.warmup // 2)):
+            e2e_step()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        ksteps = max(3, args.steps // 2)
+        for _ in range(ksteps):
+            e2e_step()
+        el = time.perf_counter() - t0
+        te = torch.tensor([el], dtype=torch.float64, device=device)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": float(H * W) * ksteps * world / float(te.item()) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(H * W * 8),
+               "steps": ksteps, "timing": "wall clock around blocking API calls, max over ranks"}
+
+    result = None
+    if rank == 0:
+        hbm, sm_max, peak_kind = measured_peaks()
+        bpp = BYTES_PER_PX[args.config]
+        per_launch_px = H * W  # final pass covers H x W (iterations > 1 adds extended passes)
+        tile_avg_ms = tile_ms.value / max(1, tile_n.value)
+        launches_per_step = tile_n.value / max(1, args.steps)
+        achieved = bpp * H * W * iters / (tile_ms.value / max(1, args.steps) * 1e-3) / 1e9
+        # fp64 issue bound: B200 has 64 fp64 lanes per SM; DP instructions
+        # per pixel measured with ncu (profiles/ncu_r01_summary.md)
+        dp_per_px = DP_INST_PER_PX.get(args.config)
+        fp64 = None
+        if dp_per_px:
+            peak_dp = 148 * 64 * sm_max * 1e6  # DP lane-ops / s at max clock
+            got_dp = dp_per_px * H * W * iters / (tile_ms.value / max(1, args.steps) * 1e-3)
+            fp64 = {"achieved_dp_ops_per_s": got_dp, "peak_dp_ops_per_s": peak_dp,
+                    "frac": got_dp / peak_dp, "dp_inst_per_px": dp_per_px,
+                    "peak_at_clock_mhz": sm_max, "source": "ncu sm__sass_thread_inst_executed_op_fp64 per px"}
+        traffic = TRAFFIC_PER_LAUNCH.get(args.config)
+        result = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOADS[args.config], "image": [H, W], "iterations": iters,
+                       "per_rank_images_per_step": 1,
+                       "l2": "4 rotating input/output sets per rank (working set > 126 MB L2)",
+                       "path": "fused LUT mapping + filter (rubs_b200_filter_params)" if args.config != "1"
+                       else "drop-in (H,W,4) field (rubs_b200_filter)"},
+            "e2e": e2e,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                         "frac": achieved / hbm, "traffic": traffic,
+                         "kernel": "tile_filter_kernel", "kernel_ms_avg": tile_avg_ms,
+                         "algorithmic_bytes_per_px": bpp, "peak_source": peak_kind,
+                         "binding_bound": "fp64 issue (see fp64)"},
+            "fp64": fp64,
+            "gpu_launches": launches,
+            "launches_per_step": launches / max(1, args.steps),
+            "tile_kernel_launches_per_step": launches_per_step,
+            "kernel_share_of_step": all_ms.value / max(ms_total, 1e-9),
+            "clocks": clk,
+        }
+    if world > 1:
+        dist.destroy_process_group()
+    return result
+
+
+WORKLOADS = {
+    "2": "config2: 2048^2 fp64 uniform[0,1) seed 0; N=4 ZP box spline; sigma [2,16], rho [1,4], "
+         "theta [0,pi) smooth fields (LUT mapping, f32 params)",
+    "1": "config1: 256^2 fp64 uniform[0,1) seed 0; sigma 2->8 along x, rho 1->3 radial, "
+         "theta=atan2 mod pi; exact optimiser field",
+    "4": "config4 image: 4096^2 fp32 uniform[0,1); sigma [2,24], rho [1,4], smooth theta; 2 passes",
+}
+# filled from the committed ncu captures (profiles/); None until measured
+DP_INST_PER_PX = {}
+TRAFFIC_PER_LAUNCH = {}
+
+
+# ---------------------------------------------------------------------------
+_PORT = {}
+
+
+def _band_worker(band):
+    """One CPU-port row band (oracle B); returns pixels produced."""
+    import oracle.port as port
+    f, field, iters = _PORT["f"], _PORT["field"], _PORT["iters"]
+    lo, hi = band
+    port.filter_band(f, field, lo, hi, iters)
+    return (hi - lo) * f.shape[1]
+
+
+class CpuPort:
+    """The reference algorithm (oracle/port.py, a numpy restatement of the
+    reference fast path) on row bands of the config's image, one process per
+    host core (exact by linearity + zero padding)."""
+
+    def __init__(self, cfg: str, workers: int | None = None, min_rows: int = 64):
+        import multiprocessing as mp
+        from oracle import port
+        from paper_1003_2022_b200 import default_lut, workloads
+        if cfg == "1":
+            w = workloads.config1()
+            field = w["field"]
+        else:
+            w = workloads.config2() if cfg == "2" else workloads.config4_image(0)
+            lut = default_lut()
+            field = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, w["size"].numpy(),
+                                     w["elong"].numpy(), w["orient"].numpy())
+        f = np.asarray(w["f"], dtype=np.float64)
+        _PORT.update(f=f, field=field, iters=int(w["iterations"]))
+        self.H, self.W = f.shape
+        self.cfg = cfg
+        self.cores = workers or os.cpu_count() or 1
+        rows = max(min_rows, -(-self.H // self.cores))
+        self.bands = [(lo, min(self.H, lo + rows)) for lo in range(0, self.H, rows)][: self.cores]
+        self.cores = len(self.bands)
+        os.environ["OMP_NUM_THREADS"] = "1"
+        self.pool = mp.get_context("fork").Pool(self.cores)
+        self.rows = rows
+
+    def step(self):
+        t0 = time.perf_counter()
+        px = sum(self.pool.map(_band_worker, self.bands))
+        return px, time.perf_counter() - t0
+
+    def sample(self):
+        return (f"{len(self.bands)} row bands of {self.rows} rows x {self.W} cols "
+                f"({sum(h - l for l, h in self.bands)} of {self.H} rows) of {WORKLOADS[self.cfg].split(':')[0]}, "
+                f"halo rows recomputed per band; numpy port of the reference fast path "
+                f"(oracle/port.py), {self.cores} processes x 1 thread")
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
+def cpu_port_throughput(cfg: str, steps: int = 1, warmup: int = 1):
+    cp = CpuPort(cfg)
+    try:
+        for _ in range(warmup):
+            cp.step()
+        px = el = 0.0
+        for _ in range(steps):
+            p, e = cp.step()
+            px += p
+            el += e
+        return px / el / 1e6, cp.cores, cp.sample(), el
+    finally:
+        cp.close()
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return None
+    mpx, cores, sample, el = cpu_port_throughput(args.config, steps=args.steps, warmup=args.warmup)
+    v = mpx / 1e3  # Gpixel/s
+    H = 2048 if args.config == "2" else (256 if args.config == "1" else 4096)
+    return {
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": WORKLOADS[args.config], "image": [H, H]},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        res = run_reference(args, rank, world)
+        if res is not None:
+            print(json.dumps(res), flush=True)
+        return
+    res = run_ours(args, rank, world, local)
+    if rank == 0 and res is not None:
+        if world == 1 and not args.no_cpu_baseline:
+            mpx, cores, sample, el = cpu_port_throughput(args.config, steps=1, warmup=0)
+            res["cpu_baseline"] = {"value": mpx / 1e3, "unit": UNIT, "cores": cores, "kind": "port",
+                                   "sample": sample, "wall_s": el}
+        print(json.dumps(res), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -56,6 +56,14 @@ const char *rubs_b200_last_error(void);
 int64_t rubs_b200_launch_count(void);
 void rubs_b200_reset_launch_count(void);
 
+/* Optional device timing of the library's own kernels (CUDA events on the
+ * launching stream, read back at the end of each call).  kind: 0 = tile
+ * filter kernel, 1 = margin pre-pass, 2 = all kernels.  Totals accumulate
+ * until reset.  Used by bench.py for the roofline's per-launch duration. */
+void rubs_b200_set_profiling(int enable);
+void rubs_b200_kernel_time(int kind, double *total_ms, int64_t *launches);
+void rubs_b200_reset_kernel_time(void);
+
 /*
  * Space-variant filter, per-pixel scale field.
  * Replaces engine.filter_space_variant (pkg/src/rubs/engine.py:265-324).

@@ -64,6 +64,18 @@ VERTEX_BITS = ((np.arange(16)[:, None] >> np.arange(4)[None, :]) & 1).astype(np.
 VERTEX_SIGNS = np.where(VERTEX_BITS.sum(axis=1) % 2 == 0, 1.0, -1.0)
 
 
+def load_table_dump(text):
+    """Coefficients (4, 7, 6) from zp.dump_polynomial_table() text, in this
+    module's offset order."""
+    out = ZP_COEFFS.copy()
+    for ln in text.splitlines()[1:]:
+        v = ln.split()
+        q, dx, dy = int(v[0]), int(v[1]), int(v[2])
+        j = [tuple(o) for o in ZP_OFFSETS[q]].index((dx, dy))
+        out[q, j] = [float(t) for t in v[3:]]
+    return out
+
+
 def _quad(c, d1, d2):
     return c[0] + d1 * (c[1] + c[3] * d1 + c[4] * d2) + d2 * (c[2] + c[5] * d2)
 
@@ -72,8 +84,11 @@ def partition(d1, d2):
     return 2 * (np.asarray(d1 + d2) >= 0.0).astype(np.int64) + (np.asarray(d1 - d2) >= 0.0)
 
 
-def interpolate(plane, col0, row0, x1, x2):
-    """F(x) = sum_n plane[n] Z(x - n), reads clamped to the plane edge."""
+def interpolate(plane, col0, row0, x1, x2, coeffs=None):
+    """F(x) = sum_n plane[n] Z(x - n), reads clamped to the plane edge.
+    ``coeffs`` overrides the exact dyadic table (e.g. with the reference's
+    least-squares fit, to reproduce its rounding)."""
+    table = ZP_COEFFS if coeffs is None else coeffs
     x1 = np.asarray(x1, dtype=np.float64)
     x2 = np.asarray(x2, dtype=np.float64)
     shape = np.broadcast_shapes(x1.shape, x2.shape)
@@ -98,7 +113,7 @@ def interpolate(plane, col0, row0, x1, x2):
             dx, dy = ZP_OFFSETS[p, j]
             cc = np.clip(cb + dx, 0, cols - 1)
             rr = np.clip(rb + dy, 0, rows - 1)
-            acc += _quad(ZP_COEFFS[p, j], e1, e2) * flat[rr * cols + cc]
+            acc += _quad(table[p, j], e1, e2) * flat[rr * cols + cc]
         res[idx] = acc
     return res.reshape(shape)
 
@@ -146,7 +161,7 @@ def mesh_pieces(field):
     return a1, a3, p2, p4, t1, t2, w
 
 
-def apply_mesh(plane, c_lo, r_lo, field, cols, rows):
+def apply_mesh(plane, c_lo, r_lo, field, cols, rows, coeffs=None):
     a1, a3, p2, p4, t1, t2, w = mesh_pieces(field)
     xb = cols[None, :] + t1
     yb = rows[:, None] + t2
@@ -154,7 +169,8 @@ def apply_mesh(plane, c_lo, r_lo, field, cols, rows):
     for i in range(16):
         b1, b2, b3, b4 = VERTEX_BITS[i]
         acc += VERTEX_SIGNS[i] * interpolate(
-            plane, c_lo, r_lo, xb - (b1 * a1 + b2 * p2 - b4 * p4), yb - (b2 * p2 + b3 * a3 + b4 * p4))
+            plane, c_lo, r_lo, xb - (b1 * a1 + b2 * p2 - b4 * p4), yb - (b2 * p2 + b3 * a3 + b4 * p4),
+            coeffs)
     return acc * w
 
 
@@ -178,7 +194,7 @@ def prepare_field(field, shape, iterations):
     return np.maximum(field, SCALE_FLOOR) / math.sqrt(iterations)
 
 
-def filter_space_variant(f, field, iterations=1, guard=True):
+def filter_space_variant(f, field, iterations=1, guard=True, coeffs=None):
     """The reference engine's output (engine.py:265-324), same canvases."""
     f = np.asarray(f, dtype=np.float64)
     if f.ndim != 2:
@@ -197,7 +213,8 @@ def filter_space_variant(f, field, iterations=1, guard=True):
         plane, c_lo, r_lo = preintegrate(
             cur, col0, row0, (pc - left, pc + pw - 1 + right), (pr - below, pr + ph - 1 + above), guard)
         cur = apply_mesh(plane, c_lo, r_lo, fp,
-                         np.arange(pc, pc + pw, dtype=np.float64), np.arange(pr, pr + ph, dtype=np.float64))
+                         np.arange(pc, pc + pw, dtype=np.float64), np.arange(pr, pr + ph, dtype=np.float64),
+                         coeffs)
         col0, row0 = pc, pr
     return cur
 

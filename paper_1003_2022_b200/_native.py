@@ -55,6 +55,9 @@ SIGNATURES = {
     "rubs_b200_last_error": (ctypes.c_char_p, []),
     "rubs_b200_launch_count": (_i64, []),
     "rubs_b200_reset_launch_count": (None, []),
+    "rubs_b200_set_profiling": (None, [_int]),
+    "rubs_b200_kernel_time": (None, [_int, _dp, _lp]),
+    "rubs_b200_reset_kernel_time": (None, []),
     "rubs_b200_filter": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _int, _i64, _int, _vp, _i64, _vp]),
     "rubs_b200_filter_host": (_int, [_vp, _int, _i64, _i64, _vp, _int, _int, _vp]),
     "rubs_b200_lut_create": (_int, [_vp, _vp, _vp, _int, _int, ctypes.POINTER(_vp)]),
@@ -90,10 +93,6 @@ def load(path: str | None = None):
     if path is None:
         _lib = L
     return L
-
-
-class OutOfGridError(ValueError):
-    pass
 
 
 def check(rc: int) -> None:

@@ -45,6 +45,61 @@ constexpr int kRegionCap = kSmemBytes / 8;  // doubles
 thread_local std::string t_last_error;
 thread_local int64_t t_launches = 0;
 
+// optional per-kernel event timing (bench.py roofline)
+struct KTimer {
+  bool on = false;
+  double ms[2] = {0.0, 0.0};
+  int64_t n[2] = {0, 0};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> pool;
+};
+thread_local KTimer t_timer;
+
+cudaEvent_t timer_event() {
+  if (!t_timer.pool.empty()) {
+    cudaEvent_t e = t_timer.pool.back();
+    t_timer.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Bracket one launch: returns the start event (or null when off).
+struct TimedLaunch {
+  int kind;
+  cudaEvent_t a = nullptr;
+  cudaStream_t s;
+  TimedLaunch(int k, cudaStream_t st) : kind(k), s(st) {
+    if (t_timer.on) {
+      a = timer_event();
+      cudaEventRecord(a, s);
+    }
+  }
+  ~TimedLaunch() {
+    if (a) {
+      cudaEvent_t b = timer_event();
+      cudaEventRecord(b, s);
+      t_timer.pending.push_back({kind, {a, b}});
+    }
+  }
+};
+
+// Called after the stream was synchronised.
+void timer_collect() {
+  for (auto &p : t_timer.pending) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) {
+      t_timer.ms[p.first] += ms;
+      t_timer.n[p.first] += 1;
+    }
+    t_timer.pool.push_back(p.second.first);
+    t_timer.pool.push_back(p.second.second);
+  }
+  t_timer.pending.clear();
+}
+
 int set_error(int code, const std::string &msg) {
   t_last_error = msg;
   return code;
@@ -535,6 +590,7 @@ int fetch_status(cudaStream_t s, Status &out) {
                                 cudaMemcpyDeviceToHost, s));
   RUBS_CUDA_TRY(cudaStreamSynchronize(s));
   out = *t_scr.h_status;
+  timer_collect();
   return RUBS_OK;
 }
 
@@ -544,8 +600,11 @@ int launch_cells(const FieldSpec &F, const DomainSpec &D, int global_out, cudaSt
   const int cells_y = (D.ph + kCell - 1) / kCell;
   int rc = ensure_cells((size_t)cells_x * cells_y);
   if (rc) return rc;
-  cell_margins_kernel<<<cells_x * cells_y, 256, 0, s>>>(F, D, cells_x, t_scr.d_cells,
-                                                        t_scr.d_status, global_out);
+  {
+    TimedLaunch tl(1, s);
+    cell_margins_kernel<<<cells_x * cells_y, 256, 0, s>>>(F, D, cells_x, t_scr.d_cells,
+                                                          t_scr.d_status, global_out);
+  }
   ++t_launches;
   RUBS_CUDA_TRY(cudaGetLastError());
   return RUBS_OK;
@@ -554,8 +613,11 @@ int launch_cells(const FieldSpec &F, const DomainSpec &D, int global_out, cudaSt
 int launch_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int cells_x,
                 cudaStream_t s) {
   const int tiles_x = (D.pw + kTile - 1) / kTile, tiles_y = (D.ph + kTile - 1) / kTile;
-  tile_filter_kernel<<<tiles_x * tiles_y, kThreads, kSmemBytes, s>>>(
-      I, F, D, t_scr.d_cells, cells_x, tiles_x, kRegionCap, t_scr.d_status);
+  {
+    TimedLaunch tl(0, s);
+    tile_filter_kernel<<<tiles_x * tiles_y, kThreads, kSmemBytes, s>>>(
+        I, F, D, t_scr.d_cells, cells_x, tiles_x, kRegionCap, t_scr.d_status);
+  }
   ++t_launches;
   RUBS_CUDA_TRY(cudaGetLastError());
   return RUBS_OK;
@@ -675,6 +737,25 @@ FieldSpec lut_field(const rubs_lut *lut, const void *size, const void *elong, co
 extern "C" {
 
 const char *rubs_b200_version(void) { return "rubs_b200 0.1.0 (sm_100a)"; }
+
+void rubs_b200_set_profiling(int enable) { t_timer.on = enable != 0; }
+
+void rubs_b200_kernel_time(int kind, double *total_ms, int64_t *launches) {
+  double ms = 0.0;
+  int64_t n = 0;
+  for (int k = 0; k < 2; ++k)
+    if (kind == k || kind == 2) {
+      ms += t_timer.ms[k];
+      n += t_timer.n[k];
+    }
+  if (total_ms) *total_ms = ms;
+  if (launches) *launches = n;
+}
+
+void rubs_b200_reset_kernel_time(void) {
+  t_timer.ms[0] = t_timer.ms[1] = 0.0;
+  t_timer.n[0] = t_timer.n[1] = 0;
+}
 const char *rubs_b200_last_error(void) { return t_last_error.c_str(); }
 int64_t rubs_b200_launch_count(void) { return t_launches; }
 void rubs_b200_reset_launch_count(void) { t_launches = 0; }

@@ -1,0 +1,390 @@
+"""Parity of the CUDA path (through the C ABI) with the oracle.
+
+Mirrors the reference's own engine tests (pkg/tests/test_engine.py,
+test_acceptance.py 01/02/09, test_zp.py) with the checker swapped for the
+pinned oracle (oracle/), then adds the BASELINE configs at full size:
+sampled exact-dense checks plus size-independent properties (linearity,
+impulse response = exact kernel, zero padding).
+
+Tolerances: abs 1e-12 where the reference asserts 1e-12 (impulses), 1e-9
+(relative to max |output|) against the exact dense oracle everywhere else
+-- the north_star's target, tighter than the reference's own fast path
+manages beyond 256^2.
+"""
+
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from oracle import port
+from conftest import golden, impulse, smooth_random_field
+import paper_1003_2022_b200 as rb
+from paper_1003_2022_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+REL_TOL = 1e-9
+
+
+def kernel_at_offsets(a, shape, center):
+    h, w = shape
+    cy, cx = center
+    return oracle.kernel_values(a, np.arange(w, dtype=float)[None, :] - cx,
+                                np.arange(h, dtype=float)[:, None] - cy)
+
+
+def rel_err(got, ref):
+    return float(np.abs(got - ref).max() / max(np.abs(ref).max(), 1e-300))
+
+
+def sample_points(rng, H, W, n, extra=()):
+    pts = np.stack([rng.integers(0, H, n), rng.integers(0, W, n)], axis=1)
+    border = [[0, 0], [0, W - 1], [H - 1, 0], [H - 1, W - 1], [0, W // 2], [H - 1, W // 3],
+              [H // 2, 0], [H // 3, W - 1], [1, 1], [H - 2, W - 2]]
+    return np.concatenate([pts, np.array(border), np.array(list(extra), dtype=np.int64).reshape(-1, 2)])
+
+
+# --- reference test_engine.py, through the drop-in API ---------------------
+
+
+def test_impulse_matches_exact_kernel(cuda, rng):
+    for _ in range(10):
+        a = rng.uniform(0.7, 2.8, size=4)
+        out = rb.filter_space_invariant(impulse((33, 33)), a)
+        assert np.abs(out - kernel_at_offsets(a, (33, 33), (16, 16))).max() < 1e-12
+
+
+def test_impulse_golden(cuda):
+    g = golden("engine_small.npz")
+    for a, ref in zip(g["impulse_a"], g["impulse_out"]):
+        out = rb.filter_space_invariant(impulse((33, 33)), a)
+        assert np.abs(out - kernel_at_offsets(a, (33, 33), (16, 16))).max() < 1e-12
+        assert np.abs(out - ref).max() < 1e-12
+    out = rb.filter_space_invariant(impulse((25, 31), at=(7, 22)), [1.1, 2.3, 0.8, 1.6])
+    assert np.abs(out - kernel_at_offsets([1.1, 2.3, 0.8, 1.6], (25, 31), (7, 22))).max() < 1e-12
+
+
+@pytest.mark.parametrize("case,m", [("uni", 1), ("var", 1), ("it2", 2)])
+def test_matches_dense_oracle_golden(cuda, case, m):
+    g = golden("engine_small.npz")
+    f = g[f"{case}_f"]
+    fld = g["uni_a"] if case == "uni" else g[f"{case}_field"]
+    out = rb.filter_space_variant(f, fld, m)
+    assert np.abs(out - g[f"{case}_dense"]).max() < 1e-9
+    assert np.abs(out - oracle.dense(f, fld, m)).max() < 1e-9
+
+
+def test_three_passes_and_floor(cuda):
+    g = golden("engine_small.npz")
+    f, fld = g["it3_f"], g["it3_field"]
+    assert np.abs(rb.filter_space_variant(f, fld) - g["floor_dense"]).max() < 1e-9
+    out3 = rb.filter_space_variant(f, fld, 3)
+    assert np.abs(out3 - oracle.dense(f, fld, 3)).max() < 1e-9
+    assert np.abs(out3 - g["it3_ref"]).max() < 1e-8
+
+
+def test_config1_style_golden(cuda):
+    g = golden("engine_small.npz")
+    out = rb.filter_space_variant(g["c1s_f"], g["c1s_field"])
+    assert np.abs(out - g["c1s_dense"]).max() < 1e-9
+
+
+def test_invariant_is_variant_bitwise(cuda, rng):
+    f = rng.random((17, 19))
+    a = np.array([1.2, 1.7, 2.4, 1.1])
+    assert np.array_equal(rb.filter_space_variant(f, rb.ScaleField.uniform(f.shape, a)),
+                          rb.filter_space_invariant(f, a))
+
+
+def test_constant_preserved_for_integer_straight_widths(cuda):
+    out = rb.filter_space_invariant(np.ones((28, 28)), [2.0, 1.3, 3.0, 2.6])
+    assert np.abs(out[7:-7, 7:-7] - 1.0).max() < 1e-10
+
+
+def test_fractional_widths_shift_the_constant(cuda):
+    out = rb.filter_space_invariant(np.ones((28, 28)), [1.3, 1.1, 0.9, 1.2])
+    dev = np.abs(out[8:-8, 8:-8] - 1.0).max()
+    assert 1e-3 < dev < 0.1
+
+
+def test_linearity(cuda, rng):
+    a = np.array([1.5, 1.0, 2.0, 1.3])
+    f = rng.standard_normal((15, 13))
+    g = rng.standard_normal((15, 13))
+    lhs = rb.filter_space_invariant(1.5 * f - 0.25 * g, a)
+    rhs = 1.5 * rb.filter_space_invariant(f, a) - 0.25 * rb.filter_space_invariant(g, a)
+    assert np.abs(lhs - rhs).max() < 1e-10
+
+
+def test_zero_padding_consistency(cuda, rng):
+    f = rng.random((12, 12))
+    a = np.array([1.8, 1.2, 1.5, 2.1])
+    padded = np.zeros((24, 24))
+    padded[6:18, 6:18] = f
+    assert np.abs(rb.filter_space_invariant(padded, a)[6:18, 6:18] - rb.filter_space_invariant(f, a)).max() < 1e-11
+
+
+def test_scale_floor_clamps_bitwise(cuda):
+    f = impulse((15, 15))
+    assert np.array_equal(rb.filter_space_invariant(f, [0.01] * 4),
+                          rb.filter_space_invariant(f, [rb.SCALE_FLOOR] * 4))
+
+
+def test_overflow_guard_raises(cuda):
+    with pytest.raises(OverflowError):
+        rb.filter_space_invariant(np.full((64, 256), 1e14), [1.0, 1.0, 1.0, 1.0])
+
+
+def test_nonfinite_field_raises(cuda):
+    fld = np.ones((6, 7, 4))
+    fld[3, 2, 1] = np.nan
+    with pytest.raises(ValueError):
+        rb.filter_space_variant(np.ones((6, 7)), fld)
+    fld[3, 2, 1] = np.inf
+    with pytest.raises(ValueError):
+        rb.filter_space_variant(np.ones((6, 7)), fld)
+
+
+def test_raw_nonpositive_entries_are_floored(cuda):
+    # raw arrays with <= 0 entries are floored, not rejected (engine.py:292)
+    f = impulse((11, 11))
+    assert np.array_equal(rb.filter_space_variant(f, np.full((11, 11, 4), -3.0)),
+                          rb.filter_space_invariant(f, [0.05] * 4))
+
+
+def test_iterated_impulse_point_symmetry(cuda):
+    a = np.array([1.6, 1.8, 2.0, 1.4])
+    for m in (1, 2, 3):
+        out = rb.filter_space_invariant(impulse((41, 41)), a, iterations=m)
+        assert np.abs(out - out[::-1, ::-1]).max() < 1e-11
+
+
+def test_empty_and_ragged_shapes(cuda, rng):
+    assert rb.filter_space_invariant(np.zeros((0, 5)), [1.0] * 4).shape == (0, 5)
+    for shape in [(1, 1), (1, 37), (37, 1), (33, 65), (65, 31)]:
+        f = rng.random(shape)
+        fld = rng.uniform(0.5, 3.0, size=shape + (4,))
+        assert np.abs(rb.filter_space_variant(f, fld) - oracle.dense(f, fld)).max() < 1e-9
+
+
+def test_float32_input_is_upcast(cuda, rng):
+    f32 = rng.random((40, 30)).astype(np.float32)
+    fld = rng.uniform(0.8, 2.5, size=(40, 30, 4))
+    out = rb.filter_space_variant(f32, fld)
+    assert out.dtype == np.float64
+    assert np.array_equal(out, rb.filter_space_variant(f32.astype(np.float64), fld))
+
+
+# --- reference test_acceptance.py ------------------------------------------
+
+
+def test_acceptance_01_space_variant_matches_dense_oracle(cuda, rng):
+    shape = (64, 64)
+    for _ in range(2):
+        f = rng.uniform(0.0, 1.0, size=shape)
+        flat = np.broadcast_to(rng.uniform(0.8, 2.4, size=4), shape + (4,)).copy()
+        wavy = np.stack([smooth_random_field(rng, shape, 0.7, 2.6) for _ in range(4)], axis=-1)
+        for field in (flat, wavy):
+            assert np.abs(rb.filter_space_variant(f, field) - oracle.dense(f, field)).max() < 1e-9
+
+
+def test_acceptance_02_impulse_response_is_sampled_kernel(cuda, rng):
+    for a in rng.uniform(0.6, 2.8, size=(25, 4)):
+        out = rb.filter_space_invariant(impulse((33, 33)), a)
+        assert np.abs(out - kernel_at_offsets(a, (33, 33), (16, 16))).max() < 1e-12
+
+
+def test_acceptance_03_runtime_flat_across_kernel_sizes(cuda):
+    torch = cuda
+    f = torch.from_numpy(np.random.default_rng(1).uniform(0.0, 1.0, size=(512, 512))).cuda()
+    means = []
+    for s in (1.0, 2.0, 4.0, 8.0, 16.0):
+        a = np.full(4, math.sqrt(3.0 * s))
+        rb.filter_space_invariant(f, a)
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record()
+        for _ in range(20):
+            rb.filter_space_invariant(f, a)
+        t1.record()
+        torch.cuda.synchronize()
+        means.append(t0.elapsed_time(t1) / 20)
+    assert max(means) / min(means) < 1.5, means
+
+
+# --- ZP interpolation and global pre-integration (API parity) --------------
+
+
+def test_interpolate_matches_reference_golden(cuda):
+    g = golden("interpolate.npz")
+    img = rb.IntegratedImage(g["plane"], int(g["col0"]), int(g["row0"]))
+    got = rb.interpolate(img, g["x1"], g["x2"])
+    assert np.abs(got - g["values"]).max() < 1e-12
+
+
+def test_interpolate_matches_support_sum(cuda, rng):
+    plane = rng.standard_normal((40, 40))
+    q1 = rng.uniform(4.0, 35.0, size=10000)
+    q2 = rng.uniform(4.0, 35.0, size=10000)
+    fast = rb.interpolate(rb.IntegratedImage(plane), q1, q2)
+    brute = np.zeros_like(fast)
+    n1, n2 = np.round(q1).astype(int), np.round(q2).astype(int)
+    unit = np.array([1.0, math.sqrt(2.0), 1.0, math.sqrt(2.0)])
+    for d1 in range(-3, 4):
+        for d2 in range(-3, 4):
+            brute += plane[n2 + d2, n1 + d1] * oracle.kernel_values(unit, q1 - n1 - d1, q2 - n2 - d2)
+    assert np.abs(fast - brute).max() < 1e-12
+
+
+def test_interpolate_polynomial_reproduction(cuda, rng):
+    cc, rr = np.meshgrid(np.arange(15.0), np.arange(12.0))
+    q1 = rng.uniform(3.0, 11.0, size=200)
+    q2 = rng.uniform(3.0, 8.0, size=200)
+    got = rb.interpolate(rb.IntegratedImage(2.0 + 0.3 * cc - 0.7 * rr), q1, q2)
+    assert np.abs(got - (2.0 + 0.3 * q1 - 0.7 * q2)).max() < 1e-12
+
+    def quad(x1, x2):
+        return 2.0 + 0.3 * x1 - 0.7 * x2 + 0.05 * x1 * x1 - 0.11 * x1 * x2 + 0.09 * x2 * x2
+    got = rb.interpolate(rb.IntegratedImage(quad(cc, rr)), q1, q2)
+    assert np.abs(got - quad(q1, q2) - 0.5 * 0.25 * (2 * 0.05 + 2 * 0.09)).max() < 1e-10
+
+
+def test_preintegrate_matches_reference_golden(cuda):
+    g = golden("preintegrate.npz")
+    img = rb.preintegrate(g["f"], col0=-3, row0=4, need_cols=(-9, 11), need_rows=(-1, 19))
+    assert (img.col0, img.row0) == (int(g["col0"]), int(g["row0"]))
+    assert np.abs(img.plane - g["plane"]).max() <= 1e-13 * np.abs(g["plane"]).max()
+    img0 = rb.preintegrate(g["f"])
+    assert img0.plane.shape == g["plane0"].shape
+    assert np.abs(img0.plane - g["plane0"]).max() <= 1e-13 * np.abs(g["plane0"]).max()
+
+
+def test_preintegrate_guard(cuda):
+    with pytest.raises(OverflowError):
+        rb.preintegrate(np.full((64, 256), 1e14))
+
+
+# --- LUT mapping ------------------------------------------------------------
+
+
+def test_lookup_many_matches_reference_golden(cuda):
+    g = golden("solver.npz")
+    lut = rb.ScaleLut(g["rho_grid"], g["phi_grid"], g["entries"])
+    got = rb.lookup_many(lut, g["size"], g["rho"], g["theta"])
+    assert np.abs(got - g["lookup"]).max() <= 1e-14 * np.abs(g["lookup"]).max()
+
+
+def test_lookup_out_of_grid_and_invalid(cuda):
+    lut = rb.default_lut()
+    with pytest.raises(rb.OutOfGrid):
+        rb.lookup_many(lut, [1.0], [6.5], [0.3])
+    with pytest.raises(ValueError):
+        rb.lookup_many(lut, [1.0], [2.0], [math.pi])
+    with pytest.raises(ValueError):
+        rb.lookup_many(lut, [-1.0], [2.0], [0.3])
+    with pytest.raises(ValueError):
+        rb.lookup_many(lut, [1.0], [0.5], [0.3])
+
+
+def test_fused_params_path_equals_field_path_bitwise(cuda, rng):
+    lut = rb.default_lut()
+    H, W = 70, 90
+    f = rng.random((H, W))
+    size = rng.uniform(0.5, 40.0, (H, W))
+    rho = rng.uniform(1.0, 5.0, (H, W))
+    th = rng.uniform(0.0, math.pi, (H, W))
+    fld = rb.lookup_many(lut, size, rho, th)
+    assert np.array_equal(rb.filter_space_variant_params(f, size, rho, th, lut), rb.filter_space_variant(f, fld))
+    fld_port = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, size, rho, th)
+    assert np.abs(fld - fld_port).max() < 1e-13 * fld.max()
+
+
+def test_fused_params_errors(cuda):
+    with pytest.raises(rb.OutOfGrid):
+        rb.filter_space_variant_params(np.ones((8, 8)), np.ones((8, 8)), np.full((8, 8), 9.0), np.zeros((8, 8)))
+    with pytest.raises(ValueError):
+        rb.filter_space_variant_params(np.ones((8, 8)), np.zeros((8, 8)), np.ones((8, 8)), np.zeros((8, 8)))
+
+
+def test_torch_device_path_matches_host_path(cuda, rng):
+    torch = cuda
+    f = rng.random((50, 70))
+    fld = rng.uniform(0.6, 3.0, size=(50, 70, 4))
+    host = rb.filter_space_variant(f, fld, 2)
+    dev = rb.filter_space_variant(torch.from_numpy(f).cuda(), torch.from_numpy(fld).cuda(), 2)
+    assert dev.is_cuda and dev.dtype == torch.float64
+    assert np.array_equal(dev.cpu().numpy(), host)
+
+
+# --- BASELINE configs at full size ------------------------------------------
+
+
+def test_config1_full(cuda, rng):
+    w = workloads.config1()
+    out = rb.filter_space_variant(w["f"], w["field"])
+    floored = np.argwhere((w["field"] < rb.SCALE_FLOOR).any(axis=-1))
+    extra = floored[rng.choice(len(floored), min(200, len(floored)), replace=False)] if len(floored) else []
+    pts = sample_points(rng, 256, 256, 1500, extra)
+    ref = oracle.points(w["f"], w["field"], pts)
+    assert rel_err(out[pts[:, 0], pts[:, 1]], ref) < REL_TOL
+
+
+def _config2_device(cuda):
+    torch = cuda
+    w = workloads.config2(device="cuda", param_dtype=torch.float32)
+    f = torch.from_numpy(w["f"]).cuda()
+    return w, f
+
+
+def test_config2_full_sampled_exact(cuda, rng):
+    w, f = _config2_device(cuda)
+    out = rb.filter_space_variant_params(f, w["size"], w["elong"], w["orient"]).cpu().numpy()
+    lut = rb.default_lut()
+    s, r, t = (v.double().cpu().numpy() for v in (w["size"], w["elong"], w["orient"]))
+    fld = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, s, r, t)
+    floored = np.argwhere((fld < rb.SCALE_FLOOR).any(axis=-1))
+    extra = floored[rng.choice(len(floored), min(100, len(floored)), replace=False)] if len(floored) else []
+    big = np.argwhere(s > 0.95 * s.max())
+    extra = list(extra) + list(big[rng.choice(len(big), min(100, len(big)), replace=False)])
+    pts = sample_points(rng, 2048, 2048, 1200, extra)
+    ref = oracle.points(w["f"], fld, pts)
+    assert rel_err(out[pts[:, 0], pts[:, 1]], ref) < REL_TOL
+
+
+def test_config2_full_linearity_and_impulses(cuda, rng):
+    torch = cuda
+    w, f = _config2_device(cuda)
+    args = (w["size"], w["elong"], w["orient"])
+    g = torch.from_numpy(rng.standard_normal((2048, 2048))).cuda()
+    lhs = rb.filter_space_variant_params(1.5 * f - 0.25 * g, *args)
+    rhs = 1.5 * rb.filter_space_variant_params(f, *args) - 0.25 * rb.filter_space_variant_params(g, *args)
+    assert (lhs - rhs).abs().max().item() < 1e-9 * rhs.abs().max().item()
+    # sparse impulses far apart: each response is the exact kernel of the
+    # OUTPUT pixel's own scale-vector (space-variant impulse response)
+    imp = torch.zeros((2048, 2048), dtype=torch.float64, device="cuda")
+    centres = [(300, 300), (1000, 1700), (1800, 400), (5, 2040), (1024, 1024)]
+    for (y, x) in centres:
+        imp[y, x] = 1.0
+    out = rb.filter_space_variant_params(imp, *args).cpu().numpy()
+    lut = rb.default_lut()
+    for (y, x) in centres:
+        ys, xs = np.mgrid[max(0, y - 12):min(2048, y + 13), max(0, x - 12):min(2048, x + 13)]
+        fld = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, *(v.double().cpu().numpy()[ys, xs] for v in args))
+        fld = np.maximum(fld, rb.SCALE_FLOOR)
+        ref = np.array([oracle.kernel_values(fld[i, j], xs[i, j] - x, ys[i, j] - y)
+                        for i in range(ys.shape[0]) for j in range(ys.shape[1])]).reshape(ys.shape)
+        assert np.abs(out[ys, xs] - ref).max() < 1e-12
+
+
+def test_config4_one_image_two_passes(cuda, rng):
+    torch = cuda
+    w = workloads.config4_image(0, 1024, 1024, device="cuda", param_dtype=torch.float32)
+    f = torch.from_numpy(w["f"]).cuda()
+    out = rb.filter_space_variant_params(f, w["size"], w["elong"], w["orient"], iterations=2).cpu().numpy()
+    lut = rb.default_lut()
+    s, r, t = (v.double().cpu().numpy() for v in (w["size"], w["elong"], w["orient"]))
+    fld = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, s, r, t)
+    pts = sample_points(rng, 1024, 1024, 24)
+    ref = oracle.points(w["f"].astype(np.float64), fld, pts, iterations=2)
+    assert rel_err(out[pts[:, 0], pts[:, 1]], ref) < REL_TOL
