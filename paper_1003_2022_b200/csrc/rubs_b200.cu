@@ -37,7 +37,6 @@ using namespace rubs;
 namespace {
 
 constexpr int kTile = 32;        // output tile edge
-constexpr int kCell = 16;        // margin cell edge
 constexpr int kThreads = 512;    // tile kernel CTA size
 constexpr int kSmemBytes = 225 * 1024;  // dynamic shared memory per tile CTA (+ static <= 227 KiB)
 constexpr int kRegionCap = kSmemBytes / 8;  // doubles
@@ -115,257 +114,373 @@ int set_error(int code, const std::string &msg) {
 // ---------------------------------------------------------------------------
 // Kernels
 
-// Pass-domain cell margins.  One CTA per 16x16 cell: every pixel fetches its
-// scale-vector (field, uniform or LUT-mapped), the CTA reduces the four
-// integer read margins.  With `global_out` it also folds them into the
-// status word (the reference's whole-field _read_margins, engine.py:247-262).
-__global__ void __launch_bounds__(256) cell_margins_kernel(FieldSpec F, DomainSpec D,
-                                                           int cells_x, int4 *cells,
-                                                           Status *st, int global_out) {
+// Whole-field margins (the reference's _read_margins, engine.py:247-262),
+// needed before launch only when iterations > 1 (they size the extended
+// pass canvases).  One CTA per 16x16 cell, exact reference arithmetic.
+__global__ void __launch_bounds__(256) global_margins_kernel(FieldSpec F, DomainSpec D,
+                                                             int cells_x, Status *st) {
   const int cx = blockIdx.x % cells_x, cy = blockIdx.x / cells_x;
-  const int x = cx * kCell + (threadIdx.x & 15), y = cy * kCell + (threadIdx.x >> 4);
+  const int x = cx * 16 + (threadIdx.x & 15), y = cy * 16 + (threadIdx.x >> 4);
   unsigned flags = 0;
   int4 m = make_int4(0, 0, 0, 0);
   if (x < D.pw && y < D.ph) {
     double a[4];
-    field_at(F, D.pc_lo + x, D.pr_lo + y, a, flags);
+    field_at_rt(F, D.pc_lo + x, D.pr_lo + y, a, flags);
     m = pixel_margins(a);
   }
-  // warp reduce
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    m.x = max(m.x, __shfl_xor_sync(0xffffffffu, m.x, o));
-    m.y = max(m.y, __shfl_xor_sync(0xffffffffu, m.y, o));
-    m.z = max(m.z, __shfl_xor_sync(0xffffffffu, m.z, o));
-    m.w = max(m.w, __shfl_xor_sync(0xffffffffu, m.w, o));
-    flags |= __shfl_xor_sync(0xffffffffu, flags, o);
-  }
-  __shared__ int4 red[8];
-  __shared__ unsigned redf[8];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
-    red[warp] = m;
-    redf[warp] = flags;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int4 r = red[0];
-    unsigned f = redf[0];
-    for (int w = 1; w < 8; ++w) {
-      r.x = max(r.x, red[w].x);
-      r.y = max(r.y, red[w].y);
-      r.z = max(r.z, red[w].z);
-      r.w = max(r.w, red[w].w);
-      f |= redf[w];
-    }
-    cells[blockIdx.x] = r;
-    if (f) atomicOr(&st->flags, f);
-    if (global_out) {
-      atomicMax(&st->gm[0], r.x);
-      atomicMax(&st->gm[1], r.y);
-      atomicMax(&st->gm[2], r.z);
-      atomicMax(&st->gm[3], r.w);
-    }
+  m.x = __reduce_max_sync(0xffffffffu, m.x);
+  m.y = __reduce_max_sync(0xffffffffu, m.y);
+  m.z = __reduce_max_sync(0xffffffffu, m.z);
+  m.w = __reduce_max_sync(0xffffffffu, m.w);
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if ((threadIdx.x & 31) == 0) {
+    if (flags) atomicOr(&st->flags, flags);
+    atomicMax(&st->gm[0], m.x);
+    atomicMax(&st->gm[1], m.y);
+    atomicMax(&st->gm[2], m.z);
+    atomicMax(&st->gm[3], m.w);
   }
 }
 
 // Load the image over region lattice [rc0, rc0+RW) x [rr0, rr0+RH) into
 // shared memory as fp64, zero outside the image (zero padding, engine.py:155).
+// One warp per row, lanes over columns, several loads in flight per lane.
+template <int DT>
 __device__ __forceinline__ void load_region(double *S, int P, const ImageSpec &I, int rc0,
                                             int rr0, int RW, int RH) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  for (int r = warp; r < RH; r += nw) {
-    const int ir = rr0 + r - I.row0;
-    double *row = S + r * P;
-    const bool rin = (ir >= 0 && ir < I.h);
-    for (int c = lane; c < RW; c += 32) {
-      const int ic = rc0 + c - I.col0;
-      double v = 0.0;
-      if (rin && ic >= 0 && ic < I.w) v = load_scalar(I.f, I.dt, (int64_t)ir * I.ld + ic);
-      row[c] = v;
+  const int ic0 = rc0 - I.col0, ir0 = rr0 - I.row0;
+  const bool inside = ic0 >= 0 && ir0 >= 0 && ic0 + RW <= I.w && ir0 + RH <= I.h;
+  if (inside) {
+    for (int r = warp; r < RH; r += nw) {
+      const int64_t g = (int64_t)(ir0 + r) * I.ld + ic0;
+      double *row = S + r * P;
+      int c = lane;
+      for (; c + 96 < RW; c += 128) {
+        const double v0 = load_px<DT>(I.f, g + c), v1 = load_px<DT>(I.f, g + c + 32);
+        const double v2 = load_px<DT>(I.f, g + c + 64), v3 = load_px<DT>(I.f, g + c + 96);
+        row[c] = v0;
+        row[c + 32] = v1;
+        row[c + 64] = v2;
+        row[c + 96] = v3;
+      }
+      for (; c < RW; c += 32) row[c] = load_px<DT>(I.f, g + c);
+    }
+  } else {
+    for (int r = warp; r < RH; r += nw) {
+      const int ir = ir0 + r;
+      double *row = S + r * P;
+      const bool rin = (ir >= 0 && ir < I.h);
+      const int64_t g = (int64_t)ir * I.ld + ic0;
+      for (int c = lane; c < RW; c += 32) {
+        const int ic = ic0 + c;
+        row[c] = (rin && ic >= 0 && ic < I.w) ? load_px<DT>(I.f, g + c) : 0.0;
+      }
     }
   }
 }
 
-// The four running-sum sweeps of engine.py:186-193 on the region, with the
-// sums started at the region edge.  Returns (via gmax) max |plane|.
-__device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, double &gmax) {
+// The four running sums of engine.py:186-193 on the region, started at the
+// region edge.  The two x sqrt(2) scalings are folded into the output weight
+// (the pipeline is linear), so the plane here is g / 2.  RS2 and RS4 run
+// row-synchronously inside a warp (lane = line) so every shared access of a
+// warp hits consecutive addresses.  Tracks max high word of |plane| for the
+// 2^53 guard.
+__device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, unsigned &ghi) {
   const int tid = threadIdx.x, nt = blockDim.x;
-  // RS1: cumulative sum along +x, then x sqrt2
+  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+  // RS1: along +x (one thread per row)
   for (int r = tid; r < RH; r += nt) {
     double *p = S + r * P;
     double s = 0.0;
-    for (int c = 0; c < RW; ++c) {
+    int c = 0;
+    for (; c + 4 <= RW; c += 4) {
+      const double v0 = p[c], v1 = p[c + 1], v2 = p[c + 2], v3 = p[c + 3];
+      s += v0; p[c] = s;
+      s += v1; p[c + 1] = s;
+      s += v2; p[c + 2] = s;
+      s += v3; p[c + 3] = s;
+    }
+    for (; c < RW; ++c) {
       s += p[c];
-      p[c] = s * kSqrt2;
+      p[c] = s;
     }
   }
   __syncthreads();
-  // RS2: g[r][c] += g[r-1][c-1] (lines c - r = const)
-  for (int L = tid; L < RH + RW - 1; L += nt) {
-    const int k = L - (RH - 1);
-    const int r0 = k < 0 ? -k : 0, c0 = k < 0 ? 0 : k;
-    const int len = min(RH - r0, RW - c0);
-    double *p = S + r0 * P + c0;
+  // RS2: g[r][c] += g[r-1][c-1]; lines k = c - r in [-(RH-1), RW-1]
+  const int nlines = RH + RW - 1;
+  for (int lb = warp * 32; lb < nlines; lb += nw * 32) {
+    const int kb = lb - (RH - 1), k = kb + lane;
+    const int t0 = max(0, -(kb + 31)), t1 = min(RH - 1, RW - 1 - kb);
     double s = 0.0;
-    for (int j = 0; j < len; ++j) {
-      s += *p;
-      *p = s;
-      p += P + 1;
+    double *p = S + t0 * P + t0 + k;
+    for (int t = t0; t <= t1; ++t, p += P + 1) {
+      const int c = t + k;
+      if (c >= 0 && c < RW) {
+        s += *p;
+        *p = s;
+      }
     }
   }
   __syncthreads();
-  // RS3: cumulative sum along +y, then x sqrt2
+  // RS3: along +y (one thread per column)
   for (int c = tid; c < RW; c += nt) {
     double *p = S + c;
     double s = 0.0;
-    for (int r = 0; r < RH; ++r) {
+    int r = 0;
+    for (; r + 4 <= RH; r += 4) {
+      const double v0 = p[0], v1 = p[P], v2 = p[2 * P], v3 = p[3 * P];
+      s += v0; p[0] = s;
+      s += v1; p[P] = s;
+      s += v2; p[2 * P] = s;
+      s += v3; p[3 * P] = s;
+      p += 4 * P;
+    }
+    for (; r < RH; ++r, p += P) {
       s += *p;
-      *p = s * kSqrt2;
-      p += P;
+      *p = s;
     }
   }
   __syncthreads();
-  // RS4: g[r][c] += g[r-1][c+1] (lines c + r = const)
-  double gm = 0.0;
-  for (int k = tid; k < RH + RW - 1; k += nt) {
-    const int r0 = max(0, k - (RW - 1)), c0 = k - r0;
-    const int len = min(RH - r0, c0 + 1);
-    double *p = S + r0 * P + c0;
+  // RS4: g[r][c] += g[r-1][c+1]; lines k = c + r in [0, RH+RW-2]
+  unsigned gh = 0;
+  for (int kb = warp * 32; kb < nlines; kb += nw * 32) {
+    const int k = kb + lane;
+    const int t0 = max(0, kb - (RW - 1)), t1 = min(RH - 1, kb + 31);
     double s = 0.0;
-    for (int j = 0; j < len; ++j) {
-      s += *p;
-      *p = s;
-      gm = fmax(gm, fabs(s));
-      p += P - 1;
+    double *p = S + t0 * P + (k - t0);
+    for (int t = t0; t <= t1; ++t, p += P - 1) {
+      const int c = k - t;
+      if (c >= 0 && c < RW) {
+        s += *p;
+        *p = s;
+        gh = max(gh, (unsigned)__double2hiint(s) & 0x7fffffffu);
+      }
     }
   }
-  gmax = fmax(gmax, gm);
+  ghi = max(ghi, gh);
   __syncthreads();
 }
 
-// Filter one pixel from the region plane (engine.py:219-244).
-//   n1, n2: lattice coordinates of the pixel; off0 = rr0 * P + rc0.
-__device__ __forceinline__ double pixel_fd(const double *__restrict__ S, int P, int off0,
-                                           int n1, int n2, const double a[4]) {
+// Per-pixel finite difference (engine.py:219-244) over the region plane,
+// 16 vertices x 7 ZP taps.  Sb = shared byte address of region element
+// (0, 0) shifted so that (m2 * P + m1) * 8 is the element at lattice
+// (m1, m2):  Sb = base - (rr0 * P + rc0) * 8.
+//
+// The 4 x 7 quadratic table of zp.py (exact multiples of 1/8)
+// folds into one canonical wedge: partition q (zp.py:82-86) only decides
+// which axis is "major" (q in {0, 3}: x) and the sign of the major residual,
+// which is +1 exactly when d1 + d2 >= 0 in both cases.  The seven taps are
+// the centre, the two major neighbours N (-sign) and P (+sign), the two
+// minor neighbours Bm/Bp and the two corners on the N side Cm/Cp.
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+// One ZP read (x 8) at the vertex whose nearest lattice element is at shared
+// byte address c, residual (d1, d2).
+__device__ __forceinline__ double zp_read8(uint32_t c, int P8, double d1, double d2) {
+  const bool gp = d1 >= -d2;  // d1 + d2 >= 0
+  const bool gm = d1 >= d2;   // d1 - d2 >= 0
+  const bool xmaj = (gp == gm);
+  int sA = xmaj ? 8 : P8;
+  sA = gp ? sA : -sA;
+  const int sB = xmaj ? P8 : 8;
+  const double u = dabs(xmaj ? d1 : d2);
+  const double v = xmaj ? d2 : d1;
+  const double g0 = lds64(c);
+  const double N = lds64(c - sA);
+  const double Pp = lds64(c + sA);
+  const double Bm = lds64(c - sB);
+  const double Bp = lds64(c + sB);
+  const double Cm = lds64(c - sA - sB);
+  const double Cp = lds64(c - sA + sB);
+  const double sBv = Bm + Bp, dBv = Bm - Bp, sC = Cm + Cp, dC = Cm - Cp;
+  const double A0 = fma(4.0, g0, N + Pp) + sBv;
+  const double L1 = N - Pp;
+  const double Caa2 = fma(2.0, Pp - g0, sC - sBv);
+  const double Cab4 = dC - dBv;
+  const double Cbb2 = fma(-2.0, g0 + N, sC + sBv);
+  const double V = v + v;
+  const double i1 = fma(u, Caa2, fma(V, Cab4, L1 + L1));
+  const double i2 = fma(v, Cbb2, dBv + dBv);
+  return fma(u + u, i1, fma(V, i2, A0));
+}
+
+// Per-pixel finite difference (engine.py:219-244) over the region plane,
+// 16 vertices x 7 ZP taps.  Sb = shared byte address such that
+// Sb + (m2 * P + m1) * 8 is the region element at lattice (m1, m2).
+//
+// The 4 x 7 quadratic table of zp.py (exact multiples of 1/8)
+// folds into one canonical wedge: partition q (zp.py:82-86) only decides
+// which axis is "major" (q in {0, 3}: x) and the sign of the major residual,
+// which is +1 exactly when d1 + d2 >= 0 in both cases.  The seven taps are
+// the centre, the two major neighbours N (-sign) and P (+sign), the two
+// minor neighbours Bm/Bp and the two corners on the N side Cm/Cp.
+__device__ __forceinline__ double pixel_fd(uint32_t Sb, int P, int n1, int n2, const double a[4]) {
   const double a1 = a[0], a2 = a[1], a3 = a[2], a4 = a[3];
   const double p2 = a2 * kInvSqrt2, p4 = a4 * kInvSqrt2;
   const double t1 = 0.5 * a1 + 0.5 * (p2 - p4) - 0.5;
   const double t2 = 0.5 * a3 + 0.5 * (p2 + p4) - 1.5;
-  const double w = 0.125 / (a1 * a2 * a3 * a4);
+  // 1/8 of the ZP table and the factor 2 folded out of the sweeps
+  const double w = 0.25 / (a1 * a2 * a3 * a4);
   const double xb = (double)n1 + t1, yb = (double)n2 + t2;
-  // distinct vertex abscissae: index q1 | q2 << 1 | q4 << 2
-  // x = xb - (q1 a1 + q2 p2 - q4 p4)     (engine.py:240)
-  // distinct ordinates:       index q2 | q3 << 1 | q4 << 2
-  // y = yb - (q2 p2 + q3 a3 + q4 p4)     (engine.py:241)
-  const double ox[8] = {0.0, a1, p2, a1 + p2, -p4, a1 - p4, p2 - p4, (a1 + p2) - p4};
-  const double oy[8] = {0.0, p2, a3, p2 + a3, p4, p2 + p4, a3 + p4, (p2 + a3) + p4};
-  int mx[8], my[8];
-  double dx[8], dy[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) {
-    lattice_split(xb - ox[k], mx[k], dx[k]);
-    lattice_split(yb - oy[k], my[k], dy[k]);
-    my[k] = my[k] * P - off0;
-  }
+  const int P8 = P * 8;
   double acc = 0.0;
+  // vertex i = q1 | q2 << 1 | q3 << 2 | q4 << 4; sign (-1)^popcount
+  //   x = xb - (q1 a1 + q2 p2 - q4 p4)   (engine.py:240)
+  //   y = yb - (q2 p2 + q3 a3 + q4 p4)   (engine.py:241)
 #pragma unroll
-  for (int i = 0; i < 16; ++i) {
-    const int q1 = i & 1, q2 = (i >> 1) & 1, q3 = (i >> 2) & 1, q4 = (i >> 3) & 1;
-    const int ix = q1 | (q2 << 1) | (q4 << 2);
-    const int iy = q2 | (q3 << 1) | (q4 << 2);
-    const double v = zp_read8(S, my[iy] + mx[ix], P, dx[ix], dy[iy]);
-    if (__popc(i) & 1)
-      acc -= v;
-    else
-      acc += v;
+  for (int q4 = 0; q4 < 2; ++q4) {
+    const double ox[4] = {q4 ? -p4 : 0.0, q4 ? a1 - p4 : a1, q4 ? p2 - p4 : p2,
+                          q4 ? (a1 + p2) - p4 : a1 + p2};  // index q1 | q2 << 1
+    const double oy[4] = {q4 ? p4 : 0.0, q4 ? p2 + p4 : p2, q4 ? a3 + p4 : a3,
+                          q4 ? (p2 + a3) + p4 : p2 + a3};  // index q2 | q3 << 1
+    uint32_t cx[4], cy[4];
+    double dx[4], dy[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int m;
+      lattice_split(xb - ox[k], m, dx[k]);
+      cx[k] = (uint32_t)(m * 8);
+      lattice_split(yb - oy[k], m, dy[k]);
+      cy[k] = Sb + (uint32_t)(m * P8);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int q1 = j & 1, q2 = (j >> 1) & 1, q3 = (j >> 2) & 1;
+      const int ix = q1 | (q2 << 1), iy = q2 | (q3 << 1);
+      const double F8 = zp_read8(cy[iy] + cx[ix], P8, dx[ix], dy[iy]);
+      if ((q1 + q2 + q3 + q4) & 1)
+        acc -= F8;
+      else
+        acc += F8;
+    }
   }
   return acc * w;
 }
 
-// One CTA per 32x32 output tile.  If the tile's region does not fit in
-// shared memory the tile is processed as its four 16x16 cells.
+// One CTA per 32x32 output tile of the pass domain (persistent-free grid).
+//   A. every thread maps its two pixels' scale-vectors (field / uniform /
+//      LUT, engine.py:291-293 + solver.py:289-335) once and keeps them in
+//      registers; the CTA reduces the read margins per 16x16 quadrant;
+//   B. the tile's region (tile + its own margins) is loaded into shared
+//      memory and pre-integrated there;
+//   C. every pixel takes its finite difference from the region.
+// A tile whose region exceeds `region_cap` doubles runs as four 16x16
+// quadrants with their own (smaller) regions.
+template <int MODE, int DT>
 __global__ void __launch_bounds__(kThreads, 1)
-    tile_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, const int4 *__restrict__ cells,
-                       int cells_x, int tiles_x, int region_cap, Status *st) {
+    tile_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int region_cap,
+                       Status *st) {
   extern __shared__ double S[];
-  __shared__ int s_sub[4][8];
+  __shared__ int s_m[4][4];  // quadrant margins (left, right, below, above)
+  __shared__ int s_plan[4][8];
   __shared__ int s_nsub;
+  const int tid = threadIdx.x;
   const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
   const int x0 = tx * kTile, y0 = ty * kTile;
-  if (threadIdx.x == 0) {
-    const int tw = min(kTile, D.pw - x0), th = min(kTile, D.ph - y0);
-    int4 cm[4];
-    int present[4];
-    for (int k = 0; k < 4; ++k) {
-      const int ccx = tx * 2 + (k & 1), ccy = ty * 2 + (k >> 1);
-      present[k] = (ccx * kCell < D.pw) && (ccy * kCell < D.ph);
-      cm[k] = present[k] ? cells[ccy * cells_x + ccx] : make_int4(0, 0, 0, 0);
+  const int lx = tid & 31, ly = tid >> 5;
+  if (tid < 16) s_m[tid >> 2][tid & 3] = 0;
+  __syncthreads();
+
+  // ---- A: scale-vectors and margins
+  unsigned flags = 0;
+  double av[2][4];
+  bool valid[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const int x = x0 + lx, y = y0 + ly + 16 * k;
+    valid[k] = (x < D.pw) && (y < D.ph);
+    int4 m = make_int4(0, 0, 0, 0);
+    if (valid[k]) {
+      field_at<MODE>(F, D.pc_lo + x, D.pr_lo + y, av[k], flags);
+      m = pixel_margins_fast(av[k]);
+    } else {
+      av[k][0] = av[k][1] = av[k][2] = av[k][3] = 1.0;
     }
-    int4 u = cm[0];
-    for (int k = 1; k < 4; ++k)
-      if (present[k]) {
-        u.x = max(u.x, cm[k].x);
-        u.y = max(u.y, cm[k].y);
-        u.z = max(u.z, cm[k].z);
-        u.w = max(u.w, cm[k].w);
-      }
-    const int RW = tw + u.x + u.y, RH = th + u.z + u.w;
-    const int P = RW | 1;
-    if (P * RH <= region_cap) {
+    // half-warp reduction (lanes 0-15 / 16-31 are different quadrants)
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      m.x = max(m.x, __shfl_xor_sync(0xffffffffu, m.x, o));
+      m.y = max(m.y, __shfl_xor_sync(0xffffffffu, m.y, o));
+      m.z = max(m.z, __shfl_xor_sync(0xffffffffu, m.z, o));
+      m.w = max(m.w, __shfl_xor_sync(0xffffffffu, m.w, o));
+    }
+    if ((lx & 15) == 0) {
+      const int q = (lx >> 4) + 2 * k;
+      atomicMax(&s_m[q][0], m.x);
+      atomicMax(&s_m[q][1], m.y);
+      atomicMax(&s_m[q][2], m.z);
+      atomicMax(&s_m[q][3], m.w);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    const int tw = min(kTile, D.pw - x0), th = min(kTile, D.ph - y0);
+    int u[4] = {0, 0, 0, 0};
+    for (int q = 0; q < 4; ++q)
+      for (int j = 0; j < 4; ++j) u[j] = max(u[j], s_m[q][j]);
+    const int RW = tw + u[0] + u[1], RH = th + u[2] + u[3];
+    if ((RW | 1) * RH <= region_cap) {
       s_nsub = 1;
-      int *d = s_sub[0];
-      d[0] = x0; d[1] = y0; d[2] = tw; d[3] = th;
-      d[4] = u.x; d[5] = u.z; d[6] = RW; d[7] = RH;
+      int *d = s_plan[0];
+      d[0] = x0; d[1] = y0; d[2] = tw; d[3] = th; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
     } else {
       int n = 0;
-      for (int k = 0; k < 4; ++k) {
-        if (!present[k]) continue;
-        const int sx = x0 + (k & 1) * kCell, sy = y0 + (k >> 1) * kCell;
-        const int sw = min(kCell, D.pw - sx), sh = min(kCell, D.ph - sy);
-        int *d = s_sub[n++];
-        d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh;
-        d[4] = cm[k].x; d[5] = cm[k].z;
-        d[6] = sw + cm[k].x + cm[k].y;
-        d[7] = sh + cm[k].z + cm[k].w;
+      for (int q = 0; q < 4; ++q) {
+        const int sx = x0 + (q & 1) * 16, sy = y0 + (q >> 1) * 16;
+        if (sx >= D.pw || sy >= D.ph) continue;
+        const int sw = min(16, D.pw - sx), sh = min(16, D.ph - sy);
+        int *d = s_plan[n++];
+        d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = s_m[q][0]; d[5] = s_m[q][2];
+        d[6] = sw + s_m[q][0] + s_m[q][1];
+        d[7] = sh + s_m[q][2] + s_m[q][3];
       }
       s_nsub = n;
     }
   }
   __syncthreads();
+
   const int nsub = s_nsub;
-  double gmax = 0.0;
-  unsigned flags = 0;
-  for (int sI = 0; sI < nsub; ++sI) {
-    const int sx = s_sub[sI][0], sy = s_sub[sI][1], sw = s_sub[sI][2], sh = s_sub[sI][3];
-    const int left = s_sub[sI][4], below = s_sub[sI][5], RW = s_sub[sI][6], RH = s_sub[sI][7];
+  unsigned ghi = 0;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S);
+  for (int si = 0; si < nsub; ++si) {
+    const int sx = s_plan[si][0], sy = s_plan[si][1], sw = s_plan[si][2], sh = s_plan[si][3];
+    const int left = s_plan[si][4], below = s_plan[si][5], RW = s_plan[si][6], RH = s_plan[si][7];
     const int P = RW | 1;
     if (P * RH > region_cap) {
-      if (threadIdx.x == 0) atomicOr(&st->flags, kFlagRegionTooLarge);
+      if (tid == 0) atomicOr(&st->flags, kFlagRegionTooLarge);
       continue;
     }
-    // region lattice origin
+    // ---- B: region load + running sums
     const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
-    load_region(S, P, I, rc0, rr0, RW, RH);
+    load_region<DT>(S, P, I, rc0, rr0, RW, RH);
     __syncthreads();
-    region_sweeps(S, P, RW, RH, gmax);
-    const int off0 = rr0 * P + rc0;
-    const int npx = sw * sh;
-    for (int p = threadIdx.x; p < npx; p += blockDim.x) {
-      const int px = sx + p % sw, py = sy + p / sw;
-      const int n1 = D.pc_lo + px, n2 = D.pr_lo + py;
-      double a[4];
-      field_at(F, n1, n2, a, flags);
-      D.out[(int64_t)py * D.ld_out + px] = pixel_fd(S, P, off0, n1, n2, a);
+    region_sweeps(S, P, RW, RH, ghi);
+    // ---- C: finite differences
+    const uint32_t Sb = sbase - (uint32_t)((rr0 * P + rc0) * 8);
+#pragma unroll 1
+    for (int k = 0; k < 2; ++k) {
+      const int x = x0 + lx, y = y0 + ly + 16 * k;
+      if (valid[k] && x >= sx && x < sx + sw && y >= sy && y < sy + sh) {
+        const int n1 = D.pc_lo + x, n2 = D.pr_lo + y;
+        double ak[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ak[j] = k ? av[1][j] : av[0][j];
+        D.out[(int64_t)y * D.ld_out + x] = pixel_fd(Sb, P, n1, n2, ak);
+      }
     }
     __syncthreads();
   }
-  // fold guard magnitude (non-negative doubles order like their bit patterns)
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) gmax = fmax(gmax, __shfl_xor_sync(0xffffffffu, gmax, o));
-  if ((threadIdx.x & 31) == 0 && gmax > 0.0)
-    atomicMax(&st->guard_bits, (unsigned long long)__double_as_longlong(gmax));
-  if (flags) atomicOr(&st->flags, flags);
+  ghi = __reduce_max_sync(0xffffffffu, ghi);
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (lx == 0) {
+    if (ghi) atomicMax(&st->guard_hi, ghi);
+    if (flags) atomicOr(&st->flags, flags);
+  }
 }
 
 // ---- standalone lookup (solver.lookup_many) ------------------------------
@@ -515,8 +630,6 @@ struct Scratch {
   int device = -1;
   Status *d_status = nullptr;
   Status *h_status = nullptr;  // pinned
-  int4 *d_cells = nullptr;
-  size_t cells_cap = 0;
   double *d_pass[2] = {nullptr, nullptr};
   size_t pass_cap[2] = {0, 0};
   bool attr_set = false;
@@ -533,19 +646,18 @@ int ensure_scratch() {
     RUBS_CUDA_TRY(cudaMallocHost(&t_scr.h_status, sizeof(Status)));
   }
   if (!t_scr.attr_set) {
-    RUBS_CUDA_TRY(cudaFuncSetAttribute(tile_filter_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemBytes));
+#define RUBS_SET_SMEM(M, T)                                                        \
+  RUBS_CUDA_TRY(cudaFuncSetAttribute(tile_filter_kernel<M, T>,                     \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                                     kSmemBytes))
+    RUBS_SET_SMEM(kModeField, 0);
+    RUBS_SET_SMEM(kModeField, 1);
+    RUBS_SET_SMEM(kModeUniform, 0);
+    RUBS_SET_SMEM(kModeUniform, 1);
+    RUBS_SET_SMEM(kModeLut, 0);
+    RUBS_SET_SMEM(kModeLut, 1);
+#undef RUBS_SET_SMEM
     t_scr.attr_set = true;
-  }
-  return RUBS_OK;
-}
-
-int ensure_cells(size_t n) {
-  if (n > t_scr.cells_cap) {
-    if (t_scr.d_cells) cudaFree(t_scr.d_cells);
-    t_scr.d_cells = nullptr;
-    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_cells, n * sizeof(int4)));
-    t_scr.cells_cap = n;
   }
   return RUBS_OK;
 }
@@ -571,9 +683,18 @@ int status_to_code(const Status &s) {
   if (s.flags & kFlagRegionTooLarge)
     return set_error(RUBS_EUNSUPPORTED,
                      "kernel support exceeds the on-chip region capacity of this build");
+  // tile planes hold g / 2 (the two sqrt(2) factors are folded into the
+  // output weight): the reference's |g| >= 2^53 is |g/2| >= 2^52, i.e. a
+  // high word >= 0x43300000.  The global canvas (rubs_b200_preintegrate)
+  // stores g itself and reports its full bits.
   double g;
   unsigned long long b = s.guard_bits;
   std::memcpy(&g, &b, sizeof(g));
+  const unsigned long long hb = (unsigned long long)s.guard_hi << 32;
+  double gt;
+  std::memcpy(&gt, &hb, sizeof(gt));
+  gt *= 2.0;
+  if (gt > g) g = gt;
   if (g >= 9007199254740992.0) {
     char buf[160];
     std::snprintf(buf, sizeof(buf),
@@ -594,29 +715,35 @@ int fetch_status(cudaStream_t s, Status &out) {
   return RUBS_OK;
 }
 
-int launch_cells(const FieldSpec &F, const DomainSpec &D, int global_out, cudaStream_t s,
-                 int &cells_x) {
-  cells_x = (D.pw + kCell - 1) / kCell;
-  const int cells_y = (D.ph + kCell - 1) / kCell;
-  int rc = ensure_cells((size_t)cells_x * cells_y);
-  if (rc) return rc;
+int launch_global_margins(const FieldSpec &F, const DomainSpec &D, cudaStream_t s) {
+  const int cells_x = (D.pw + 15) / 16, cells_y = (D.ph + 15) / 16;
   {
     TimedLaunch tl(1, s);
-    cell_margins_kernel<<<cells_x * cells_y, 256, 0, s>>>(F, D, cells_x, t_scr.d_cells,
-                                                          t_scr.d_status, global_out);
+    global_margins_kernel<<<cells_x * cells_y, 256, 0, s>>>(F, D, cells_x, t_scr.d_status);
   }
   ++t_launches;
   RUBS_CUDA_TRY(cudaGetLastError());
   return RUBS_OK;
 }
 
-int launch_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int cells_x,
-                cudaStream_t s) {
+template <int M, int T>
+void launch_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cudaStream_t s) {
   const int tiles_x = (D.pw + kTile - 1) / kTile, tiles_y = (D.ph + kTile - 1) / kTile;
+  tile_filter_kernel<M, T><<<tiles_x * tiles_y, kThreads, kSmemBytes, s>>>(
+      I, F, D, tiles_x, kRegionCap, t_scr.d_status);
+}
+
+int launch_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cudaStream_t s) {
   {
     TimedLaunch tl(0, s);
-    tile_filter_kernel<<<tiles_x * tiles_y, kThreads, kSmemBytes, s>>>(
-        I, F, D, t_scr.d_cells, cells_x, tiles_x, kRegionCap, t_scr.d_status);
+    const int m = F.mode, t = I.dt;
+    if (m == kModeField) {
+      if (t) launch_tiles<kModeField, 1>(I, F, D, s); else launch_tiles<kModeField, 0>(I, F, D, s);
+    } else if (m == kModeUniform) {
+      if (t) launch_tiles<kModeUniform, 1>(I, F, D, s); else launch_tiles<kModeUniform, 0>(I, F, D, s);
+    } else {
+      if (t) launch_tiles<kModeLut, 1>(I, F, D, s); else launch_tiles<kModeLut, 0>(I, F, D, s);
+    }
   }
   ++t_launches;
   RUBS_CUDA_TRY(cudaGetLastError());
@@ -637,13 +764,12 @@ int run_filter(const ImageSpec &img, FieldSpec F, int iterations, double *out, i
   F.scaled = iterations > 1;
   RUBS_CUDA_TRY(cudaMemsetAsync(t_scr.d_status, 0, sizeof(Status), s));
   DomainSpec D{0, 0, img.w, img.h, out, ld_out};
-  int cells_x = 0;
   if (iterations == 1) {
-    if ((rc = launch_cells(F, D, 0, s, cells_x))) return rc;
-    if ((rc = launch_pass(img, F, D, cells_x, s))) return rc;
+    // one launch: every tile computes its own scale-vectors and margins
+    if ((rc = launch_pass(img, F, D, s))) return rc;
   } else {
     // whole-field margins (engine.py:295) decide the pass canvases
-    if ((rc = launch_cells(F, D, 1, s, cells_x))) return rc;
+    if ((rc = launch_global_margins(F, D, s))) return rc;
     Status st;
     if ((rc = fetch_status(s, st))) return rc;
     if ((rc = status_to_code(st))) return rc;
@@ -665,8 +791,7 @@ int run_filter(const ImageSpec &img, FieldSpec F, int iterations, double *out, i
         Dp.out = t_scr.d_pass[k];
         Dp.ld_out = Dp.pw;
       }
-      if ((rc = launch_cells(F, Dp, 0, s, cells_x))) return rc;
-      if ((rc = launch_pass(cur, F, Dp, cells_x, s))) return rc;
+      if ((rc = launch_pass(cur, F, Dp, s))) return rc;
       cur = ImageSpec{Dp.out, 1, Dp.ld_out, Dp.ph, Dp.pw, Dp.pc_lo, Dp.pr_lo};
     }
   }
@@ -730,6 +855,8 @@ FieldSpec lut_field(const rubs_lut *lut, const void *size, const void *elong, co
   F.n_phi = lut->n_phi;
   F.rho_max = lut->rho_max;
   F.log_rho_max = std::log(lut->rho_max);
+  F.inv_log_rho_max = 1.0 / F.log_rho_max;
+  F.rho_lim = lut->rho_max * (1.0 + 1e-12);
   return F;
 }
 }  // namespace
