@@ -37,9 +37,10 @@ using namespace rubs;
 namespace {
 
 constexpr int kTile = 32;        // output tile edge
-constexpr int kThreads = 512;    // tile kernel CTA size
-constexpr int kSmemBytes = 225 * 1024;  // dynamic shared memory per tile CTA (+ static <= 227 KiB)
-constexpr int kRegionCap = kSmemBytes / 8;  // doubles
+constexpr int kThreadsSmall = 256;  // primary launch: 2 CTAs per SM
+constexpr int kThreadsLarge = 512;  // overflow launch: 1 CTA per SM
+constexpr int kSmemSmall = 112 * 1024;  // dynamic shared memory, primary CTA
+constexpr int kSmemLarge = 225 * 1024;  // overflow CTA (+ static <= 227 KiB)
 
 thread_local std::string t_last_error;
 thread_local int64_t t_launches = 0;
@@ -362,37 +363,41 @@ __device__ __forceinline__ double pixel_fd(uint32_t Sb, int P, int n1, int n2, c
   return acc * w;
 }
 
-// One CTA per 32x32 output tile of the pass domain (persistent-free grid).
-//   A. every thread maps its two pixels' scale-vectors (field / uniform /
-//      LUT, engine.py:291-293 + solver.py:289-335) once and keeps them in
+// One 32x32 output tile of the pass domain, processed by one CTA of NT
+// threads (1024 / NT pixels per thread):
+//   A. every thread maps its pixels' scale-vectors (field / uniform / LUT,
+//      engine.py:291-293 + solver.py:289-335) once and keeps them in
 //      registers; the CTA reduces the read margins per 16x16 quadrant;
 //   B. the tile's region (tile + its own margins) is loaded into shared
 //      memory and pre-integrated there;
 //   C. every pixel takes its finite difference from the region.
 // A tile whose region exceeds `region_cap` doubles runs as four 16x16
-// quadrants with their own (smaller) regions.
-template <int MODE, int DT>
-__global__ void __launch_bounds__(kThreads, 1)
-    tile_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int region_cap,
-                       Status *st) {
-  extern __shared__ double S[];
+// quadrants with their own smaller regions; if even those do not fit, the
+// tile is appended to `ovf_list` (second launch with the large-smem
+// configuration) or, without a list, flagged.
+template <int MODE, int DT, int NT>
+__device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec &F,
+                                             const DomainSpec &D, int tile, int tiles_x,
+                                             int region_cap, int *ovf_list, Status *st,
+                                             double *S, unsigned &ghi, unsigned &flags) {
+  constexpr int PPT = 1024 / NT;   // pixels per thread
+  constexpr int RS = NT / 32;      // row stride between a thread's pixels
   __shared__ int s_m[4][4];  // quadrant margins (left, right, below, above)
   __shared__ int s_plan[4][8];
   __shared__ int s_nsub;
   const int tid = threadIdx.x;
-  const int tx = blockIdx.x % tiles_x, ty = blockIdx.x / tiles_x;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x0 = tx * kTile, y0 = ty * kTile;
   const int lx = tid & 31, ly = tid >> 5;
   if (tid < 16) s_m[tid >> 2][tid & 3] = 0;
   __syncthreads();
 
   // ---- A: scale-vectors and margins
-  unsigned flags = 0;
-  double av[2][4];
-  bool valid[2];
+  double av[PPT][4];
+  bool valid[PPT];
 #pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const int x = x0 + lx, y = y0 + ly + 16 * k;
+  for (int k = 0; k < PPT; ++k) {
+    const int x = x0 + lx, y = y0 + ly + RS * k;
     valid[k] = (x < D.pw) && (y < D.ph);
     int4 m = make_int4(0, 0, 0, 0);
     if (valid[k]) {
@@ -410,7 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       m.w = max(m.w, __shfl_xor_sync(0xffffffffu, m.w, o));
     }
     if ((lx & 15) == 0) {
-      const int q = (lx >> 4) + 2 * k;
+      const int q = (lx >> 4) + 2 * ((ly + RS * k) >> 4);
       atomicMax(&s_m[q][0], m.x);
       atomicMax(&s_m[q][1], m.y);
       atomicMax(&s_m[q][2], m.z);
@@ -430,6 +435,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       d[0] = x0; d[1] = y0; d[2] = tw; d[3] = th; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
     } else {
       int n = 0;
+      bool fits = true;
       for (int q = 0; q < 4; ++q) {
         const int sx = x0 + (q & 1) * 16, sy = y0 + (q >> 1) * 16;
         if (sx >= D.pw || sy >= D.ph) continue;
@@ -438,6 +444,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = s_m[q][0]; d[5] = s_m[q][2];
         d[6] = sw + s_m[q][0] + s_m[q][1];
         d[7] = sh + s_m[q][2] + s_m[q][3];
+        fits = fits && ((d[6] | 1) * d[7] <= region_cap);
+      }
+      if (!fits && ovf_list) {
+        ovf_list[atomicAdd(&st->ovf_count, 1)] = tile;
+        n = 0;
+      } else if (!fits) {
+        atomicOr(&st->flags, kFlagRegionTooLarge);
+        n = 0;
       }
       s_nsub = n;
     }
@@ -445,16 +459,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
 
   const int nsub = s_nsub;
-  unsigned ghi = 0;
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S);
   for (int si = 0; si < nsub; ++si) {
     const int sx = s_plan[si][0], sy = s_plan[si][1], sw = s_plan[si][2], sh = s_plan[si][3];
     const int left = s_plan[si][4], below = s_plan[si][5], RW = s_plan[si][6], RH = s_plan[si][7];
     const int P = RW | 1;
-    if (P * RH > region_cap) {
-      if (tid == 0) atomicOr(&st->flags, kFlagRegionTooLarge);
-      continue;
-    }
     // ---- B: region load + running sums
     const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
     load_region<DT>(S, P, I, rc0, rr0, RW, RH);
@@ -463,24 +472,59 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---- C: finite differences
     const uint32_t Sb = sbase - (uint32_t)((rr0 * P + rc0) * 8);
 #pragma unroll 1
-    for (int k = 0; k < 2; ++k) {
-      const int x = x0 + lx, y = y0 + ly + 16 * k;
+    for (int k = 0; k < PPT; ++k) {
+      const int x = x0 + lx, y = y0 + ly + RS * k;
       if (valid[k] && x >= sx && x < sx + sw && y >= sy && y < sy + sh) {
         const int n1 = D.pc_lo + x, n2 = D.pr_lo + y;
         double ak[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) ak[j] = k ? av[1][j] : av[0][j];
+        for (int j = 0; j < 4; ++j) {
+          ak[j] = av[0][j];
+#pragma unroll
+          for (int kk = 1; kk < PPT; ++kk) ak[j] = (k == kk) ? av[kk][j] : ak[j];
+        }
         D.out[(int64_t)y * D.ld_out + x] = pixel_fd(Sb, P, n1, n2, ak);
       }
     }
     __syncthreads();
   }
+}
+
+__device__ __forceinline__ void flush_status(Status *st, unsigned ghi, unsigned flags) {
   ghi = __reduce_max_sync(0xffffffffu, ghi);
   flags = __reduce_or_sync(0xffffffffu, flags);
-  if (lx == 0) {
+  if ((threadIdx.x & 31) == 0) {
     if (ghi) atomicMax(&st->guard_hi, ghi);
     if (flags) atomicOr(&st->flags, flags);
   }
+}
+
+// Primary launch: one tile per CTA, two CTAs per SM (half the shared
+// memory each) so one CTA's load / sweeps overlap the other's gather.
+template <int MODE, int DT>
+__global__ void __launch_bounds__(kThreadsSmall, 2)
+    tile_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int region_cap,
+                       int *ovf_list, Status *st) {
+  extern __shared__ double S[];
+  unsigned ghi = 0, flags = 0;
+  process_tile<MODE, DT, kThreadsSmall>(I, F, D, blockIdx.x, tiles_x, region_cap, ovf_list, st,
+                                        S, ghi, flags);
+  flush_status(st, ghi, flags);
+}
+
+// Overflow launch: persistent CTAs with the whole shared memory for the
+// tiles whose quadrant regions did not fit the primary configuration.
+template <int MODE, int DT>
+__global__ void __launch_bounds__(kThreadsLarge, 1)
+    tile_overflow_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int region_cap,
+                         const int *ovf_list, Status *st) {
+  extern __shared__ double S[];
+  unsigned ghi = 0, flags = 0;
+  const int n = *(volatile const int *)&st->ovf_count;
+  for (int i = blockIdx.x; i < n; i += gridDim.x)
+    process_tile<MODE, DT, kThreadsLarge>(I, F, D, ovf_list[i], tiles_x, region_cap, nullptr, st,
+                                          S, ghi, flags);
+  flush_status(st, ghi, flags);
 }
 
 // ---- standalone lookup (solver.lookup_many) ------------------------------
@@ -628,6 +672,9 @@ __global__ void interpolate_kernel(const double *__restrict__ plane, int64_t row
 
 struct Scratch {
   int device = -1;
+  int sms = 148;
+  int *d_ovf = nullptr;
+  size_t ovf_cap = 0;
   Status *d_status = nullptr;
   Status *h_status = nullptr;  // pinned
   double *d_pass[2] = {nullptr, nullptr};
@@ -644,12 +691,16 @@ int ensure_scratch() {
     t_scr.device = dev;
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_status, sizeof(Status)));
     RUBS_CUDA_TRY(cudaMallocHost(&t_scr.h_status, sizeof(Status)));
+    RUBS_CUDA_TRY(cudaDeviceGetAttribute(&t_scr.sms, cudaDevAttrMultiProcessorCount, dev));
   }
   if (!t_scr.attr_set) {
-#define RUBS_SET_SMEM(M, T)                                                        \
-  RUBS_CUDA_TRY(cudaFuncSetAttribute(tile_filter_kernel<M, T>,                     \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                                     kSmemBytes))
+#define RUBS_SET_SMEM(M, T)                                                          \
+  RUBS_CUDA_TRY(cudaFuncSetAttribute(tile_filter_kernel<M, T>,                       \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                     kSmemSmall));                                  \
+  RUBS_CUDA_TRY(cudaFuncSetAttribute(tile_overflow_kernel<M, T>,                     \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                     kSmemLarge))
     RUBS_SET_SMEM(kModeField, 0);
     RUBS_SET_SMEM(kModeField, 1);
     RUBS_SET_SMEM(kModeUniform, 0);
@@ -729,14 +780,24 @@ int launch_global_margins(const FieldSpec &F, const DomainSpec &D, cudaStream_t 
 template <int M, int T>
 void launch_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cudaStream_t s) {
   const int tiles_x = (D.pw + kTile - 1) / kTile, tiles_y = (D.ph + kTile - 1) / kTile;
-  tile_filter_kernel<M, T><<<tiles_x * tiles_y, kThreads, kSmemBytes, s>>>(
-      I, F, D, tiles_x, kRegionCap, t_scr.d_status);
+  cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s);
+  tile_filter_kernel<M, T><<<tiles_x * tiles_y, kThreadsSmall, kSmemSmall, s>>>(
+      I, F, D, tiles_x, kSmemSmall / 8, t_scr.d_ovf, t_scr.d_status);
+  tile_overflow_kernel<M, T><<<t_scr.sms, kThreadsLarge, kSmemLarge, s>>>(
+      I, F, D, tiles_x, kSmemLarge / 8, t_scr.d_ovf, t_scr.d_status);
 }
 
 int launch_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cudaStream_t s) {
   {
     TimedLaunch tl(0, s);
     const int m = F.mode, t = I.dt;
+    const size_t ntiles = (size_t)((D.pw + kTile - 1) / kTile) * ((D.ph + kTile - 1) / kTile);
+    if (ntiles > t_scr.ovf_cap) {
+      if (t_scr.d_ovf) cudaFree(t_scr.d_ovf);
+      t_scr.d_ovf = nullptr;
+      RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_ovf, ntiles * sizeof(int)));
+      t_scr.ovf_cap = ntiles;
+    }
     if (m == kModeField) {
       if (t) launch_tiles<kModeField, 1>(I, F, D, s); else launch_tiles<kModeField, 0>(I, F, D, s);
     } else if (m == kModeUniform) {
@@ -745,7 +806,7 @@ int launch_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cud
       if (t) launch_tiles<kModeLut, 1>(I, F, D, s); else launch_tiles<kModeLut, 0>(I, F, D, s);
     }
   }
-  ++t_launches;
+  t_launches += 2;
   RUBS_CUDA_TRY(cudaGetLastError());
   return RUBS_OK;
 }

@@ -34,6 +34,8 @@ struct Status {
   unsigned int guard_hi;          // max over planes of the high word of |g| (IEEE)
   unsigned long long guard_bits;  // same for the global-canvas path, full bits
   int gm[4];                      // global margins left, right, below, above
+  int ovf_count;                  // tiles deferred to the large-smem launch
+  int pad2;
 };
 
 // Where the per-pixel scale-vector comes from.
