@@ -145,40 +145,66 @@ __global__ void __launch_bounds__(256) global_margins_kernel(FieldSpec F, Domain
 
 // Load the image over region lattice [rc0, rc0+RW) x [rr0, rr0+RH) into
 // shared memory as fp64, zero outside the image (zero padding, engine.py:155).
-// One warp per row, lanes over columns, several loads in flight per lane.
+// float64 images: asynchronous global->shared copies (cp.async, LDGSTS), the
+// zero fill of out-of-image elements done by the same instruction (src-size
+// 0), so every element of the region is in flight at once.  float32 images:
+// eight loads in flight per thread, widened to fp64 on the way.
+__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+
 template <int DT>
 __device__ __forceinline__ void load_region(double *S, int P, const ImageSpec &I, int rc0,
                                             int rr0, int RW, int RH) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int ic0 = rc0 - I.col0, ir0 = rr0 - I.row0;
-  const bool inside = ic0 >= 0 && ir0 >= 0 && ic0 + RW <= I.w && ir0 + RH <= I.h;
-  if (inside) {
-    for (int r = warp; r < RH; r += nw) {
-      const int64_t g = (int64_t)(ir0 + r) * I.ld + ic0;
-      double *row = S + r * P;
-      int c = lane;
-      for (; c + 96 < RW; c += 128) {
-        const double v0 = load_px<DT>(I.f, g + c), v1 = load_px<DT>(I.f, g + c + 32);
-        const double v2 = load_px<DT>(I.f, g + c + 64), v3 = load_px<DT>(I.f, g + c + 96);
-        row[c] = v0;
-        row[c + 32] = v1;
-        row[c + 64] = v2;
-        row[c + 96] = v3;
-      }
-      for (; c < RW; c += 32) row[c] = load_px<DT>(I.f, g + c);
-    }
-  } else {
+  if constexpr (DT == 1) {
+    const double *f = static_cast<const double *>(I.f);
+    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(S);
+    // columns of the region that lie inside the image
+    const int cl = max(0, -ic0), ch = min(RW, I.w - ic0);
     for (int r = warp; r < RH; r += nw) {
       const int ir = ir0 + r;
-      double *row = S + r * P;
-      const bool rin = (ir >= 0 && ir < I.h);
-      const int64_t g = (int64_t)ir * I.ld + ic0;
-      for (int c = lane; c < RW; c += 32) {
-        const int ic = ic0 + c;
-        row[c] = (rin && ic >= 0 && ic < I.w) ? load_px<DT>(I.f, g + c) : 0.0;
+      const uint32_t drow = sb + (uint32_t)(r * P) * 8u;
+      if (ir >= 0 && ir < I.h) {
+        const double *srow = f + (int64_t)ir * I.ld + ic0;
+        for (int c = lane; c < RW; c += 32) {
+          const bool in = c >= cl && c < ch;
+          cp_async8(drow + c * 8u, in ? (const void *)(srow + c) : (const void *)f, in ? 8 : 0);
+        }
+      } else {
+        for (int c = lane; c < RW; c += 32) cp_async8(drow + c * 8u, f, 0);
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else {
+    const int n = RW * RH;
+    constexpr int K = 8;
+    for (int e0 = threadIdx.x; e0 < n; e0 += K * blockDim.x) {
+      double v[K];
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int e = e0 + k * blockDim.x;
+        v[k] = 0.0;
+        if (e < n) {
+          const int r = e / RW, c = e - r * RW;
+          const int ir = ir0 + r, ic = ic0 + c;
+          if (ir >= 0 && ir < I.h && ic >= 0 && ic < I.w)
+            v[k] = load_px<DT>(I.f, (int64_t)ir * I.ld + ic);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k) {
+        const int e = e0 + k * blockDim.x;
+        if (e < n) {
+          const int r = e / RW, c = e - r * RW;
+          S[r * P + c] = v[k];
+        }
       }
     }
   }
+  (void)warp; (void)lane; (void)nw;
 }
 
 // The four running sums of engine.py:186-193 on the region, started at the
@@ -208,19 +234,27 @@ __device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, 
     }
   }
   __syncthreads();
-  // RS2: g[r][c] += g[r-1][c-1]; lines k = c - r in [-(RH-1), RW-1]
+  // RS2: g[r][c] += g[r-1][c-1]; lines k = c - r in [-(RH-1), RW-1].
+  // Lane = line, rows advance together inside a warp (consecutive shared
+  // addresses); each lane's valid rows are one contiguous range.
   const int nlines = RH + RW - 1;
   for (int lb = warp * 32; lb < nlines; lb += nw * 32) {
-    const int kb = lb - (RH - 1), k = kb + lane;
-    const int t0 = max(0, -(kb + 31)), t1 = min(RH - 1, RW - 1 - kb);
+    const int k = lb - (RH - 1) + lane;
+    const int ta = max(0, -k), tb = min(RH - 1, RW - 1 - k);
     double s = 0.0;
-    double *p = S + t0 * P + t0 + k;
-    for (int t = t0; t <= t1; ++t, p += P + 1) {
-      const int c = t + k;
-      if (c >= 0 && c < RW) {
-        s += *p;
-        *p = s;
-      }
+    double *p = S + ta * P + ta + k;
+    int t = ta;
+    for (; t + 4 <= tb + 1; t += 4) {
+      const double v0 = p[0], v1 = p[P + 1], v2 = p[2 * (P + 1)], v3 = p[3 * (P + 1)];
+      s += v0; p[0] = s;
+      s += v1; p[P + 1] = s;
+      s += v2; p[2 * (P + 1)] = s;
+      s += v3; p[3 * (P + 1)] = s;
+      p += 4 * (P + 1);
+    }
+    for (; t <= tb; ++t, p += P + 1) {
+      s += *p;
+      *p = s;
     }
   }
   __syncthreads();
@@ -247,16 +281,27 @@ __device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, 
   unsigned gh = 0;
   for (int kb = warp * 32; kb < nlines; kb += nw * 32) {
     const int k = kb + lane;
-    const int t0 = max(0, kb - (RW - 1)), t1 = min(RH - 1, kb + 31);
+    const int ta = max(0, k - (RW - 1)), tb = min(RH - 1, k);
     double s = 0.0;
-    double *p = S + t0 * P + (k - t0);
-    for (int t = t0; t <= t1; ++t, p += P - 1) {
-      const int c = k - t;
-      if (c >= 0 && c < RW) {
-        s += *p;
-        *p = s;
-        gh = max(gh, (unsigned)__double2hiint(s) & 0x7fffffffu);
-      }
+    double *p = S + ta * P + (k - ta);
+    int t = ta;
+    for (; t + 4 <= tb + 1; t += 4) {
+      const double v0 = p[0], v1 = p[P - 1], v2 = p[2 * (P - 1)], v3 = p[3 * (P - 1)];
+      s += v0; p[0] = s;
+      const unsigned h0 = (unsigned)__double2hiint(s);
+      s += v1; p[P - 1] = s;
+      const unsigned h1 = (unsigned)__double2hiint(s);
+      s += v2; p[2 * (P - 1)] = s;
+      const unsigned h2 = (unsigned)__double2hiint(s);
+      s += v3; p[3 * (P - 1)] = s;
+      const unsigned h3 = (unsigned)__double2hiint(s);
+      gh = max(gh, max(max(h0 & 0x7fffffffu, h1 & 0x7fffffffu), max(h2 & 0x7fffffffu, h3 & 0x7fffffffu)));
+      p += 4 * (P - 1);
+    }
+    for (; t <= tb; ++t, p += P - 1) {
+      s += *p;
+      *p = s;
+      gh = max(gh, (unsigned)__double2hiint(s) & 0x7fffffffu);
     }
   }
   ghi = max(ghi, gh);
@@ -392,20 +437,18 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
   if (tid < 16) s_m[tid >> 2][tid & 3] = 0;
   __syncthreads();
 
-  // ---- A: scale-vectors and margins
+  // ---- A: scale-vectors (independent per pixel: all in flight), then margins
   double av[PPT][4];
   bool valid[PPT];
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
     const int x = x0 + lx, y = y0 + ly + RS * k;
     valid[k] = (x < D.pw) && (y < D.ph);
-    int4 m = make_int4(0, 0, 0, 0);
-    if (valid[k]) {
-      field_at<MODE>(F, D.pc_lo + x, D.pr_lo + y, av[k], flags);
-      m = pixel_margins_fast(av[k]);
-    } else {
-      av[k][0] = av[k][1] = av[k][2] = av[k][3] = 1.0;
-    }
+    field_at<MODE>(F, D.pc_lo + min(x, D.pw - 1), D.pr_lo + min(y, D.ph - 1), av[k], flags);
+  }
+#pragma unroll
+  for (int k = 0; k < PPT; ++k) {
+    int4 m = valid[k] ? pixel_margins_fast(av[k]) : make_int4(0, 0, 0, 0);
     // half-warp reduction (lanes 0-15 / 16-31 are different quadrants)
 #pragma unroll
     for (int o = 8; o > 0; o >>= 1) {
