@@ -24,6 +24,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -154,10 +155,20 @@ __device__ __forceinline__ void cp_async8(uint32_t dst, const void *src, int src
                : "memory");
 }
 
-template <int DT>
+// Synchronise the NT threads of a group: the whole CTA (BAR 0) or a named
+// barrier shared by a warp-specialised subset.
+template <int NT, int BAR>
+__device__ __forceinline__ void group_sync() {
+  if constexpr (BAR == 0)
+    __syncthreads();
+  else
+    asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
+}
+
+template <int DT, int NT>
 __device__ __forceinline__ void load_region(double *S, int P, const ImageSpec &I, int rc0,
-                                            int rr0, int RW, int RH) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+                                            int rr0, int RW, int RH, int tid) {
+  const int warp = tid >> 5, lane = tid & 31, nw = NT >> 5;
   const int ic0 = rc0 - I.col0, ir0 = rr0 - I.row0;
   if constexpr (DT == 1) {
     const double *f = static_cast<const double *>(I.f);
@@ -181,11 +192,11 @@ __device__ __forceinline__ void load_region(double *S, int P, const ImageSpec &I
   } else {
     const int n = RW * RH;
     constexpr int K = 8;
-    for (int e0 = threadIdx.x; e0 < n; e0 += K * blockDim.x) {
+    for (int e0 = tid; e0 < n; e0 += K * NT) {
       double v[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const int e = e0 + k * blockDim.x;
+        const int e = e0 + k * NT;
         v[k] = 0.0;
         if (e < n) {
           const int r = e / RW, c = e - r * RW;
@@ -196,7 +207,7 @@ __device__ __forceinline__ void load_region(double *S, int P, const ImageSpec &I
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) {
-        const int e = e0 + k * blockDim.x;
+        const int e = e0 + k * NT;
         if (e < n) {
           const int r = e / RW, c = e - r * RW;
           S[r * P + c] = v[k];
@@ -213,9 +224,11 @@ __device__ __forceinline__ void load_region(double *S, int P, const ImageSpec &I
 // row-synchronously inside a warp (lane = line) so every shared access of a
 // warp hits consecutive addresses.  Tracks max high word of |plane| for the
 // 2^53 guard.
-__device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, unsigned &ghi) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+template <int NT, int BAR>
+__device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, unsigned &ghi,
+                                              int tid) {
+  constexpr int nt = NT, nw = NT >> 5;
+  const int warp = tid >> 5, lane = tid & 31;
   // RS1: along +x (one thread per row)
   for (int r = tid; r < RH; r += nt) {
     double *p = S + r * P;
@@ -233,7 +246,7 @@ __device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, 
       p[c] = s;
     }
   }
-  __syncthreads();
+  group_sync<NT, BAR>();
   // RS2: g[r][c] += g[r-1][c-1]; lines k = c - r in [-(RH-1), RW-1].
   // Lane = line, rows advance together inside a warp (consecutive shared
   // addresses); each lane's valid rows are one contiguous range.
@@ -257,7 +270,7 @@ __device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, 
       *p = s;
     }
   }
-  __syncthreads();
+  group_sync<NT, BAR>();
   // RS3: along +y (one thread per column)
   for (int c = tid; c < RW; c += nt) {
     double *p = S + c;
@@ -276,7 +289,7 @@ __device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, 
       *p = s;
     }
   }
-  __syncthreads();
+  group_sync<NT, BAR>();
   // RS4: g[r][c] += g[r-1][c+1]; lines k = c + r in [0, RH+RW-2]
   unsigned gh = 0;
   for (int kb = warp * 32; kb < nlines; kb += nw * 32) {
@@ -305,7 +318,7 @@ __device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, 
     }
   }
   ghi = max(ghi, gh);
-  __syncthreads();
+  group_sync<NT, BAR>();
 }
 
 // Per-pixel finite difference (engine.py:219-244) over the region plane,
@@ -509,9 +522,9 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
     const int P = RW | 1;
     // ---- B: region load + running sums
     const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
-    load_region<DT>(S, P, I, rc0, rr0, RW, RH);
+    load_region<DT, NT>(S, P, I, rc0, rr0, RW, RH, tid);
     __syncthreads();
-    region_sweeps(S, P, RW, RH, ghi);
+    region_sweeps<NT, 0>(S, P, RW, RH, ghi, tid);
     // ---- C: finite differences
     const uint32_t Sb = sbase - (uint32_t)((rr0 * P + rc0) * 8);
 #pragma unroll 1
@@ -567,6 +580,206 @@ __global__ void __launch_bounds__(kThreadsLarge, 1)
   for (int i = blockIdx.x; i < n; i += gridDim.x)
     process_tile<MODE, DT, kThreadsLarge>(I, F, D, ovf_list[i], tiles_x, region_cap, nullptr, st,
                                           S, ghi, flags);
+  flush_status(st, ghi, flags);
+}
+
+// ---------------------------------------------------------------------------
+// Warp-specialised pipeline (the primary path).
+//
+// One persistent CTA per SM, 16 warps: warps 0-3 produce, warps 4-15
+// consume, through two 112 KB region buffers.  For tile i+1 the producers
+// bound its read margins, plan its region, copy the image into a free
+// buffer (cp.async) and run the four running sums; meanwhile the consumers
+// map tile i's scale-vectors (the LUT runs once per pixel, here) and take
+// its 16-vertex finite differences.  Hand-off through named barriers:
+// FULL[b] (producers arrive, consumers wait), EMPTY[b] (the reverse).
+
+constexpr int kPipeProd = 128;                  // producer threads
+constexpr int kPipeCons = 384;                  // consumer threads
+constexpr int kPipeBuf = 112 * 1024 / 8;        // doubles per region buffer
+constexpr int kPipeSmem = 2 * kPipeBuf * 8;     // dynamic shared memory
+constexpr int kBarProd = 1, kBarFull = 2, kBarEmpty = 4;  // named barrier ids
+
+__device__ __forceinline__ void nbar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Upper bound of a pixel's read margins without running the LUT:
+// hx = (a1 + (a2 + a4) / sqrt2) / 2 <= 3 sqrt(C11) (Cauchy-Schwarz on
+// C11 = (2 a1^2 + a2^2 + a4^2) / 24), where the table's bilinear blend keeps
+// C11 below the largest corner node's, i.e. below the target's + 0.04 size;
+// the 0.05 floor adds at most 0.0604, the pass scaling divides by sqrt(m).
+__device__ __forceinline__ int4 lut_margin_bound(const FieldSpec &F, int n1, int n2) {
+  const int fc = min(max(n1, 0), F.FW - 1), fr = min(max(n2, 0), F.FH - 1);
+  const int64_t i = (int64_t)fr * F.pld + fc;
+  double sz = load_scalar(F.ps, F.pdt, i), rho = load_scalar(F.pr, F.pdt, i);
+  double th = load_scalar(F.pt, F.pdt, i);
+  if (!(sz > 0.0 && sz < INFINITY)) sz = 1.0;
+  if (!(rho >= 1.0 && rho < INFINITY)) rho = 1.0;
+  if (!(th >= 0.0 && th < kPi)) th = 0.0;
+  rho = fmin(rho, F.rho_max);
+  const float c = cosf((float)th), sn = sinf((float)th);
+  const float inv = 1.0f / (1.0f + (float)rho);
+  const float c11 = ((float)rho * c * c + sn * sn) * inv + 0.04f;
+  const float c22 = ((float)rho * sn * sn + c * c) * inv + 0.04f;
+  const float fl = 0.0605f;
+  const float idiv = (float)(1.0 / F.div) * 1.0001f;
+  const double hx = (double)((3.0f * sqrtf((float)sz * c11) * 1.001f + fl) * idiv);
+  const double hy = (double)((3.0f * sqrtf((float)sz * c22) * 1.001f + fl) * idiv);
+  int4 m;
+  m.x = max(0, (int)ceil(hx + 0.5) + 3);
+  m.y = max(0, (int)ceil(hx - 0.5) + 3);
+  m.z = max(0, (int)ceil(hy + 1.5) + 3);
+  m.w = max(0, (int)ceil(hy - 1.5) + 3);
+  return m;
+}
+
+struct UnitPlan {
+  int sx, sy, sw, sh;  // output rectangle (pass-domain pixels)
+  int RW, RH, P;       // region width, rows, pitch
+  int rc0, rr0;        // lattice of region element (0, 0)
+  int end;
+};
+
+template <int MODE, int DT>
+__global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
+    pipe_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int ntiles,
+                       int *ovf_list, Status *st) {
+  extern __shared__ double S[];
+  __shared__ UnitPlan plan[2];
+  __shared__ int s_m[4][4];
+  __shared__ int s_u[4][8];
+  __shared__ int s_nu;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned ghi = 0, flags = 0;
+
+  if (warp < kPipeProd / 32) {
+    // ================================================================ producer
+    int buf = 0;
+    bool used[2] = {false, false};
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int tx = tile % tiles_x, ty = tile / tiles_x;
+      const int x0 = tx * kTile, y0 = ty * kTile;
+      if (tid < 16) s_m[tid >> 2][tid & 3] = 0;
+      nbar_sync(kBarProd, kPipeProd);
+      const int ly = tid >> 5;  // 0..3
+#pragma unroll 2
+      for (int k = 0; k < 8; ++k) {
+        const int x = x0 + lane, y = y0 + ly + 4 * k;
+        int4 m = make_int4(0, 0, 0, 0);
+        if (x < D.pw && y < D.ph) {
+          if constexpr (MODE == kModeLut) {
+            m = lut_margin_bound(F, D.pc_lo + x, D.pr_lo + y);
+          } else {
+            double a[4];
+            unsigned fl = 0;
+            field_at<MODE>(F, D.pc_lo + x, D.pr_lo + y, a, fl);
+            m = pixel_margins_fast(a);
+          }
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          m.x = max(m.x, __shfl_xor_sync(0xffffffffu, m.x, o));
+          m.y = max(m.y, __shfl_xor_sync(0xffffffffu, m.y, o));
+          m.z = max(m.z, __shfl_xor_sync(0xffffffffu, m.z, o));
+          m.w = max(m.w, __shfl_xor_sync(0xffffffffu, m.w, o));
+        }
+        if ((lane & 15) == 0) {
+          const int q = (lane >> 4) + 2 * ((ly + 4 * k) >> 4);
+          atomicMax(&s_m[q][0], m.x);
+          atomicMax(&s_m[q][1], m.y);
+          atomicMax(&s_m[q][2], m.z);
+          atomicMax(&s_m[q][3], m.w);
+        }
+      }
+      nbar_sync(kBarProd, kPipeProd);
+      if (tid == 0) {
+        const int tw = min(kTile, D.pw - x0), th = min(kTile, D.ph - y0);
+        int u[4] = {0, 0, 0, 0};
+        for (int q = 0; q < 4; ++q)
+          for (int j = 0; j < 4; ++j) u[j] = max(u[j], s_m[q][j]);
+        const int RW = tw + u[0] + u[1], RH = th + u[2] + u[3];
+        int n = 0;
+        if ((RW | 1) * RH <= kPipeBuf) {
+          int *d = s_u[n++];
+          d[0] = x0; d[1] = y0; d[2] = tw; d[3] = th; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
+        } else {
+          bool fits = true;
+          for (int q = 0; q < 4; ++q) {
+            const int sx = x0 + (q & 1) * 16, sy = y0 + (q >> 1) * 16;
+            if (sx >= D.pw || sy >= D.ph) continue;
+            const int sw = min(16, D.pw - sx), sh = min(16, D.ph - sy);
+            int *d = s_u[n++];
+            d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = s_m[q][0]; d[5] = s_m[q][2];
+            d[6] = sw + s_m[q][0] + s_m[q][1];
+            d[7] = sh + s_m[q][2] + s_m[q][3];
+            fits = fits && ((d[6] | 1) * d[7] <= kPipeBuf);
+          }
+          if (!fits) {
+            ovf_list[atomicAdd(&st->ovf_count, 1)] = tile;
+            n = 0;
+          }
+        }
+        s_nu = n;
+      }
+      nbar_sync(kBarProd, kPipeProd);
+      const int nu = s_nu;
+      for (int ui = 0; ui < nu; ++ui) {
+        const int sx = s_u[ui][0], sy = s_u[ui][1], sw = s_u[ui][2], sh = s_u[ui][3];
+        const int left = s_u[ui][4], below = s_u[ui][5], RW = s_u[ui][6], RH = s_u[ui][7];
+        const int P = RW | 1;
+        const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
+        if (used[buf]) nbar_sync(kBarEmpty + buf, kPipeProd + kPipeCons);
+        double *B = S + buf * kPipeBuf;
+        load_region<DT, kPipeProd>(B, P, I, rc0, rr0, RW, RH, tid);
+        if (tid == 0) {
+          UnitPlan up;
+          up.sx = sx; up.sy = sy; up.sw = sw; up.sh = sh;
+          up.RW = RW; up.RH = RH; up.P = P; up.rc0 = rc0; up.rr0 = rr0; up.end = 0;
+          plan[buf] = up;
+        }
+        nbar_sync(kBarProd, kPipeProd);
+        region_sweeps<kPipeProd, kBarProd>(B, P, RW, RH, ghi, tid);
+        __threadfence_block();
+        nbar_arrive(kBarFull + buf, kPipeProd + kPipeCons);
+        used[buf] = true;
+        buf ^= 1;
+      }
+    }
+    // end of work: marker through the next buffer, then balance EMPTY arrivals
+    if (used[buf]) nbar_sync(kBarEmpty + buf, kPipeProd + kPipeCons);
+    if (tid == 0) plan[buf].end = 1;
+    __threadfence_block();
+    nbar_arrive(kBarFull + buf, kPipeProd + kPipeCons);
+    if (used[buf ^ 1]) nbar_sync(kBarEmpty + (buf ^ 1), kPipeProd + kPipeCons);
+  } else {
+    // ================================================================ consumer
+    const int ctid = tid - kPipeProd;
+    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S);
+    int buf = 0;
+    for (;;) {
+      nbar_sync(kBarFull + buf, kPipeProd + kPipeCons);
+      const UnitPlan up = plan[buf];
+      if (up.end) break;
+      const uint32_t Sb = sbase + (uint32_t)(buf * kPipeBuf) * 8u -
+                          (uint32_t)((up.rr0 * up.P + up.rc0) * 8);
+      const int n = up.sw * up.sh;
+#pragma unroll 1
+      for (int p = ctid; p < n; p += kPipeCons) {
+        const int yy = p / up.sw, xx = p - yy * up.sw;
+        const int x = up.sx + xx, y = up.sy + yy;
+        const int n1 = D.pc_lo + x, n2 = D.pr_lo + y;
+        double a[4];
+        field_at<MODE>(F, n1, n2, a, flags);
+        D.out[(int64_t)y * D.ld_out + x] = pixel_fd(Sb, up.P, n1, n2, a);
+      }
+      nbar_arrive(kBarEmpty + buf, kPipeProd + kPipeCons);
+      buf ^= 1;
+    }
+  }
   flush_status(st, ghi, flags);
 }
 
@@ -743,7 +956,10 @@ int ensure_scratch() {
                                      kSmemSmall));                                  \
   RUBS_CUDA_TRY(cudaFuncSetAttribute(tile_overflow_kernel<M, T>,                     \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                     kSmemLarge))
+                                     kSmemLarge));                                  \
+  RUBS_CUDA_TRY(cudaFuncSetAttribute(pipe_filter_kernel<M, T>,                       \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                     kPipeSmem))
     RUBS_SET_SMEM(kModeField, 0);
     RUBS_SET_SMEM(kModeField, 1);
     RUBS_SET_SMEM(kModeUniform, 0);
@@ -820,12 +1036,26 @@ int launch_global_margins(const FieldSpec &F, const DomainSpec &D, cudaStream_t 
   return RUBS_OK;
 }
 
+int kernel_choice() {
+  static int choice = -1;
+  if (choice < 0) {
+    const char *e = std::getenv("RUBS_B200_KERNEL");
+    choice = (e && std::strcmp(e, "pipe") == 0) ? 0 : 1;
+  }
+  return choice;
+}
+
 template <int M, int T>
 void launch_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cudaStream_t s) {
   const int tiles_x = (D.pw + kTile - 1) / kTile, tiles_y = (D.ph + kTile - 1) / kTile;
+  const int ntiles = tiles_x * tiles_y;
   cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s);
-  tile_filter_kernel<M, T><<<tiles_x * tiles_y, kThreadsSmall, kSmemSmall, s>>>(
-      I, F, D, tiles_x, kSmemSmall / 8, t_scr.d_ovf, t_scr.d_status);
+  if (kernel_choice() == 0)
+    pipe_filter_kernel<M, T><<<std::min(ntiles, t_scr.sms), kPipeProd + kPipeCons, kPipeSmem, s>>>(
+        I, F, D, tiles_x, ntiles, t_scr.d_ovf, t_scr.d_status);
+  else
+    tile_filter_kernel<M, T><<<ntiles, kThreadsSmall, kSmemSmall, s>>>(
+        I, F, D, tiles_x, kSmemSmall / 8, t_scr.d_ovf, t_scr.d_status);
   tile_overflow_kernel<M, T><<<t_scr.sms, kThreadsLarge, kSmemLarge, s>>>(
       I, F, D, tiles_x, kSmemLarge / 8, t_scr.d_ovf, t_scr.d_status);
 }
