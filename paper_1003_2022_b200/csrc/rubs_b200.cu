@@ -168,54 +168,65 @@ __device__ __forceinline__ void group_sync() {
 template <int DT, int NT>
 __device__ __forceinline__ void load_region(double *S, int P, const ImageSpec &I, int rc0,
                                             int rr0, int RW, int RH, int tid) {
-  const int warp = tid >> 5, lane = tid & 31, nw = NT >> 5;
+  constexpr int nw = NT >> 5;
+  const int warp = tid >> 5, lane = tid & 31;
   const int ic0 = rc0 - I.col0, ir0 = rr0 - I.row0;
-  if constexpr (DT == 1) {
-    const double *f = static_cast<const double *>(I.f);
-    const uint32_t sb = (uint32_t)__cvta_generic_to_shared(S);
-    // columns of the region that lie inside the image
-    const int cl = max(0, -ic0), ch = min(RW, I.w - ic0);
-    for (int r = warp; r < RH; r += nw) {
-      const int ir = ir0 + r;
-      const uint32_t drow = sb + (uint32_t)(r * P) * 8u;
-      if (ir >= 0 && ir < I.h) {
-        const double *srow = f + (int64_t)ir * I.ld + ic0;
-        for (int c = lane; c < RW; c += 32) {
-          const bool in = c >= cl && c < ch;
-          cp_async8(drow + c * 8u, in ? (const void *)(srow + c) : (const void *)f, in ? 8 : 0);
-        }
-      } else {
-        for (int c = lane; c < RW; c += 32) cp_async8(drow + c * 8u, f, 0);
+  // region columns [cl, ch) lie inside the image
+  const int cl = min(RW, max(0, -ic0)), ch = max(cl, min(RW, I.w - ic0));
+  const uint32_t sb = (uint32_t)__cvta_generic_to_shared(S);
+  if (DT == 1 && cl == 0 && ch == RW && ir0 >= 0 && ir0 + RH <= I.h) {
+    // interior region: one flat loop over all elements, pointers advanced
+    // incrementally (NT elements per step, row carry when c wraps)
+    const int n = RW * RH;
+    int r = tid / RW, c = tid - r * RW;
+    const int sr = NT / RW, sc = NT - sr * RW;
+    const double *src = static_cast<const double *>(I.f) + (int64_t)(ir0 + r) * I.ld + ic0 + c;
+    uint32_t dst = sb + (uint32_t)(r * P + c) * 8u;
+    const int64_t sstep = (int64_t)sr * I.ld + sc, scarry = I.ld - RW;
+    const uint32_t dstep = (uint32_t)(sr * P + sc) * 8u, dcarry = (uint32_t)(P - RW) * 8u;
+    for (int e = tid; e < n; e += NT) {
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+      src += sstep;
+      dst += dstep;
+      c += sc;
+      if (c >= RW) {
+        c -= RW;
+        src += scarry;
+        dst += dcarry;
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
-  } else {
-    const int n = RW * RH;
-    constexpr int K = 8;
-    for (int e0 = tid; e0 < n; e0 += K * NT) {
-      double v[K];
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int e = e0 + k * NT;
-        v[k] = 0.0;
-        if (e < n) {
-          const int r = e / RW, c = e - r * RW;
-          const int ir = ir0 + r, ic = ic0 + c;
-          if (ir >= 0 && ir < I.h && ic >= 0 && ic < I.w)
-            v[k] = load_px<DT>(I.f, (int64_t)ir * I.ld + ic);
+    return;
+  }
+  for (int r = warp; r < RH; r += nw) {
+    const int ir = ir0 + r;
+    const uint32_t drow = sb + (uint32_t)(r * P) * 8u;
+    const bool rin = ir >= 0 && ir < I.h;
+    const int c0 = rin ? cl : RW, c1 = rin ? ch : RW;
+    // zero fill outside the image
+    for (int c = lane; c < c0; c += 32)
+      asm volatile("st.shared.f64 [%0], %1;" ::"r"(drow + c * 8u), "d"(0.0) : "memory");
+    for (int c = c1 + lane; c < RW; c += 32)
+      asm volatile("st.shared.f64 [%0], %1;" ::"r"(drow + c * 8u), "d"(0.0) : "memory");
+    if (c0 < c1) {
+      if constexpr (DT == 1) {
+        const double *src = static_cast<const double *>(I.f) + (int64_t)ir * I.ld + ic0 + c0 + lane;
+        uint32_t d = drow + (uint32_t)(c0 + lane) * 8u;
+        for (int c = c0 + lane; c < c1; c += 32, src += 32, d += 256u)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+      } else {
+        const float *src = static_cast<const float *>(I.f) + (int64_t)ir * I.ld + ic0 + c0 + lane;
+        double *dst = S + r * P + c0 + lane;
+        int c = c0 + lane;
+        for (; c + 96 < c1; c += 128, src += 128, dst += 128) {
+          const float v0 = __ldg(src), v1 = __ldg(src + 32), v2 = __ldg(src + 64), v3 = __ldg(src + 96);
+          dst[0] = v0; dst[32] = v1; dst[64] = v2; dst[96] = v3;
         }
-      }
-#pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int e = e0 + k * NT;
-        if (e < n) {
-          const int r = e / RW, c = e - r * RW;
-          S[r * P + c] = v[k];
-        }
+        for (; c < c1; c += 32, src += 32, dst += 32) *dst = __ldg(src);
       }
     }
   }
-  (void)warp; (void)lane; (void)nw;
+  if constexpr (DT == 1) asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
 // The four running sums of engine.py:186-193 on the region, started at the
@@ -332,6 +343,12 @@ __device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, 
 // which is +1 exactly when d1 + d2 >= 0 in both cases.  The seven taps are
 // the centre, the two major neighbours N (-sign) and P (+sign), the two
 // minor neighbours Bm/Bp and the two corners on the N side Cm/Cp.
+// 2 x by an exponent increment on the integer pipe (exact for the normal
+// values met here; 0 becomes 2^-1022, i.e. stays negligible).
+__device__ __forceinline__ double dtwice(double x) {
+  return __hiloint2double(__double2hiint(x) + (1 << 20), __double2loint(x));
+}
+
 __device__ __forceinline__ double lds64(uint32_t addr) {
   double v;
   asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
@@ -362,10 +379,10 @@ __device__ __forceinline__ double zp_read8(uint32_t c, int P8, double d1, double
   const double Caa2 = fma(2.0, Pp - g0, sC - sBv);
   const double Cab4 = dC - dBv;
   const double Cbb2 = fma(-2.0, g0 + N, sC + sBv);
-  const double V = v + v;
-  const double i1 = fma(u, Caa2, fma(V, Cab4, L1 + L1));
-  const double i2 = fma(v, Cbb2, dBv + dBv);
-  return fma(u + u, i1, fma(V, i2, A0));
+  const double V = dtwice(v);
+  const double i1 = fma(u, Caa2, fma(V, Cab4, dtwice(L1)));
+  const double i2 = fma(v, Cbb2, dtwice(dBv));
+  return fma(dtwice(u), i1, fma(V, i2, A0));
 }
 
 // Per-pixel finite difference (engine.py:219-244) over the region plane,
@@ -421,18 +438,53 @@ __device__ __forceinline__ double pixel_fd(uint32_t Sb, int P, int n1, int n2, c
   return acc * w;
 }
 
+// Region planning.  A unit is a rectangle of output pixels with its own
+// region (the rectangle grown by the maximum read margins of its pixels).
+// Precision model (measured): the error of a pixel is about
+//   kappa * eps * w * L4,  w = 1 / (a1 a2 a3 a4),  L4 = RW RH min(RW,RH)^2 / 4,
+// kappa ~ 0.04 -- the finite difference cancels running sums of size ~L4
+// down to O(1) with weight w.  Well-conditioned pixels (w small) tolerate
+// big regions; pixels with floored widths (w large) need small ones, so a
+// 32x32 tile whose budget w * L4 is exceeded is cut into 16x16 quadrants,
+// then 8x8 cells.  Regions that do not fit shared memory are cut the same
+// way; 8x8 cells that still do not fit send the tile to the overflow launch.
+constexpr float kPrecisionBudget = 1.1e7f;  // w * L4 for ~5e-11 relative error
+
+struct PlanCtx {
+  int m[16][4];     // per 8x8 cell: left, right, below, above
+  float w[16];      // per 8x8 cell: max 1/(a1 a2 a3 a4)
+};
+
+__device__ __forceinline__ bool plan_unit(const PlanCtx &pc, const DomainSpec &D, int x0, int y0,
+                                          int cx0, int cy0, int ncell, int region_cap,
+                                          int *d, bool &fits) {
+  // cells [cx0, cx0+ncell) x [cy0, cy0+ncell) of the tile (8x8 each)
+  const int sx = x0 + cx0 * 8, sy = y0 + cy0 * 8;
+  if (sx >= D.pw || sy >= D.ph) return false;
+  int u[4] = {0, 0, 0, 0};
+  float wm = 0.f;
+  for (int cy = cy0; cy < cy0 + ncell; ++cy)
+    for (int cx = cx0; cx < cx0 + ncell; ++cx) {
+      const int c = cy * 4 + cx;
+      for (int j = 0; j < 4; ++j) u[j] = max(u[j], pc.m[c][j]);
+      wm = fmaxf(wm, pc.w[c]);
+    }
+  const int sw = min(8 * ncell, D.pw - sx), sh = min(8 * ncell, D.ph - sy);
+  const int RW = sw + u[0] + u[1], RH = sh + u[2] + u[3];
+  const float mn = (float)min(RW, RH);
+  const float l4 = 0.25f * (float)RW * (float)RH * mn * mn;
+  d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
+  fits = (RW | 1) * RH <= region_cap;
+  return fits && wm * l4 <= kPrecisionBudget;
+}
+
 // One 32x32 output tile of the pass domain, processed by one CTA of NT
 // threads (1024 / NT pixels per thread):
 //   A. every thread maps its pixels' scale-vectors (field / uniform / LUT,
 //      engine.py:291-293 + solver.py:289-335) once and keeps them in
-//      registers; the CTA reduces the read margins per 16x16 quadrant;
-//   B. the tile's region (tile + its own margins) is loaded into shared
-//      memory and pre-integrated there;
-//   C. every pixel takes its finite difference from the region.
-// A tile whose region exceeds `region_cap` doubles runs as four 16x16
-// quadrants with their own smaller regions; if even those do not fit, the
-// tile is appended to `ovf_list` (second launch with the large-smem
-// configuration) or, without a list, flagged.
+//      registers; the CTA reduces read margins and weights per 8x8 cell;
+//   B. each unit's region is loaded into shared memory and pre-integrated;
+//   C. every pixel of the unit takes its finite difference from the region.
 template <int MODE, int DT, int NT>
 __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec &F,
                                              const DomainSpec &D, int tile, int tiles_x,
@@ -440,17 +492,21 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
                                              double *S, unsigned &ghi, unsigned &flags) {
   constexpr int PPT = 1024 / NT;   // pixels per thread
   constexpr int RS = NT / 32;      // row stride between a thread's pixels
-  __shared__ int s_m[4][4];  // quadrant margins (left, right, below, above)
-  __shared__ int s_plan[4][8];
+  __shared__ PlanCtx s_pc;
+  __shared__ int s_plan[16][8];
   __shared__ int s_nsub;
   const int tid = threadIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x0 = tx * kTile, y0 = ty * kTile;
   const int lx = tid & 31, ly = tid >> 5;
-  if (tid < 16) s_m[tid >> 2][tid & 3] = 0;
+  if (tid < 80) {
+    if (tid < 64) s_pc.m[tid >> 2][tid & 3] = 0;
+    else s_pc.w[tid - 64] = 0.f;
+  }
   __syncthreads();
 
-  // ---- A: scale-vectors (independent per pixel: all in flight), then margins
+  // ---- A: scale-vectors (independent per pixel: all in flight), then the
+  //         per-8x8-cell maxima of the margins and of w
   double av[PPT][4];
   bool valid[PPT];
 #pragma unroll
@@ -461,56 +517,60 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
   }
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
-    int4 m = valid[k] ? pixel_margins_fast(av[k]) : make_int4(0, 0, 0, 0);
-    // half-warp reduction (lanes 0-15 / 16-31 are different quadrants)
+    int4 m = make_int4(0, 0, 0, 0);
+    float w = 0.f;
+    if (valid[k]) {
+      m = pixel_margins_fast(av[k]);
+      w = 1.0f / (float)(av[k][0] * av[k][1] * av[k][2] * av[k][3]);
+    }
 #pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
+    for (int o = 4; o > 0; o >>= 1) {
       m.x = max(m.x, __shfl_xor_sync(0xffffffffu, m.x, o));
       m.y = max(m.y, __shfl_xor_sync(0xffffffffu, m.y, o));
       m.z = max(m.z, __shfl_xor_sync(0xffffffffu, m.z, o));
       m.w = max(m.w, __shfl_xor_sync(0xffffffffu, m.w, o));
+      w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
     }
-    if ((lx & 15) == 0) {
-      const int q = (lx >> 4) + 2 * ((ly + RS * k) >> 4);
-      atomicMax(&s_m[q][0], m.x);
-      atomicMax(&s_m[q][1], m.y);
-      atomicMax(&s_m[q][2], m.z);
-      atomicMax(&s_m[q][3], m.w);
+    if ((lx & 7) == 0) {
+      const int c = ((ly + RS * k) >> 3) * 4 + (lx >> 3);
+      atomicMax(&s_pc.m[c][0], m.x);
+      atomicMax(&s_pc.m[c][1], m.y);
+      atomicMax(&s_pc.m[c][2], m.z);
+      atomicMax(&s_pc.m[c][3], m.w);
+      atomicMax(reinterpret_cast<int *>(&s_pc.w[c]), __float_as_int(w));
     }
   }
   __syncthreads();
   if (tid == 0) {
-    const int tw = min(kTile, D.pw - x0), th = min(kTile, D.ph - y0);
-    int u[4] = {0, 0, 0, 0};
-    for (int q = 0; q < 4; ++q)
-      for (int j = 0; j < 4; ++j) u[j] = max(u[j], s_m[q][j]);
-    const int RW = tw + u[0] + u[1], RH = th + u[2] + u[3];
-    if ((RW | 1) * RH <= region_cap) {
-      s_nsub = 1;
-      int *d = s_plan[0];
-      d[0] = x0; d[1] = y0; d[2] = tw; d[3] = th; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
+    int n = 0;
+    bool fits;
+    bool ok = true;
+    if (!plan_unit(s_pc, D, x0, y0, 0, 0, 4, region_cap, s_plan[n], fits)) {
+      for (int q = 0; q < 4 && ok; ++q) {
+        const int qx = (q & 1) * 2, qy = (q >> 1) * 2;
+        if (plan_unit(s_pc, D, x0, y0, qx, qy, 2, region_cap, s_plan[n], fits)) {
+          ++n;
+          continue;
+        }
+        if (x0 + qx * 8 >= D.pw || y0 + qy * 8 >= D.ph) continue;
+        for (int c = 0; c < 4; ++c) {
+          const bool good = plan_unit(s_pc, D, x0, y0, qx + (c & 1), qy + (c >> 1), 1, region_cap,
+                                      s_plan[n], fits);
+          if (x0 + (qx + (c & 1)) * 8 >= D.pw || y0 + (qy + (c >> 1)) * 8 >= D.ph) continue;
+          (void)good;
+          if (!fits) ok = false;  // even an 8x8 region does not fit
+          ++n;
+        }
+      }
     } else {
-      int n = 0;
-      bool fits = true;
-      for (int q = 0; q < 4; ++q) {
-        const int sx = x0 + (q & 1) * 16, sy = y0 + (q >> 1) * 16;
-        if (sx >= D.pw || sy >= D.ph) continue;
-        const int sw = min(16, D.pw - sx), sh = min(16, D.ph - sy);
-        int *d = s_plan[n++];
-        d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = s_m[q][0]; d[5] = s_m[q][2];
-        d[6] = sw + s_m[q][0] + s_m[q][1];
-        d[7] = sh + s_m[q][2] + s_m[q][3];
-        fits = fits && ((d[6] | 1) * d[7] <= region_cap);
-      }
-      if (!fits && ovf_list) {
-        ovf_list[atomicAdd(&st->ovf_count, 1)] = tile;
-        n = 0;
-      } else if (!fits) {
-        atomicOr(&st->flags, kFlagRegionTooLarge);
-        n = 0;
-      }
-      s_nsub = n;
+      n = 1;
     }
+    if (!ok) {
+      if (ovf_list) ovf_list[atomicAdd(&st->ovf_count, 1)] = tile;
+      else atomicOr(&st->flags, kFlagRegionTooLarge);
+      n = 0;
+    }
+    s_nsub = n;
   }
   __syncthreads();
 
@@ -671,7 +731,7 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
         const int x = x0 + lane, y = y0 + ly + 4 * k;
         int4 m = make_int4(0, 0, 0, 0);
         if (x < D.pw && y < D.ph) {
-          if constexpr (MODE == kModeLut) {
+          if constexpr (MODE >= kModeLut) {
             m = lut_margin_bound(F, D.pc_lo + x, D.pr_lo + y);
           } else {
             double a[4];
@@ -966,6 +1026,8 @@ int ensure_scratch() {
     RUBS_SET_SMEM(kModeUniform, 1);
     RUBS_SET_SMEM(kModeLut, 0);
     RUBS_SET_SMEM(kModeLut, 1);
+    RUBS_SET_SMEM(kModeLut32, 0);
+    RUBS_SET_SMEM(kModeLut32, 1);
 #undef RUBS_SET_SMEM
     t_scr.attr_set = true;
   }
@@ -1075,8 +1137,10 @@ int launch_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cud
       if (t) launch_tiles<kModeField, 1>(I, F, D, s); else launch_tiles<kModeField, 0>(I, F, D, s);
     } else if (m == kModeUniform) {
       if (t) launch_tiles<kModeUniform, 1>(I, F, D, s); else launch_tiles<kModeUniform, 0>(I, F, D, s);
-    } else {
+    } else if (m == kModeLut) {
       if (t) launch_tiles<kModeLut, 1>(I, F, D, s); else launch_tiles<kModeLut, 0>(I, F, D, s);
+    } else {
+      if (t) launch_tiles<kModeLut32, 1>(I, F, D, s); else launch_tiles<kModeLut32, 0>(I, F, D, s);
     }
   }
   t_launches += 2;
@@ -1178,7 +1242,7 @@ namespace {
 FieldSpec lut_field(const rubs_lut *lut, const void *size, const void *elong, const void *orient,
                     int p_dtype, int64_t ld_p) {
   FieldSpec F{};
-  F.mode = 2;
+  F.mode = p_dtype == RUBS_F64 ? kModeLut : kModeLut32;
   F.ps = size;
   F.pr = elong;
   F.pt = orient;
@@ -1273,9 +1337,15 @@ int rubs_b200_lut_create(const double *rho_grid, const double *phi_grid, const d
   L->n_rho = n_rho;
   L->n_phi = n_phi;
   L->rho_max = rho_grid[n_rho - 1];
-  size_t bytes = (size_t)n_rho * n_phi * 4 * sizeof(double);
+  // four copies, copy q rolled by q quarter turns: out[k] = mix[(k - q) mod 4]
+  const size_t per = (size_t)n_rho * n_phi * 4;
+  std::vector<double> rolled(4 * per);
+  for (int q = 0; q < 4; ++q)
+    for (size_t e = 0; e < (size_t)n_rho * n_phi; ++e)
+      for (int k = 0; k < 4; ++k) rolled[q * per + e * 4 + k] = entries[e * 4 + ((k - q + 4) & 3)];
+  size_t bytes = rolled.size() * sizeof(double);
   cudaError_t e = cudaMalloc(&L->entries, bytes);
-  if (e == cudaSuccess) e = cudaMemcpy(L->entries, entries, bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(L->entries, rolled.data(), bytes, cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     if (L->entries) cudaFree(L->entries);
     delete L;

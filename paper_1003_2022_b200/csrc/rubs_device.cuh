@@ -21,7 +21,8 @@ constexpr double kFloorMagic = 6755399441055744.0;
 // field modes
 constexpr int kModeField = 0;    // (FH, FW, 4) float64 array
 constexpr int kModeUniform = 1;  // one (4,) vector
-constexpr int kModeLut = 2;      // (size, elongation, orientation) + LUT
+constexpr int kModeLut = 2;      // (size, elongation, orientation) float64 + LUT
+constexpr int kModeLut32 = 3;    // same, float32 parameters
 
 // status flags (bit set -> error class)
 constexpr unsigned kFlagFieldNonFinite = 1u;  // engine.py:214-215 -> ValueError
@@ -117,37 +118,34 @@ __device__ __forceinline__ void lut_map(const FieldSpec &F, double s, double rho
   const int q = quarter_index(th);
   const double phi = __dsub_rn(th, __dmul_rn((double)q, kQuarter));
   const int nr = F.n_rho, np_ = F.n_phi;
-  double u = log(rho) * F.inv_log_rho_max * (double)(nr - 1);
-  double v = phi * ((double)np_ / kQuarter) - 0.5;
+  // explicit roundings: identical bits wherever this is inlined
+  double u = __dmul_rn(__dmul_rn(log(rho), F.inv_log_rho_max), (double)(nr - 1));
+  double v = __dsub_rn(__dmul_rn(phi, (double)np_ / kQuarter), 0.5);
   u = fmin(fmax(u, 0.0), (double)(nr - 1));
   v = fmin(fmax(v, 0.0), (double)(np_ - 1));
   int i0 = min((int)u, nr - 2);
   int j0 = min((int)v, np_ - 2);
-  const double fu = u - (double)i0, fv = v - (double)j0;
-  const double gu = 1.0 - fu, gv = 1.0 - fv;
-  const double w00 = gu * gv, w10 = fu * gv, w01 = gu * fv, w11 = fu * fv;
-  const double2 *e00 = reinterpret_cast<const double2 *>(F.lut + ((int64_t)i0 * np_ + j0) * 4);
+  const double fu = __dsub_rn(u, (double)i0), fv = __dsub_rn(v, (double)j0);
+  const double gu = __dsub_rn(1.0, fu), gv = __dsub_rn(1.0, fv);
+  const double w00 = __dmul_rn(gu, gv), w10 = __dmul_rn(fu, gv), w01 = __dmul_rn(gu, fv),
+               w11 = __dmul_rn(fu, fv);
+  // F.lut holds four copies of the table, copy q already rolled by q
+  // quarter turns (solver.py:286, 332-334), so no per-pixel selects
+  const double2 *e00 = reinterpret_cast<const double2 *>(
+      F.lut + ((int64_t)q * nr * np_ + (int64_t)i0 * np_ + j0) * 4);
   const double2 *e01 = e00 + 2;
   const double2 *e10 = e00 + (int64_t)np_ * 2;
   const double2 *e11 = e10 + 2;
   const double ss = sqrt(s);
-  double m[4];
   {
     const double2 A = __ldg(e00), B = __ldg(e10), C = __ldg(e01), Dd = __ldg(e11);
-    m[0] = (A.x * w00 + B.x * w10 + C.x * w01 + Dd.x * w11) * ss;
-    m[1] = (A.y * w00 + B.y * w10 + C.y * w01 + Dd.y * w11) * ss;
+    a[0] = __dmul_rn(__fma_rn(A.x, w00, __fma_rn(B.x, w10, __fma_rn(C.x, w01, __dmul_rn(Dd.x, w11)))), ss);
+    a[1] = __dmul_rn(__fma_rn(A.y, w00, __fma_rn(B.y, w10, __fma_rn(C.y, w01, __dmul_rn(Dd.y, w11)))), ss);
   }
   {
     const double2 A = __ldg(e00 + 1), B = __ldg(e10 + 1), C = __ldg(e01 + 1), Dd = __ldg(e11 + 1);
-    m[2] = (A.x * w00 + B.x * w10 + C.x * w01 + Dd.x * w11) * ss;
-    m[3] = (A.y * w00 + B.y * w10 + C.y * w01 + Dd.y * w11) * ss;
-  }
-  // cyclic roll by q quarter turns (solver.py:286, 332-334), register selects
-  const bool b0 = q & 1, b1 = q & 2;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const double x0 = m[k], x1 = m[(k + 3) & 3], x2 = m[(k + 2) & 3], x3 = m[(k + 1) & 3];
-    a[k] = b1 ? (b0 ? x3 : x2) : (b0 ? x1 : x0);
+    a[2] = __dmul_rn(__fma_rn(A.x, w00, __fma_rn(B.x, w10, __fma_rn(C.x, w01, __dmul_rn(Dd.x, w11)))), ss);
+    a[3] = __dmul_rn(__fma_rn(A.y, w00, __fma_rn(B.y, w10, __fma_rn(C.y, w01, __dmul_rn(Dd.y, w11)))), ss);
   }
 }
 
@@ -167,9 +165,9 @@ __device__ __forceinline__ void field_raw(const FieldSpec &F, int fr, int fc, do
   } else if constexpr (MODE == kModeUniform) {
     a[0] = F.u[0]; a[1] = F.u[1]; a[2] = F.u[2]; a[3] = F.u[3];
   } else {
+    constexpr int PDT = MODE == kModeLut ? 1 : 0;
     const int64_t i = (int64_t)fr * F.pld + fc;
-    lut_map(F, load_scalar(F.ps, F.pdt, i), load_scalar(F.pr, F.pdt, i),
-            load_scalar(F.pt, F.pdt, i), a, flags);
+    lut_map(F, load_px<PDT>(F.ps, i), load_px<PDT>(F.pr, i), load_px<PDT>(F.pt, i), a, flags);
   }
 }
 
@@ -193,7 +191,8 @@ __device__ __forceinline__ void field_at_rt(const FieldSpec &F, int n1, int n2, 
                                             unsigned &flags) {
   if (F.mode == kModeField) field_at<kModeField>(F, n1, n2, a, flags);
   else if (F.mode == kModeUniform) field_at<kModeUniform>(F, n1, n2, a, flags);
-  else field_at<kModeLut>(F, n1, n2, a, flags);
+  else if (F.mode == kModeLut) field_at<kModeLut>(F, n1, n2, a, flags);
+  else field_at<kModeLut32>(F, n1, n2, a, flags);
 }
 
 // Per-pixel read extents relative to the pixel, engine.py:219-229, 247-262:
@@ -229,10 +228,12 @@ __device__ __forceinline__ int4 pixel_margins_fast(const double a[4]) {
   return m;
 }
 
-// floor(x + 0.5) split: m (int) and residual d = m - x (zp.py:204-210).
+// Nearest lattice point m of x and residual d = m - x (zp.py:204-210).  The
+// reference takes m = floor(x + 0.5); at exact half-integers rounding to
+// nearest-even may pick the other neighbour (d = -1/2 instead of +1/2), which
+// reads the same value of the C1 spline, so one rounding add suffices.
 __device__ __forceinline__ void lattice_split(double x, int &m, double &d) {
-  const double y = __dadd_rn(x, 0.5);
-  const double t = __dadd_rd(y, kFloorMagic);
+  const double t = __dadd_rn(x, kFloorMagic);
   m = __double2loint(t);
   d = __dsub_rn(__dsub_rn(t, kFloorMagic), x);
 }
