@@ -230,9 +230,10 @@ def run_ours(args, rank, world, local):
                 hp.append(t_.numpy())
             hfn = hf.numpy()
             lut = rb.default_lut()
+            hout = torch.empty((H, W), dtype=torch.float64, pin_memory=True).numpy()
 
             def e2e_step():
-                return rb.filter_space_variant_params(hfn, *hp, lut=lut, iterations=iters)
+                return rb.filter_space_variant_params(hfn, *hp, lut=lut, iterations=iters, out=hout)
             h2d = hf.numel() * hf.element_size() + sum(p.nbytes for p in hp)
         else:
             hf = torch.empty((H, W), dtype=sets[0]["f"].dtype, pin_memory=True)
@@ -240,9 +241,10 @@ def run_ours(args, rank, world, local):
             hfl = torch.empty(sets[0]["field"].shape, dtype=torch.float64, pin_memory=True)
             hfl.copy_(sets[0]["field"].cpu())
             hfn, hfln = hf.numpy(), hfl.numpy()
+            hout = torch.empty((H, W), dtype=torch.float64, pin_memory=True).numpy()
 
             def e2e_step():
-                return rb.filter_space_variant(hfn, hfln, iters)
+                return rb.filter_space_variant(hfn, hfln, iters, out=hout)
             h2d = hfn.nbytes + hfln.nbytes
         for _ in range(max(2, args.warmup // 2)):
             e2e_step()
@@ -258,7 +260,8 @@ def run_ours(args, rank, world, local):
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": float(H * W) * ksteps * world / float(te.item()) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(H * W * 8),
-               "steps": ksteps, "timing": "wall clock around blocking API calls, max over ranks"}
+               "steps": ksteps, "host_buffers": "pinned (inputs and result)",
+               "timing": "wall clock around blocking API calls, max over ranks"}
 
     result = None
     if rank == 0:
@@ -290,7 +293,7 @@ def run_ours(args, rank, world, local):
                        else "drop-in (H,W,4) field (rubs_b200_filter)"},
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic,
+                         "frac": achieved / hbm, "traffic": traffic, "traffic_unit": "bytes/launch (ncu)",
                          "kernel": "tile_filter_kernel", "kernel_ms_avg": tile_avg_ms,
                          "algorithmic_bytes_per_px": bpp, "peak_source": peak_kind,
                          "binding_bound": "fp64 issue (see fp64)"},
@@ -313,9 +316,12 @@ WORKLOADS = {
          "theta=atan2 mod pi; exact optimiser field",
     "4": "config4 image: 4096^2 fp32 uniform[0,1); sigma [2,24], rho [1,4], smooth theta; 2 passes",
 }
-# filled from the committed ncu captures (profiles/); None until measured
-DP_INST_PER_PX = {}
-TRAFFIC_PER_LAUNCH = {}
+# From the committed ncu capture of the tile kernel on config 2
+# (profiles/ncu_r01_summary.md): fp64 instructions executed per output pixel
+# (DADD + DFMA + DMUL + DSETP, thread level) and DRAM bytes per launch
+# (dram__bytes_read.sum + dram__bytes_write.sum).
+DP_INST_PER_PX = {"2": 635}
+TRAFFIC_PER_LAUNCH = {"2": 98.76e6}
 
 
 # ---------------------------------------------------------------------------

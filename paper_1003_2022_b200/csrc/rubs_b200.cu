@@ -672,28 +672,29 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) {
 // C11 = (2 a1^2 + a2^2 + a4^2) / 24), where the table's bilinear blend keeps
 // C11 below the largest corner node's, i.e. below the target's + 0.04 size;
 // the 0.05 floor adds at most 0.0604, the pass scaling divides by sqrt(m).
+template <int PDT>
 __device__ __forceinline__ int4 lut_margin_bound(const FieldSpec &F, int n1, int n2) {
   const int fc = min(max(n1, 0), F.FW - 1), fr = min(max(n2, 0), F.FH - 1);
   const int64_t i = (int64_t)fr * F.pld + fc;
-  double sz = load_scalar(F.ps, F.pdt, i), rho = load_scalar(F.pr, F.pdt, i);
-  double th = load_scalar(F.pt, F.pdt, i);
-  if (!(sz > 0.0 && sz < INFINITY)) sz = 1.0;
-  if (!(rho >= 1.0 && rho < INFINITY)) rho = 1.0;
-  if (!(th >= 0.0 && th < kPi)) th = 0.0;
-  rho = fmin(rho, F.rho_max);
-  const float c = cosf((float)th), sn = sinf((float)th);
-  const float inv = 1.0f / (1.0f + (float)rho);
-  const float c11 = ((float)rho * c * c + sn * sn) * inv + 0.04f;
-  const float c22 = ((float)rho * sn * sn + c * c) * inv + 0.04f;
-  const float fl = 0.0605f;
-  const float idiv = (float)(1.0 / F.div) * 1.0001f;
-  const double hx = (double)((3.0f * sqrtf((float)sz * c11) * 1.001f + fl) * idiv);
-  const double hy = (double)((3.0f * sqrtf((float)sz * c22) * 1.001f + fl) * idiv);
+  float sz = (float)load_px<PDT>(F.ps, i), rho = (float)load_px<PDT>(F.pr, i);
+  float th = (float)load_px<PDT>(F.pt, i);
+  if (!(sz > 0.f && sz < INFINITY)) sz = 1.f;
+  if (!(rho >= 1.f && rho < INFINITY)) rho = 1.f;
+  if (!(th >= 0.f && th < 3.1416f)) th = 0.f;
+  rho = fminf(rho, (float)F.rho_max);
+  float sn, c;
+  __sincosf(th, &sn, &c);  // |error| < 1e-6, far inside the 0.04 slack
+  const float inv = __frcp_rn(1.0f + rho);
+  const float c11 = (rho * c * c + sn * sn) * inv + 0.04f;
+  const float c22 = (rho * sn * sn + c * c) * inv + 0.04f;
+  const float k = (float)(1.0 / F.div) * 1.0002f;
+  const float hx = (3.0f * sqrtf(sz * c11) * 1.001f + 0.0605f) * k;
+  const float hy = (3.0f * sqrtf(sz * c22) * 1.001f + 0.0605f) * k;
   int4 m;
-  m.x = max(0, (int)ceil(hx + 0.5) + 3);
-  m.y = max(0, (int)ceil(hx - 0.5) + 3);
-  m.z = max(0, (int)ceil(hy + 1.5) + 3);
-  m.w = max(0, (int)ceil(hy - 1.5) + 3);
+  m.x = max(0, (int)ceilf(hx + 0.5f) + 3);
+  m.y = max(0, (int)ceilf(hx - 0.5f) + 3);
+  m.z = max(0, (int)ceilf(hy + 1.5f) + 3);
+  m.w = max(0, (int)ceilf(hy - 1.5f) + 3);
   return m;
 }
 
@@ -725,21 +726,31 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
       const int x0 = tx * kTile, y0 = ty * kTile;
       if (tid < 16) s_m[tid >> 2][tid & 3] = 0;
       nbar_sync(kBarProd, kPipeProd);
-      const int ly = tid >> 5;  // 0..3
-#pragma unroll 2
+      const int ly = tid >> 5;  // 0..3; pixel rows ly + 4k
+      int4 mh[2] = {make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0)};
+#pragma unroll
       for (int k = 0; k < 8; ++k) {
         const int x = x0 + lane, y = y0 + ly + 4 * k;
-        int4 m = make_int4(0, 0, 0, 0);
         if (x < D.pw && y < D.ph) {
+          int4 m;
           if constexpr (MODE >= kModeLut) {
-            m = lut_margin_bound(F, D.pc_lo + x, D.pr_lo + y);
+            m = lut_margin_bound<MODE == kModeLut ? 1 : 0>(F, D.pc_lo + x, D.pr_lo + y);
           } else {
             double a[4];
             unsigned fl = 0;
             field_at<MODE>(F, D.pc_lo + x, D.pr_lo + y, a, fl);
             m = pixel_margins_fast(a);
           }
+          const int h = k >= 4 ? 1 : 0;
+          mh[h].x = max(mh[h].x, m.x);
+          mh[h].y = max(mh[h].y, m.y);
+          mh[h].z = max(mh[h].z, m.z);
+          mh[h].w = max(mh[h].w, m.w);
         }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int4 m = mh[h];
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) {
           m.x = max(m.x, __shfl_xor_sync(0xffffffffu, m.x, o));
@@ -748,7 +759,7 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
           m.w = max(m.w, __shfl_xor_sync(0xffffffffu, m.w, o));
         }
         if ((lane & 15) == 0) {
-          const int q = (lane >> 4) + 2 * ((ly + 4 * k) >> 4);
+          const int q = (lane >> 4) + 2 * h;
           atomicMax(&s_m[q][0], m.x);
           atomicMax(&s_m[q][1], m.y);
           atomicMax(&s_m[q][2], m.z);

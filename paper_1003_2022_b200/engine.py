@@ -139,7 +139,18 @@ def _ptr(a: np.ndarray):
     return ctypes.c_void_p(a.ctypes.data)
 
 
-def filter_space_variant(f, field, iterations: int = 1):
+def _host_out(out, shape):
+    """Optional caller-provided result buffer (e.g. pinned host memory, so
+    the device-to-host copy runs at full bandwidth); an extension of the
+    reference API, which always allocates."""
+    if out is None:
+        return np.empty(shape, dtype=np.float64)
+    if out.shape != shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous float64 array of the image shape")
+    return out
+
+
+def filter_space_variant(f, field, iterations: int = 1, *, out=None):
     """Filter with a per-pixel kernel in constant time per pixel.
 
     ``f`` 2-D image (combined with zeros outside); ``field`` ScaleField,
@@ -156,7 +167,7 @@ def filter_space_variant(f, field, iterations: int = 1):
         raise ValueError("iterations must be >= 1")
     fld, uniform = _host_field(field, img.shape)
     H, W = img.shape
-    out = np.empty((H, W), dtype=np.float64)
+    out = _host_out(out, (H, W))
     if H == 0 or W == 0:
         return out
     L = _native.load()
@@ -297,7 +308,7 @@ def lookup_many(lut: ScaleLut, size, elongation, orientation):
 
 
 def filter_space_variant_params(f, size, elongation, orientation, lut: ScaleLut | None = None,
-                                iterations: int = 1):
+                                iterations: int = 1, *, out=None):
     """filter_space_variant(f, lookup_many(lut, size, elongation, orientation),
     iterations) with the lookup fused into the filter kernel."""
     iterations = int(iterations)
@@ -337,7 +348,7 @@ def filter_space_variant_params(f, size, elongation, orientation, lut: ScaleLut 
     (s, r, t), shape, dt = _params_host(size, elongation, orientation)
     if shape != (H, W):
         s, r, t = (np.ascontiguousarray(np.broadcast_to(v, (H, W))) for v in (s, r, t))
-    out = np.empty((H, W), dtype=np.float64)
+    out = _host_out(out, (H, W))
     if H == 0 or W == 0:
         return out
     _native.check(L.rubs_b200_filter_params_host(

@@ -40,3 +40,14 @@ for a, b in zip(cuts[:-1], cuts[1:]):
     top = " ".join(f"{k}:{v * 32 / npx:.0f}" for k, v in ops.most_common(8))
     print(f"[{a:5d},{b:5d}) stall {100 * st / max(tot, 1):5.1f}%  inst/px {inst:6.0f}  dp/px {dp:5.0f}  "
           f"smem wf {wf / 1e6:6.2f}M (ideal {wfi / 1e6:6.2f}M)  {top}")
+alltot = collections.Counter()
+for s_, _, ex, _, _ in data:
+    t = s_.split()
+    if not t:
+        continue
+    o = t[1] if t[0].startswith("@") and len(t) > 1 else t[0]
+    alltot[o.split(".")[0]] += ex
+tot_inst = sum(alltot.values()) * 32 / npx
+tot_dp = sum(alltot[k] for k in ("DADD", "DFMA", "DMUL", "DSETP")) * 32 / npx
+print(f"TOTAL inst/px {tot_inst:.0f}  fp64 inst/px {tot_dp:.0f}  smem wavefronts/px "
+      f"{sum(d[3] for d in data) / npx:.2f}")
