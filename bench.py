@@ -46,7 +46,7 @@ METRIC = "Gpixel/s filtered"
 UNIT = "Gpixel/s"
 # Algorithmic bytes per output pixel for the fused path: f64 image (8) +
 # three f32 params (12) + f64 output (8) = 28.
-BYTES_PER_PX = {"2": 28, "1": 48, "4": 52}
+BYTES_PER_PX = {"2": 28, "1": 48, "3": 24, "4": 52, "5": 24}
 
 
 def parse():
@@ -55,7 +55,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="2", choices=["1", "2", "4"])
+    p.add_argument("--config", default="2", choices=["1", "2", "3", "4", "5"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
@@ -144,9 +144,17 @@ def make_inputs(cfg: str, torch, device, copies: int, rank: int):
         w = workloads.config2(device=device, param_dtype=torch.float32)
     elif cfg == "1":
         w = workloads.config1()
+    elif cfg == "3":
+        w = workloads.config3(device=device, param_dtype=torch.float32)
+        copies = 1  # inputs alone exceed L2
+    elif cfg == "5":
+        w = workloads.config5(device=device, param_dtype=torch.float32, image_device=device)
+        copies = 1
     else:
         w = workloads.config4_image(rank, device=device, param_dtype=torch.float32)
     f = torch.as_tensor(w["f"]).to(device)
+    if copies == 1:
+        return w, [{"f": f, "p": [w["size"], w["elong"], w["orient"]]}]
     sets = []
     for _ in range(copies):
         if "field" in w:
@@ -171,7 +179,6 @@ def run_ours(args, rank, world, local):
     w, sets = make_inputs(args.config, torch, device, 4, rank)
     iters = int(w["iterations"])
     H, W = w["f"].shape
-    outs = [torch.empty((H, W), dtype=torch.float64, device=device) for _ in sets]
 
     def step(i):
         s = sets[i % len(sets)]
@@ -310,6 +317,10 @@ def run_ours(args, rank, world, local):
 
 
 WORKLOADS = {
+    "3": "config3 shapes: 8192^2 fp32 rectangles + N(0,0.05^2) noise; sigma [1,32], rho [1,6] "
+         "clamped, smooth theta; N=4 ZP element (the reference has no N=3 path)",
+    "5": "config5: 32768^2 fp32 uniform[0,1) (torch Philox seed 0); sigma [2,256], rho [1,8] "
+         "clamped to the LUT, smooth theta; single GPU",
     "2": "config2: 2048^2 fp64 uniform[0,1) seed 0; N=4 ZP box spline; sigma [2,16], rho [1,4], "
          "theta [0,pi) smooth fields (LUT mapping, f32 params)",
     "1": "config1: 256^2 fp64 uniform[0,1) seed 0; sigma 2->8 along x, rho 1->3 radial, "

@@ -26,7 +26,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
+#include <tuple>
 #include <string>
 #include <vector>
 
@@ -355,24 +357,31 @@ __device__ __forceinline__ double lds64(uint32_t addr) {
   return v;
 }
 
-// One ZP read (x 8) at the vertex whose nearest lattice element is at shared
-// byte address c, residual (d1, d2).
-__device__ __forceinline__ double zp_read8(uint32_t c, int P8, double d1, double d2) {
+__device__ __forceinline__ double ld64(uint32_t a) { return lds64(a); }
+__device__ __forceinline__ double ld64(const char *p) {
+  return __ldg(reinterpret_cast<const double *>(p));
+}
+
+// One ZP read (x 8) at the vertex whose nearest lattice element is at byte
+// address c (shared: 32-bit address; global: pointer), residual (d1, d2),
+// row pitch P8 bytes.
+template <class A, class S>
+__device__ __forceinline__ double zp_read8(A c, S P8, double d1, double d2) {
   const bool gp = d1 >= -d2;  // d1 + d2 >= 0
   const bool gm = d1 >= d2;   // d1 - d2 >= 0
   const bool xmaj = (gp == gm);
-  int sA = xmaj ? 8 : P8;
+  S sA = xmaj ? (S)8 : P8;
   sA = gp ? sA : -sA;
-  const int sB = xmaj ? P8 : 8;
+  const S sB = xmaj ? P8 : (S)8;
   const double u = dabs(xmaj ? d1 : d2);
   const double v = xmaj ? d2 : d1;
-  const double g0 = lds64(c);
-  const double N = lds64(c - sA);
-  const double Pp = lds64(c + sA);
-  const double Bm = lds64(c - sB);
-  const double Bp = lds64(c + sB);
-  const double Cm = lds64(c - sA - sB);
-  const double Cp = lds64(c - sA + sB);
+  const double g0 = ld64(c);
+  const double N = ld64(c - sA);
+  const double Pp = ld64(c + sA);
+  const double Bm = ld64(c - sB);
+  const double Bp = ld64(c + sB);
+  const double Cm = ld64(c - sA - sB);
+  const double Cp = ld64(c - sA + sB);
   const double sBv = Bm + Bp, dBv = Bm - Bp, sC = Cm + Cp, dC = Cm - Cp;
   const double A0 = fma(4.0, g0, N + Pp) + sBv;
   const double L1 = N - Pp;
@@ -385,9 +394,9 @@ __device__ __forceinline__ double zp_read8(uint32_t c, int P8, double d1, double
   return fma(dtwice(u), i1, fma(V, i2, A0));
 }
 
-// Per-pixel finite difference (engine.py:219-244) over the region plane,
-// 16 vertices x 7 ZP taps.  Sb = shared byte address such that
-// Sb + (m2 * P + m1) * 8 is the region element at lattice (m1, m2).
+// Per-pixel finite difference (engine.py:219-244) over a region plane,
+// 16 vertices x 7 ZP taps.  Sb = byte address such that
+// Sb + m2 * P8 + m1 * 8 is the region element at lattice (m1, m2).
 //
 // The 4 x 7 quadratic table of zp.py (exact multiples of 1/8)
 // folds into one canonical wedge: partition q (zp.py:82-86) only decides
@@ -395,7 +404,8 @@ __device__ __forceinline__ double zp_read8(uint32_t c, int P8, double d1, double
 // which is +1 exactly when d1 + d2 >= 0 in both cases.  The seven taps are
 // the centre, the two major neighbours N (-sign) and P (+sign), the two
 // minor neighbours Bm/Bp and the two corners on the N side Cm/Cp.
-__device__ __forceinline__ double pixel_fd(uint32_t Sb, int P, int n1, int n2, const double a[4]) {
+template <class A, class S>
+__device__ __forceinline__ double pixel_fd_t(A Sb, S P8, int n1, int n2, const double a[4]) {
   const double a1 = a[0], a2 = a[1], a3 = a[2], a4 = a[3];
   const double p2 = a2 * kInvSqrt2, p4 = a4 * kInvSqrt2;
   const double t1 = 0.5 * a1 + 0.5 * (p2 - p4) - 0.5;
@@ -403,7 +413,6 @@ __device__ __forceinline__ double pixel_fd(uint32_t Sb, int P, int n1, int n2, c
   // 1/8 of the ZP table and the factor 2 folded out of the sweeps
   const double w = 0.25 / (a1 * a2 * a3 * a4);
   const double xb = (double)n1 + t1, yb = (double)n2 + t2;
-  const int P8 = P * 8;
   double acc = 0.0;
   // vertex i = q1 | q2 << 1 | q3 << 2 | q4 << 4; sign (-1)^popcount
   //   x = xb - (q1 a1 + q2 p2 - q4 p4)   (engine.py:240)
@@ -414,21 +423,22 @@ __device__ __forceinline__ double pixel_fd(uint32_t Sb, int P, int n1, int n2, c
                           q4 ? (a1 + p2) - p4 : a1 + p2};  // index q1 | q2 << 1
     const double oy[4] = {q4 ? p4 : 0.0, q4 ? p2 + p4 : p2, q4 ? a3 + p4 : a3,
                           q4 ? (p2 + a3) + p4 : p2 + a3};  // index q2 | q3 << 1
-    uint32_t cx[4], cy[4];
+    S cx[4];
+    A cy[4];
     double dx[4], dy[4];
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       int m;
       lattice_split(xb - ox[k], m, dx[k]);
-      cx[k] = (uint32_t)(m * 8);
+      cx[k] = (S)m * 8;
       lattice_split(yb - oy[k], m, dy[k]);
-      cy[k] = Sb + (uint32_t)(m * P8);
+      cy[k] = Sb + (S)m * P8;
     }
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
       const int q1 = j & 1, q2 = (j >> 1) & 1, q3 = (j >> 2) & 1;
       const int ix = q1 | (q2 << 1), iy = q2 | (q3 << 1);
-      const double F8 = zp_read8(cy[iy] + cx[ix], P8, dx[ix], dy[iy]);
+      const double F8 = zp_read8<A, S>(cy[iy] + cx[ix], P8, dx[ix], dy[iy]);
       if ((q1 + q2 + q3 + q4) & 1)
         acc -= F8;
       else
@@ -436,6 +446,10 @@ __device__ __forceinline__ double pixel_fd(uint32_t Sb, int P, int n1, int n2, c
     }
   }
   return acc * w;
+}
+
+__device__ __forceinline__ double pixel_fd(uint32_t Sb, int P, int n1, int n2, const double a[4]) {
+  return pixel_fd_t<uint32_t, int>(Sb, P * 8, n1, n2, a);
 }
 
 // Region planning.  A unit is a rectangle of output pixels with its own
@@ -566,8 +580,19 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
       n = 1;
     }
     if (!ok) {
-      if (ovf_list) ovf_list[atomicAdd(&st->ovf_count, 1)] = tile;
-      else atomicOr(&st->flags, kFlagRegionTooLarge);
+      if (ovf_list) {
+        OvfRec r;
+        r.tile = tile;
+        r.m[0] = r.m[1] = r.m[2] = r.m[3] = 0;
+        r.w = 0.f;
+        for (int c = 0; c < 16; ++c) {
+          for (int j = 0; j < 4; ++j) r.m[j] = max(r.m[j], s_pc.m[c][j]);
+          r.w = fmaxf(r.w, s_pc.w[c]);
+        }
+        reinterpret_cast<OvfRec *>(ovf_list)[atomicAdd(&st->ovf_count, 1)] = r;
+      } else {
+        atomicOr(&st->flags, kFlagRegionTooLarge);
+      }
       n = 0;
     }
     s_nsub = n;
@@ -633,10 +658,9 @@ __global__ void __launch_bounds__(kThreadsSmall, 2)
 template <int MODE, int DT>
 __global__ void __launch_bounds__(kThreadsLarge, 1)
     tile_overflow_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int region_cap,
-                         const int *ovf_list, Status *st) {
+                         const int *ovf_list, int n, Status *st) {
   extern __shared__ double S[];
   unsigned ghi = 0, flags = 0;
-  const int n = *(volatile const int *)&st->ovf_count;
   for (int i = blockIdx.x; i < n; i += gridDim.x)
     process_tile<MODE, DT, kThreadsLarge>(I, F, D, ovf_list[i], tiles_x, region_cap, nullptr, st,
                                           S, ghi, flags);
@@ -790,7 +814,11 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
             fits = fits && ((d[6] | 1) * d[7] <= kPipeBuf);
           }
           if (!fits) {
-            ovf_list[atomicAdd(&st->ovf_count, 1)] = tile;
+            OvfRec r;
+            r.tile = tile;
+            for (int j = 0; j < 4; ++j) r.m[j] = u[j];
+            r.w = 0.f;
+            reinterpret_cast<OvfRec *>(ovf_list)[atomicAdd(&st->ovf_count, 1)] = r;
             n = 0;
           }
         }
@@ -852,6 +880,144 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
     }
   }
   flush_status(st, ghi, flags);
+}
+
+// ---------------------------------------------------------------------------
+// Large-halo path: regions in global memory (configs 3 and 5).
+//
+// Tiles whose 8x8 regions exceed even the 225 KB configuration are grouped
+// on the host into square blocks of S = 2^k >= 2 h pixels (h = the tile's
+// largest margin; S shrunk further if the w * L4 precision budget demands).
+// Each block's region -- its member tiles' bounding box grown by their
+// maximum margins -- is pre-integrated in a global scratch buffer by three
+// grid-wide kernels (fill + RS1 as one warp scan per row; RS2 / RS3 / RS4
+// one lane per line, a warp walking 32 neighbouring lines row by row so
+// every access is coalesced), then gathered by a tile kernel that reads the
+// taps through L1/L2.  Member tiles are gathered in block-raster order, so
+// neighbouring CTAs share the rows their vertices touch in L2.
+
+struct BigRegion {
+  int64_t off;       // element offset of region element (0, 0) in scratch
+  int rc0, rr0;      // lattice of region element (0, 0)
+  int RW, RH, P, pad;
+};
+struct BigTile {
+  int tile, region;
+};
+
+template <int DT>
+__global__ void __launch_bounds__(256) big_fill_rs1_kernel(ImageSpec I, const BigRegion *R,
+                                                           double *scratch) {
+  const BigRegion g = R[blockIdx.y];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int row = blockIdx.x * 8 + warp;
+  if (row >= g.RH) return;
+  double *dst = scratch + g.off + (int64_t)row * g.P;
+  const int ir = g.rr0 + row - I.row0;
+  const bool rin = ir >= 0 && ir < I.h;
+  const int64_t gi = (int64_t)ir * I.ld;
+  double carry = 0.0;
+  for (int c0 = 0; c0 < g.RW; c0 += 32) {
+    const int c = c0 + lane;
+    const int ic = g.rc0 + c - I.col0;
+    double v = (rin && c < g.RW && ic >= 0 && ic < I.w) ? load_px<DT>(I.f, gi + ic) : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double t = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += t;
+    }
+    v += carry;
+    if (c < g.RW) dst[c] = v;
+    carry = __shfl_sync(0xffffffffu, v, 31);
+  }
+}
+
+// dir 2: g[r][c] += g[r-1][c-1];  3: g[r][c] += g[r-1][c];  4: g[r][c] += g[r-1][c+1]
+template <int DIR>
+__global__ void __launch_bounds__(256) big_line_kernel(const BigRegion *R, double *scratch,
+                                                       Status *st) {
+  const BigRegion g = R[blockIdx.y];
+  const int lane = threadIdx.x & 31;
+  const int lb = (blockIdx.x * 256 + threadIdx.x) & ~31;  // first line of this warp
+  const int nlines = DIR == 3 ? g.RW : g.RH + g.RW - 1;
+  if (lb >= nlines) return;
+  double *base = scratch + g.off;
+  // line of this lane and its element in row t:
+  //   DIR 2: k = L - (RH-1), column t + k;  DIR 3: column L;  DIR 4: column L - t
+  const int L = lb + lane;
+  int ta, tb, cw;  // warp's row range
+  if (DIR == 2) {
+    const int kb = lb - (g.RH - 1);
+    ta = max(0, -(kb + 31));
+    tb = min(g.RH - 1, g.RW - 1 - kb);
+    cw = 0;
+  } else if (DIR == 3) {
+    ta = 0;
+    tb = g.RH - 1;
+    cw = 0;
+  } else {
+    ta = max(0, lb - (g.RW - 1));
+    tb = min(g.RH - 1, lb + 31);
+    cw = 0;
+  }
+  (void)cw;
+  const int k2 = L - (g.RH - 1);
+  double s = 0.0;
+  unsigned gh = 0;
+  for (int t = ta; t <= tb; t += 4) {
+    double v[4];
+    int64_t idx[4];
+    bool ok[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int tt = t + u;
+      const int c = DIR == 2 ? tt + k2 : (DIR == 3 ? L : L - tt);
+      ok[u] = tt <= tb && c >= 0 && c < g.RW && L < nlines;
+      idx[u] = (int64_t)tt * g.P + c;
+      v[u] = ok[u] ? base[idx[u]] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (ok[u]) {
+        s += v[u];
+        base[idx[u]] = s;
+        if (DIR == 4) gh = max(gh, (unsigned)__double2hiint(s) & 0x7fffffffu);
+      }
+    }
+  }
+  if (DIR == 4) {
+    gh = __reduce_max_sync(0xffffffffu, gh);
+    if (lane == 0 && gh) atomicMax(&st->guard_hi, gh);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) big_gather_kernel(FieldSpec F, DomainSpec D, int tiles_x,
+                                                         const BigTile *tl, int nt,
+                                                         const BigRegion *R, const double *scratch,
+                                                         Status *st) {
+  unsigned flags = 0;
+  const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
+  for (int i = blockIdx.x; i < nt; i += gridDim.x) {
+    const BigTile bt = tl[i];
+    const BigRegion g = R[bt.region];
+    const int x0 = (bt.tile % tiles_x) * kTile, y0 = (bt.tile / tiles_x) * kTile;
+    const char *Sb = reinterpret_cast<const char *>(scratch + g.off) -
+                     ((int64_t)g.rr0 * g.P + g.rc0) * 8;
+    const int64_t P8 = (int64_t)g.P * 8;
+#pragma unroll 1
+    for (int k = 0; k < 4; ++k) {
+      const int x = x0 + lx, y = y0 + ly + 8 * k;
+      if (x < D.pw && y < D.ph) {
+        const int n1 = D.pc_lo + x, n2 = D.pr_lo + y;
+        double a[4];
+        field_at<MODE>(F, n1, n2, a, flags);
+        D.out[(int64_t)y * D.ld_out + x] = pixel_fd_t<const char *, int64_t>(Sb, P8, n1, n2, a);
+      }
+    }
+  }
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (lx == 0 && flags) atomicOr(&st->flags, flags);
 }
 
 // ---- standalone lookup (solver.lookup_many) ------------------------------
@@ -1000,8 +1166,16 @@ __global__ void interpolate_kernel(const double *__restrict__ plane, int64_t row
 struct Scratch {
   int device = -1;
   int sms = 148;
-  int *d_ovf = nullptr;
+  int *d_ovf = nullptr;  // OvfRec records
   size_t ovf_cap = 0;
+  int *d_list = nullptr;
+  size_t list_cap = 0;
+  double *d_big = nullptr;
+  size_t big_cap = 0;
+  BigRegion *d_regs = nullptr;
+  size_t regs_cap = 0;
+  BigTile *d_btiles = nullptr;
+  size_t btiles_cap = 0;
   Status *d_status = nullptr;
   Status *h_status = nullptr;  // pinned
   double *d_pass[2] = {nullptr, nullptr};
@@ -1129,8 +1303,154 @@ void launch_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, c
   else
     tile_filter_kernel<M, T><<<ntiles, kThreadsSmall, kSmemSmall, s>>>(
         I, F, D, tiles_x, kSmemSmall / 8, t_scr.d_ovf, t_scr.d_status);
-  tile_overflow_kernel<M, T><<<t_scr.sms, kThreadsLarge, kSmemLarge, s>>>(
-      I, F, D, tiles_x, kSmemLarge / 8, t_scr.d_ovf, t_scr.d_status);
+}
+
+template <class V>
+int upload(std::vector<V> &h, V *&d, size_t &cap, cudaStream_t s) {
+  if (h.size() > cap) {
+    if (d) cudaFree(d);
+    d = nullptr;
+    RUBS_CUDA_TRY(cudaMalloc(&d, h.size() * sizeof(V)));
+    cap = h.size();
+  }
+  if (!h.empty())
+    RUBS_CUDA_TRY(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(V), cudaMemcpyHostToDevice, s));
+  return RUBS_OK;
+}
+
+// Tiles deferred by the primary launch: those whose 8x8 regions fit the
+// 225 KB configuration go to the shared-memory overflow kernel, the rest to
+// the global-memory block path (see big_* kernels).
+template <int M, int T>
+int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int n_ovf,
+                    cudaStream_t s) {
+  std::vector<OvfRec> recs(n_ovf);
+  RUBS_CUDA_TRY(cudaMemcpyAsync(recs.data(), t_scr.d_ovf, n_ovf * sizeof(OvfRec),
+                                cudaMemcpyDeviceToHost, s));
+  RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+  const int tiles_x = (D.pw + kTile - 1) / kTile;
+  std::vector<int> smem_list;
+  struct Blk {
+    int S = 0, x0 = 1 << 30, y0 = 1 << 30, x1 = 0, y1 = 0;
+    int m[4] = {0, 0, 0, 0};
+    std::vector<int> tiles;
+  };
+  std::map<std::tuple<int, int, int>, Blk> blocks;
+  const int cap_large = kSmemLarge / 8;
+  for (const OvfRec &r : recs) {
+    const int x0 = (r.tile % tiles_x) * kTile, y0 = (r.tile / tiles_x) * kTile;
+    const int tw = std::min(kTile, D.pw - x0), th = std::min(kTile, D.ph - y0);
+    if (((std::min(8, tw) + r.m[0] + r.m[1]) | 1) * (std::min(8, th) + r.m[2] + r.m[3]) <= cap_large) {
+      smem_list.push_back(r.tile);
+      continue;
+    }
+    const int h = std::max(std::max(r.m[0], r.m[1]), std::max(r.m[2], r.m[3]));
+    int S = 64;
+    while (S < 2 * h && S < 8192) S *= 2;
+    while (S > kTile) {
+      const double RW = S + r.m[0] + r.m[1], RH = S + r.m[2] + r.m[3];
+      const double mn = std::min(RW, RH);
+      if ((double)r.w * 0.25 * RW * RH * mn * mn <= (double)kPrecisionBudget) break;
+      S /= 2;
+    }
+    Blk &b = blocks[std::make_tuple(S, x0 / S, y0 / S)];
+    b.S = S;
+    b.x0 = std::min(b.x0, x0);
+    b.y0 = std::min(b.y0, y0);
+    b.x1 = std::max(b.x1, x0 + tw);
+    b.y1 = std::max(b.y1, y0 + th);
+    for (int j = 0; j < 4; ++j) b.m[j] = std::max(b.m[j], r.m[j]);
+    b.tiles.push_back(r.tile);
+  }
+  int rc;
+  if (!smem_list.empty()) {
+    std::sort(smem_list.begin(), smem_list.end());
+    if ((rc = upload(smem_list, t_scr.d_list, t_scr.list_cap, s))) return rc;
+    tile_overflow_kernel<M, T><<<std::min((int)smem_list.size(), t_scr.sms), kThreadsLarge,
+                                 kSmemLarge, s>>>(I, F, D, tiles_x, kSmemLarge / 8, t_scr.d_list,
+                                                  (int)smem_list.size(), t_scr.d_status);
+    ++t_launches;
+    RUBS_CUDA_TRY(cudaGetLastError());
+  }
+  if (blocks.empty()) return RUBS_OK;
+  // batches of blocks under a scratch budget (elements)
+  const int64_t budget = (int64_t)1 << 29;  // 4 GiB of fp64
+  std::vector<BigRegion> regs;
+  std::vector<BigTile> tl;
+  int64_t used = 0;
+  auto flush = [&]() -> int {
+    if (regs.empty()) return RUBS_OK;
+    if (used > (int64_t)t_scr.big_cap) {
+      if (t_scr.d_big) cudaFree(t_scr.d_big);
+      t_scr.d_big = nullptr;
+      RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_big, (size_t)used * sizeof(double)));
+      t_scr.big_cap = (size_t)used;
+    }
+    int r2;
+    if ((r2 = upload(regs, t_scr.d_regs, t_scr.regs_cap, s))) return r2;
+    if ((r2 = upload(tl, t_scr.d_btiles, t_scr.btiles_cap, s))) return r2;
+    int maxRH = 0, maxL = 0;
+    for (const BigRegion &g : regs) {
+      maxRH = std::max(maxRH, g.RH);
+      maxL = std::max(maxL, g.RH + g.RW - 1);
+    }
+    const int nreg = (int)regs.size();
+    big_fill_rs1_kernel<T><<<dim3((maxRH + 7) / 8, nreg), 256, 0, s>>>(I, t_scr.d_regs, t_scr.d_big);
+    big_line_kernel<2><<<dim3((maxL + 255) / 256, nreg), 256, 0, s>>>(t_scr.d_regs, t_scr.d_big,
+                                                                       t_scr.d_status);
+    big_line_kernel<3><<<dim3((maxL + 255) / 256, nreg), 256, 0, s>>>(t_scr.d_regs, t_scr.d_big,
+                                                                       t_scr.d_status);
+    big_line_kernel<4><<<dim3((maxL + 255) / 256, nreg), 256, 0, s>>>(t_scr.d_regs, t_scr.d_big,
+                                                                       t_scr.d_status);
+    big_gather_kernel<M><<<std::min((int)tl.size(), t_scr.sms * 8), 256, 0, s>>>(
+        F, D, tiles_x, t_scr.d_btiles, (int)tl.size(), t_scr.d_regs, t_scr.d_big, t_scr.d_status);
+    t_launches += 5;
+    RUBS_CUDA_TRY(cudaGetLastError());
+    // the next batch reuses the scratch: wait for this one
+    RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+    regs.clear();
+    tl.clear();
+    used = 0;
+    return RUBS_OK;
+  };
+  for (auto &kv : blocks) {
+    Blk &b = kv.second;
+    BigRegion g;
+    g.RW = (b.x1 - b.x0) + b.m[0] + b.m[1];
+    g.RH = (b.y1 - b.y0) + b.m[2] + b.m[3];
+    g.P = g.RW;
+    g.rc0 = D.pc_lo + b.x0 - b.m[0];
+    g.rr0 = D.pr_lo + b.y0 - b.m[2];
+    g.pad = 0;
+    const int64_t n = (int64_t)g.P * g.RH;
+    if (!regs.empty() && used + n > budget)
+      if ((rc = flush())) return rc;
+    g.off = used;
+    used += n;
+    std::sort(b.tiles.begin(), b.tiles.end());
+    for (int t : b.tiles) tl.push_back(BigTile{t, (int)regs.size()});
+    regs.push_back(g);
+  }
+  return flush();
+}
+
+template <int M, int T>
+int overflow_dispatch(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int n,
+                      cudaStream_t s) {
+  return handle_overflow<M, T>(I, F, D, n, s);
+}
+
+int run_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int n,
+                 cudaStream_t s) {
+  const int m = F.mode, t = I.dt;
+  if (m == kModeField) return t ? overflow_dispatch<kModeField, 1>(I, F, D, n, s)
+                                : overflow_dispatch<kModeField, 0>(I, F, D, n, s);
+  if (m == kModeUniform) return t ? overflow_dispatch<kModeUniform, 1>(I, F, D, n, s)
+                                  : overflow_dispatch<kModeUniform, 0>(I, F, D, n, s);
+  if (m == kModeLut) return t ? overflow_dispatch<kModeLut, 1>(I, F, D, n, s)
+                              : overflow_dispatch<kModeLut, 0>(I, F, D, n, s);
+  return t ? overflow_dispatch<kModeLut32, 1>(I, F, D, n, s)
+           : overflow_dispatch<kModeLut32, 0>(I, F, D, n, s);
 }
 
 int launch_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cudaStream_t s) {
@@ -1141,7 +1461,7 @@ int launch_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cud
     if (ntiles > t_scr.ovf_cap) {
       if (t_scr.d_ovf) cudaFree(t_scr.d_ovf);
       t_scr.d_ovf = nullptr;
-      RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_ovf, ntiles * sizeof(int)));
+      RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_ovf, ntiles * sizeof(OvfRec)));
       t_scr.ovf_cap = ntiles;
     }
     if (m == kModeField) {
@@ -1154,8 +1474,22 @@ int launch_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cud
       if (t) launch_tiles<kModeLut32, 1>(I, F, D, s); else launch_tiles<kModeLut32, 0>(I, F, D, s);
     }
   }
-  t_launches += 2;
+  ++t_launches;
   RUBS_CUDA_TRY(cudaGetLastError());
+  return RUBS_OK;
+}
+
+// Complete a pass: status fetch (one sync), then the deferred tiles if the
+// primary launch recorded any.
+int finish_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cudaStream_t s,
+                Status &st) {
+  int rc;
+  if ((rc = fetch_status(s, st))) return rc;
+  if (st.ovf_count > 0 && !(st.flags & (kFlagFieldNonFinite | kFlagParamInvalid))) {
+    if ((rc = run_overflow(I, F, D, st.ovf_count, s))) return rc;
+    RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s));
+    if ((rc = fetch_status(s, st))) return rc;
+  }
   return RUBS_OK;
 }
 
@@ -1176,6 +1510,9 @@ int run_filter(const ImageSpec &img, FieldSpec F, int iterations, double *out, i
   if (iterations == 1) {
     // one launch: every tile computes its own scale-vectors and margins
     if ((rc = launch_pass(img, F, D, s))) return rc;
+    Status st;
+    if ((rc = finish_pass(img, F, D, s, st))) return rc;
+    return status_to_code(st);
   } else {
     // whole-field margins (engine.py:295) decide the pass canvases
     if ((rc = launch_global_margins(F, D, s))) return rc;
@@ -1201,6 +1538,9 @@ int run_filter(const ImageSpec &img, FieldSpec F, int iterations, double *out, i
         Dp.ld_out = Dp.pw;
       }
       if ((rc = launch_pass(cur, F, Dp, s))) return rc;
+      Status stp;
+      if ((rc = finish_pass(cur, F, Dp, s, stp))) return rc;
+      if ((rc = status_to_code(stp))) return rc;
       cur = ImageSpec{Dp.out, 1, Dp.ld_out, Dp.ph, Dp.pw, Dp.pc_lo, Dp.pr_lo};
     }
   }

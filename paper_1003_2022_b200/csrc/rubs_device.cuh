@@ -39,6 +39,15 @@ struct Status {
   int pad2;
 };
 
+// A tile deferred by the primary launch (its regions exceed the primary
+// configuration's shared memory): tile index, tile-wide read margins
+// (left, right, below, above) and max 1/(a1 a2 a3 a4).
+struct OvfRec {
+  int tile;
+  int m[4];
+  float w;
+};
+
 // Where the per-pixel scale-vector comes from.
 struct FieldSpec {
   int mode;

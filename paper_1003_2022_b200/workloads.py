@@ -8,8 +8,9 @@ Conventions (recorded in DESIGN.md):
   * x = column, y = row; sigma (BASELINE.json) -> size s = 2 sigma^2.
   * smooth(seed): min-max normalised sum of three sinusoids
     sin(2 pi (fx x / W + fy y / H) + phi), fx, fy ~ U(0.5, 3), phi ~ U(0, 2 pi).
-  * rho is clamped to min(rho, 0.95 U(theta), 5.8 (1 - 1e-9)) like
-    tensor.py:140 and tensor.py:216.
+  * rho is clamped to min(rho, 0.95 U(theta), 5.8 (1 - 1e-6)) like
+    tensor.py:140 and tensor.py:216 (which use 1 - 1e-9; float32 parameters
+    need the wider margin to stay inside the table after rounding).
   * config 3's N=3 directions have no reference implementation; its shapes
     run with the N=4 ZP element.
 """
@@ -20,7 +21,8 @@ import math
 
 import numpy as np
 
-RHO_LUT_CAP = 5.8 * (1.0 - 1e-9)
+# a margin that survives float32 rounding (5.8 itself would round up)
+RHO_LUT_CAP = 5.8 * (1.0 - 1e-6)
 
 
 def _torch():
@@ -46,7 +48,7 @@ def smooth(seed: int, H: int, W: int, device="cpu", dtype=None):
 
 
 def clamp_rho(rho, theta):
-    """rho <- min(rho, 0.95 U(theta), 5.8 (1 - 1e-9)) (torch, elementwise)."""
+    """rho <- min(rho, 0.95 U(theta), RHO_LUT_CAP) (torch, elementwise)."""
     torch = _torch()
     s2 = torch.sin(2.0 * theta)
     c2 = torch.cos(2.0 * theta)

@@ -394,3 +394,61 @@ def test_config4_one_image_two_passes(cuda, rng):
     pts = sample_points(rng, 1024, 1024, 24)
     ref = oracle.points(w["f"].astype(np.float64), fld, pts, iterations=2)
     assert rel_err(out[pts[:, 0], pts[:, 1]], ref) < REL_TOL
+
+
+# --- large halos (regions beyond shared memory: configs 3 and 5) ----------
+
+
+def test_large_uniform_kernel_global_regions(cuda, rng):
+    # a ~ 150 -> support half-extent ~180 px: 8x8 regions exceed 225 KB,
+    # so every tile runs through the global-memory block path
+    f = rng.random((700, 600))
+    a = np.array([150.0, 131.0, 120.0, 170.0])
+    out = rb.filter_space_invariant(f, a)
+    pts = sample_points(rng, 700, 600, 24)
+    ref = oracle.points(f, a, pts)
+    assert rel_err(out[pts[:, 0], pts[:, 1]], ref) < REL_TOL
+
+
+def _param_impulse_check(out, imp_centres, args, lut, radius):
+    for (y, x) in imp_centres:
+        ys, xs = np.mgrid[max(0, y - radius):min(out.shape[0], y + radius + 1):7,
+                          max(0, x - radius):min(out.shape[1], x + radius + 1):7]
+        fld = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries,
+                               *(v[ys, xs] for v in args))
+        fld = np.maximum(fld, rb.SCALE_FLOOR)
+        ref = np.array([oracle.kernel_values(fld[i, j], xs[i, j] - x, ys[i, j] - y)
+                        for i in range(ys.shape[0]) for j in range(ys.shape[1])]).reshape(ys.shape)
+        scale = max(np.abs(ref).max(), 1e-300)
+        assert np.abs(out[ys, xs] - ref).max() < 1e-9 * scale + 1e-15
+
+
+def test_config3_shapes_sampled_exact(cuda, rng):
+    # config 3 image and fields at 1024^2 (sigma in [1, 32], rho in [1, 6]
+    # clamped), N=4 element: mixes the shared-memory and the block path
+    torch = cuda
+    w = workloads.config3(1024, 1024, device="cuda", param_dtype=torch.float32)
+    f = torch.from_numpy(w["f"]).cuda()
+    out = rb.filter_space_variant_params(f, w["size"], w["elong"], w["orient"]).cpu().numpy()
+    lut = rb.default_lut()
+    s, r, t = (v.double().cpu().numpy() for v in (w["size"], w["elong"], w["orient"]))
+    fld = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, s, r, t)
+    big = np.argwhere(s > 0.9 * s.max())
+    extra = big[rng.choice(len(big), min(12, len(big)), replace=False)]
+    pts = sample_points(rng, 1024, 1024, 24, extra)
+    ref = oracle.points(w["f"].astype(np.float64), fld, pts)
+    assert rel_err(out[pts[:, 0], pts[:, 1]], ref) < REL_TOL
+
+
+def test_config5_fields_impulse_response(cuda, rng):
+    # config 5's field (sigma up to 256) on 4096^2 with sparse impulses: the
+    # response near each impulse is the exact kernel of each output pixel
+    torch = cuda
+    w = workloads.config5(4096, 4096, device="cuda", param_dtype=torch.float32)
+    imp = torch.zeros((4096, 4096), dtype=torch.float64, device="cuda")
+    centres = [(700, 800), (2000, 3300), (3500, 1200), (4000, 4000)]
+    for (y, x) in centres:
+        imp[y, x] = 1.0
+    out = rb.filter_space_variant_params(imp, w["size"], w["elong"], w["orient"]).cpu().numpy()
+    args = [v.double().cpu().numpy() for v in (w["size"], w["elong"], w["orient"])]
+    _param_impulse_check(out, centres, args, rb.default_lut(), 60)
