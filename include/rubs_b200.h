@@ -127,6 +127,44 @@ int rubs_b200_filter_params_host(const void *f, int f_dtype, int64_t H, int64_t 
                                  double *out);
 
 /*
+ * Row bands (multi-GPU sharding of one large image): one pass
+ * over output rows [out_row0, out_row0 + out_rows) of an H_total x W image.
+ *   f          device rows [f_row0, f_row0 + f_rows) of the image (the band
+ *              plus the halo rows received from the neighbouring ranks)
+ *   field / size, elong, orient
+ *              device rows [*_row0, ...) of the per-pixel arrays, covering
+ *              at least the output rows
+ * Rows of the image outside [f_row0, f_row0 + f_rows) read as zero, so the
+ * halo must cover the read margins of the output rows (the whole-image
+ * result is then reproduced exactly).  iterations = 1.
+ */
+int rubs_b200_filter_rows(const void *f, int f_dtype, int64_t f_row0, int64_t f_rows, int64_t W,
+                          int64_t ld_f, int64_t H_total, const double *field, int64_t field_row0,
+                          int64_t ld_field, int64_t out_row0, int64_t out_rows, double *out,
+                          int64_t ld_out, void *stream);
+int rubs_b200_filter_params_rows(const void *f, int f_dtype, int64_t f_row0, int64_t f_rows,
+                                 int64_t W, int64_t ld_f, int64_t H_total, const void *size,
+                                 const void *elong, const void *orient, int p_dtype,
+                                 int64_t p_row0, int64_t ld_p, const rubs_lut *lut,
+                                 int64_t out_row0, int64_t out_rows, double *out, int64_t ld_out,
+                                 void *stream);
+
+/*
+ * Read margins (left, right, below, above) of the floored, pass-scaled
+ * scale-vectors over rows [row0, row0 + rows) -- the reference's
+ * _read_margins (pkg/src/rubs/engine.py:247-262), exact arithmetic.  Row
+ * bands use them to size the halo exchanged between ranks.  Arrays hold
+ * global rows from row0 on; H_total is the full image height.
+ */
+int rubs_b200_read_margins(const double *field, int field_is_uniform, int64_t rows, int64_t W,
+                           int64_t ld_field, int64_t H_total, int64_t row0, int iterations,
+                           int *out4, void *stream);
+int rubs_b200_read_margins_params(const void *size, const void *elong, const void *orient,
+                                  int p_dtype, int64_t rows, int64_t W, int64_t ld_p,
+                                  int64_t H_total, int64_t row0, const rubs_lut *lut,
+                                  int iterations, int *out4, void *stream);
+
+/*
  * Global pre-integration with the reference's canvas semantics.
  * Replaces engine.preintegrate (pkg/src/rubs/engine.py:145-201).
  * rubs_b200_preintegrate_shape returns the canvas geometry for the given

@@ -67,6 +67,14 @@ SIGNATURES = {
                                        _int, _vp, _i64, _vp]),
     "rubs_b200_filter_params_host": (_int, [_vp, _int, _i64, _i64, _vp, _vp, _vp, _int, _vp, _int,
                                             _vp]),
+    "rubs_b200_filter_rows": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64,
+                                     _i64, _vp, _i64, _vp]),
+    "rubs_b200_filter_params_rows": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _int,
+                                            _i64, _i64, _vp, _i64, _i64, _vp, _i64, _vp]),
+    "rubs_b200_read_margins": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _int,
+                                      ctypes.POINTER(_int), _vp]),
+    "rubs_b200_read_margins_params": (_int, [_vp, _vp, _vp, _int, _i64, _i64, _i64, _i64, _i64, _vp,
+                                             _int, ctypes.POINTER(_int), _vp]),
     "rubs_b200_preintegrate_shape": (_int, [_i64, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _lp,
                                             _lp, _lp, _lp]),
     "rubs_b200_preintegrate": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _i64,

@@ -698,7 +698,7 @@ __device__ __forceinline__ void nbar_arrive(int id, int n) {
 // the 0.05 floor adds at most 0.0604, the pass scaling divides by sqrt(m).
 template <int PDT>
 __device__ __forceinline__ int4 lut_margin_bound(const FieldSpec &F, int n1, int n2) {
-  const int fc = min(max(n1, 0), F.FW - 1), fr = min(max(n2, 0), F.FH - 1);
+  const int fc = min(max(n1, 0), F.FW - 1), fr = min(max(n2, 0), F.FH - 1) - F.fr_off;
   const int64_t i = (int64_t)fr * F.pld + fc;
   float sz = (float)load_px<PDT>(F.ps, i), rho = (float)load_px<PDT>(F.pr, i);
   float th = (float)load_px<PDT>(F.pt, i);
@@ -1549,6 +1549,28 @@ int run_filter(const ImageSpec &img, FieldSpec F, int iterations, double *out, i
   return status_to_code(st);
 }
 
+// One pass over output rows [out_row0, out_row0 + out_rows) of an image
+// whose rows [I.row0, I.row0 + I.h) are given (row bands);
+// field / parameter arrays hold global rows from F.fr_off on.
+int run_band(const ImageSpec &I, FieldSpec F, int64_t H_total, int64_t out_row0,
+             int64_t out_rows, double *out, int64_t ld_out, cudaStream_t s) {
+  int rc = ensure_scratch();
+  if (rc) return rc;
+  if (out_rows <= 0 || I.w == 0) return RUBS_OK;
+  if (out_row0 < 0 || out_row0 + out_rows > H_total)
+    return set_error(RUBS_EVALUE, "output rows outside the image");
+  F.FH = (int)H_total;
+  F.FW = I.w;
+  F.div = 1.0;
+  F.scaled = 0;
+  RUBS_CUDA_TRY(cudaMemsetAsync(t_scr.d_status, 0, sizeof(Status), s));
+  DomainSpec D{0, (int)out_row0, I.w, (int)out_rows, out, ld_out};
+  if ((rc = launch_pass(I, F, D, s))) return rc;
+  Status st;
+  if ((rc = finish_pass(I, F, D, s, st))) return rc;
+  return status_to_code(st);
+}
+
 // Host-buffer staging for the _host entry points (copies inside the call).
 struct HostStage {
   void *buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -1764,6 +1786,80 @@ int rubs_b200_filter_params_host(const void *f, int f_dtype, int64_t H, int64_t 
   RUBS_CUDA_TRY(cudaMemcpyAsync(out, dout, npx * 8, cudaMemcpyDeviceToHost, s));
   RUBS_CUDA_TRY(cudaStreamSynchronize(s));
   return RUBS_OK;
+}
+
+int rubs_b200_filter_rows(const void *f, int f_dtype, int64_t f_row0, int64_t f_rows, int64_t W,
+                          int64_t ld_f, int64_t H_total, const double *field, int64_t field_row0,
+                          int64_t ld_field, int64_t out_row0, int64_t out_rows, double *out,
+                          int64_t ld_out, void *stream) {
+  if (f_dtype != RUBS_F32 && f_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  ImageSpec I{f, f_dtype, ld_f, (int)f_rows, (int)W, 0, (int)f_row0};
+  FieldSpec F{};
+  F.mode = kModeField;
+  F.a = field;
+  F.ld = ld_field;
+  F.fr_off = (int)field_row0;
+  return run_band(I, F, H_total, out_row0, out_rows, out, ld_out, static_cast<cudaStream_t>(stream));
+}
+
+int rubs_b200_filter_params_rows(const void *f, int f_dtype, int64_t f_row0, int64_t f_rows,
+                                 int64_t W, int64_t ld_f, int64_t H_total, const void *size,
+                                 const void *elong, const void *orient, int p_dtype,
+                                 int64_t p_row0, int64_t ld_p, const rubs_lut *lut,
+                                 int64_t out_row0, int64_t out_rows, double *out, int64_t ld_out,
+                                 void *stream) {
+  if (f_dtype != RUBS_F32 && f_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (p_dtype != RUBS_F32 && p_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (!lut) return set_error(RUBS_EVALUE, "lut is NULL");
+  ImageSpec I{f, f_dtype, ld_f, (int)f_rows, (int)W, 0, (int)f_row0};
+  FieldSpec F = lut_field(lut, size, elong, orient, p_dtype, ld_p);
+  F.fr_off = (int)p_row0;
+  return run_band(I, F, H_total, out_row0, out_rows, out, ld_out, static_cast<cudaStream_t>(stream));
+}
+
+// _read_margins (engine.py:247-262) over rows [row0, row0 + rows) of a field
+// or parameter set: out4 = (left, right, below, above), reference arithmetic.
+static int read_margins(FieldSpec F, int64_t rows, int64_t W, int64_t H_total, int64_t row0,
+                        int iterations, int *out4, cudaStream_t s) {
+  int rc = ensure_scratch();
+  if (rc) return rc;
+  if (iterations < 1) return set_error(RUBS_EVALUE, "iterations must be >= 1");
+  F.FH = (int)H_total;
+  F.FW = (int)W;
+  F.fr_off = (int)row0;
+  F.div = std::sqrt((double)iterations);
+  F.scaled = iterations > 1;
+  RUBS_CUDA_TRY(cudaMemsetAsync(t_scr.d_status, 0, sizeof(Status), s));
+  DomainSpec D{0, (int)row0, (int)W, (int)rows, nullptr, 0};
+  if (rows > 0 && W > 0 && (rc = launch_global_margins(F, D, s))) return rc;
+  Status st;
+  if ((rc = fetch_status(s, st))) return rc;
+  for (int k = 0; k < 4; ++k) out4[k] = st.gm[k];
+  return status_to_code(st);
+}
+
+int rubs_b200_read_margins(const double *field, int field_is_uniform, int64_t rows, int64_t W,
+                           int64_t ld_field, int64_t H_total, int64_t row0, int iterations,
+                           int *out4, void *stream) {
+  FieldSpec F{};
+  if (field_is_uniform) {
+    F.mode = kModeUniform;
+    for (int k = 0; k < 4; ++k) F.u[k] = field[k];
+  } else {
+    F.mode = kModeField;
+    F.a = field;
+    F.ld = ld_field;
+  }
+  return read_margins(F, rows, W, H_total, row0, iterations, out4, static_cast<cudaStream_t>(stream));
+}
+
+int rubs_b200_read_margins_params(const void *size, const void *elong, const void *orient,
+                                  int p_dtype, int64_t rows, int64_t W, int64_t ld_p,
+                                  int64_t H_total, int64_t row0, const rubs_lut *lut,
+                                  int iterations, int *out4, void *stream) {
+  if (!lut) return set_error(RUBS_EVALUE, "lut is NULL");
+  FieldSpec F = lut_field(lut, size, elong, orient, p_dtype, ld_p);
+  return read_margins(F, rows, W, H_total, row0, iterations, out4, static_cast<cudaStream_t>(stream));
 }
 
 int rubs_b200_preintegrate_shape(int64_t h, int64_t w, int64_t col0, int64_t row0,

@@ -62,6 +62,7 @@ struct FieldSpec {
   double rho_max, log_rho_max, inv_log_rho_max;
   double rho_lim;  // rho_max * (1 + 1e-12)
   int FH, FW;      // field grid, edge-clamped (np.pad mode="edge", engine.py:306-314)
+  int fr_off;      // global row of the first row held in the arrays (row bands)
   double div;      // sqrt(iterations), engine.py:293
   int scaled;      // iterations > 1
 };
@@ -186,7 +187,7 @@ template <int MODE>
 __device__ __forceinline__ void field_at(const FieldSpec &F, int n1, int n2, double a[4],
                                          unsigned &flags) {
   const int fc = min(max(n1, 0), F.FW - 1);
-  const int fr = min(max(n2, 0), F.FH - 1);
+  const int fr = min(max(n2, 0), F.FH - 1) - F.fr_off;
   field_raw<MODE>(F, fr, fc, a, flags);
 #pragma unroll
   for (int k = 0; k < 4; ++k) {

@@ -452,3 +452,29 @@ def test_config5_fields_impulse_response(cuda, rng):
     out = rb.filter_space_variant_params(imp, w["size"], w["elong"], w["orient"]).cpu().numpy()
     args = [v.double().cpu().numpy() for v in (w["size"], w["elong"], w["orient"])]
     _param_impulse_check(out, centres, args, rb.default_lut(), 60)
+
+
+# --- row bands (multi-GPU partition, emulated rank by rank on one GPU) -----
+
+
+def test_row_bands_reproduce_whole_image_bitwise(cuda):
+    torch = cuda
+    from paper_1003_2022_b200 import sharding
+    H, W = 1024, 768
+    w = workloads.config2(H, W, device="cuda", param_dtype=torch.float32)
+    f = torch.from_numpy(w["f"]).cuda()
+    params = (w["size"], w["elong"], w["orient"])
+    whole = rb.filter_space_variant_params(f, *params)
+    lut = rb.default_lut()
+    for world in (2, 3, 8):
+        parts = []
+        for band in sharding.band_bounds(H, world):
+            pb = [p[band[0]:band[1]] for p in params]
+            m = sharding.read_margins_params(*pb, band[0], H)
+            fld = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries,
+                                   *(p.double().cpu().numpy() for p in pb))
+            assert tuple(m) == port.read_margins(np.maximum(fld, rb.SCALE_FLOOR))
+            n0, n1 = sharding.needed_rows(band, m, H)
+            parts.append(sharding.filter_rows_params(f[n0:n1], n0, H, *pb, band[0], band[0],
+                                                     band[1] - band[0]))
+        assert torch.equal(torch.cat(parts), whole)
