@@ -167,6 +167,12 @@ __device__ __forceinline__ void group_sync() {
     asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
 }
 
+// Region row pitch (doubles): >= RW and = 4 (mod 16).  With the 4x8-pixel
+// warp shape of the gather, the rows a half-warp reads are about one pitch
+// apart, i.e. 4 bank pairs apart, so its 16 near-consecutive taps spread over
+// all 16 bank pairs.  All sweeps are conflict-free for any pitch.
+__host__ __device__ __forceinline__ int region_pitch(int RW) { return RW + ((20 - (RW & 15)) & 15); }
+
 template <int DT, int NT>
 __device__ __forceinline__ void load_region(double *S, int P, const ImageSpec &I, int rc0,
                                             int rr0, int RW, int RH, int tid) {
@@ -242,45 +248,56 @@ __device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, 
                                               int tid) {
   constexpr int nt = NT, nw = NT >> 5;
   const int warp = tid >> 5, lane = tid & 31;
-  // RS1: along +x (one thread per row)
+  // RS1: along +x, one thread per row.  Thread r runs s_r = (P-1) r mod 16
+  // steps late, so at every step the 16 rows of a half-warp touch bank pair
+  // (r + step) mod 16 -- conflict-free for any pitch.
   for (int r = tid; r < RH; r += nt) {
-    double *p = S + r * P;
+    const int sk = ((P - 1) * r) & 15;
+    double *p = S + r * P - sk;  // p[j] = column j - sk
+    const unsigned span = (unsigned)RW;
     double s = 0.0;
-    int c = 0;
-    for (; c + 4 <= RW; c += 4) {
-      const double v0 = p[c], v1 = p[c + 1], v2 = p[c + 2], v3 = p[c + 3];
-      s += v0; p[c] = s;
-      s += v1; p[c + 1] = s;
-      s += v2; p[c + 2] = s;
-      s += v3; p[c + 3] = s;
-    }
-    for (; c < RW; ++c) {
-      s += p[c];
-      p[c] = s;
+    for (int j = 0; j < RW + 15; j += 4) {
+      double v[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ok[u] = (unsigned)(j + u - sk) < span;
+        v[u] = ok[u] ? p[j + u] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s += v[u];
+        if (ok[u]) p[j + u] = s;
+      }
     }
   }
   group_sync<NT, BAR>();
   // RS2: g[r][c] += g[r-1][c-1]; lines k = c - r in [-(RH-1), RW-1].
-  // Lane = line, rows advance together inside a warp (consecutive shared
-  // addresses); each lane's valid rows are one contiguous range.
+  // Lane = line, all lanes of a warp on the same row: consecutive columns;
+  // lane k is active on rows [ta, tb] of its line.
   const int nlines = RH + RW - 1;
   for (int lb = warp * 32; lb < nlines; lb += nw * 32) {
-    const int k = lb - (RH - 1) + lane;
-    const int ta = max(0, -k), tb = min(RH - 1, RW - 1 - k);
+    const int kb = lb - (RH - 1), k = kb + lane;
+    const int t0 = max(0, -(kb + 31)), t1 = min(RH - 1, RW - 1 - kb);
+    const int ta = max(t0, -k), tb = min(t1, RW - 1 - k);
+    const unsigned span = (unsigned)(tb - ta);
+    const bool any = tb >= ta;
+    double *p = S + t0 * (P + 1) + k;
+    const int st = P + 1;
     double s = 0.0;
-    double *p = S + ta * P + ta + k;
-    int t = ta;
-    for (; t + 4 <= tb + 1; t += 4) {
-      const double v0 = p[0], v1 = p[P + 1], v2 = p[2 * (P + 1)], v3 = p[3 * (P + 1)];
-      s += v0; p[0] = s;
-      s += v1; p[P + 1] = s;
-      s += v2; p[2 * (P + 1)] = s;
-      s += v3; p[3 * (P + 1)] = s;
-      p += 4 * (P + 1);
-    }
-    for (; t <= tb; ++t, p += P + 1) {
-      s += *p;
-      *p = s;
+    for (int t = t0; t <= t1; t += 4, p += 4 * st) {
+      double v[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ok[u] = any && (unsigned)(t + u - ta) <= span;
+        v[u] = ok[u] ? p[u * st] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s += v[u];
+        if (ok[u]) p[u * st] = s;
+      }
     }
   }
   group_sync<NT, BAR>();
@@ -303,31 +320,34 @@ __device__ __forceinline__ void region_sweeps(double *S, int P, int RW, int RH, 
     }
   }
   group_sync<NT, BAR>();
-  // RS4: g[r][c] += g[r-1][c+1]; lines k = c + r in [0, RH+RW-2]
+  // RS4: g[r][c] += g[r-1][c+1]; lines k = c + r in [0, RH+RW-2], lane =
+  // line, all lanes of a warp on the same row.
   unsigned gh = 0;
   for (int kb = warp * 32; kb < nlines; kb += nw * 32) {
     const int k = kb + lane;
-    const int ta = max(0, k - (RW - 1)), tb = min(RH - 1, k);
+    const int t0 = max(0, kb - (RW - 1)), t1 = min(RH - 1, kb + 31);
+    const int ta = max(t0, k - (RW - 1)), tb = min(t1, k);
+    const unsigned span = (unsigned)(tb - ta);
+    const bool any = tb >= ta;
+    const int st = P - 1;
+    double *p = S + t0 * st + k;
     double s = 0.0;
-    double *p = S + ta * P + (k - ta);
-    int t = ta;
-    for (; t + 4 <= tb + 1; t += 4) {
-      const double v0 = p[0], v1 = p[P - 1], v2 = p[2 * (P - 1)], v3 = p[3 * (P - 1)];
-      s += v0; p[0] = s;
-      const unsigned h0 = (unsigned)__double2hiint(s);
-      s += v1; p[P - 1] = s;
-      const unsigned h1 = (unsigned)__double2hiint(s);
-      s += v2; p[2 * (P - 1)] = s;
-      const unsigned h2 = (unsigned)__double2hiint(s);
-      s += v3; p[3 * (P - 1)] = s;
-      const unsigned h3 = (unsigned)__double2hiint(s);
-      gh = max(gh, max(max(h0 & 0x7fffffffu, h1 & 0x7fffffffu), max(h2 & 0x7fffffffu, h3 & 0x7fffffffu)));
-      p += 4 * (P - 1);
-    }
-    for (; t <= tb; ++t, p += P - 1) {
-      s += *p;
-      *p = s;
-      gh = max(gh, (unsigned)__double2hiint(s) & 0x7fffffffu);
+    for (int t = t0; t <= t1; t += 4, p += 4 * st) {
+      double v[4];
+      bool ok[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        ok[u] = any && (unsigned)(t + u - ta) <= span;
+        v[u] = ok[u] ? p[u * st] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        s += v[u];
+        if (ok[u]) {
+          p[u * st] = s;
+          gh = max(gh, (unsigned)__double2hiint(s) & 0x7fffffffu);
+        }
+      }
     }
   }
   ghi = max(ghi, gh);
@@ -488,7 +508,7 @@ __device__ __forceinline__ bool plan_unit(const PlanCtx &pc, const DomainSpec &D
   const float mn = (float)min(RW, RH);
   const float l4 = 0.25f * (float)RW * (float)RH * mn * mn;
   d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
-  fits = (RW | 1) * RH <= region_cap;
+  fits = region_pitch(RW) * RH <= region_cap;
   return fits && wm * l4 <= kPrecisionBudget;
 }
 
@@ -505,14 +525,24 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
                                              int region_cap, int *ovf_list, Status *st,
                                              double *S, unsigned &ghi, unsigned &flags) {
   constexpr int PPT = 1024 / NT;   // pixels per thread
-  constexpr int RS = NT / 32;      // row stride between a thread's pixels
+  constexpr int NW = NT / 32;      // warps
   __shared__ PlanCtx s_pc;
   __shared__ int s_plan[16][8];
   __shared__ int s_nsub;
   const int tid = threadIdx.x;
   const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x0 = tx * kTile, y0 = ty * kTile;
-  const int lx = tid & 31, ly = tid >> 5;
+  const int lane = tid & 31, warp = tid >> 5;
+  // pixel k of this thread: 4x8-pixel block b = warp + NW k of the tile
+  // (8 blocks across, 4 down); lane = column (l & 3) and row (l >> 2).
+  // With the region pitch = 4 (mod 16) a half-warp's 4 rows x 4 columns of
+  // near-consecutive taps land in distinct bank pairs (64-bit shared loads
+  // are served per half-warp): 1.66x ideal wavefronts, 2.05x for 32x1.
+  auto px_of = [&](int k, int &x, int &y) {
+    const int b = warp + NW * k;
+    x = x0 + 4 * (b & 7) + (lane & 3);
+    y = y0 + 8 * (b >> 3) + (lane >> 2);
+  };
   if (tid < 80) {
     if (tid < 64) s_pc.m[tid >> 2][tid & 3] = 0;
     else s_pc.w[tid - 64] = 0.f;
@@ -520,12 +550,14 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
   __syncthreads();
 
   // ---- A: scale-vectors (independent per pixel: all in flight), then the
-  //         per-8x8-cell maxima of the margins and of w
+  //         per-8x8-cell maxima of the margins and of w (one cell per warp
+  //         and k: a full-warp reduction)
   double av[PPT][4];
   bool valid[PPT];
 #pragma unroll
   for (int k = 0; k < PPT; ++k) {
-    const int x = x0 + lx, y = y0 + ly + RS * k;
+    int x, y;
+    px_of(k, x, y);
     valid[k] = (x < D.pw) && (y < D.ph);
     field_at<MODE>(F, D.pc_lo + min(x, D.pw - 1), D.pr_lo + min(y, D.ph - 1), av[k], flags);
   }
@@ -537,21 +569,19 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
       m = pixel_margins_fast(av[k]);
       w = 1.0f / (float)(av[k][0] * av[k][1] * av[k][2] * av[k][3]);
     }
-#pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      m.x = max(m.x, __shfl_xor_sync(0xffffffffu, m.x, o));
-      m.y = max(m.y, __shfl_xor_sync(0xffffffffu, m.y, o));
-      m.z = max(m.z, __shfl_xor_sync(0xffffffffu, m.z, o));
-      m.w = max(m.w, __shfl_xor_sync(0xffffffffu, m.w, o));
-      w = fmaxf(w, __shfl_xor_sync(0xffffffffu, w, o));
-    }
-    if ((lx & 7) == 0) {
-      const int c = ((ly + RS * k) >> 3) * 4 + (lx >> 3);
+    m.x = __reduce_max_sync(0xffffffffu, m.x);
+    m.y = __reduce_max_sync(0xffffffffu, m.y);
+    m.z = __reduce_max_sync(0xffffffffu, m.z);
+    m.w = __reduce_max_sync(0xffffffffu, m.w);
+    const int wi = __reduce_max_sync(0xffffffffu, __float_as_int(w));  // w >= 0
+    if (lane == 0) {
+      const int b = warp + NW * k;
+      const int c = (b >> 3) * 4 + ((b & 7) >> 1);
       atomicMax(&s_pc.m[c][0], m.x);
       atomicMax(&s_pc.m[c][1], m.y);
       atomicMax(&s_pc.m[c][2], m.z);
       atomicMax(&s_pc.m[c][3], m.w);
-      atomicMax(reinterpret_cast<int *>(&s_pc.w[c]), __float_as_int(w));
+      atomicMax(reinterpret_cast<int *>(&s_pc.w[c]), wi);
     }
   }
   __syncthreads();
@@ -604,7 +634,7 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
   for (int si = 0; si < nsub; ++si) {
     const int sx = s_plan[si][0], sy = s_plan[si][1], sw = s_plan[si][2], sh = s_plan[si][3];
     const int left = s_plan[si][4], below = s_plan[si][5], RW = s_plan[si][6], RH = s_plan[si][7];
-    const int P = RW | 1;
+    const int P = region_pitch(RW);
     // ---- B: region load + running sums
     const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
     load_region<DT, NT>(S, P, I, rc0, rr0, RW, RH, tid);
@@ -614,7 +644,8 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
     const uint32_t Sb = sbase - (uint32_t)((rr0 * P + rc0) * 8);
 #pragma unroll 1
     for (int k = 0; k < PPT; ++k) {
-      const int x = x0 + lx, y = y0 + ly + RS * k;
+      int x, y;
+      px_of(k, x, y);
       if (valid[k] && x >= sx && x < sx + sw && y >= sy && y < sy + sh) {
         const int n1 = D.pc_lo + x, n2 = D.pr_lo + y;
         double ak[4];
@@ -798,7 +829,7 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
           for (int j = 0; j < 4; ++j) u[j] = max(u[j], s_m[q][j]);
         const int RW = tw + u[0] + u[1], RH = th + u[2] + u[3];
         int n = 0;
-        if ((RW | 1) * RH <= kPipeBuf) {
+        if (region_pitch(RW) * RH <= kPipeBuf) {
           int *d = s_u[n++];
           d[0] = x0; d[1] = y0; d[2] = tw; d[3] = th; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
         } else {
@@ -811,7 +842,7 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
             d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = s_m[q][0]; d[5] = s_m[q][2];
             d[6] = sw + s_m[q][0] + s_m[q][1];
             d[7] = sh + s_m[q][2] + s_m[q][3];
-            fits = fits && ((d[6] | 1) * d[7] <= kPipeBuf);
+            fits = fits && (region_pitch(d[6]) * d[7] <= kPipeBuf);
           }
           if (!fits) {
             OvfRec r;
@@ -829,7 +860,7 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
       for (int ui = 0; ui < nu; ++ui) {
         const int sx = s_u[ui][0], sy = s_u[ui][1], sw = s_u[ui][2], sh = s_u[ui][3];
         const int left = s_u[ui][4], below = s_u[ui][5], RW = s_u[ui][6], RH = s_u[ui][7];
-        const int P = RW | 1;
+        const int P = region_pitch(RW);
         const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
         if (used[buf]) nbar_sync(kBarEmpty + buf, kPipeProd + kPipeCons);
         double *B = S + buf * kPipeBuf;
@@ -1340,7 +1371,7 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
   for (const OvfRec &r : recs) {
     const int x0 = (r.tile % tiles_x) * kTile, y0 = (r.tile / tiles_x) * kTile;
     const int tw = std::min(kTile, D.pw - x0), th = std::min(kTile, D.ph - y0);
-    if (((std::min(8, tw) + r.m[0] + r.m[1]) | 1) * (std::min(8, th) + r.m[2] + r.m[3]) <= cap_large) {
+    if (region_pitch(std::min(8, tw) + r.m[0] + r.m[1]) * (std::min(8, th) + r.m[2] + r.m[3]) <= cap_large) {
       smem_list.push_back(r.tile);
       continue;
     }
