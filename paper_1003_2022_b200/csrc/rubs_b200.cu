@@ -755,10 +755,35 @@ __device__ __forceinline__ int4 lut_margin_bound(const FieldSpec &F, int n1, int
 
 struct UnitPlan {
   int sx, sy, sw, sh;  // output rectangle (pass-domain pixels)
-  int RW, RH, P;       // region width, rows, pitch
-  int rc0, rr0;        // lattice of region element (0, 0)
-  int end;
+  int P, rc0, rr0;     // region pitch and lattice of element (0, 0)
+  int nbx, nblk;       // 4x8 blocks across, total (-1: end of work)
+  int tile;
+  int m[4];            // unit margins (for a precision re-run)
+  float l4;            // region L4 (precision model)
 };
+
+// Precision guard of the pipeline: a consumer whose pixel's w * L4 exceeds
+// the budget in the unit's region flags the unit (max w in s_pw[buf]); the
+// producer, reclaiming the buffer, records the unit's tile once for the
+// overflow pass, which recomputes it with precision-split regions.  At most
+// four records per tile (one per unit).
+__device__ __forceinline__ void pipe_precision_flag(const UnitPlan &up, const double a[4],
+                                                    int *pw) {
+  const float w = 1.0f / (float)(a[0] * a[1] * a[2] * a[3]);
+  if (w * up.l4 > kPrecisionBudget) atomicMax(pw, __float_as_int(w));
+}
+
+__device__ __forceinline__ void pipe_reclaim(const UnitPlan &up, int *pw, int *ovf_list,
+                                             Status *st) {
+  if (*pw) {
+    OvfRec r;
+    r.tile = up.tile;
+    for (int j = 0; j < 4; ++j) r.m[j] = up.m[j];
+    r.w = __int_as_float(*pw);
+    reinterpret_cast<OvfRec *>(ovf_list)[atomicAdd(&st->ovf_count, 1)] = r;
+    *pw = 0;
+  }
+}
 
 template <int MODE, int DT>
 __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
@@ -769,8 +794,12 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
   __shared__ int s_m[4][4];
   __shared__ int s_u[4][8];
   __shared__ int s_nu;
+  __shared__ int s_pw[2];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned ghi = 0, flags = 0;
+  constexpr int NB = kPipeProd + kPipeCons;
+  if (tid < 2) s_pw[tid] = 0;
+  __syncthreads();
 
   if (warp < kPipeProd / 32) {
     // ================================================================ producer
@@ -862,51 +891,74 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
         const int left = s_u[ui][4], below = s_u[ui][5], RW = s_u[ui][6], RH = s_u[ui][7];
         const int P = region_pitch(RW);
         const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
-        if (used[buf]) nbar_sync(kBarEmpty + buf, kPipeProd + kPipeCons);
+        if (used[buf]) {
+          nbar_sync(kBarEmpty + buf, NB);
+          if (tid == 0) pipe_reclaim(plan[buf], &s_pw[buf], ovf_list, st);
+        }
         double *B = S + buf * kPipeBuf;
         load_region<DT, kPipeProd>(B, P, I, rc0, rr0, RW, RH, tid);
         if (tid == 0) {
           UnitPlan up;
           up.sx = sx; up.sy = sy; up.sw = sw; up.sh = sh;
-          up.RW = RW; up.RH = RH; up.P = P; up.rc0 = rc0; up.rr0 = rr0; up.end = 0;
+          up.P = P; up.rc0 = rc0; up.rr0 = rr0;
+          up.nbx = (sw + 3) / 4;
+          up.nblk = up.nbx * ((sh + 7) / 8);
+          up.tile = tile;
+          up.m[0] = left; up.m[1] = RW - sw - left; up.m[2] = below; up.m[3] = RH - sh - below;
+          const float mn = (float)min(RW, RH);
+          up.l4 = 0.25f * (float)RW * (float)RH * mn * mn;
           plan[buf] = up;
         }
         nbar_sync(kBarProd, kPipeProd);
         region_sweeps<kPipeProd, kBarProd>(B, P, RW, RH, ghi, tid);
         __threadfence_block();
-        nbar_arrive(kBarFull + buf, kPipeProd + kPipeCons);
+        nbar_arrive(kBarFull + buf, NB);
         used[buf] = true;
         buf ^= 1;
       }
     }
-    // end of work: marker through the next buffer, then balance EMPTY arrivals
-    if (used[buf]) nbar_sync(kBarEmpty + buf, kPipeProd + kPipeCons);
-    if (tid == 0) plan[buf].end = 1;
+    // end of work through the next buffer; balance the EMPTY arrivals
+    if (used[buf]) {
+      nbar_sync(kBarEmpty + buf, NB);
+      if (tid == 0) pipe_reclaim(plan[buf], &s_pw[buf], ovf_list, st);
+    }
+    if (tid == 0) plan[buf].nblk = -1;
     __threadfence_block();
-    nbar_arrive(kBarFull + buf, kPipeProd + kPipeCons);
-    if (used[buf ^ 1]) nbar_sync(kBarEmpty + (buf ^ 1), kPipeProd + kPipeCons);
+    nbar_arrive(kBarFull + buf, NB);
+    if (used[buf ^ 1]) {
+      nbar_sync(kBarEmpty + (buf ^ 1), NB);
+      if (tid == 0) pipe_reclaim(plan[buf ^ 1], &s_pw[buf ^ 1], ovf_list, st);
+    }
   } else {
     // ================================================================ consumer
-    const int ctid = tid - kPipeProd;
+    // the 4x8-pixel blocks of all units form one stream; consumer warp cw
+    // takes blocks cw, cw + 12, cw + 24, ... of it
+    constexpr int NCW = kPipeCons / 32;
+    const int cw = warp - kPipeProd / 32;
     const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S);
-    int buf = 0;
+    int buf = 0, cum = 0;
     for (;;) {
-      nbar_sync(kBarFull + buf, kPipeProd + kPipeCons);
+      nbar_sync(kBarFull + buf, NB);
       const UnitPlan up = plan[buf];
-      if (up.end) break;
+      if (up.nblk < 0) break;
       const uint32_t Sb = sbase + (uint32_t)(buf * kPipeBuf) * 8u -
                           (uint32_t)((up.rr0 * up.P + up.rc0) * 8);
-      const int n = up.sw * up.sh;
+      int j = cum + (((cw - cum) % NCW) + NCW) % NCW;
 #pragma unroll 1
-      for (int p = ctid; p < n; p += kPipeCons) {
-        const int yy = p / up.sw, xx = p - yy * up.sw;
-        const int x = up.sx + xx, y = up.sy + yy;
-        const int n1 = D.pc_lo + x, n2 = D.pr_lo + y;
-        double a[4];
-        field_at<MODE>(F, n1, n2, a, flags);
-        D.out[(int64_t)y * D.ld_out + x] = pixel_fd(Sb, up.P, n1, n2, a);
+      for (; j < cum + up.nblk; j += NCW) {
+        const int b = j - cum;
+        const int by = b / up.nbx, bx = b - by * up.nbx;
+        const int x = up.sx + 4 * bx + (lane & 3), y = up.sy + 8 * by + (lane >> 2);
+        if (x < up.sx + up.sw && y < up.sy + up.sh) {
+          const int n1 = D.pc_lo + x, n2 = D.pr_lo + y;
+          double a[4];
+          field_at<MODE>(F, n1, n2, a, flags);
+          pipe_precision_flag(up, a, &s_pw[buf]);
+          D.out[(int64_t)y * D.ld_out + x] = pixel_fd(Sb, up.P, n1, n2, a);
+        }
       }
-      nbar_arrive(kBarEmpty + buf, kPipeProd + kPipeCons);
+      cum += up.nblk;
+      nbar_arrive(kBarEmpty + buf, NB);
       buf ^= 1;
     }
   }
@@ -1355,10 +1407,21 @@ int upload(std::vector<V> &h, V *&d, size_t &cap, cudaStream_t s) {
 template <int M, int T>
 int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int n_ovf,
                     cudaStream_t s) {
-  std::vector<OvfRec> recs(n_ovf);
-  RUBS_CUDA_TRY(cudaMemcpyAsync(recs.data(), t_scr.d_ovf, n_ovf * sizeof(OvfRec),
+  std::vector<OvfRec> raw(n_ovf);
+  RUBS_CUDA_TRY(cudaMemcpyAsync(raw.data(), t_scr.d_ovf, n_ovf * sizeof(OvfRec),
                                 cudaMemcpyDeviceToHost, s));
   RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+  // one record per tile (the pipeline records a tile once per unit)
+  std::sort(raw.begin(), raw.end(), [](const OvfRec &a, const OvfRec &b) { return a.tile < b.tile; });
+  std::vector<OvfRec> recs;
+  for (const OvfRec &r : raw) {
+    if (!recs.empty() && recs.back().tile == r.tile) {
+      for (int j = 0; j < 4; ++j) recs.back().m[j] = std::max(recs.back().m[j], r.m[j]);
+      recs.back().w = std::max(recs.back().w, r.w);
+    } else {
+      recs.push_back(r);
+    }
+  }
   const int tiles_x = (D.pw + kTile - 1) / kTile;
   std::vector<int> smem_list;
   struct Blk {
@@ -1489,11 +1552,12 @@ int launch_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cud
     TimedLaunch tl(0, s);
     const int m = F.mode, t = I.dt;
     const size_t ntiles = (size_t)((D.pw + kTile - 1) / kTile) * ((D.ph + kTile - 1) / kTile);
-    if (ntiles > t_scr.ovf_cap) {
+    // at most one record per tile (tile kernel) or per unit (pipeline)
+    if (4 * ntiles > t_scr.ovf_cap) {
       if (t_scr.d_ovf) cudaFree(t_scr.d_ovf);
       t_scr.d_ovf = nullptr;
-      RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_ovf, ntiles * sizeof(OvfRec)));
-      t_scr.ovf_cap = ntiles;
+      RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_ovf, 4 * ntiles * sizeof(OvfRec)));
+      t_scr.ovf_cap = 4 * ntiles;
     }
     if (m == kModeField) {
       if (t) launch_tiles<kModeField, 1>(I, F, D, s); else launch_tiles<kModeField, 0>(I, F, D, s);
