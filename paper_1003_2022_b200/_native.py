@@ -15,7 +15,8 @@ import subprocess
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _REPO = os.path.dirname(_PKG)
 LIB_DIR = os.path.join(_PKG, "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "librubs_b200.so")
+# RUBS_B200_LIB: load an alternative build (A/B experiments; see build_native)
+LIB_PATH = os.environ.get("RUBS_B200_LIB") or os.path.join(LIB_DIR, "librubs_b200.so")
 CSRC = os.path.join(_PKG, "csrc")
 INCLUDE = os.path.join(_REPO, "include")
 
@@ -29,16 +30,19 @@ RUBS_OK, RUBS_EVALUE, RUBS_EOVERFLOW, RUBS_EOUTOFGRID, RUBS_ECUDA, RUBS_EUNSUPPO
 RUBS_F32, RUBS_F64 = 0, 1
 
 
-def build_native(verbose: bool = False) -> str:
-    """Compile csrc/*.cu into the in-tree shared library (sm_100a)."""
+def build_native(verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile csrc/*.cu into the in-tree shared library (sm_100a).
+    ``defines``/``out`` build a variant library for A/B runs."""
     os.makedirs(LIB_DIR, exist_ok=True)
+    out = out or LIB_PATH
     srcs = [os.path.join(CSRC, "rubs_b200.cu")]
-    cmd = ["nvcc", *NVCC_FLAGS, "-I", INCLUDE, "-o", LIB_PATH + ".tmp", *srcs]
+    cmd = ["nvcc", *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", INCLUDE, "-o", out + ".tmp",
+           *srcs]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)
-    os.replace(LIB_PATH + ".tmp", LIB_PATH)
-    return LIB_PATH
+    os.replace(out + ".tmp", out)
+    return out
 
 
 _lib = None

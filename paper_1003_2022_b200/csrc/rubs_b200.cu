@@ -18,7 +18,9 @@
 //   * Each pixel then takes its 16-vertex finite difference (engine.py:232-244)
 //     reading the region through the 7-tap ZP interpolant (zp.py:186-228) in
 //     one canonical-wedge form (rubs_device.cuh: zp_read8).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <atomic>
@@ -148,14 +150,10 @@ __global__ void __launch_bounds__(256) global_margins_kernel(FieldSpec F, Domain
 
 // Load the image over region lattice [rc0, rc0+RW) x [rr0, rr0+RH) into
 // shared memory as fp64, zero outside the image (zero padding, engine.py:155).
-// float64 images: asynchronous global->shared copies (cp.async, LDGSTS), the
-// zero fill of out-of-image elements done by the same instruction (src-size
-// 0), so every element of the region is in flight at once.  float32 images:
-// eight loads in flight per thread, widened to fp64 on the way.
-__device__ __forceinline__ void cp_async8(uint32_t dst, const void *src, int src_bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
-               : "memory");
-}
+// float64 images: asynchronous global->shared copies (cp.async, LDGSTS) of
+// the in-image part of each row, plain zero stores outside, so every element
+// of the region is in flight at once.  float32 images: eight loads in flight
+// per thread, widened to fp64 on the way.
 
 // Synchronise the NT threads of a group: the whole CTA (BAR 0) or a named
 // barrier shared by a warp-specialised subset.
@@ -172,13 +170,85 @@ __device__ __forceinline__ void group_sync() {
 // apart, i.e. 4 bank pairs apart, so its 16 near-consecutive taps spread over
 // all 16 bank pairs.  All sweeps are conflict-free for any pitch.
 __host__ __device__ __forceinline__ int region_pitch(int RW) { return RW + ((20 - (RW & 15)) & 15); }
+// Shared-memory footprint (doubles) of an RW x RH region: rows rounded up to
+// the 8-row TMA box.
+__host__ __device__ __forceinline__ int region_elems(int RW, int RH) {
+  return region_pitch(RW) * ((RH + 7) & ~7);
+}
+// float64 regions start on an even image column (a TMA box's first column
+// must be 16-byte aligned): grow the region one column to the left when
+// needed.  Exact -- any region containing the read support is (see top).
+template <int DT>
+__device__ __forceinline__ void align_region(const ImageSpec &I, int x_lattice, int &left,
+                                             int &RW) {
+  if (DT == 1 && ((x_lattice - left - I.col0) & 1)) {
+    ++left;
+    ++RW;
+  }
+}
 
-template <int DT, int NT>
+// Tensor-memory-accelerator (TMA) region loads for float64 images: one 2-D
+// tensor map per region pitch P = 20 + 16 k (box P columns x 8 rows, so a
+// box lands with exactly the region's row pitch); out-of-image elements are
+// zero-filled by the TMA unit itself.  A region takes ceil(RH / 8) box copies
+// issued by one thread, completing on an mbarrier.  Columns [RW, P) and rows
+// [RH, ceil8(RH)) receive real image data the sweeps never read.
+constexpr int kTmaP0 = 20, kTmaMaps = 15;  // P = 20 .. 244
+struct TmaMaps {
+  CUtensorMap m[kTmaMaps];
+  unsigned valid;  // bit k: map k usable
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(mbar) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "RUBS_MBAR_WAIT%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra RUBS_MBAR_WAIT%=;\n}" ::"r"(mbar),
+      "r"(phase)
+      : "memory");
+}
+
+template <int DT, int NT, int BAR>
 __device__ __forceinline__ void load_region(double *S, int P, const ImageSpec &I, int rc0,
-                                            int rr0, int RW, int RH, int tid) {
+                                            int rr0, int RW, int RH, int tid,
+                                            const TmaMaps *tm, uint32_t mbar, uint32_t &phase) {
   constexpr int nw = NT >> 5;
   const int warp = tid >> 5, lane = tid & 31;
   const int ic0 = rc0 - I.col0, ir0 = rr0 - I.row0;
+  if constexpr (DT == 1) {
+    const int k = (P - kTmaP0) >> 4;
+    // (the box's first column must be 16-byte aligned: align_region makes
+    // ic0 even; anything else takes the copy loop below)
+    if (tm != nullptr && k < kTmaMaps && ((tm->valid >> k) & 1u) && (ic0 & 1) == 0) {
+      // order this group's earlier generic accesses of the buffer before the
+      // async-proxy writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      group_sync<NT, BAR>();
+      if (tid == 0) {
+        const int nbox = (RH + 7) >> 3;
+        const uint32_t bytes = (uint32_t)nbox * 64u * (uint32_t)P;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar),
+                     "r"(bytes)
+                     : "memory");
+        const uint32_t sb = (uint32_t)__cvta_generic_to_shared(S);
+        const uint64_t map = reinterpret_cast<uint64_t>(&tm->m[k]);
+        for (int b = 0; b < nbox; ++b)
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3}], [%4];" ::"r"(sb + (uint32_t)b * 64u * (uint32_t)P),
+              "l"(map), "r"(ic0), "r"(ir0 + 8 * b), "r"(mbar)
+              : "memory");
+      }
+      mbar_wait(mbar, phase);
+      phase ^= 1u;
+      return;
+    }
+  }
   // region columns [cl, ch) lie inside the image
   const int cl = min(RW, max(0, -ic0)), ch = max(cl, min(RW, I.w - ic0));
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(S);
@@ -505,10 +575,11 @@ __device__ __forceinline__ bool plan_unit(const PlanCtx &pc, const DomainSpec &D
     }
   const int sw = min(8 * ncell, D.pw - sx), sh = min(8 * ncell, D.ph - sy);
   const int RW = sw + u[0] + u[1], RH = sh + u[2] + u[3];
-  const float mn = (float)min(RW, RH);
-  const float l4 = 0.25f * (float)RW * (float)RH * mn * mn;
+  // (+1: the region may grow a column to start on an even image column)
+  const float mn = (float)min(RW + 1, RH);
+  const float l4 = 0.25f * (float)(RW + 1) * (float)RH * mn * mn;
   d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
-  fits = region_pitch(RW) * RH <= region_cap;
+  fits = region_elems(RW + 1, RH) <= region_cap;
   return fits && wm * l4 <= kPrecisionBudget;
 }
 
@@ -523,7 +594,8 @@ template <int MODE, int DT, int NT>
 __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec &F,
                                              const DomainSpec &D, int tile, int tiles_x,
                                              int region_cap, int *ovf_list, Status *st,
-                                             double *S, unsigned &ghi, unsigned &flags) {
+                                             double *S, unsigned &ghi, unsigned &flags,
+                                             const TmaMaps *tm, uint32_t mbar, uint32_t &phase) {
   constexpr int PPT = 1024 / NT;   // pixels per thread
   constexpr int NW = NT / 32;      // warps
   __shared__ PlanCtx s_pc;
@@ -633,11 +705,13 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
   const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S);
   for (int si = 0; si < nsub; ++si) {
     const int sx = s_plan[si][0], sy = s_plan[si][1], sw = s_plan[si][2], sh = s_plan[si][3];
-    const int left = s_plan[si][4], below = s_plan[si][5], RW = s_plan[si][6], RH = s_plan[si][7];
+    const int below = s_plan[si][5], RH = s_plan[si][7];
+    int left = s_plan[si][4], RW = s_plan[si][6];
+    align_region<DT>(I, D.pc_lo + sx, left, RW);
     const int P = region_pitch(RW);
     // ---- B: region load + running sums
     const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
-    load_region<DT, NT>(S, P, I, rc0, rr0, RW, RH, tid);
+    load_region<DT, NT, 0>(S, P, I, rc0, rr0, RW, RH, tid, tm, mbar, phase);
     __syncthreads();
     region_sweeps<NT, 0>(S, P, RW, RH, ghi, tid);
     // ---- C: finite differences
@@ -676,11 +750,16 @@ __device__ __forceinline__ void flush_status(Status *st, unsigned ghi, unsigned 
 template <int MODE, int DT>
 __global__ void __launch_bounds__(kThreadsSmall, 2)
     tile_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int region_cap,
-                       int *ovf_list, Status *st) {
-  extern __shared__ double S[];
+                       int *ovf_list, Status *st, const __grid_constant__ TmaMaps tm) {
+  extern __shared__ __align__(128) double S[];
+  __shared__ uint64_t s_mbar;
+  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+  if (threadIdx.x == 0) mbar_init(mbar);
+  __syncthreads();
   unsigned ghi = 0, flags = 0;
+  uint32_t phase = 0;
   process_tile<MODE, DT, kThreadsSmall>(I, F, D, blockIdx.x, tiles_x, region_cap, ovf_list, st,
-                                        S, ghi, flags);
+                                        S, ghi, flags, &tm, mbar, phase);
   flush_status(st, ghi, flags);
 }
 
@@ -689,12 +768,18 @@ __global__ void __launch_bounds__(kThreadsSmall, 2)
 template <int MODE, int DT>
 __global__ void __launch_bounds__(kThreadsLarge, 1)
     tile_overflow_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int region_cap,
-                         const int *ovf_list, int n, Status *st) {
-  extern __shared__ double S[];
+                         const int *ovf_list, int n, Status *st,
+                         const __grid_constant__ TmaMaps tm) {
+  extern __shared__ __align__(128) double S[];
+  __shared__ uint64_t s_mbar;
+  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+  if (threadIdx.x == 0) mbar_init(mbar);
+  __syncthreads();
   unsigned ghi = 0, flags = 0;
+  uint32_t phase = 0;
   for (int i = blockIdx.x; i < n; i += gridDim.x)
     process_tile<MODE, DT, kThreadsLarge>(I, F, D, ovf_list[i], tiles_x, region_cap, nullptr, st,
-                                          S, ghi, flags);
+                                          S, ghi, flags, &tm, mbar, phase);
   flush_status(st, ghi, flags);
 }
 
@@ -709,8 +794,11 @@ __global__ void __launch_bounds__(kThreadsLarge, 1)
 // its 16-vertex finite differences.  Hand-off through named barriers:
 // FULL[b] (producers arrive, consumers wait), EMPTY[b] (the reverse).
 
-constexpr int kPipeProd = 128;                  // producer threads
-constexpr int kPipeCons = 384;                  // consumer threads
+#ifndef RUBS_PIPE_PROD
+#define RUBS_PIPE_PROD 256
+#endif
+constexpr int kPipeProd = RUBS_PIPE_PROD;       // producer threads
+constexpr int kPipeCons = 512 - kPipeProd;      // consumer threads
 constexpr int kPipeBuf = 112 * 1024 / 8;        // doubles per region buffer
 constexpr int kPipeSmem = 2 * kPipeBuf * 8;     // dynamic shared memory
 constexpr int kBarProd = 1, kBarFull = 2, kBarEmpty = 4;  // named barrier ids
@@ -745,12 +833,7 @@ __device__ __forceinline__ int4 lut_margin_bound(const FieldSpec &F, int n1, int
   const float k = (float)(1.0 / F.div) * 1.0002f;
   const float hx = (3.0f * sqrtf(sz * c11) * 1.001f + 0.0605f) * k;
   const float hy = (3.0f * sqrtf(sz * c22) * 1.001f + 0.0605f) * k;
-  int4 m;
-  m.x = max(0, (int)ceilf(hx + 0.5f) + 3);
-  m.y = max(0, (int)ceilf(hx - 0.5f) + 3);
-  m.z = max(0, (int)ceilf(hy + 1.5f) + 3);
-  m.w = max(0, (int)ceilf(hy - 1.5f) + 3);
-  return m;
+  return margins_from_extent(hx, hy);
 }
 
 struct UnitPlan {
@@ -788,8 +871,9 @@ __device__ __forceinline__ void pipe_reclaim(const UnitPlan &up, int *pw, int *o
 template <int MODE, int DT>
 __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
     pipe_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int ntiles,
-                       int *ovf_list, Status *st) {
-  extern __shared__ double S[];
+                       int *ovf_list, Status *st, const __grid_constant__ TmaMaps tm) {
+  extern __shared__ __align__(128) double S[];
+  __shared__ uint64_t s_mbar;
   __shared__ UnitPlan plan[2];
   __shared__ int s_m[4][4];
   __shared__ int s_u[4][8];
@@ -798,24 +882,28 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned ghi = 0, flags = 0;
   constexpr int NB = kPipeProd + kPipeCons;
+  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
   if (tid < 2) s_pw[tid] = 0;
+  if (tid == 0) mbar_init(mbar);
   __syncthreads();
 
   if (warp < kPipeProd / 32) {
     // ================================================================ producer
     int buf = 0;
+    uint32_t phase = 0;
     bool used[2] = {false, false};
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
       const int tx = tile % tiles_x, ty = tile / tiles_x;
       const int x0 = tx * kTile, y0 = ty * kTile;
       if (tid < 16) s_m[tid >> 2][tid & 3] = 0;
       nbar_sync(kBarProd, kPipeProd);
-      const int ly = tid >> 5;  // 0..3; pixel rows ly + 4k
+      constexpr int NWP = kPipeProd / 32;
+      const int ly = tid >> 5;  // pixel rows ly + NWP k
       int4 mh[2] = {make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0)};
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int x = x0 + lane, y = y0 + ly + 4 * k;
-        if (x < D.pw && y < D.ph) {
+      for (int k = 0; k < (32 + NWP - 1) / NWP; ++k) {
+        const int x = x0 + lane, y = y0 + ly + NWP * k;
+        if (ly + NWP * k < kTile && x < D.pw && y < D.ph) {
           int4 m;
           if constexpr (MODE >= kModeLut) {
             m = lut_margin_bound<MODE == kModeLut ? 1 : 0>(F, D.pc_lo + x, D.pr_lo + y);
@@ -825,7 +913,7 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
             field_at<MODE>(F, D.pc_lo + x, D.pr_lo + y, a, fl);
             m = pixel_margins_fast(a);
           }
-          const int h = k >= 4 ? 1 : 0;
+          const int h = (ly + NWP * k) >= 16 ? 1 : 0;
           mh[h].x = max(mh[h].x, m.x);
           mh[h].y = max(mh[h].y, m.y);
           mh[h].z = max(mh[h].z, m.z);
@@ -858,7 +946,7 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
           for (int j = 0; j < 4; ++j) u[j] = max(u[j], s_m[q][j]);
         const int RW = tw + u[0] + u[1], RH = th + u[2] + u[3];
         int n = 0;
-        if (region_pitch(RW) * RH <= kPipeBuf) {
+        if (region_elems(RW + 1, RH) <= kPipeBuf) {
           int *d = s_u[n++];
           d[0] = x0; d[1] = y0; d[2] = tw; d[3] = th; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
         } else {
@@ -871,7 +959,7 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
             d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = s_m[q][0]; d[5] = s_m[q][2];
             d[6] = sw + s_m[q][0] + s_m[q][1];
             d[7] = sh + s_m[q][2] + s_m[q][3];
-            fits = fits && (region_pitch(d[6]) * d[7] <= kPipeBuf);
+            fits = fits && (region_elems(d[6] + 1, d[7]) <= kPipeBuf);
           }
           if (!fits) {
             OvfRec r;
@@ -888,7 +976,9 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
       const int nu = s_nu;
       for (int ui = 0; ui < nu; ++ui) {
         const int sx = s_u[ui][0], sy = s_u[ui][1], sw = s_u[ui][2], sh = s_u[ui][3];
-        const int left = s_u[ui][4], below = s_u[ui][5], RW = s_u[ui][6], RH = s_u[ui][7];
+        const int below = s_u[ui][5], RH = s_u[ui][7];
+        int left = s_u[ui][4], RW = s_u[ui][6];
+        align_region<DT>(I, D.pc_lo + sx, left, RW);
         const int P = region_pitch(RW);
         const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
         if (used[buf]) {
@@ -896,7 +986,7 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
           if (tid == 0) pipe_reclaim(plan[buf], &s_pw[buf], ovf_list, st);
         }
         double *B = S + buf * kPipeBuf;
-        load_region<DT, kPipeProd>(B, P, I, rc0, rr0, RW, RH, tid);
+        load_region<DT, kPipeProd, kBarProd>(B, P, I, rc0, rr0, RW, RH, tid, &tm, mbar, phase);
         if (tid == 0) {
           UnitPlan up;
           up.sx = sx; up.sy = sy; up.sw = sw; up.sh = sh;
@@ -1366,6 +1456,49 @@ int launch_global_margins(const FieldSpec &F, const DomainSpec &D, cudaStream_t 
   return RUBS_OK;
 }
 
+// Tensor maps of a float64 image for the TMA region loads (cached per image
+// geometry: encoding is a host-side call, ~1 us each).
+struct TmaCache {
+  const void *f = nullptr;
+  int64_t ld = 0;
+  int h = 0, w = 0;
+  TmaMaps maps{};
+};
+thread_local TmaCache t_tma;
+
+const TmaMaps &tma_maps(const ImageSpec &I) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &fn, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  TmaCache &c = t_tma;
+  if (c.f == I.f && c.ld == I.ld && c.h == I.h && c.w == I.w) return c.maps;
+  c.f = I.f; c.ld = I.ld; c.h = I.h; c.w = I.w;
+  c.maps.valid = 0;
+  if (std::getenv("RUBS_B200_NO_TMA")) return c.maps;
+  const bool ok = encode != nullptr && I.dt == 1 && I.w > 0 && I.h > 0 &&
+                  (reinterpret_cast<uintptr_t>(I.f) & 15) == 0 && ((I.ld * 8) & 15) == 0;
+  if (!ok) return c.maps;
+  for (int k = 0; k < kTmaMaps; ++k) {
+    const cuuint64_t dims[2] = {(cuuint64_t)I.w, (cuuint64_t)I.h};
+    const cuuint64_t strides[1] = {(cuuint64_t)I.ld * 8};
+    const cuuint32_t box[2] = {(cuuint32_t)(kTmaP0 + 16 * k), 8};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r =
+        encode(&c.maps.m[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(I.f), dims,
+               strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS) c.maps.valid |= 1u << k;
+  }
+  return c.maps;
+}
+
 int kernel_choice() {
   static int choice = -1;
   if (choice < 0) {
@@ -1382,10 +1515,10 @@ void launch_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, c
   cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s);
   if (kernel_choice() == 0)
     pipe_filter_kernel<M, T><<<std::min(ntiles, t_scr.sms), kPipeProd + kPipeCons, kPipeSmem, s>>>(
-        I, F, D, tiles_x, ntiles, t_scr.d_ovf, t_scr.d_status);
+        I, F, D, tiles_x, ntiles, t_scr.d_ovf, t_scr.d_status, tma_maps(I));
   else
     tile_filter_kernel<M, T><<<ntiles, kThreadsSmall, kSmemSmall, s>>>(
-        I, F, D, tiles_x, kSmemSmall / 8, t_scr.d_ovf, t_scr.d_status);
+        I, F, D, tiles_x, kSmemSmall / 8, t_scr.d_ovf, t_scr.d_status, tma_maps(I));
 }
 
 template <class V>
@@ -1434,7 +1567,7 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
   for (const OvfRec &r : recs) {
     const int x0 = (r.tile % tiles_x) * kTile, y0 = (r.tile / tiles_x) * kTile;
     const int tw = std::min(kTile, D.pw - x0), th = std::min(kTile, D.ph - y0);
-    if (region_pitch(std::min(8, tw) + r.m[0] + r.m[1]) * (std::min(8, th) + r.m[2] + r.m[3]) <= cap_large) {
+    if (region_elems(std::min(8, tw) + r.m[0] + r.m[1] + 1, std::min(8, th) + r.m[2] + r.m[3]) <= cap_large) {
       smem_list.push_back(r.tile);
       continue;
     }
@@ -1462,7 +1595,8 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
     if ((rc = upload(smem_list, t_scr.d_list, t_scr.list_cap, s))) return rc;
     tile_overflow_kernel<M, T><<<std::min((int)smem_list.size(), t_scr.sms), kThreadsLarge,
                                  kSmemLarge, s>>>(I, F, D, tiles_x, kSmemLarge / 8, t_scr.d_list,
-                                                  (int)smem_list.size(), t_scr.d_status);
+                                                  (int)smem_list.size(), t_scr.d_status,
+                                                  tma_maps(I));
     ++t_launches;
     RUBS_CUDA_TRY(cudaGetLastError());
   }

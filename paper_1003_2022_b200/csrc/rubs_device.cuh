@@ -227,15 +227,21 @@ __device__ __forceinline__ int4 pixel_margins(const double a[4]) {
 // below = ceil(hy + 3/2) + 2, above = ceil(hy - 3/2) + 2, computed with one
 // extra unit of slack so any rounding of the gather's own arithmetic stays
 // inside the region.
+// Tight read margins from the half-extents of the vertex cloud.  With
+// t1, t2 of pixel_fd_t, vertex x - n1 lies in [-hx - 1/2, hx - 1/2] and
+// y - n2 in [-hy - 3/2, hy - 3/2] (hx = (a1 + (a2 + a4)/sqrt2) / 2, hy the
+// same with a3); the nearest lattice point is within 1/2 of a vertex and the
+// ZP taps within 1 of it, so the taps span columns n1 - floor(hx) - 2 ..
+// n1 + floor(hx) + 1 and rows n2 - floor(hy) - 3 .. n2 + floor(hy).  The
+// 1e-6 covers the rounding of the vertex arithmetic.
+__device__ __forceinline__ int4 margins_from_extent(double hx, double hy) {
+  const int fx = (int)floor(hx + 1e-6), fy = (int)floor(hy + 1e-6);
+  return make_int4(fx + 2, fx + 1, fy + 3, fy);
+}
+
 __device__ __forceinline__ int4 pixel_margins_fast(const double a[4]) {
   const double d = (a[1] + a[3]) * kInvSqrt2;
-  const double hx = 0.5 * (a[0] + d), hy = 0.5 * (a[2] + d);
-  int4 m;
-  m.x = max(0, (int)ceil(hx + 0.5) + 3);
-  m.y = max(0, (int)ceil(hx - 0.5) + 3);
-  m.z = max(0, (int)ceil(hy + 1.5) + 3);
-  m.w = max(0, (int)ceil(hy - 1.5) + 3);
-  return m;
+  return margins_from_extent(0.5 * (a[0] + d), 0.5 * (a[2] + d));
 }
 
 // Nearest lattice point m of x and residual d = m - x (zp.py:204-210).  The

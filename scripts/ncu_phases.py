@@ -11,6 +11,9 @@ rows = list(csv.reader(raw.splitlines()))
 hdr = rows[1]
 col = {k: hdr.index(k) for k in ("Source", "Warp Stall Sampling (All Samples)", "Instructions Executed",
                                  "L1 Wavefronts Shared", "L1 Wavefronts Shared Ideal")}
+reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
+rcol = [hdr.index(h) for h in reasons]
+stalls = []
 data = []
 for r in rows[2:]:
     if len(r) <= col["Instructions Executed"]:
@@ -18,6 +21,7 @@ for r in rows[2:]:
     g = lambda k: int(r[col[k]] or 0) if r[col[k]].strip().isdigit() else 0  # noqa: E731
     data.append((r[col["Source"]], g("Warp Stall Sampling (All Samples)"), g("Instructions Executed"),
                  g("L1 Wavefronts Shared"), g("L1 Wavefronts Shared Ideal")))
+    stalls.append([int(r[c]) if r[c].strip().isdigit() else 0 for c in rcol])
 cuts = [0] + [i + 1 for i, d in enumerate(data) if "BAR.SYNC" in d[0]] + [len(data)]
 tot = sum(d[1] for d in data)
 print(f"total stall samples {tot}")
@@ -40,6 +44,11 @@ for a, b in zip(cuts[:-1], cuts[1:]):
     top = " ".join(f"{k}:{v * 32 / npx:.0f}" for k, v in ops.most_common(8))
     print(f"[{a:5d},{b:5d}) stall {100 * st / max(tot, 1):5.1f}%  inst/px {inst:6.0f}  dp/px {dp:5.0f}  "
           f"smem wf {wf / 1e6:6.2f}M (ideal {wfi / 1e6:6.2f}M)  {top}")
+    rs = [sum(x[i] for x in stalls[a:b]) for i in range(len(reasons))]
+    rt = sum(rs) or 1
+    top_r = sorted(zip(rs, reasons), reverse=True)[:5]
+    if st > 0.01 * tot:
+        print("        reasons: " + " ".join(f"{n[6:]}:{100 * v / rt:.0f}%" for v, n in top_r if v))
 alltot = collections.Counter()
 for s_, _, ex, _, _ in data:
     t = s_.split()
