@@ -16,10 +16,12 @@ Printed JSON (rank 0, one line) carries the driver's keys plus
                (H2D of image + params and D2H of the result inside the
                timed region; wall clock around calls that return only when
                the result is on the host)
-  roofline     dominant kernel (tile_filter_kernel): algorithmic bytes per
+  roofline     dominant kernel (wide_filter_kernel): algorithmic bytes per
                launch / CUDA-event kernel time, against MEASURED_PEAKS.json
-  fp64         the same kernel against the fp64 issue rate (the bound that
-               binds)
+  fp64         the same kernel against the fp64 pipe rate
+  smem         the same kernel against the shared-memory wavefront rate
+               (1 per SM per clock) -- with issue, the bounds that bind
+               (DESIGN.md)
   cpu_baseline the reference algorithm (oracle/port.py, numpy) on a bounded
                sample of the same workload, all host cores, rank 0 at N=1
 `--impl reference` prints the same line for the CPU port alone.
@@ -303,6 +305,14 @@ def run_ours(args, rank, world, local):
             fp64 = {"achieved_dp_ops_per_s": got_dp, "peak_dp_ops_per_s": peak_dp,
                     "frac": got_dp / peak_dp, "dp_inst_per_px": dp_per_px,
                     "peak_at_clock_mhz": sm_max, "source": "ncu sm__sass_thread_inst_executed_op_fp64 per px"}
+        smem = None
+        wf_per_px = SMEM_WF_PER_PX.get(args.config)
+        if wf_per_px:
+            peak_wf = 148 * sm_max * 1e6  # wavefronts / s at max clock
+            got_wf = wf_per_px * H * W * iters / (tile_ms.value / max(1, args.steps) * 1e-3)
+            smem = {"achieved_wavefronts_per_s": got_wf, "peak_wavefronts_per_s": peak_wf,
+                    "frac": got_wf / peak_wf, "wavefronts_per_px": wf_per_px,
+                    "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum per px"}
         traffic = TRAFFIC_PER_LAUNCH.get(args.config)
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -317,10 +327,11 @@ def run_ours(args, rank, world, local):
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "traffic_unit": "bytes/launch (ncu)",
-                         "kernel": "tile_filter_kernel", "kernel_ms_avg": tile_avg_ms,
+                         "kernel": "wide_filter_kernel", "kernel_ms_avg": tile_avg_ms,
                          "algorithmic_bytes_per_px": bpp, "peak_source": peak_kind,
-                         "binding_bound": "fp64 issue (see fp64)"},
+                         "binding_bound": "shared-memory wavefronts and issue (see smem, fp64)"},
             "fp64": fp64,
+            "smem": smem,
             "gpu_launches": launches,
             "launches_per_step": launches / max(1, args.steps),
             "tile_kernel_launches_per_step": launches_per_step,
@@ -343,12 +354,14 @@ WORKLOADS = {
          "theta=atan2 mod pi; exact optimiser field",
     "4": "config4 image: 4096^2 fp32 uniform[0,1); sigma [2,24], rho [1,4], smooth theta; 2 passes",
 }
-# From the committed ncu capture of the tile kernel on config 2
-# (profiles/ncu_r01_summary.md): fp64 instructions executed per output pixel
-# (DADD + DFMA + DMUL + DSETP, thread level) and DRAM bytes per launch
+# From the committed ncu capture of the primary kernel (wide_filter_kernel)
+# on config 2 (profiles/ncu_r01_wide_summary.md): fp64 instructions executed
+# per output pixel (DADD + DFMA + DMUL + DSETP, thread level), shared-memory
+# wavefronts per output pixel, and DRAM bytes per launch
 # (dram__bytes_read.sum + dram__bytes_write.sum).
-DP_INST_PER_PX = {"2": 635}
-TRAFFIC_PER_LAUNCH = {"2": 98.76e6}
+DP_INST_PER_PX = {"2": 602}
+SMEM_WF_PER_PX = {"2": 15.55}
+TRAFFIC_PER_LAUNCH = {"2": 105.07e6}
 
 
 # ---------------------------------------------------------------------------

@@ -784,7 +784,8 @@ __global__ void __launch_bounds__(kThreadsLarge, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Warp-specialised pipeline (the primary path).
+// Warp-specialised pipeline (experimental, RUBS_B200_KERNEL=pipe; measured
+// slower than the two-CTA tile kernel -- DESIGN.md).
 //
 // One persistent CTA per SM, 16 warps: warps 0-3 produce, warps 4-15
 // consume, through two 112 KB region buffers.  For tile i+1 the producers
@@ -1052,6 +1053,321 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
       buf ^= 1;
     }
   }
+  flush_status(st, ghi, flags);
+}
+
+// ---------------------------------------------------------------------------
+// Primary launch: 64 x 32-pixel tiles, two CTAs of 256 threads per SM.
+//
+// A wide tile halves the halo overhead of a 32 x 32 one at config-2 margins
+// (region elements per pixel ~8.3 -> ~5.6).  To keep registers free for the
+// gather, the exact scale-vectors are NOT held across the tile: planning
+// uses cheap float32 bounds (read margins, and 1/(a1 a2 a3 a4) from a
+// per-LUT-cell table), and each pixel's exact scale-vector is computed in
+// the gather loop, one 4 x 8 block ahead, so its global loads overlap the
+// previous block's finite differences.
+constexpr int kWideW = 64, kWideH = 32;
+constexpr int kSmemWide = 110 * 1024;  // x2 CTAs + static + reserved <= 228 KB
+constexpr int kMaxSmId = 256;          // bound of %smid (scale-vector slots)
+#ifndef RUBS_WIDE_THREADS
+#define RUBS_WIDE_THREADS 384
+#endif
+constexpr int kThreadsWide = RUBS_WIDE_THREADS;  // 2 CTAs per SM
+
+// Planning bounds of one pixel: read margins (left, right, below, above)
+// covering its taps, and an upper bound of w = 1 / (a1 a2 a3 a4).
+template <int MODE>
+__device__ __forceinline__ void pixel_bound(const FieldSpec &F, int n1, int n2, int4 &m,
+                                            float &w) {
+  if constexpr (MODE >= kModeLut) {
+    // the LUT mapping of lut_map in float32 (quarter index exact, in fp64:
+    // it is the one discontinuous choice), accurate to ~1e-6 relative
+    constexpr int PDT = MODE == kModeLut ? 1 : 0;
+    const int fc = min(max(n1, 0), F.FW - 1), fr = min(max(n2, 0), F.FH - 1) - F.fr_off;
+    const int64_t i = (int64_t)fr * F.pld + fc;
+    const double thd = load_px<PDT>(F.pt, i);
+    float sz = (float)load_px<PDT>(F.ps, i), rho = (float)load_px<PDT>(F.pr, i);
+    if (!(sz > 0.f && sz < INFINITY)) sz = 1.f;
+    if (!(rho >= 1.f && rho < INFINITY)) rho = 1.f;
+    const bool thok = thd >= 0.0 && thd < kPi;
+    const int q = thok ? quarter_index(thd) : 0;
+    const float phi = thok ? (float)(thd - (double)q * kQuarter) : 0.f;
+    const int nr = F.n_rho, np_ = F.n_phi;
+    float u = __logf(rho) * (float)F.inv_log_rho_max * (float)(nr - 1);
+    float v = phi * (float)(np_ / kQuarter) - 0.5f;
+    u = fminf(fmaxf(u, 0.f), (float)(nr - 1));
+    v = fminf(fmaxf(v, 0.f), (float)(np_ - 1));
+    const int i0 = min((int)u, nr - 2), j0 = min((int)v, np_ - 2);
+    const float fu = u - (float)i0, fv = v - (float)j0;
+    const float4 *e00 =
+        reinterpret_cast<const float4 *>(F.lutf) + ((int64_t)q * nr + i0) * np_ + j0;
+    const float4 A = __ldg(e00), C = __ldg(e00 + 1), B = __ldg(e00 + np_), Dd = __ldg(e00 + np_ + 1);
+    const float w00 = (1.f - fu) * (1.f - fv), w10 = fu * (1.f - fv), w01 = (1.f - fu) * fv,
+                w11 = fu * fv;
+    const float ss = sqrtf(sz), inv_div = (float)(1.0 / F.div);
+    float af[4] = {A.x * w00 + B.x * w10 + C.x * w01 + Dd.x * w11,
+                   A.y * w00 + B.y * w10 + C.y * w01 + Dd.y * w11,
+                   A.z * w00 + B.z * w10 + C.z * w01 + Dd.z * w11,
+                   A.w * w00 + B.w * w10 + C.w * w01 + Dd.w * w11};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) af[k] = fmaxf(af[k] * ss, (float)kScaleFloor) * inv_div;
+    const float d = (af[1] + af[3]) * 0.70710678f;
+    const float hx = 0.5f * (af[0] + d) * 1.00002f + 2e-4f;
+    const float hy = 0.5f * (af[2] + d) * 1.00002f + 2e-4f;
+    m = margins_from_extent(hx, hy);
+    w = 1.0002f / (af[0] * af[1] * af[2] * af[3]);
+  } else {
+    double a[4];
+    unsigned fl = 0;
+    field_at<MODE>(F, n1, n2, a, fl);
+    m = pixel_margins_fast(a);
+    w = 1.0f / (float)(a[0] * a[1] * a[2] * a[3]);
+  }
+}
+
+template <int MODE, int DT, int NT>
+__global__ void __launch_bounds__(NT, 2)
+    wide_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int tiles_x32,
+                       int region_cap, int *ovf_list, Status *st, double *aslots,
+                       unsigned *slotmask, const __grid_constant__ TmaMaps tm) {
+  constexpr int NW = NT / 32;
+  constexpr int NCX = kWideW / 8, NCY = kWideH / 8;  // 8 x 4 cells of 8 x 8
+  extern __shared__ __align__(128) double S[];
+  __shared__ uint64_t s_mbar;
+  __shared__ int s_cm[NCX * NCY][4];
+  __shared__ float s_cw[NCX * NCY];
+  __shared__ int s_unit[NCX * NCY][8];
+  __shared__ int s_nu;
+  __shared__ int s_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
+  // LUT modes: the exact scale-vectors of the tile are computed once (phase
+  // A) and parked in an L2-resident slot of this SM (two CTAs per SM: two
+  // slots, claimed with an atomic bit) until the gather reads them back
+  constexpr bool kPark = MODE >= kModeLut;
+  unsigned smid = 0;
+  if (tid == 0) {
+    mbar_init(mbar);
+    if (kPark) {
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      int slot = -1;
+      while (slot < 0) {
+        for (int b = 0; b < 2 && slot < 0; ++b)
+          if (!(atomicOr(&slotmask[smid], 1u << b) & (1u << b))) slot = (int)smid * 2 + b;
+      }
+      s_slot = slot;
+    }
+  }
+  if (tid < 4 * NCX * NCY) (&s_cm[0][0])[tid] = 0;
+  if (tid < NCX * NCY) s_cw[tid] = 0.f;
+  __syncthreads();
+  unsigned ghi = 0, flags = 0;
+  uint32_t phase = 0;
+  const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
+  const int x0 = tx * kWideW, y0 = ty * kWideH;
+
+  double *const apark =
+      kPark ? aslots + (size_t)s_slot * (kWideW * kWideH * 4) : nullptr;
+  // ---- A: read margins and weights of the 2048 pixels; thread = one
+  //         column, rows (tid >> 6) + 4 k; 8-lane groups share an 8 x 8 cell
+  {
+    constexpr int RS = NT / kWideW;  // rows per sweep of the CTA over the tile
+    const int px = tid & 63, py = tid / kWideW;  // py is warp-uniform
+    int cur = -1;
+    int4 acc = make_int4(0, 0, 0, 0);
+    float wacc = 0.f;
+    // reduce (m, w) over the 8 lanes of each 8 x 8 cell, merge into the cell
+    auto flush = [&](int r) {
+      int wi = __float_as_int(wacc);  // w >= 0: int order = float order
+#pragma unroll
+      for (int o = 1; o < 8; o <<= 1) {
+        acc.x = max(acc.x, __shfl_xor_sync(0xffffffffu, acc.x, o));
+        acc.y = max(acc.y, __shfl_xor_sync(0xffffffffu, acc.y, o));
+        acc.z = max(acc.z, __shfl_xor_sync(0xffffffffu, acc.z, o));
+        acc.w = max(acc.w, __shfl_xor_sync(0xffffffffu, acc.w, o));
+        wi = max(wi, __shfl_xor_sync(0xffffffffu, wi, o));
+      }
+      if ((lane & 7) == 0) {
+        const int c = r * NCX + (px >> 3);
+        atomicMax(&s_cm[c][0], acc.x);
+        atomicMax(&s_cm[c][1], acc.y);
+        atomicMax(&s_cm[c][2], acc.z);
+        atomicMax(&s_cm[c][3], acc.w);
+        atomicMax(reinterpret_cast<int *>(&s_cw[c]), wi);
+      }
+      acc = make_int4(0, 0, 0, 0);
+      wacc = 0.f;
+    };
+#pragma unroll
+    for (int k = 0; k < (kWideH + RS - 1) / RS; ++k) {
+      const int ty_ = py + RS * k;  // tile row (warp-uniform)
+      if (ty_ < kWideH) {
+        if ((ty_ >> 3) != cur) {
+          if (cur >= 0) flush(cur);
+          cur = ty_ >> 3;
+        }
+        const int x = x0 + px, y = y0 + ty_;
+        if (x < D.pw && y < D.ph) {
+          int4 m;
+          float w;
+          if constexpr (kPark) {
+            double a[4];
+            field_at<MODE>(F, D.pc_lo + x, D.pr_lo + y, a, flags);
+            m = pixel_margins_fast(a);
+            w = 1.0f / (float)(a[0] * a[1] * a[2] * a[3]);
+            double2 *dst = reinterpret_cast<double2 *>(apark + (ty_ * kWideW + px) * 4);
+            dst[0] = make_double2(a[0], a[1]);
+            dst[1] = make_double2(a[2], a[3]);
+          } else {
+            pixel_bound<MODE>(F, D.pc_lo + x, D.pr_lo + y, m, w);
+          }
+          acc.x = max(acc.x, m.x);
+          acc.y = max(acc.y, m.y);
+          acc.z = max(acc.z, m.z);
+          acc.w = max(acc.w, m.w);
+          wacc = fmaxf(wacc, w);
+        }
+      }
+    }
+    if (cur >= 0) flush(cur);
+  }
+  __syncthreads();
+
+  // ---- plan: the whole tile if its region fits and meets the precision
+  //      budget, else split the longer side recursively down to 8 x 8
+  //      cells; a cell that still fails sends its 32 x 32 half of the tile
+  //      (a tile of the overflow launches' 32-pixel grid) to the overflow pass
+  if (tid == 0) {
+    int n = 0;
+    unsigned ovf_half = 0;
+    int stk[16][4];
+    int sp = 0;
+    stk[sp][0] = 0; stk[sp][1] = 0; stk[sp][2] = NCX; stk[sp][3] = NCY; ++sp;
+    while (sp > 0) {
+      --sp;
+      const int cx0 = stk[sp][0], cy0 = stk[sp][1], ncx = stk[sp][2], ncy = stk[sp][3];
+      const int sx = x0 + 8 * cx0, sy = y0 + 8 * cy0;
+      if (sx >= D.pw || sy >= D.ph) continue;
+      const int sw = min(8 * ncx, D.pw - sx), sh = min(8 * ncy, D.ph - sy);
+      int u[4] = {0, 0, 0, 0};
+      float wm = 0.f;
+      for (int cy = cy0; cy < cy0 + ncy; ++cy)
+        for (int cx = cx0; cx < cx0 + ncx; ++cx) {
+          const int c = cy * NCX + cx;
+          for (int j = 0; j < 4; ++j) u[j] = max(u[j], s_cm[c][j]);
+          wm = fmaxf(wm, s_cw[c]);
+        }
+      const int RW = sw + u[0] + u[1], RH = sh + u[2] + u[3];
+      const float mn = (float)min(RW + 1, RH);
+      const float l4 = 0.25f * (float)(RW + 1) * (float)RH * mn * mn;
+      if (region_elems(RW + 1, RH) <= region_cap && wm * l4 <= kPrecisionBudget) {
+        int *d = s_unit[n++];
+        d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
+        continue;
+      }
+      if (ncx * ncy == 1) {
+        ovf_half |= 1u << (cx0 >> 2);
+        continue;
+      }
+      if (ncx >= ncy) {
+        const int h = ncx >> 1;
+        stk[sp][0] = cx0; stk[sp][1] = cy0; stk[sp][2] = h; stk[sp][3] = ncy; ++sp;
+        stk[sp][0] = cx0 + h; stk[sp][1] = cy0; stk[sp][2] = ncx - h; stk[sp][3] = ncy; ++sp;
+      } else {
+        const int h = ncy >> 1;
+        stk[sp][0] = cx0; stk[sp][1] = cy0; stk[sp][2] = ncx; stk[sp][3] = h; ++sp;
+        stk[sp][0] = cx0; stk[sp][1] = cy0 + h; stk[sp][2] = ncx; stk[sp][3] = ncy - h; ++sp;
+      }
+    }
+    if (ovf_half) {
+      // units never straddle the halves (the first split is the halves)
+      int k = 0;
+      for (int i = 0; i < n; ++i) {
+        const int hx = (s_unit[i][0] - x0) >> 5;
+        if (!((ovf_half >> hx) & 1u)) {
+          if (k != i)
+            for (int j = 0; j < 8; ++j) s_unit[k][j] = s_unit[i][j];
+          ++k;
+        }
+      }
+      n = k;
+      for (int h = 0; h < 2; ++h) {
+        if (!((ovf_half >> h) & 1u)) continue;
+        OvfRec r;
+        r.tile = ty * tiles_x32 + 2 * tx + h;
+        r.m[0] = r.m[1] = r.m[2] = r.m[3] = 0;
+        r.w = 0.f;
+        for (int cy = 0; cy < NCY; ++cy)
+          for (int cx = 4 * h; cx < 4 * h + 4; ++cx) {
+            const int c = cy * NCX + cx;
+            for (int j = 0; j < 4; ++j) r.m[j] = max(r.m[j], s_cm[c][j]);
+            r.w = fmaxf(r.w, s_cw[c]);
+          }
+        reinterpret_cast<OvfRec *>(ovf_list)[atomicAdd(&st->ovf_count, 1)] = r;
+      }
+    }
+    s_nu = n;
+  }
+  __syncthreads();
+
+  const int nu = s_nu;
+  const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S);
+  for (int ui = 0; ui < nu; ++ui) {
+    const int sx = s_unit[ui][0], sy = s_unit[ui][1], sw = s_unit[ui][2], sh = s_unit[ui][3];
+    const int below = s_unit[ui][5], RH = s_unit[ui][7];
+    int left = s_unit[ui][4], RW = s_unit[ui][6];
+    align_region<DT>(I, D.pc_lo + sx, left, RW);
+    const int P = region_pitch(RW);
+    // ---- B: region load (TMA for float64) + running sums
+    const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
+    load_region<DT, NT, 0>(S, P, I, rc0, rr0, RW, RH, tid, &tm, mbar, phase);
+    __syncthreads();
+    region_sweeps<NT, 0>(S, P, RW, RH, ghi, tid);
+    // ---- C: 4 x 8-pixel blocks of the unit, warp-strided; the exact
+    //         scale-vector of the next block is fetched before this one's
+    //         finite differences
+    const uint32_t Sb = sbase - (uint32_t)((rr0 * P + rc0) * 8);
+    const int nbx = (sw + 3) >> 2, nblk = nbx * ((sh + 7) >> 3);
+    auto block_px = [&](int b, int &x, int &y) {
+      const int by = b / nbx, bx = b - by * nbx;
+      x = sx + 4 * bx + (lane & 3);
+      y = sy + 8 * by + (lane >> 2);
+    };
+    auto fetch = [&](int x, int y, double a[4]) {
+      x = min(x, sx + sw - 1);
+      y = min(y, sy + sh - 1);
+      if constexpr (kPark) {
+        const double2 *p =
+            reinterpret_cast<const double2 *>(apark + ((y - y0) * kWideW + (x - x0)) * 4);
+        const double2 lo = p[0], hi = p[1];
+        a[0] = lo.x; a[1] = lo.y; a[2] = hi.x; a[3] = hi.y;
+      } else {
+        field_at<MODE>(F, D.pc_lo + x, D.pr_lo + y, a, flags);
+      }
+    };
+    int b = warp;
+    double an[4] = {1.0, 1.0, 1.0, 1.0};
+    if (b < nblk) {
+      int x, y;
+      block_px(b, x, y);
+      fetch(x, y, an);
+    }
+#pragma unroll 1
+    for (; b < nblk; b += NW) {
+      double ac[4] = {an[0], an[1], an[2], an[3]};
+      int x, y;
+      block_px(b, x, y);
+      if (b + NW < nblk) {
+        int xn, yn;
+        block_px(b + NW, xn, yn);
+        fetch(xn, yn, an);
+      }
+      if (x < sx + sw && y < sy + sh)
+        D.out[(int64_t)y * D.ld_out + x] = pixel_fd(Sb, P, D.pc_lo + x, D.pr_lo + y, ac);
+    }
+    __syncthreads();
+  }
+  if (kPark && tid == 0) atomicAnd(&slotmask[smid], ~(1u << (s_slot & 1)));
   flush_status(st, ghi, flags);
 }
 
@@ -1353,6 +1669,8 @@ struct Scratch {
   Status *h_status = nullptr;  // pinned
   double *d_pass[2] = {nullptr, nullptr};
   size_t pass_cap[2] = {0, 0};
+  double *d_aslot = nullptr;     // wide kernel: per-(SM, slot) scale-vectors
+  unsigned *d_slotmask = nullptr;
   bool attr_set = false;
 };
 thread_local Scratch t_scr;
@@ -1366,6 +1684,10 @@ int ensure_scratch() {
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_status, sizeof(Status)));
     RUBS_CUDA_TRY(cudaMallocHost(&t_scr.h_status, sizeof(Status)));
     RUBS_CUDA_TRY(cudaDeviceGetAttribute(&t_scr.sms, cudaDevAttrMultiProcessorCount, dev));
+    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_aslot, (size_t)kMaxSmId * 2 * kWideW * kWideH * 4 *
+                                                 sizeof(double)));
+    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_slotmask, kMaxSmId * sizeof(unsigned)));
+    RUBS_CUDA_TRY(cudaMemset(t_scr.d_slotmask, 0, kMaxSmId * sizeof(unsigned)));
   }
   if (!t_scr.attr_set) {
 #define RUBS_SET_SMEM(M, T)                                                          \
@@ -1377,7 +1699,10 @@ int ensure_scratch() {
                                      kSmemLarge));                                  \
   RUBS_CUDA_TRY(cudaFuncSetAttribute(pipe_filter_kernel<M, T>,                       \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                     kPipeSmem))
+                                     kPipeSmem));                                   \
+  RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<M, T, kThreadsWide>,                       \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                     kSmemWide))
     RUBS_SET_SMEM(kModeField, 0);
     RUBS_SET_SMEM(kModeField, 1);
     RUBS_SET_SMEM(kModeUniform, 0);
@@ -1503,7 +1828,7 @@ int kernel_choice() {
   static int choice = -1;
   if (choice < 0) {
     const char *e = std::getenv("RUBS_B200_KERNEL");
-    choice = (e && std::strcmp(e, "pipe") == 0) ? 0 : 1;
+    choice = (e && std::strcmp(e, "pipe") == 0) ? 0 : (e && std::strcmp(e, "tile") == 0) ? 1 : 2;
   }
   return choice;
 }
@@ -1513,7 +1838,12 @@ void launch_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, c
   const int tiles_x = (D.pw + kTile - 1) / kTile, tiles_y = (D.ph + kTile - 1) / kTile;
   const int ntiles = tiles_x * tiles_y;
   cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s);
-  if (kernel_choice() == 0)
+  if (kernel_choice() == 2) {
+    const int wx = (D.pw + kWideW - 1) / kWideW, wy = (D.ph + kWideH - 1) / kWideH;
+    wide_filter_kernel<M, T, kThreadsWide><<<wx * wy, kThreadsWide, kSmemWide, s>>>(
+        I, F, D, wx, tiles_x, kSmemWide / 8, t_scr.d_ovf, t_scr.d_status, t_scr.d_aslot,
+        t_scr.d_slotmask, tma_maps(I));
+  } else if (kernel_choice() == 0)
     pipe_filter_kernel<M, T><<<std::min(ntiles, t_scr.sms), kPipeProd + kPipeCons, kPipeSmem, s>>>(
         I, F, D, tiles_x, ntiles, t_scr.d_ovf, t_scr.d_status, tma_maps(I));
   else
@@ -1836,6 +2166,7 @@ int stage_stream(cudaStream_t *s) {
 
 struct rubs_lut {
   double *entries = nullptr;
+  float *lutf = nullptr;
   int n_rho = 0, n_phi = 0;
   double rho_max = 0.0;
 };
@@ -1851,6 +2182,7 @@ FieldSpec lut_field(const rubs_lut *lut, const void *size, const void *elong, co
   F.pdt = p_dtype;
   F.pld = ld_p;
   F.lut = lut->entries;
+  F.lutf = lut->lutf;
   F.n_rho = lut->n_rho;
   F.n_phi = lut->n_phi;
   F.rho_max = lut->rho_max;
@@ -1946,10 +2278,16 @@ int rubs_b200_lut_create(const double *rho_grid, const double *phi_grid, const d
     for (size_t e = 0; e < (size_t)n_rho * n_phi; ++e)
       for (int k = 0; k < 4; ++k) rolled[q * per + e * 4 + k] = entries[e * 4 + ((k - q + 4) & 3)];
   size_t bytes = rolled.size() * sizeof(double);
+  // float32 copy for the planning pass (float4 per entry, same layout)
+  std::vector<float> rolledf(rolled.begin(), rolled.end());
   cudaError_t e = cudaMalloc(&L->entries, bytes);
   if (e == cudaSuccess) e = cudaMemcpy(L->entries, rolled.data(), bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&L->lutf, rolledf.size() * sizeof(float));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(L->lutf, rolledf.data(), rolledf.size() * sizeof(float), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     if (L->entries) cudaFree(L->entries);
+    if (L->lutf) cudaFree(L->lutf);
     delete L;
     return set_error(RUBS_ECUDA, std::string("lut upload: ") + cudaGetErrorString(e));
   }
@@ -1960,6 +2298,7 @@ int rubs_b200_lut_create(const double *rho_grid, const double *phi_grid, const d
 void rubs_b200_lut_destroy(rubs_lut *lut) {
   if (!lut) return;
   if (lut->entries) cudaFree(lut->entries);
+  if (lut->lutf) cudaFree(lut->lutf);
   delete lut;
 }
 

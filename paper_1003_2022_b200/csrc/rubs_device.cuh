@@ -58,6 +58,7 @@ struct FieldSpec {
   int pdt;  // 0 f32, 1 f64
   int64_t pld;
   const double *lut;  // (n_rho, n_phi, 4)
+  const float *lutf;  // float32 copy (planning pass)
   int n_rho, n_phi;
   double rho_max, log_rho_max, inv_log_rho_max;
   double rho_lim;  // rho_max * (1 + 1e-12)
@@ -222,11 +223,6 @@ __device__ __forceinline__ int4 pixel_margins(const double a[4]) {
   return m;
 }
 
-// Same margins from the closed form hx = (a1 + p2 + p4) / 2,
-// hy = (a3 + p2 + p4) / 2: left = ceil(hx + 1/2) + 2, right = ceil(hx - 1/2) + 2,
-// below = ceil(hy + 3/2) + 2, above = ceil(hy - 3/2) + 2, computed with one
-// extra unit of slack so any rounding of the gather's own arithmetic stays
-// inside the region.
 // Tight read margins from the half-extents of the vertex cloud.  With
 // t1, t2 of pixel_fd_t, vertex x - n1 lies in [-hx - 1/2, hx - 1/2] and
 // y - n2 in [-hy - 3/2, hy - 3/2] (hx = (a1 + (a2 + a4)/sqrt2) / 2, hy the
