@@ -1129,7 +1129,7 @@ template <int MODE, int DT, int NT>
 __global__ void __launch_bounds__(NT, 2)
     wide_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int tiles_x32,
                        int region_cap, int *ovf_list, Status *st, double *aslots,
-                       unsigned *slotmask, const __grid_constant__ TmaMaps tm) {
+                       unsigned *slotmask, int tile_base, const __grid_constant__ TmaMaps tm) {
   constexpr int NW = NT / 32;
   constexpr int NCX = kWideW / 8, NCY = kWideH / 8;  // 8 x 4 cells of 8 x 8
   extern __shared__ __align__(128) double S[];
@@ -1163,7 +1163,7 @@ __global__ void __launch_bounds__(NT, 2)
   __syncthreads();
   unsigned ghi = 0, flags = 0;
   uint32_t phase = 0;
-  const int tile = blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
+  const int tile = tile_base + blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
   const int x0 = tx * kWideW, y0 = ty * kWideH;
 
   double *const apark =
@@ -1833,16 +1833,43 @@ int kernel_choice() {
   return choice;
 }
 
+// Wide-kernel tiles of rows [wy0, wy1) of the 64 x 32 grid over domain D.
+template <int M, int T>
+void launch_wide_rows(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int wy0,
+                      int wy1, cudaStream_t s) {
+  const int tiles_x = (D.pw + kTile - 1) / kTile;
+  const int wx = (D.pw + kWideW - 1) / kWideW;
+  if (wy1 <= wy0) return;
+  wide_filter_kernel<M, T, kThreadsWide><<<wx * (wy1 - wy0), kThreadsWide, kSmemWide, s>>>(
+      I, F, D, wx, tiles_x, kSmemWide / 8, t_scr.d_ovf, t_scr.d_status, t_scr.d_aslot,
+      t_scr.d_slotmask, wy0 * wx, tma_maps(I));
+}
+
+void launch_wide_rows_rt(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int wy0,
+                         int wy1, cudaStream_t s) {
+  const int m = F.mode, t = I.dt;
+  if (m == kModeField) {
+    if (t) launch_wide_rows<kModeField, 1>(I, F, D, wy0, wy1, s);
+    else launch_wide_rows<kModeField, 0>(I, F, D, wy0, wy1, s);
+  } else if (m == kModeUniform) {
+    if (t) launch_wide_rows<kModeUniform, 1>(I, F, D, wy0, wy1, s);
+    else launch_wide_rows<kModeUniform, 0>(I, F, D, wy0, wy1, s);
+  } else if (m == kModeLut) {
+    if (t) launch_wide_rows<kModeLut, 1>(I, F, D, wy0, wy1, s);
+    else launch_wide_rows<kModeLut, 0>(I, F, D, wy0, wy1, s);
+  } else {
+    if (t) launch_wide_rows<kModeLut32, 1>(I, F, D, wy0, wy1, s);
+    else launch_wide_rows<kModeLut32, 0>(I, F, D, wy0, wy1, s);
+  }
+}
+
 template <int M, int T>
 void launch_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cudaStream_t s) {
   const int tiles_x = (D.pw + kTile - 1) / kTile, tiles_y = (D.ph + kTile - 1) / kTile;
   const int ntiles = tiles_x * tiles_y;
   cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s);
   if (kernel_choice() == 2) {
-    const int wx = (D.pw + kWideW - 1) / kWideW, wy = (D.ph + kWideH - 1) / kWideH;
-    wide_filter_kernel<M, T, kThreadsWide><<<wx * wy, kThreadsWide, kSmemWide, s>>>(
-        I, F, D, wx, tiles_x, kSmemWide / 8, t_scr.d_ovf, t_scr.d_status, t_scr.d_aslot,
-        t_scr.d_slotmask, tma_maps(I));
+    launch_wide_rows<M, T>(I, F, D, 0, (D.ph + kWideH - 1) / kWideH, s);
   } else if (kernel_choice() == 0)
     pipe_filter_kernel<M, T><<<std::min(ntiles, t_scr.sms), kPipeProd + kPipeCons, kPipeSmem, s>>>(
         I, F, D, tiles_x, ntiles, t_scr.d_ovf, t_scr.d_status, tma_maps(I));
@@ -2011,18 +2038,25 @@ int run_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, in
            : overflow_dispatch<kModeLut32, 0>(I, F, D, n, s);
 }
 
+// Overflow-record capacity for a pass over D: at most one record per tile
+// of the 32-pixel grid (tile kernel) or per unit (pipeline).
+int ensure_ovf(const DomainSpec &D) {
+  const size_t ntiles = (size_t)((D.pw + kTile - 1) / kTile) * ((D.ph + kTile - 1) / kTile);
+  if (4 * ntiles > t_scr.ovf_cap) {
+    if (t_scr.d_ovf) cudaFree(t_scr.d_ovf);
+    t_scr.d_ovf = nullptr;
+    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_ovf, 4 * ntiles * sizeof(OvfRec)));
+    t_scr.ovf_cap = 4 * ntiles;
+  }
+  return RUBS_OK;
+}
+
 int launch_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cudaStream_t s) {
   {
     TimedLaunch tl(0, s);
     const int m = F.mode, t = I.dt;
-    const size_t ntiles = (size_t)((D.pw + kTile - 1) / kTile) * ((D.ph + kTile - 1) / kTile);
-    // at most one record per tile (tile kernel) or per unit (pipeline)
-    if (4 * ntiles > t_scr.ovf_cap) {
-      if (t_scr.d_ovf) cudaFree(t_scr.d_ovf);
-      t_scr.d_ovf = nullptr;
-      RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_ovf, 4 * ntiles * sizeof(OvfRec)));
-      t_scr.ovf_cap = 4 * ntiles;
-    }
+    int rc = ensure_ovf(D);
+    if (rc) return rc;
     if (m == kModeField) {
       if (t) launch_tiles<kModeField, 1>(I, F, D, s); else launch_tiles<kModeField, 0>(I, F, D, s);
     } else if (m == kModeUniform) {
@@ -2162,6 +2196,101 @@ int stage_stream(cudaStream_t *s) {
   return RUBS_OK;
 }
 
+// Host-buffer calls, one pass: a pipeline over bands of output rows.  The
+// image goes up whole, then each band's per-pixel inputs; a band's tiles
+// launch as soon as its inputs have landed and its output rows go back
+// while later bands are still in flight -- both copy engines and the SMs
+// busy at once.  (The image must be complete first: a band's regions read
+// rows beyond it by the read margins.)
+struct HostPlane {
+  const void *host;
+  void *dev;
+  size_t row_bytes;
+};
+
+struct StreamSet {
+  int device = -1;
+  cudaStream_t h2d = nullptr, cmp = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> ev;
+};
+thread_local StreamSet t_ss;
+
+int stream_set(size_t nev) {
+  int dev = 0;
+  RUBS_CUDA_TRY(cudaGetDevice(&dev));
+  if (t_ss.device != dev) {
+    t_ss = StreamSet();
+    t_ss.device = dev;
+    RUBS_CUDA_TRY(cudaStreamCreateWithFlags(&t_ss.h2d, cudaStreamNonBlocking));
+    RUBS_CUDA_TRY(cudaStreamCreateWithFlags(&t_ss.cmp, cudaStreamNonBlocking));
+    RUBS_CUDA_TRY(cudaStreamCreateWithFlags(&t_ss.d2h, cudaStreamNonBlocking));
+  }
+  while (t_ss.ev.size() < nev) {
+    cudaEvent_t e;
+    RUBS_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    t_ss.ev.push_back(e);
+  }
+  return RUBS_OK;
+}
+
+int run_streamed(const ImageSpec &I, FieldSpec F, const void *f_host,
+                 const std::vector<HostPlane> &planes, double *dout, double *out_host) {
+  int rc = ensure_scratch();
+  if (rc) return rc;
+  const int H = I.h, W = I.w;
+  F.FH = H;
+  F.FW = W;
+  F.div = 1.0;
+  F.scaled = 0;
+  const int wy = (H + kWideH - 1) / kWideH;
+  const int nb = std::max(1, std::min(16, wy / 2));
+  const int per = (wy + nb - 1) / nb;  // wide-tile rows per band
+  if ((rc = stream_set(2 * (size_t)nb))) return rc;
+  const cudaStream_t h2d = t_ss.h2d, cmp = t_ss.cmp, d2h = t_ss.d2h;
+  DomainSpec D{0, 0, W, H, dout, W};
+  if ((rc = ensure_ovf(D))) return rc;
+  RUBS_CUDA_TRY(cudaMemsetAsync(t_scr.d_status, 0, sizeof(Status), cmp));
+  const size_t esz = I.dt ? 8 : 4;
+  RUBS_CUDA_TRY(cudaMemcpyAsync(const_cast<void *>(I.f), f_host, (size_t)H * W * esz,
+                                cudaMemcpyHostToDevice, h2d));
+  for (int b = 0; b < nb; ++b) {
+    const int t0 = b * per, t1 = std::min(wy, (b + 1) * per);
+    if (t0 >= t1) break;
+    const int r0 = t0 * kWideH, r1 = std::min(H, t1 * kWideH);
+    for (const HostPlane &pl : planes)
+      RUBS_CUDA_TRY(cudaMemcpyAsync(static_cast<char *>(pl.dev) + r0 * pl.row_bytes,
+                                    static_cast<const char *>(pl.host) + r0 * pl.row_bytes,
+                                    (size_t)(r1 - r0) * pl.row_bytes, cudaMemcpyHostToDevice, h2d));
+    RUBS_CUDA_TRY(cudaEventRecord(t_ss.ev[2 * b], h2d));
+    RUBS_CUDA_TRY(cudaStreamWaitEvent(cmp, t_ss.ev[2 * b], 0));
+    launch_wide_rows_rt(I, F, D, t0, t1, cmp);
+    ++t_launches;
+    RUBS_CUDA_TRY(cudaGetLastError());
+    RUBS_CUDA_TRY(cudaEventRecord(t_ss.ev[2 * b + 1], cmp));
+    RUBS_CUDA_TRY(cudaStreamWaitEvent(d2h, t_ss.ev[2 * b + 1], 0));
+    RUBS_CUDA_TRY(cudaMemcpyAsync(out_host + (size_t)r0 * W, dout + (size_t)r0 * W,
+                                  (size_t)(r1 - r0) * W * 8, cudaMemcpyDeviceToHost, d2h));
+  }
+  RUBS_CUDA_TRY(cudaStreamSynchronize(d2h));
+  Status st;
+  if ((rc = fetch_status(cmp, st))) return rc;
+  if (st.ovf_count > 0 && !(st.flags & (kFlagFieldNonFinite | kFlagParamInvalid))) {
+    // deferred tiles: computed now, then every row goes back once more
+    if ((rc = run_overflow(I, F, D, st.ovf_count, cmp))) return rc;
+    RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), cmp));
+    if ((rc = fetch_status(cmp, st))) return rc;
+    RUBS_CUDA_TRY(cudaMemcpyAsync(out_host, dout, (size_t)H * W * 8, cudaMemcpyDeviceToHost, cmp));
+    RUBS_CUDA_TRY(cudaStreamSynchronize(cmp));
+  }
+  return status_to_code(st);
+}
+
+// The streamed path serves one-pass calls on the default (wide) kernel.
+bool streamable(int iterations, int64_t H, int64_t W) {
+  return iterations == 1 && kernel_choice() == 2 && H >= 2 * kWideH && W > 0 &&
+         !std::getenv("RUBS_B200_NO_STREAM");
+}
+
 }  // namespace
 
 struct rubs_lut {
@@ -2250,6 +2379,27 @@ int rubs_b200_filter_host(const void *f, int f_dtype, int64_t H, int64_t W, cons
   void *df, *dfield = nullptr, *dout;
   if ((rc = stage_buf(0, npx * esz, &df))) return rc;
   if ((rc = stage_buf(2, npx * 8, &dout))) return rc;
+  if (f_dtype != RUBS_F32 && f_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (streamable(iterations, H, W)) {
+    ImageSpec I{df, f_dtype, W, (int)H, (int)W, 0, 0};
+    FieldSpec F{};
+    std::vector<HostPlane> planes;
+    if (H > (1 << 30) || W > (1 << 30)) return set_error(RUBS_EUNSUPPORTED, "image too large");
+    if (field_is_uniform) {
+      F.mode = kModeUniform;
+      for (int k = 0; k < 4; ++k) {
+        F.u[k] = field[k];
+        if (!std::isfinite(field[k])) return set_error(RUBS_EVALUE, "scale field entries must be finite");
+      }
+    } else {
+      if ((rc = stage_buf(1, npx * 32, &dfield))) return rc;
+      F.mode = kModeField;
+      F.a = static_cast<const double *>(dfield);
+      F.ld = W;
+      planes.push_back({field, dfield, (size_t)W * 32});
+    }
+    return run_streamed(I, F, f, planes, (double *)dout, out);
+  }
   RUBS_CUDA_TRY(cudaMemcpyAsync(df, f, npx * esz, cudaMemcpyHostToDevice, s));
   if (!field_is_uniform) {
     if ((rc = stage_buf(1, npx * 32, &dfield))) return rc;
@@ -2344,6 +2494,17 @@ int rubs_b200_filter_params_host(const void *f, int f_dtype, int64_t H, int64_t 
   if ((rc = stage_buf(1, npx * psz * 3, &dp))) return rc;
   if ((rc = stage_buf(2, npx * 8, &dout))) return rc;
   char *pb = static_cast<char *>(dp);
+  if (f_dtype != RUBS_F32 && f_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (p_dtype != RUBS_F32 && p_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (!lut) return set_error(RUBS_EVALUE, "lut is NULL");
+  if (streamable(iterations, H, W)) {
+    ImageSpec I{df, f_dtype, W, (int)H, (int)W, 0, 0};
+    FieldSpec F = lut_field(lut, pb, pb + npx * psz, pb + 2 * npx * psz, p_dtype, W);
+    const size_t rb = (size_t)W * psz;
+    std::vector<HostPlane> planes = {{size, pb, rb}, {elong, pb + npx * psz, rb},
+                                     {orient, pb + 2 * npx * psz, rb}};
+    return run_streamed(I, F, f, planes, (double *)dout, out);
+  }
   RUBS_CUDA_TRY(cudaMemcpyAsync(df, f, npx * esz, cudaMemcpyHostToDevice, s));
   RUBS_CUDA_TRY(cudaMemcpyAsync(pb, size, npx * psz, cudaMemcpyHostToDevice, s));
   RUBS_CUDA_TRY(cudaMemcpyAsync(pb + npx * psz, elong, npx * psz, cudaMemcpyHostToDevice, s));

@@ -323,6 +323,29 @@ def test_torch_device_path_matches_host_path(cuda, rng):
     assert np.array_equal(dev.cpu().numpy(), host)
 
 
+def test_streamed_host_path_equals_device_path(cuda, rng):
+    # host buffers take the banded H2D / compute / D2H pipeline; device
+    # tensors the single launch -- the same tiles, so the same bits
+    torch = cuda
+    H, W = 600, 520
+    w = workloads.config2(H, W, device="cuda", param_dtype=torch.float32)
+    f = w["f"]
+    params = (w["size"], w["elong"], w["orient"])
+    dev = rb.filter_space_variant_params(torch.from_numpy(f).cuda(), *params).cpu().numpy()
+    host = rb.filter_space_variant_params(f, *(p.cpu().numpy() for p in params))
+    assert np.array_equal(host, dev)
+    # field mode with a block of very wide pixels: their tiles go through
+    # the deferred (overflow) launches after the pipeline, rows re-copied
+    fld = rng.uniform(0.6, 3.0, size=(H, W, 4))
+    fld[300:310, 200:210] = 70.0
+    dev = rb.filter_space_variant(torch.from_numpy(f).cuda(), torch.from_numpy(fld).cuda())
+    host = rb.filter_space_variant(f, fld)
+    assert np.array_equal(host, dev.cpu().numpy())
+    pts = sample_points(rng, H, W, 12, extra=[(305, 205), (300, 200), (250, 260)])
+    ref = oracle.points(f, fld, pts)
+    assert rel_err(host[pts[:, 0], pts[:, 1]], ref) < REL_TOL
+
+
 # --- BASELINE configs at full size ------------------------------------------
 
 
