@@ -191,6 +191,38 @@ int rubs_b200_interpolate(const double *plane, int64_t rows, int64_t cols, int64
                           int64_t col0, int64_t row0, const double *x1, const double *x2,
                           int64_t n, double *out, void *stream);
 
+/*
+ * The reference's own caller of the hot path: structure-tensor driven
+ * adaptive smoothing (pkg/src/rubs/tensor.py), on the device.
+ *
+ * rubs_b200_structure_tensor replaces tensor.structure_tensor
+ * (tensor.py:52-75): j = (H, W, 3) float64 (J11, J12, J22), central
+ * differences on the reflect-padded image, averaged with the isotropic
+ * filter of width max(window_sigma sqrt(6), 0.05) (0 disables it).
+ *
+ * rubs_b200_anisotropy replaces tensor.anisotropy_from_tensor
+ * (tensor.py:90-171): size / elong / orient float64 (H, W), isotropic
+ * (H, W) bytes (may be NULL); size_range = {min, max} or NULL for the
+ * default (0.5, 3 noise_sigma^2 + 0.5).  RUBS_EVALUE for a bad
+ * bound_fraction or size_range, as the reference raises ValueError.
+ *
+ * rubs_b200_adaptive_smooth replaces tensor.adaptive_smooth
+ * (tensor.py:174-224): the above, the LUT mapping and filter of f and of
+ * a flat image (iterations passes), and the per-pixel gain correction.
+ * All pointers are device pointers; work is queued on `stream`.
+ */
+int rubs_b200_structure_tensor(const void *f, int f_dtype, int64_t H, int64_t W, int64_t ld_f,
+                               double window_sigma, double *j, void *stream);
+int rubs_b200_anisotropy(const double *j, int64_t H, int64_t W, double noise_sigma,
+                         const double *size_range, double bound_fraction, double iso_gain,
+                         double *size, double *elong, double *orient, unsigned char *isotropic,
+                         void *stream);
+int rubs_b200_adaptive_smooth(const void *f, int f_dtype, int64_t H, int64_t W, int64_t ld_f,
+                              double noise_sigma, double window_sigma, int iterations,
+                              const rubs_lut *lut, double bound_fraction,
+                              const double *size_range, double iso_gain, double *out,
+                              int64_t ld_out, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

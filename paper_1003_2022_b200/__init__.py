@@ -35,10 +35,15 @@ from .geometry import (
     sigma_to_size,
 )
 from .solver import Infeasible, OutOfGrid, ScaleLut, build_lut, default_lut, optimize_scale_vector
+from .tensor import AnisotropyMaps, adaptive_smooth, anisotropy_from_tensor, structure_tensor
 
 __version__ = "0.1.0"
 
 __all__ = [
+    "AnisotropyMaps",
+    "adaptive_smooth",
+    "anisotropy_from_tensor",
+    "structure_tensor",
     "SCALE_FLOOR",
     "DeviceLut",
     "FdMesh",

@@ -35,7 +35,7 @@ def build_native(verbose: bool = False, defines=(), out: str | None = None) -> s
     ``defines``/``out`` build a variant library for A/B runs."""
     os.makedirs(LIB_DIR, exist_ok=True)
     out = out or LIB_PATH
-    srcs = [os.path.join(CSRC, "rubs_b200.cu")]
+    srcs = [os.path.join(CSRC, "rubs_b200.cu"), os.path.join(CSRC, "rubs_tensor.cu")]
     cmd = ["nvcc", *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", INCLUDE, "-o", out + ".tmp",
            *srcs]
     if verbose:
@@ -52,6 +52,7 @@ _i64 = ctypes.c_int64
 _int = ctypes.c_int
 _dp = ctypes.POINTER(ctypes.c_double)
 _lp = ctypes.POINTER(ctypes.c_int64)
+_dbl = ctypes.c_double
 
 # name -> (restype, argtypes); kept identical to include/rubs_b200.h
 SIGNATURES = {
@@ -84,6 +85,10 @@ SIGNATURES = {
     "rubs_b200_preintegrate": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _i64,
                                       _i64, _vp, _i64, _vp]),
     "rubs_b200_interpolate": (_int, [_vp, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _i64, _vp, _vp]),
+    "rubs_b200_structure_tensor": (_int, [_vp, _int, _i64, _i64, _i64, _dbl, _vp, _vp]),
+    "rubs_b200_anisotropy": (_int, [_vp, _i64, _i64, _dbl, _vp, _dbl, _dbl, _vp, _vp, _vp, _vp, _vp]),
+    "rubs_b200_adaptive_smooth": (_int, [_vp, _int, _i64, _i64, _i64, _dbl, _dbl, _int, _vp, _dbl, _vp,
+                                         _dbl, _vp, _i64, _vp]),
 }
 
 

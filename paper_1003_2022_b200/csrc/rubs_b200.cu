@@ -36,6 +36,7 @@
 
 #include "../../include/rubs_b200.h"
 #include "rubs_device.cuh"
+#include "rubs_internal.h"
 
 using namespace rubs;
 
@@ -546,14 +547,17 @@ __device__ __forceinline__ double pixel_fd(uint32_t Sb, int P, int n1, int n2, c
 // region (the rectangle grown by the maximum read margins of its pixels).
 // Precision model (measured): the error of a pixel is about
 //   kappa * eps * w * L4,  w = 1 / (a1 a2 a3 a4),  L4 = RW RH min(RW,RH)^2 / 4,
-// kappa ~ 0.04 -- the finite difference cancels running sums of size ~L4
-// down to O(1) with weight w.  Well-conditioned pixels (w small) tolerate
-// big regions; pixels with floored widths (w large) need small ones, so a
-// 32x32 tile whose budget w * L4 is exceeded is cut into 16x16 quadrants,
-// then 8x8 cells.  Regions that do not fit shared memory are cut the same
-// way; 8x8 cells that still do not fit send the tile to the overflow launch.
-constexpr float kPrecisionBudget = 1.1e7f;  // w * L4 for ~5e-11 relative error
-
+// -- the finite difference cancels running sums of size ~L4 down to O(1)
+// with weight w.  kappa is ~0.04 for round kernels but reaches ~0.5 for
+// kernels with one floored direction (adaptive_smooth's small kernels:
+// a = (1.5, 1.9, 0.3, 0.05) gave 7e-10 at w L4 = 1.1e7), so the budget is
+// w L4 <= 5e5, i.e. <= ~3e-11 for round and <= ~1e-10 for skewed kernels.
+// Well-conditioned pixels (w small) tolerate big regions; pixels with
+// floored widths (w large) need small ones, so a unit whose budget is
+// exceeded is cut in halves / quadrants down to 8x8 cells.  Regions that do
+// not fit shared memory are cut the same way; 8x8 cells that still do not
+// fit send the tile to the overflow launch.  (Config 2 never splits for
+// precision: its smallest kernels have w ~ 0.1.)
 struct PlanCtx {
   int m[16][4];     // per 8x8 cell: left, right, below, above
   float w[16];      // per 8x8 cell: max 1/(a1 a2 a3 a4)
@@ -2666,3 +2670,8 @@ int rubs_b200_interpolate(const double *plane, int64_t rows, int64_t cols, int64
 }
 
 }  // extern "C"
+
+namespace rubs_internal {
+int set_error(int code, const std::string &msg) { return ::set_error(code, msg); }
+double lut_rho_max(const rubs_lut *lut) { return lut->rho_max; }
+}  // namespace rubs_internal

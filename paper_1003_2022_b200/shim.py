@@ -9,8 +9,9 @@ so replacing the hot path means patching each of those module attributes.
     shim.install(rubs)            # rubs.filter_space_variant now runs on the B200
     rubs.adaptive_smooth(img, 0.1)  # the reference's own caller, accelerated
 
-Only the filtering path is replaced; everything else in the
-reference (solver, CLI, I/O, oracle) keeps running as shipped.
+Only the filtering path and its own caller, the structure-tensor pipeline
+(tensor.py), are replaced; everything else in the reference
+(solver, CLI, I/O, oracle) keeps running as shipped.
 """
 
 from __future__ import annotations
@@ -18,7 +19,7 @@ from __future__ import annotations
 import importlib
 import sys
 
-from . import engine
+from . import engine, tensor
 
 # (module suffix, attribute) -> replacement
 _TARGETS = {
@@ -34,6 +35,13 @@ _TARGETS = {
     ("", "filter_space_invariant"): engine.filter_space_invariant,
     ("", "preintegrate"): engine.preintegrate,
     ("", "interpolate"): engine.interpolate,
+    # the reference's own caller of the path (tensor.py), SURVEY.md §8f
+    ("tensor", "structure_tensor"): tensor.structure_tensor,
+    ("tensor", "anisotropy_from_tensor"): tensor.anisotropy_from_tensor,
+    ("tensor", "adaptive_smooth"): tensor.adaptive_smooth,
+    ("cli", "adaptive_smooth"): tensor.adaptive_smooth,
+    ("", "adaptive_smooth"): tensor.adaptive_smooth,
+    ("", "structure_tensor"): tensor.structure_tensor,
 }
 
 _SAVED: dict = {}

@@ -11,6 +11,7 @@ Every array here comes out of the reference's public functions:
   rubs.engine.filter_space_variant / filter_space_invariant / preintegrate
   rubs.oracle.dense_convolve  (oracle.py:177)
   rubs.solver.build_lut / lookup_many / optimize_scale_vector
+  rubs.tensor.structure_tensor / anisotropy_from_tensor / adaptive_smooth
 """
 
 from __future__ import annotations
@@ -175,7 +176,55 @@ def config2_style(rng):
                         theta=th, field=field, ref=out)
 
 
+def tensor_golden():
+    """structure_tensor / anisotropy_from_tensor / adaptive_smooth
+    (tensor.py:52-224) on stripes + noise, a step edge with flat areas, a
+    constant image, and the reference tests' hand-made tensors."""
+    from rubs import tensor
+    rng = np.random.default_rng(77)
+    cases = {}
+    stripes = oracle.stripe_image((48, 56), period=7.0, angle=0.5)
+    noisy = stripes + rng.normal(0.0, 0.08, stripes.shape)
+    step = np.zeros((40, 44))
+    step[:, 20:] = 1.0
+    step[12:30, 5:12] += rng.normal(0.0, 0.05, (18, 7))
+    cases["noisy"], cases["step"] = noisy, step
+    for name, img in (("noisy", noisy), ("step", step)):
+        cases[f"{name}_j0"] = tensor.structure_tensor(img, window_sigma=0.0)
+        j = tensor.structure_tensor(img, window_sigma=1.5)
+        cases[f"{name}_j"] = j
+        m = tensor.anisotropy_from_tensor(j, 0.1)
+        for k in ("size", "elongation", "orientation", "isotropic"):
+            cases[f"{name}_{k}"] = getattr(m, k)
+        cases[f"{name}_smooth"] = tensor.adaptive_smooth(img, 0.1)
+    cases["noisy_smooth2"] = tensor.adaptive_smooth(noisy, 0.2, iterations=2, size_range=(0.5, 4.0))
+    cases["flat_smooth"] = tensor.adaptive_smooth(np.full((24, 24), 0.75), 0.1)
+    # the reference tests' tensor fields (test_tensor.py:54-110)
+    g = np.array([math.cos(0.35), math.sin(0.35)])
+    jm = 2.5 * np.outer(g, g)
+    phi_g = math.pi / 8 + math.pi / 2
+    g2 = np.array([math.cos(phi_g), math.sin(phi_g)])
+    jm2 = 10.0 * np.outer(g2, g2)
+    hand = np.zeros((6, 6, 3))
+    hand[0, :] = (4.0, 0.0, 1.0)
+    hand[1, :] = (6.0, 0.0, 2.0)
+    hand[2, :] = (jm[0, 0], jm[0, 1], jm[1, 1])
+    hand[3, :] = 0.0
+    hand[4, :] = (jm2[0, 0], jm2[0, 1], jm2[1, 1])
+    hand[5, :3] = (1.0, 0.0, 0.0)
+    hand[5, 3:] = (9.0, 0.0, 0.0)
+    cases["hand_j"] = hand
+    m = tensor.anisotropy_from_tensor(hand, 0.1, size_range=(0.5, 4.0))
+    for k in ("size", "elongation", "orientation", "isotropic"):
+        cases[f"hand_{k}"] = getattr(m, k)
+    np.savez_compressed(os.path.join(OUT, "tensor.npz"), **cases)
+
+
 def main():
+    if sys.argv[1:] == ["tensor"]:
+        tensor_golden()
+        print("tensor fixtures written to", OUT)
+        return
     rng = np.random.default_rng(20240817)
     kernels(rng)
     zp_golden(rng)
@@ -183,6 +232,7 @@ def main():
     preint_golden(rng)
     solver_golden(rng)
     config2_style(rng)
+    tensor_golden()
     print("golden fixtures written to", OUT, "(rubs", rubs.__version__, ")")
 
 
