@@ -558,6 +558,11 @@ __device__ __forceinline__ double pixel_fd(uint32_t Sb, int P, int n1, int n2, c
 // not fit shared memory are cut the same way; 8x8 cells that still do not
 // fit send the tile to the overflow launch.  (Config 2 never splits for
 // precision: its smallest kernels have w ~ 0.1.)
+#ifndef RUBS_PREC_BUDGET
+#define RUBS_PREC_BUDGET 5e5f
+#endif
+constexpr float kPrecisionBudget = RUBS_PREC_BUDGET;  // w * L4 (see above)
+
 struct PlanCtx {
   int m[16][4];     // per 8x8 cell: left, right, below, above
   float w[16];      // per 8x8 cell: max 1/(a1 a2 a3 a4)
