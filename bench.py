@@ -48,7 +48,7 @@ METRIC = "Gpixel/s filtered"
 UNIT = "Gpixel/s"
 # Algorithmic bytes per output pixel for the fused path: f64 image (8) +
 # three f32 params (12) + f64 output (8) = 28.
-BYTES_PER_PX = {"2": 28, "1": 48, "3": 24, "4": 52, "5": 24}
+BYTES_PER_PX = {"2": 28, "1": 48, "3": 24, "4": 52, "5": 24, "A": 16}
 
 
 def parse():
@@ -57,7 +57,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="2", choices=["1", "2", "3", "4", "5"])
+    p.add_argument("--config", default="2", choices=["1", "2", "3", "4", "5", "A"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
@@ -152,6 +152,10 @@ def make_inputs(cfg: str, torch, device, copies: int, rank: int):
     elif cfg == "5":
         w = workloads.config5(device=device, param_dtype=torch.float32, image_device=device)
         copies = 1
+    elif cfg == "A":
+        w = workloads.adaptive_image()
+        f = torch.as_tensor(w["f"]).to(device)
+        return w, [{"f": f.clone(), "adaptive": True} for _ in range(copies)]
     else:
         w = workloads.config4_image(rank, device=device, param_dtype=torch.float32)
     f = torch.as_tensor(w["f"]).to(device)
@@ -197,6 +201,8 @@ def run_ours(args, rank, world, local):
         if row_bands:
             return sharding.filter_row_band(own, band, H, *pb)
         s = sets[i % len(sets)]
+        if "adaptive" in s:
+            return rb.adaptive_smooth(s["f"], w["noise_sigma"])
         if "p" in s:
             return rb.filter_space_variant_params(s["f"], *s["p"], iterations=iters)
         return rb.filter_space_variant(s["f"], s["field"], iters)
@@ -244,7 +250,16 @@ def run_ours(args, rank, world, local):
     # ---- end to end through the public API with host buffers ----
     e2e = None
     if not args.no_e2e and not row_bands:
-        if "p" in sets[0]:
+        if "adaptive" in sets[0]:
+            hf = torch.empty((H, W), dtype=torch.float64, pin_memory=True)
+            hf.copy_(sets[0]["f"].cpu())
+            hfn = hf.numpy()
+            hout = torch.empty((H, W), dtype=torch.float64, pin_memory=True).numpy()
+
+            def e2e_step():
+                return rb.adaptive_smooth(hfn, w["noise_sigma"], out=hout)
+            h2d = hfn.nbytes
+        elif "p" in sets[0]:
             hf = torch.empty((H, W), dtype=sets[0]["f"].dtype, pin_memory=True)
             hf.copy_(sets[0]["f"].cpu())
             hp = []
@@ -353,6 +368,9 @@ WORKLOADS = {
     "1": "config1: 256^2 fp64 uniform[0,1) seed 0; sigma 2->8 along x, rho 1->3 radial, "
          "theta=atan2 mod pi; exact optimiser field",
     "4": "config4 image: 4096^2 fp32 uniform[0,1); sigma [2,24], rho [1,4], smooth theta; 2 passes",
+    "A": "adaptive_smooth pipeline (tensor.py; SURVEY 8f): 2048^2 fp64 stripes + N(0,0.1^2), "
+         "noise_sigma 0.1, window 1.5; structure tensor (3 window filters), percentiles, anisotropy, "
+         "LUT filter of image and flat image, gain correction",
 }
 # From the committed ncu capture of the primary kernel (wide_filter_kernel)
 # on config 2 (profiles/ncu_r01_wide_summary.md): fp64 instructions executed
@@ -366,6 +384,18 @@ TRAFFIC_PER_LAUNCH = {"2": 105.07e6}
 
 # ---------------------------------------------------------------------------
 _PORT = {}
+
+
+def _adaptive_worker(k):
+    """One independent adaptive_smooth pipeline (oracle/tensor_port.py with
+    the reference fast-path port as its filter) on crop k; returns pixels."""
+    import oracle.port as port
+    from oracle import tensor_port
+    f, lut, noise, c = _PORT["f"], _PORT["lut"], _PORT["noise"], _PORT["crop"]
+    r0 = (k * c) % (f.shape[0] - c)
+    crop = f[r0:r0 + c, :c]
+    tensor_port.adaptive_smooth(crop, noise, lut, filt=lambda a, fld, m=1: port.filter_space_variant(a, fld, m))
+    return c * c
 
 
 def _band_worker(band):
@@ -386,6 +416,18 @@ class CpuPort:
         import multiprocessing as mp
         from oracle import port
         from paper_1003_2022_b200 import default_lut, workloads
+        self.cfg = cfg
+        self.cores = workers or os.cpu_count() or 1
+        if cfg == "A":
+            w = workloads.adaptive_image()
+            lut = default_lut()
+            _PORT.update(f=w["f"], lut=(lut.rho_grid, lut.phi_grid, lut.entries),
+                         noise=w["noise_sigma"], crop=256)
+            self.H, self.W = w["f"].shape
+            self.jobs = list(range(self.cores))
+            os.environ["OMP_NUM_THREADS"] = "1"
+            self.pool = mp.get_context("fork").Pool(self.cores)
+            return
         if cfg == "1":
             w = workloads.config1()
             field = w["field"]
@@ -408,10 +450,17 @@ class CpuPort:
 
     def step(self):
         t0 = time.perf_counter()
-        px = sum(self.pool.map(_band_worker, self.bands))
+        if self.cfg == "A":
+            px = sum(self.pool.map(_adaptive_worker, self.jobs))
+        else:
+            px = sum(self.pool.map(_band_worker, self.bands))
         return px, time.perf_counter() - t0
 
     def sample(self):
+        if self.cfg == "A":
+            return (f"{self.cores} independent adaptive_smooth pipelines on 256x256 crops of the "
+                    f"workload image (numpy restatement of tensor.py with the reference fast-path "
+                    f"port as filter, oracle/tensor_port.py), {self.cores} processes x 1 thread")
         return (f"{len(self.bands)} row bands of {self.rows} rows x {self.W} cols "
                 f"({sum(h - l for l, h in self.bands)} of {self.H} rows) of {WORKLOADS[self.cfg].split(':')[0]}, "
                 f"halo rows recomputed per band; numpy port of the reference fast path "
@@ -442,7 +491,7 @@ def run_reference(args, rank, world):
         return None
     mpx, cores, sample, el = cpu_port_throughput(args.config, steps=args.steps, warmup=args.warmup)
     v = mpx / 1e3  # Gpixel/s
-    H = 2048 if args.config == "2" else (256 if args.config == "1" else 4096)
+    H = 2048 if args.config in ("2", "A") else (256 if args.config == "1" else 4096)
     return {
         "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,

@@ -124,10 +124,12 @@ def anisotropy_from_tensor(j, noise_sigma: float, *, size_range=None, bound_frac
 
 def adaptive_smooth(f, noise_sigma: float, *, window_sigma: float = 1.5, iterations: int = 1,
                     lut: ScaleLut | None = None, bound_fraction: float = 0.95, size_range=None,
-                    iso_gain: float = 1.0):
+                    iso_gain: float = 1.0, out=None):
     """Smooth an image with per-pixel oriented elliptical kernels
     (tensor.py:174-224): structure tensor, anisotropy maps, LUT mapping,
-    the space-variant filter of f and of a flat image, gain correction."""
+    the space-variant filter of f and of a flat image, gain correction.
+    ``out`` (extension): a C-contiguous float64 host array (e.g. pinned) to
+    receive a numpy caller's result."""
     t, host = _device_image(f)
     if noise_sigma < 0.0:
         raise ValueError("noise_sigma must be >= 0")
@@ -144,12 +146,19 @@ def adaptive_smooth(f, noise_sigma: float, *, window_sigma: float = 1.5, iterati
     torch = _torch()
     dl = device_lut(lut if lut is not None else default_lut())
     H, W = t.shape
-    out = torch.empty((H, W), dtype=torch.float64, device=t.device)
+    res = torch.empty((H, W), dtype=torch.float64, device=t.device)
     if H and W:
         sr = (ctypes.c_double * 2)(*size_range) if size_range is not None else None
         with torch.cuda.device(t.device):
             _native.check(_native.load().rubs_b200_adaptive_smooth(
                 _vp(t), _dtype_code(t), H, W, W, float(noise_sigma), float(window_sigma),
-                int(iterations), dl.handle, float(bound_fraction), sr, float(iso_gain), _vp(out), W,
+                int(iterations), dl.handle, float(bound_fraction), sr, float(iso_gain), _vp(res), W,
                 _stream_handle()))
-    return out.cpu().numpy() if host else out
+    if not host:
+        return res
+    if out is None:
+        return res.cpu().numpy()
+    if out.shape != (H, W) or out.dtype != np.float64 or not out.flags.c_contiguous:
+        raise ValueError("out must be a C-contiguous float64 array of the image shape")
+    torch.from_numpy(out).copy_(res)
+    return out

@@ -143,3 +143,15 @@ def config5(H: int = 32768, W: int = 32768, device="cpu", param_dtype=None, imag
     f = torch.rand((H, W), generator=g, device=image_device or device, dtype=torch.float32)
     size, rho, theta = _param_fields(H, W, 2.0, 256.0, 8.0, (51, 52, 53), device, param_dtype)
     return {"name": "config5", "f": f, "size": size, "elong": rho, "orient": theta, "iterations": 1}
+
+
+def adaptive_image(H: int = 2048, W: int = 2048, seed: int = 0, noise: float = 0.1):
+    """Workload of the adaptive_smooth pipeline (tensor.py:174-224; SURVEY.md
+    §8f): oriented stripes (period 11 px, angle 0.7 rad, oracle.py:351-363
+    recipe) plus N(0, noise^2) seeded noise, float64; noise_sigma = noise."""
+    x1 = np.arange(W, dtype=np.float64)[None, :]
+    x2 = np.arange(H, dtype=np.float64)[:, None]
+    phase = -math.sin(0.7) * x1 + math.cos(0.7) * x2
+    clean = 0.5 * (np.sin(2.0 * math.pi * phase / 11.0) + 1.0)
+    f = clean + np.random.default_rng(seed).normal(0.0, noise, (H, W))
+    return {"name": "adaptive", "f": f, "clean": clean, "noise_sigma": noise, "iterations": 1}
