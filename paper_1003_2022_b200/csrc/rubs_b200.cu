@@ -1075,6 +1075,12 @@ __global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
 // per-LUT-cell table), and each pixel's exact scale-vector is computed in
 // the gather loop, one 4 x 8 block ahead, so its global loads overlap the
 // previous block's finite differences.
+#ifndef RUBS_DEV_SKIP_SWEEPS
+#define RUBS_DEV_SKIP_SWEEPS 0  // dev timing experiments only
+#endif
+#ifndef RUBS_DEV_SKIP_GATHER
+#define RUBS_DEV_SKIP_GATHER 0
+#endif
 constexpr int kWideW = 64, kWideH = 32;
 constexpr int kSmemWide = 110 * 1024;  // x2 CTAs + static + reserved <= 228 KB
 constexpr int kMaxSmId = 256;          // bound of %smid (scale-vector slots)
@@ -1331,7 +1337,7 @@ __global__ void __launch_bounds__(NT, 2)
     const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
     load_region<DT, NT, 0>(S, P, I, rc0, rr0, RW, RH, tid, &tm, mbar, phase);
     __syncthreads();
-    region_sweeps<NT, 0>(S, P, RW, RH, ghi, tid);
+    if (!RUBS_DEV_SKIP_SWEEPS) region_sweeps<NT, 0>(S, P, RW, RH, ghi, tid);
     // ---- C: 4 x 8-pixel blocks of the unit, warp-strided; the exact
     //         scale-vector of the next block is fetched before this one's
     //         finite differences
@@ -1372,7 +1378,7 @@ __global__ void __launch_bounds__(NT, 2)
         fetch(xn, yn, an);
       }
       if (x < sx + sw && y < sy + sh)
-        D.out[(int64_t)y * D.ld_out + x] = pixel_fd(Sb, P, D.pc_lo + x, D.pr_lo + y, ac);
+        D.out[(int64_t)y * D.ld_out + x] = RUBS_DEV_SKIP_GATHER ? ac[0] : pixel_fd(Sb, P, D.pc_lo + x, D.pr_lo + y, ac);
     }
     __syncthreads();
   }
@@ -2335,6 +2341,7 @@ FieldSpec lut_field(const rubs_lut *lut, const void *size, const void *elong, co
   F.rho_max = lut->rho_max;
   F.log_rho_max = std::log(lut->rho_max);
   F.inv_log_rho_max = 1.0 / F.log_rho_max;
+  F.phi_scale = (double)lut->n_phi / kQuarter;
   F.rho_lim = lut->rho_max * (1.0 + 1e-12);
   return F;
 }

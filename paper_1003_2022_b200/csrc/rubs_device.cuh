@@ -61,6 +61,7 @@ struct FieldSpec {
   const float *lutf;  // float32 copy (planning pass)
   int n_rho, n_phi;
   double rho_max, log_rho_max, inv_log_rho_max;
+  double phi_scale;  // n_phi / (pi / 4)
   double rho_lim;  // rho_max * (1 + 1e-12)
   int FH, FW;      // field grid, edge-clamped (np.pad mode="edge", engine.py:306-314)
   int fr_off;      // global row of the first row held in the arrays (row bands)
@@ -131,7 +132,9 @@ __device__ __forceinline__ void lut_map(const FieldSpec &F, double s, double rho
   const int nr = F.n_rho, np_ = F.n_phi;
   // explicit roundings: identical bits wherever this is inlined
   double u = __dmul_rn(__dmul_rn(log(rho), F.inv_log_rho_max), (double)(nr - 1));
-  double v = __dsub_rn(__dmul_rn(phi, (double)np_ / kQuarter), 0.5);
+  // n_phi / quarter is a runtime division: hoisted to the host (F.phi_scale,
+  // the same correctly rounded quotient)
+  double v = __dsub_rn(__dmul_rn(phi, F.phi_scale), 0.5);
   u = fmin(fmax(u, 0.0), (double)(nr - 1));
   v = fmin(fmax(v, 0.0), (double)(np_ - 1));
   int i0 = min((int)u, nr - 2);
@@ -191,9 +194,10 @@ __device__ __forceinline__ void field_at(const FieldSpec &F, int n1, int n2, dou
   const int fr = min(max(n2, 0), F.FH - 1) - F.fr_off;
   field_raw<MODE>(F, fr, fc, a, flags);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    double v = fmax(a[k], kScaleFloor);  // fmax(NaN, x) = x; NaN already flagged
-    a[k] = F.scaled ? __ddiv_rn(v, F.div) : v;
+  for (int k = 0; k < 4; ++k) a[k] = fmax(a[k], kScaleFloor);  // fmax(NaN, x) = x; NaN flagged
+  if (F.scaled) {  // uniform branch: the divisions only for iterated passes
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = __ddiv_rn(a[k], F.div);
   }
 }
 
