@@ -428,11 +428,23 @@ class CpuPort:
             os.environ["OMP_NUM_THREADS"] = "1"
             self.pool = mp.get_context("fork").Pool(self.cores)
             return
+        self.note = ""
         if cfg == "1":
             w = workloads.config1()
             field = w["field"]
         else:
-            w = workloads.config2() if cfg == "2" else workloads.config4_image(0)
+            if cfg == "2":
+                w = workloads.config2()
+            elif cfg == "3":
+                # a 2048^2 instance of config 3's recipe (same sigma / rho
+                # ranges; the full 8192^2 CPU run would take hours)
+                w = workloads.config3(2048, 2048)
+                self.note = " (2048^2 instance of the config-3 recipe)"
+            elif cfg == "5":
+                w = workloads.config5(2048, 2048)
+                self.note = " (2048^2 instance of the config-5 recipe)"
+            else:
+                w = workloads.config4_image(0)
             lut = default_lut()
             field = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, w["size"].numpy(),
                                      w["elong"].numpy(), w["orient"].numpy())
@@ -462,7 +474,8 @@ class CpuPort:
                     f"workload image (numpy restatement of tensor.py with the reference fast-path "
                     f"port as filter, oracle/tensor_port.py), {self.cores} processes x 1 thread")
         return (f"{len(self.bands)} row bands of {self.rows} rows x {self.W} cols "
-                f"({sum(h - l for l, h in self.bands)} of {self.H} rows) of {WORKLOADS[self.cfg].split(':')[0]}, "
+                f"({sum(h - l for l, h in self.bands)} of {self.H} rows) of {WORKLOADS[self.cfg].split(':')[0]}"
+                f"{self.note}, "
                 f"halo rows recomputed per band; numpy port of the reference fast path "
                 f"(oracle/port.py), {self.cores} processes x 1 thread")
 
