@@ -309,14 +309,15 @@ def run_ours(args, rank, world, local):
         per_launch_px = H * W  # final pass covers H x W (iterations > 1 adds extended passes)
         tile_avg_ms = tile_ms.value / max(1, tile_n.value)
         launches_per_step = tile_n.value / max(1, args.steps)
-        achieved = bpp * H * W * iters / (tile_ms.value / max(1, args.steps) * 1e-3) / 1e9
+        kern_s = max(tile_ms.value, 1e-9) / max(1, args.steps) * 1e-3
+        achieved = bpp * H * W * iters / kern_s / 1e9
         # fp64 issue bound: B200 has 64 fp64 lanes per SM; DP instructions
         # per pixel measured with ncu (profiles/ncu_r01_summary.md)
         dp_per_px = DP_INST_PER_PX.get(args.config)
         fp64 = None
         if dp_per_px:
             peak_dp = 148 * 64 * sm_max * 1e6  # DP lane-ops / s at max clock
-            got_dp = dp_per_px * H * W * iters / (tile_ms.value / max(1, args.steps) * 1e-3)
+            got_dp = dp_per_px * H * W * iters / kern_s
             fp64 = {"achieved_dp_ops_per_s": got_dp, "peak_dp_ops_per_s": peak_dp,
                     "frac": got_dp / peak_dp, "dp_inst_per_px": dp_per_px,
                     "peak_at_clock_mhz": sm_max, "source": "ncu sm__sass_thread_inst_executed_op_fp64 per px"}
@@ -324,7 +325,7 @@ def run_ours(args, rank, world, local):
         wf_per_px = SMEM_WF_PER_PX.get(args.config)
         if wf_per_px:
             peak_wf = 148 * sm_max * 1e6  # wavefronts / s at max clock
-            got_wf = wf_per_px * H * W * iters / (tile_ms.value / max(1, args.steps) * 1e-3)
+            got_wf = wf_per_px * H * W * iters / kern_s
             smem = {"achieved_wavefronts_per_s": got_wf, "peak_wavefronts_per_s": peak_wf,
                     "frac": got_wf / peak_wf, "wavefronts_per_px": wf_per_px,
                     "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum per px"}

@@ -543,6 +543,89 @@ __device__ __forceinline__ double pixel_fd(uint32_t Sb, int P, int n1, int n2, c
   return pixel_fd_t<uint32_t, int>(Sb, P * 8, n1, n2, a);
 }
 
+// Several planes in shared memory, PSTRIDE bytes apart, filtered with the
+// same per-pixel kernel (the adaptive_smooth pipeline's channels): the
+// vertex geometry, lattice splits and ZP partition choice are computed once
+// and each plane is read at the same seven taps.  Per plane the arithmetic
+// is that of zp_read8 / pixel_fd_t.
+template <int NCH, int PSTRIDE>
+__device__ __forceinline__ void zp_read8_n(uint32_t c, int P8, double d1, double d2,
+                                           double F8[NCH]) {
+  const bool gp = d1 >= -d2;
+  const bool gm = d1 >= d2;
+  const bool xmaj = (gp == gm);
+  int sA = xmaj ? 8 : P8;
+  sA = gp ? sA : -sA;
+  const int sB = xmaj ? P8 : 8;
+  const double u = dabs(xmaj ? d1 : d2);
+  const double v = xmaj ? d2 : d1;
+  const double V = dtwice(v), U2 = dtwice(u);
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) {
+    const uint32_t b = c + (uint32_t)(ch * PSTRIDE);
+    const double g0 = lds64(b);
+    const double N = lds64(b - sA);
+    const double Pp = lds64(b + sA);
+    const double Bm = lds64(b - sB);
+    const double Bp = lds64(b + sB);
+    const double Cm = lds64(b - sA - sB);
+    const double Cp = lds64(b - sA + sB);
+    const double sBv = Bm + Bp, dBv = Bm - Bp, sC = Cm + Cp, dC = Cm - Cp;
+    const double A0 = fma(4.0, g0, N + Pp) + sBv;
+    const double L1 = N - Pp;
+    const double Caa2 = fma(2.0, Pp - g0, sC - sBv);
+    const double Cab4 = dC - dBv;
+    const double Cbb2 = fma(-2.0, g0 + N, sC + sBv);
+    const double i1 = fma(u, Caa2, fma(V, Cab4, dtwice(L1)));
+    const double i2 = fma(v, Cbb2, dtwice(dBv));
+    F8[ch] = fma(U2, i1, fma(V, i2, A0));
+  }
+}
+
+template <int NCH, int PSTRIDE>
+__device__ __forceinline__ void pixel_fd_n(uint32_t Sb, int P8, int n1, int n2, const double a[4],
+                                           double out[NCH]) {
+  const double a1 = a[0], a2 = a[1], a3 = a[2], a4 = a[3];
+  const double p2 = a2 * kInvSqrt2, p4 = a4 * kInvSqrt2;
+  const double t1 = 0.5 * a1 + 0.5 * (p2 - p4) - 0.5;
+  const double t2 = 0.5 * a3 + 0.5 * (p2 + p4) - 1.5;
+  const double w = 0.25 / (a1 * a2 * a3 * a4);
+  const double xb = (double)n1 + t1, yb = (double)n2 + t2;
+  double acc[NCH];
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) acc[ch] = 0.0;
+#pragma unroll 1
+  for (int q4 = 0; q4 < 2; ++q4) {
+    const double ox[4] = {q4 ? -p4 : 0.0, q4 ? a1 - p4 : a1, q4 ? p2 - p4 : p2,
+                          q4 ? (a1 + p2) - p4 : a1 + p2};
+    const double oy[4] = {q4 ? p4 : 0.0, q4 ? p2 + p4 : p2, q4 ? a3 + p4 : a3,
+                          q4 ? (p2 + a3) + p4 : p2 + a3};
+    int cx[4];
+    uint32_t cy[4];
+    double dx[4], dy[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int m;
+      lattice_split(xb - ox[k], m, dx[k]);
+      cx[k] = m * 8;
+      lattice_split(yb - oy[k], m, dy[k]);
+      cy[k] = Sb + (uint32_t)(m * P8);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int q1 = j & 1, q2 = (j >> 1) & 1, q3 = (j >> 2) & 1;
+      const int ix = q1 | (q2 << 1), iy = q2 | (q3 << 1);
+      double F8[NCH];
+      zp_read8_n<NCH, PSTRIDE>(cy[iy] + cx[ix], P8, dx[ix], dy[iy], F8);
+      const bool neg = (q1 + q2 + q3 + q4) & 1;
+#pragma unroll
+      for (int ch = 0; ch < NCH; ++ch) acc[ch] = neg ? acc[ch] - F8[ch] : acc[ch] + F8[ch];
+    }
+  }
+#pragma unroll
+  for (int ch = 0; ch < NCH; ++ch) out[ch] = acc[ch] * w;
+}
+
 // Region planning.  A unit is a rectangle of output pixels with its own
 // region (the rectangle grown by the maximum read margins of its pixels).
 // Precision model (measured): the error of a pixel is about
@@ -1140,11 +1223,29 @@ __device__ __forceinline__ void pixel_bound(const FieldSpec &F, int n1, int n2, 
   }
 }
 
-template <int MODE, int DT, int NT>
+// Channels of a multi-channel launch: images (same geometry and dtype as
+// the ImageSpec) and outputs (same row stride as the DomainSpec).
+struct MultiChan {
+  const void *f[3];
+  double *out[3];
+};
+template <int NCH>
+struct TmaMapsN {
+  TmaMaps m[NCH];
+};
+// shared memory per channel region (doubles, 128-byte multiple)
+template <int NCH>
+__host__ __device__ constexpr int wide_cap() {
+  return (kSmemWide / 8 / NCH) & ~15;
+}
+
+template <int MODE, int DT, int NT, int NCH>
 __global__ void __launch_bounds__(NT, 2)
     wide_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int tiles_x32,
                        int region_cap, int *ovf_list, Status *st, double *aslots,
-                       unsigned *slotmask, int tile_base, const __grid_constant__ TmaMaps tm) {
+                       unsigned *slotmask, int tile_base, MultiChan mc,
+                       const __grid_constant__ TmaMapsN<NCH> tm) {
+  constexpr int CAP = wide_cap<NCH>();
   constexpr int NW = NT / 32;
   constexpr int NCX = kWideW / 8, NCY = kWideH / 8;  // 8 x 4 cells of 8 x 8
   extern __shared__ __align__(128) double S[];
@@ -1335,9 +1436,16 @@ __global__ void __launch_bounds__(NT, 2)
     const int P = region_pitch(RW);
     // ---- B: region load (TMA for float64) + running sums
     const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
-    load_region<DT, NT, 0>(S, P, I, rc0, rr0, RW, RH, tid, &tm, mbar, phase);
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ++ch) {
+      ImageSpec Ic = I;
+      Ic.f = mc.f[ch];
+      load_region<DT, NT, 0>(S + ch * CAP, P, Ic, rc0, rr0, RW, RH, tid, &tm.m[ch], mbar, phase);
+    }
     __syncthreads();
-    if (!RUBS_DEV_SKIP_SWEEPS) region_sweeps<NT, 0>(S, P, RW, RH, ghi, tid);
+#pragma unroll 1
+    for (int ch = 0; ch < NCH; ++ch)
+      if (!RUBS_DEV_SKIP_SWEEPS) region_sweeps<NT, 0>(S + ch * CAP, P, RW, RH, ghi, tid);
     // ---- C: 4 x 8-pixel blocks of the unit, warp-strided; the exact
     //         scale-vector of the next block is fetched before this one's
     //         finite differences
@@ -1377,8 +1485,17 @@ __global__ void __launch_bounds__(NT, 2)
         block_px(b + NW, xn, yn);
         fetch(xn, yn, an);
       }
-      if (x < sx + sw && y < sy + sh)
-        D.out[(int64_t)y * D.ld_out + x] = RUBS_DEV_SKIP_GATHER ? ac[0] : pixel_fd(Sb, P, D.pc_lo + x, D.pr_lo + y, ac);
+      if (x < sx + sw && y < sy + sh) {
+        if constexpr (NCH == 1) {
+          D.out[(int64_t)y * D.ld_out + x] =
+              RUBS_DEV_SKIP_GATHER ? ac[0] : pixel_fd(Sb, P, D.pc_lo + x, D.pr_lo + y, ac);
+        } else {
+          double o[NCH];
+          pixel_fd_n<NCH, CAP * 8>(Sb, P * 8, D.pc_lo + x, D.pr_lo + y, ac, o);
+#pragma unroll
+          for (int ch = 0; ch < NCH; ++ch) mc.out[ch][(int64_t)y * D.ld_out + x] = o[ch];
+        }
+      }
     }
     __syncthreads();
   }
@@ -1715,7 +1832,7 @@ int ensure_scratch() {
   RUBS_CUDA_TRY(cudaFuncSetAttribute(pipe_filter_kernel<M, T>,                       \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                      kPipeSmem));                                   \
-  RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<M, T, kThreadsWide>,                       \
+  RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<M, T, kThreadsWide, 1>,                       \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                      kSmemWide))
     RUBS_SET_SMEM(kModeField, 0);
@@ -1727,6 +1844,13 @@ int ensure_scratch() {
     RUBS_SET_SMEM(kModeLut32, 0);
     RUBS_SET_SMEM(kModeLut32, 1);
 #undef RUBS_SET_SMEM
+    // multi-channel instantiations (adaptive_smooth pipeline)
+    RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<kModeUniform, 1, kThreadsWide, 3>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWide));
+    RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<kModeLut, 1, kThreadsWide, 2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWide));
+    RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<kModeLut, 0, kThreadsWide, 2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWide));
     t_scr.attr_set = true;
   }
   return RUBS_OK;
@@ -1801,10 +1925,12 @@ int launch_global_margins(const FieldSpec &F, const DomainSpec &D, cudaStream_t 
 struct TmaCache {
   const void *f = nullptr;
   int64_t ld = 0;
-  int h = 0, w = 0;
+  int h = 0, w = 0, dt = -1;
   TmaMaps maps{};
 };
-thread_local TmaCache t_tma;
+constexpr int kTmaCacheSlots = 8;  // multi-channel launches use several images
+thread_local TmaCache t_tma[kTmaCacheSlots];
+thread_local int t_tma_next = 0;
 
 const TmaMaps &tma_maps(const ImageSpec &I) {
   static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
@@ -1817,9 +1943,11 @@ const TmaMaps &tma_maps(const ImageSpec &I) {
         q == cudaDriverEntryPointSuccess)
       encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   });
-  TmaCache &c = t_tma;
-  if (c.f == I.f && c.ld == I.ld && c.h == I.h && c.w == I.w) return c.maps;
-  c.f = I.f; c.ld = I.ld; c.h = I.h; c.w = I.w;
+  for (TmaCache &e : t_tma)
+    if (e.f == I.f && e.ld == I.ld && e.h == I.h && e.w == I.w && e.dt == I.dt) return e.maps;
+  TmaCache &c = t_tma[t_tma_next];
+  t_tma_next = (t_tma_next + 1) % kTmaCacheSlots;
+  c.f = I.f; c.ld = I.ld; c.h = I.h; c.w = I.w; c.dt = I.dt;
   c.maps.valid = 0;
   if (std::getenv("RUBS_B200_NO_TMA")) return c.maps;
   const bool ok = encode != nullptr && I.dt == 1 && I.w > 0 && I.h > 0 &&
@@ -1849,15 +1977,28 @@ int kernel_choice() {
 }
 
 // Wide-kernel tiles of rows [wy0, wy1) of the 64 x 32 grid over domain D.
-template <int M, int T>
+template <int M, int T, int NCH = 1>
 void launch_wide_rows(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int wy0,
-                      int wy1, cudaStream_t s) {
+                      int wy1, cudaStream_t s, const MultiChan *mcp = nullptr) {
   const int tiles_x = (D.pw + kTile - 1) / kTile;
   const int wx = (D.pw + kWideW - 1) / kWideW;
   if (wy1 <= wy0) return;
-  wide_filter_kernel<M, T, kThreadsWide><<<wx * (wy1 - wy0), kThreadsWide, kSmemWide, s>>>(
-      I, F, D, wx, tiles_x, kSmemWide / 8, t_scr.d_ovf, t_scr.d_status, t_scr.d_aslot,
-      t_scr.d_slotmask, wy0 * wx, tma_maps(I));
+  MultiChan mc{};
+  TmaMapsN<NCH> tm;
+  if (mcp) {
+    mc = *mcp;
+  } else {
+    mc.f[0] = I.f;
+    mc.out[0] = D.out;
+  }
+  for (int ch = 0; ch < NCH; ++ch) {
+    ImageSpec Ic = I;
+    Ic.f = mc.f[ch];
+    tm.m[ch] = tma_maps(Ic);
+  }
+  wide_filter_kernel<M, T, kThreadsWide, NCH><<<wx * (wy1 - wy0), kThreadsWide, kSmemWide, s>>>(
+      I, F, D, wx, tiles_x, wide_cap<NCH>(), t_scr.d_ovf, t_scr.d_status, t_scr.d_aslot,
+      t_scr.d_slotmask, wy0 * wx, mc, tm);
 }
 
 void launch_wide_rows_rt(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int wy0,
@@ -2160,6 +2301,62 @@ int run_filter(const ImageSpec &img, FieldSpec F, int iterations, double *out, i
 // One pass over output rows [out_row0, out_row0 + out_rows) of an image
 // whose rows [I.row0, I.row0 + I.h) are given (row bands);
 // field / parameter arrays hold global rows from F.fr_off on.
+// One pass over an H x W image for several channels that share the field
+// (the adaptive_smooth pipeline): one multi-channel launch, then the
+// deferred tiles of every channel through the single-channel overflow path.
+// Supported: uniform field with 3 float64 channels, LUT field (float64
+// params) with 2 channels; anything else runs channel by channel.
+int run_multi(const ImageSpec &I, const MultiChan &mc, int nch, FieldSpec F, int64_t ld_out,
+              cudaStream_t s) {
+  int rc = ensure_scratch();
+  if (rc) return rc;
+  if (I.h == 0 || I.w == 0) return RUBS_OK;
+  F.FH = I.h;
+  F.FW = I.w;
+  F.div = 1.0;
+  F.scaled = 0;
+  DomainSpec D{0, 0, I.w, I.h, mc.out[0], ld_out};
+  const bool fused = kernel_choice() == 2 &&
+                     ((F.mode == kModeUniform && I.dt == 1 && nch == 3) ||
+                      (F.mode == kModeLut && nch == 2));
+  if (!fused) {
+    for (int ch = 0; ch < nch; ++ch) {
+      ImageSpec Ic = I;
+      Ic.f = mc.f[ch];
+      if ((rc = run_filter(Ic, F, 1, mc.out[ch], ld_out, s))) return rc;
+    }
+    return RUBS_OK;
+  }
+  if ((rc = ensure_ovf(D))) return rc;
+  RUBS_CUDA_TRY(cudaMemsetAsync(t_scr.d_status, 0, sizeof(Status), s));
+  const int wy = (I.h + kWideH - 1) / kWideH;
+  {
+    TimedLaunch tl(0, s);
+    if (F.mode == kModeUniform)
+      launch_wide_rows<kModeUniform, 1, 3>(I, F, D, 0, wy, s, &mc);
+    else if (I.dt == 1)
+      launch_wide_rows<kModeLut, 1, 2>(I, F, D, 0, wy, s, &mc);
+    else
+      launch_wide_rows<kModeLut, 0, 2>(I, F, D, 0, wy, s, &mc);
+  }
+  ++t_launches;
+  RUBS_CUDA_TRY(cudaGetLastError());
+  Status st;
+  if ((rc = fetch_status(s, st))) return rc;
+  if (st.ovf_count > 0 && !(st.flags & (kFlagFieldNonFinite | kFlagParamInvalid))) {
+    for (int ch = 0; ch < nch; ++ch) {
+      ImageSpec Ic = I;
+      Ic.f = mc.f[ch];
+      DomainSpec Dc = D;
+      Dc.out = mc.out[ch];
+      if ((rc = run_overflow(Ic, F, Dc, st.ovf_count, s))) return rc;
+    }
+    RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s));
+    if ((rc = fetch_status(s, st))) return rc;
+  }
+  return status_to_code(st);
+}
+
 int run_band(const ImageSpec &I, FieldSpec F, int64_t H_total, int64_t out_row0,
              int64_t out_rows, double *out, int64_t ld_out, cudaStream_t s) {
   int rc = ensure_scratch();
@@ -2686,4 +2883,40 @@ int rubs_b200_interpolate(const double *plane, int64_t rows, int64_t cols, int64
 namespace rubs_internal {
 int set_error(int code, const std::string &msg) { return ::set_error(code, msg); }
 double lut_rho_max(const rubs_lut *lut) { return lut->rho_max; }
+
+int filter_uniform_multi(const double *const *f, int nch, int64_t H, int64_t W, int64_t ld,
+                         const double a[4], double *const *out, int64_t ld_out, void *stream) {
+  if (nch < 1 || nch > 3) return ::set_error(RUBS_EVALUE, "1 to 3 channels");
+  ImageSpec I{f[0], 1, ld, (int)H, (int)W, 0, 0};
+  FieldSpec F{};
+  F.mode = kModeUniform;
+  for (int k = 0; k < 4; ++k) {
+    F.u[k] = a[k];
+    if (!std::isfinite(a[k])) return ::set_error(RUBS_EVALUE, "scale field entries must be finite");
+  }
+  MultiChan mc{};
+  for (int ch = 0; ch < nch; ++ch) {
+    mc.f[ch] = f[ch];
+    mc.out[ch] = out[ch];
+  }
+  return run_multi(I, mc, nch, F, ld_out, static_cast<cudaStream_t>(stream));
+}
+
+int filter_params_multi(const void *const *f, int f_dtype, int nch, int64_t H, int64_t W,
+                        int64_t ld, const void *size, const void *elong, const void *orient,
+                        int p_dtype, int64_t ld_p, const rubs_lut *lut, double *const *out,
+                        int64_t ld_out, void *stream) {
+  if (nch < 1 || nch > 3) return ::set_error(RUBS_EVALUE, "1 to 3 channels");
+  if (f_dtype != RUBS_F32 && f_dtype != RUBS_F64) return ::set_error(RUBS_EVALUE, "bad dtype");
+  if (p_dtype != RUBS_F32 && p_dtype != RUBS_F64) return ::set_error(RUBS_EVALUE, "bad dtype");
+  if (!lut) return ::set_error(RUBS_EVALUE, "lut is NULL");
+  ImageSpec I{f[0], f_dtype, ld, (int)H, (int)W, 0, 0};
+  FieldSpec F = lut_field(lut, size, elong, orient, p_dtype, ld_p);
+  MultiChan mc{};
+  for (int ch = 0; ch < nch; ++ch) {
+    mc.f[ch] = f[ch];
+    mc.out[ch] = out[ch];
+  }
+  return run_multi(I, mc, nch, F, ld_out, static_cast<cudaStream_t>(stream));
+}
 }  // namespace rubs_internal

@@ -2,6 +2,7 @@
 // (not part of the C ABI).
 #pragma once
 
+#include <cstdint>
 #include <string>
 
 struct rubs_lut;
@@ -14,5 +15,15 @@ int set_error(int code, const std::string &msg);
 
 // Largest elongation of a LUT's rho grid.
 double lut_rho_max(const rubs_lut *lut);
+
+// One filter pass of 1-3 channels (same geometry / dtype / strides) that
+// share the per-pixel kernel: a uniform scale-vector, or LUT parameters.
+// Results equal the single-channel calls bit for bit.
+int filter_uniform_multi(const double *const *f, int nch, int64_t H, int64_t W, int64_t ld,
+                         const double a[4], double *const *out, int64_t ld_out, void *stream);
+int filter_params_multi(const void *const *f, int f_dtype, int nch, int64_t H, int64_t W,
+                        int64_t ld, const void *size, const void *elong, const void *orient,
+                        int p_dtype, int64_t ld_p, const rubs_lut *lut, double *const *out,
+                        int64_t ld_out, void *stream);
 
 }  // namespace rubs_internal

@@ -269,7 +269,8 @@ __global__ void gain_correct_kernel(double *out, int64_t ld_out, const double *g
   }
 }
 
-__global__ void fill_kernel(double *p, int64_t n, double v) {
+template <class T>
+__global__ void fill_kernel(T *p, int64_t n, T v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     p[i] = v;
@@ -338,14 +339,14 @@ int structure_tensor_impl(const void *f, int f_dtype, int64_t H, int64_t W, int6
   RT_CUDA_TRY(cudaGetLastError());
   const double *src[3] = {g[0], g[1], g[2]};
   if (window_sigma > 0.0) {
-    // isotropic scale-vector c (1,1,1,1): covariance c^2/6 I (tensor.py:72-74)
+    // isotropic scale-vector c (1,1,1,1): covariance c^2/6 I (tensor.py:72-74);
+    // the three channels share the kernel: one three-channel pass
     const double c = std::max(window_sigma * std::sqrt(6.0), kScaleFloor);
     const double a[4] = {c, c, c, c};
-    for (int k = 0; k < 3; ++k) {
-      double *dst = (double *)b[3 + k];
-      if ((rc = rubs_b200_filter(g[k], RUBS_F64, H, W, W, a, 1, 0, 1, dst, W, s))) return rc;
-      src[k] = dst;
-    }
+    double *dst[3] = {(double *)b[3], (double *)b[4], (double *)b[5]};
+    const double *chans[3] = {g[0], g[1], g[2]};
+    if ((rc = rubs_internal::filter_uniform_multi(chans, 3, H, W, W, a, dst, W, s))) return rc;
+    for (int k = 0; k < 3; ++k) src[k] = dst[k];
   }
   interleave3_kernel<<<grid_for(n), 256, 0, s>>>(src[0], src[1], src[2], n, j);
   RT_CUDA_TRY(cudaGetLastError());
@@ -406,15 +407,27 @@ int rubs_b200_adaptive_smooth(const void *f, int f_dtype, int64_t H, int64_t W, 
                             rubs_internal::lut_rho_max(lut) * (1.0 - 1e-9), size, rho, theta,
                             nullptr, s)))
     return rc;
-  // out = filter(f), gain = filter(1) with the same per-pixel kernels
-  if ((rc = rubs_b200_filter_params(f, f_dtype, H, W, ld_f, size, rho, theta, RUBS_F64, W, lut,
-                                    iterations, out, ld_out, s)))
-    return rc;
-  fill_kernel<<<grid_for(n), 256, 0, s>>>(ones, n, 1.0);
+  // out = filter(f), gain = filter(1) with the same per-pixel kernels: one
+  // two-channel pass (a flat image of f's dtype next to f) when possible
+  if (f_dtype == RUBS_F32)
+    fill_kernel<float><<<grid_for(n), 256, 0, s>>>(reinterpret_cast<float *>(ones), n, 1.0f);
+  else
+    fill_kernel<double><<<grid_for(n), 256, 0, s>>>(ones, n, 1.0);
   RT_CUDA_TRY(cudaGetLastError());
-  if ((rc = rubs_b200_filter_params(ones, RUBS_F64, H, W, W, size, rho, theta, RUBS_F64, W, lut,
-                                    iterations, gain, W, s)))
-    return rc;
+  if (iterations == 1 && ld_f == W && ld_out == W) {
+    const void *chans[2] = {f, ones};
+    double *dst[2] = {out, gain};
+    if ((rc = rubs_internal::filter_params_multi(chans, f_dtype, 2, H, W, W, size, rho, theta,
+                                                 RUBS_F64, W, lut, dst, W, s)))
+      return rc;
+  } else {
+    if ((rc = rubs_b200_filter_params(f, f_dtype, H, W, ld_f, size, rho, theta, RUBS_F64, W, lut,
+                                      iterations, out, ld_out, s)))
+      return rc;
+    if ((rc = rubs_b200_filter_params(ones, f_dtype, H, W, W, size, rho, theta, RUBS_F64, W, lut,
+                                      iterations, gain, W, s)))
+      return rc;
+  }
   gain_correct_kernel<<<grid_for(n), 256, 0, s>>>(out, ld_out, gain, (int)H, (int)W);
   RT_CUDA_TRY(cudaGetLastError());
   return RUBS_OK;
