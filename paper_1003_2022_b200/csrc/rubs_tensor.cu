@@ -137,14 +137,21 @@ struct SelectPass {
   int shift;  // bits below the byte being counted
 };
 
-__global__ void select_hist_kernel(const double *j, int64_t n, SelectPass sp, unsigned *hist) {
+// tr = J11 + J22 (tensor.py:117), compacted once for the select passes
+__global__ void trace_kernel(const double *j, int64_t n, double *tr) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    tr[i] = j[3 * i] + j[3 * i + 2];
+}
+
+__global__ void select_hist_kernel(const double *tr, int64_t n, SelectPass sp, unsigned *hist) {
   __shared__ unsigned h[4][256];
   for (int t = threadIdx.x; t < 4 * 256; t += blockDim.x) (&h[0][0])[t] = 0;
   __syncthreads();
   const int hi = sp.shift + 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = order_key(j[3 * i] + j[3 * i + 2]);  // tr = J11 + J22 (tensor.py:117)
+    const uint64_t k = order_key(tr[i]);
     const unsigned byte = (unsigned)(k >> sp.shift) & 255u;
     for (int r = 0; r < sp.nr; ++r)
       if (hi >= 64 || (k >> hi) == (sp.prefix[r] >> hi)) atomicAdd(&h[r][byte], 1u);
@@ -156,8 +163,8 @@ __global__ void select_hist_kernel(const double *j, int64_t n, SelectPass sp, un
   }
 }
 
-// values[r] = the element of rank ranks[r] (0-based, ascending) of the trace
-int select_trace(const double *j, int64_t n, const int64_t *ranks, int nr, double *values,
+// values[r] = the element of rank ranks[r] (0-based, ascending) of tr
+int select_trace(const double *tr, int64_t n, const int64_t *ranks, int nr, double *values,
                  cudaStream_t s) {
   if (!t_ts.d_hist) {
     RT_CUDA_TRY(cudaMalloc(&t_ts.d_hist, 4 * 256 * sizeof(unsigned)));
@@ -174,7 +181,7 @@ int select_trace(const double *j, int64_t n, const int64_t *ranks, int nr, doubl
   for (int shift = 56; shift >= 0; shift -= 8) {
     sp.shift = shift;
     RT_CUDA_TRY(cudaMemsetAsync(t_ts.d_hist, 0, 4 * 256 * sizeof(unsigned), s));
-    select_hist_kernel<<<grid, 256, 0, s>>>(j, n, sp, t_ts.d_hist);
+    select_hist_kernel<<<grid, 256, 0, s>>>(tr, n, sp, t_ts.d_hist);
     RT_CUDA_TRY(cudaGetLastError());
     RT_CUDA_TRY(cudaMemcpyAsync(t_ts.h_hist, t_ts.d_hist, nr * 256 * sizeof(unsigned),
                                 cudaMemcpyDeviceToHost, s));
@@ -305,8 +312,12 @@ int anisotropy_impl(const double *j, int64_t H, int64_t W, double noise_sigma,
   percentile_ranks(n, 95.0, r95lo, r95hi, t95);
   const int64_t ranks[4] = {r5lo, r5hi, r95lo, r95hi};
   double v[4];
-  int rc = select_trace(j, n, ranks, 4, v, s);
+  void *trb;
+  int rc = tbuf(0, n * sizeof(double), &trb);
   if (rc) return rc;
+  trace_kernel<<<grid_for(n), 256, 0, s>>>(j, n, static_cast<double *>(trb));
+  RT_CUDA_TRY(cudaGetLastError());
+  if ((rc = select_trace(static_cast<const double *>(trb), n, ranks, 4, v, s))) return rc;
   p.q05 = lerp_np(v[0], v[1], t5);
   p.q95 = lerp_np(v[2], v[3], t95);
   p.has_spread = (p.q95 - p.q05) > 1e-300;
