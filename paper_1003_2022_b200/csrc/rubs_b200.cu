@@ -208,7 +208,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t phase) {
   asm volatile(
       "{\n .reg .pred p;\n"
       "RUBS_MBAR_WAIT%=:\n"
-      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n"
       " @!p bra RUBS_MBAR_WAIT%=;\n}" ::"r"(mbar),
       "r"(phase)
       : "memory");
@@ -1451,10 +1451,18 @@ __global__ void __launch_bounds__(NT, 2)
     //         finite differences
     const uint32_t Sb = sbase - (uint32_t)((rr0 * P + rc0) * 8);
     const int nbx = (sw + 3) >> 2, nblk = nbx * ((sh + 7) >> 3);
-    auto block_px = [&](int b, int &x, int &y) {
-      const int by = b / nbx, bx = b - by * nbx;
+    // block b = by * nbx + bx, walked in steps of NW without a division:
+    // (cbx, cby) is the current block, (nbx_, nby_) the next one
+    auto block_xy = [&](int bx, int by, int &x, int &y) {
       x = sx + 4 * bx + (lane & 3);
       y = sy + 8 * by + (lane >> 2);
+    };
+    auto advance = [&](int &bx, int &by) {
+      bx += NW;
+      while (bx >= nbx) {
+        bx -= nbx;
+        ++by;
+      }
     };
     auto fetch = [&](int x, int y, double a[4]) {
       x = min(x, sx + sw - 1);
@@ -1469,20 +1477,26 @@ __global__ void __launch_bounds__(NT, 2)
       }
     };
     int b = warp;
+    int cbx = warp, cby = 0;
+    while (cbx >= nbx) {
+      cbx -= nbx;
+      ++cby;
+    }
     double an[4] = {1.0, 1.0, 1.0, 1.0};
     if (b < nblk) {
       int x, y;
-      block_px(b, x, y);
+      block_xy(cbx, cby, x, y);
       fetch(x, y, an);
     }
 #pragma unroll 1
     for (; b < nblk; b += NW) {
       double ac[4] = {an[0], an[1], an[2], an[3]};
       int x, y;
-      block_px(b, x, y);
+      block_xy(cbx, cby, x, y);
+      advance(cbx, cby);
       if (b + NW < nblk) {
         int xn, yn;
-        block_px(b + NW, xn, yn);
+        block_xy(cbx, cby, xn, yn);
         fetch(xn, yn, an);
       }
       if (x < sx + sw && y < sy + sh) {
@@ -1820,6 +1834,14 @@ int ensure_scratch() {
                                                  sizeof(double)));
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_slotmask, kMaxSmId * sizeof(unsigned)));
     RUBS_CUDA_TRY(cudaMemset(t_scr.d_slotmask, 0, kMaxSmId * sizeof(unsigned)));
+    {  // log table of log_ge1 (rubs_device.cuh)
+      double2 tab[128];
+      for (int i = 0; i < 128; ++i) {
+        const double c = 1.0 + (i + 0.5) / 128.0;
+        tab[i] = make_double2(1.0 / c, std::log(c));
+      }
+      RUBS_CUDA_TRY(cudaMemcpyToSymbol(g_logtab, tab, sizeof tab));
+    }
   }
   if (!t_scr.attr_set) {
 #define RUBS_SET_SMEM(M, T)                                                          \
