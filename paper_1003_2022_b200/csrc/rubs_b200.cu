@@ -876,279 +876,6 @@ __global__ void __launch_bounds__(kThreadsLarge, 1)
 }
 
 // ---------------------------------------------------------------------------
-// Warp-specialised pipeline (experimental, RUBS_B200_KERNEL=pipe; measured
-// slower than the two-CTA tile kernel -- DESIGN.md).
-//
-// One persistent CTA per SM, 16 warps: warps 0-3 produce, warps 4-15
-// consume, through two 112 KB region buffers.  For tile i+1 the producers
-// bound its read margins, plan its region, copy the image into a free
-// buffer (cp.async) and run the four running sums; meanwhile the consumers
-// map tile i's scale-vectors (the LUT runs once per pixel, here) and take
-// its 16-vertex finite differences.  Hand-off through named barriers:
-// FULL[b] (producers arrive, consumers wait), EMPTY[b] (the reverse).
-
-#ifndef RUBS_PIPE_PROD
-#define RUBS_PIPE_PROD 256
-#endif
-constexpr int kPipeProd = RUBS_PIPE_PROD;       // producer threads
-constexpr int kPipeCons = 512 - kPipeProd;      // consumer threads
-constexpr int kPipeBuf = 112 * 1024 / 8;        // doubles per region buffer
-constexpr int kPipeSmem = 2 * kPipeBuf * 8;     // dynamic shared memory
-constexpr int kBarProd = 1, kBarFull = 2, kBarEmpty = 4;  // named barrier ids
-
-__device__ __forceinline__ void nbar_sync(int id, int n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void nbar_arrive(int id, int n) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-// Upper bound of a pixel's read margins without running the LUT:
-// hx = (a1 + (a2 + a4) / sqrt2) / 2 <= 3 sqrt(C11) (Cauchy-Schwarz on
-// C11 = (2 a1^2 + a2^2 + a4^2) / 24), where the table's bilinear blend keeps
-// C11 below the largest corner node's, i.e. below the target's + 0.04 size;
-// the 0.05 floor adds at most 0.0604, the pass scaling divides by sqrt(m).
-template <int PDT>
-__device__ __forceinline__ int4 lut_margin_bound(const FieldSpec &F, int n1, int n2) {
-  const int fc = min(max(n1, 0), F.FW - 1), fr = min(max(n2, 0), F.FH - 1) - F.fr_off;
-  const int64_t i = (int64_t)fr * F.pld + fc;
-  float sz = (float)load_px<PDT>(F.ps, i), rho = (float)load_px<PDT>(F.pr, i);
-  float th = (float)load_px<PDT>(F.pt, i);
-  if (!(sz > 0.f && sz < INFINITY)) sz = 1.f;
-  if (!(rho >= 1.f && rho < INFINITY)) rho = 1.f;
-  if (!(th >= 0.f && th < 3.1416f)) th = 0.f;
-  rho = fminf(rho, (float)F.rho_max);
-  float sn, c;
-  __sincosf(th, &sn, &c);  // |error| < 1e-6, far inside the 0.04 slack
-  const float inv = __frcp_rn(1.0f + rho);
-  const float c11 = (rho * c * c + sn * sn) * inv + 0.04f;
-  const float c22 = (rho * sn * sn + c * c) * inv + 0.04f;
-  const float k = (float)(1.0 / F.div) * 1.0002f;
-  const float hx = (3.0f * sqrtf(sz * c11) * 1.001f + 0.0605f) * k;
-  const float hy = (3.0f * sqrtf(sz * c22) * 1.001f + 0.0605f) * k;
-  return margins_from_extent(hx, hy);
-}
-
-struct UnitPlan {
-  int sx, sy, sw, sh;  // output rectangle (pass-domain pixels)
-  int P, rc0, rr0;     // region pitch and lattice of element (0, 0)
-  int nbx, nblk;       // 4x8 blocks across, total (-1: end of work)
-  int tile;
-  int m[4];            // unit margins (for a precision re-run)
-  float l4;            // region L4 (precision model)
-};
-
-// Precision guard of the pipeline: a consumer whose pixel's w * L4 exceeds
-// the budget in the unit's region flags the unit (max w in s_pw[buf]); the
-// producer, reclaiming the buffer, records the unit's tile once for the
-// overflow pass, which recomputes it with precision-split regions.  At most
-// four records per tile (one per unit).
-__device__ __forceinline__ void pipe_precision_flag(const UnitPlan &up, const double a[4],
-                                                    int *pw) {
-  const float w = 1.0f / (float)(a[0] * a[1] * a[2] * a[3]);
-  if (w * up.l4 > kPrecisionBudget) atomicMax(pw, __float_as_int(w));
-}
-
-__device__ __forceinline__ void pipe_reclaim(const UnitPlan &up, int *pw, int *ovf_list,
-                                             Status *st) {
-  if (*pw) {
-    OvfRec r;
-    r.tile = up.tile;
-    for (int j = 0; j < 4; ++j) r.m[j] = up.m[j];
-    r.w = __int_as_float(*pw);
-    reinterpret_cast<OvfRec *>(ovf_list)[atomicAdd(&st->ovf_count, 1)] = r;
-    *pw = 0;
-  }
-}
-
-template <int MODE, int DT>
-__global__ void __launch_bounds__(kPipeProd + kPipeCons, 1)
-    pipe_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int ntiles,
-                       int *ovf_list, Status *st, const __grid_constant__ TmaMaps tm) {
-  extern __shared__ __align__(128) double S[];
-  __shared__ uint64_t s_mbar;
-  __shared__ UnitPlan plan[2];
-  __shared__ int s_m[4][4];
-  __shared__ int s_u[4][8];
-  __shared__ int s_nu;
-  __shared__ int s_pw[2];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  unsigned ghi = 0, flags = 0;
-  constexpr int NB = kPipeProd + kPipeCons;
-  const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
-  if (tid < 2) s_pw[tid] = 0;
-  if (tid == 0) mbar_init(mbar);
-  __syncthreads();
-
-  if (warp < kPipeProd / 32) {
-    // ================================================================ producer
-    int buf = 0;
-    uint32_t phase = 0;
-    bool used[2] = {false, false};
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-      const int tx = tile % tiles_x, ty = tile / tiles_x;
-      const int x0 = tx * kTile, y0 = ty * kTile;
-      if (tid < 16) s_m[tid >> 2][tid & 3] = 0;
-      nbar_sync(kBarProd, kPipeProd);
-      constexpr int NWP = kPipeProd / 32;
-      const int ly = tid >> 5;  // pixel rows ly + NWP k
-      int4 mh[2] = {make_int4(0, 0, 0, 0), make_int4(0, 0, 0, 0)};
-#pragma unroll
-      for (int k = 0; k < (32 + NWP - 1) / NWP; ++k) {
-        const int x = x0 + lane, y = y0 + ly + NWP * k;
-        if (ly + NWP * k < kTile && x < D.pw && y < D.ph) {
-          int4 m;
-          if constexpr (MODE >= kModeLut) {
-            m = lut_margin_bound<MODE == kModeLut ? 1 : 0>(F, D.pc_lo + x, D.pr_lo + y);
-          } else {
-            double a[4];
-            unsigned fl = 0;
-            field_at<MODE>(F, D.pc_lo + x, D.pr_lo + y, a, fl);
-            m = pixel_margins_fast(a);
-          }
-          const int h = (ly + NWP * k) >= 16 ? 1 : 0;
-          mh[h].x = max(mh[h].x, m.x);
-          mh[h].y = max(mh[h].y, m.y);
-          mh[h].z = max(mh[h].z, m.z);
-          mh[h].w = max(mh[h].w, m.w);
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int4 m = mh[h];
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {
-          m.x = max(m.x, __shfl_xor_sync(0xffffffffu, m.x, o));
-          m.y = max(m.y, __shfl_xor_sync(0xffffffffu, m.y, o));
-          m.z = max(m.z, __shfl_xor_sync(0xffffffffu, m.z, o));
-          m.w = max(m.w, __shfl_xor_sync(0xffffffffu, m.w, o));
-        }
-        if ((lane & 15) == 0) {
-          const int q = (lane >> 4) + 2 * h;
-          atomicMax(&s_m[q][0], m.x);
-          atomicMax(&s_m[q][1], m.y);
-          atomicMax(&s_m[q][2], m.z);
-          atomicMax(&s_m[q][3], m.w);
-        }
-      }
-      nbar_sync(kBarProd, kPipeProd);
-      if (tid == 0) {
-        const int tw = min(kTile, D.pw - x0), th = min(kTile, D.ph - y0);
-        int u[4] = {0, 0, 0, 0};
-        for (int q = 0; q < 4; ++q)
-          for (int j = 0; j < 4; ++j) u[j] = max(u[j], s_m[q][j]);
-        const int RW = tw + u[0] + u[1], RH = th + u[2] + u[3];
-        int n = 0;
-        if (region_elems(RW + 1, RH) <= kPipeBuf) {
-          int *d = s_u[n++];
-          d[0] = x0; d[1] = y0; d[2] = tw; d[3] = th; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
-        } else {
-          bool fits = true;
-          for (int q = 0; q < 4; ++q) {
-            const int sx = x0 + (q & 1) * 16, sy = y0 + (q >> 1) * 16;
-            if (sx >= D.pw || sy >= D.ph) continue;
-            const int sw = min(16, D.pw - sx), sh = min(16, D.ph - sy);
-            int *d = s_u[n++];
-            d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = s_m[q][0]; d[5] = s_m[q][2];
-            d[6] = sw + s_m[q][0] + s_m[q][1];
-            d[7] = sh + s_m[q][2] + s_m[q][3];
-            fits = fits && (region_elems(d[6] + 1, d[7]) <= kPipeBuf);
-          }
-          if (!fits) {
-            OvfRec r;
-            r.tile = tile;
-            for (int j = 0; j < 4; ++j) r.m[j] = u[j];
-            r.w = 0.f;
-            reinterpret_cast<OvfRec *>(ovf_list)[atomicAdd(&st->ovf_count, 1)] = r;
-            n = 0;
-          }
-        }
-        s_nu = n;
-      }
-      nbar_sync(kBarProd, kPipeProd);
-      const int nu = s_nu;
-      for (int ui = 0; ui < nu; ++ui) {
-        const int sx = s_u[ui][0], sy = s_u[ui][1], sw = s_u[ui][2], sh = s_u[ui][3];
-        const int below = s_u[ui][5], RH = s_u[ui][7];
-        int left = s_u[ui][4], RW = s_u[ui][6];
-        align_region<DT>(I, D.pc_lo + sx, left, RW);
-        const int P = region_pitch(RW);
-        const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
-        if (used[buf]) {
-          nbar_sync(kBarEmpty + buf, NB);
-          if (tid == 0) pipe_reclaim(plan[buf], &s_pw[buf], ovf_list, st);
-        }
-        double *B = S + buf * kPipeBuf;
-        load_region<DT, kPipeProd, kBarProd>(B, P, I, rc0, rr0, RW, RH, tid, &tm, mbar, phase);
-        if (tid == 0) {
-          UnitPlan up;
-          up.sx = sx; up.sy = sy; up.sw = sw; up.sh = sh;
-          up.P = P; up.rc0 = rc0; up.rr0 = rr0;
-          up.nbx = (sw + 3) / 4;
-          up.nblk = up.nbx * ((sh + 7) / 8);
-          up.tile = tile;
-          up.m[0] = left; up.m[1] = RW - sw - left; up.m[2] = below; up.m[3] = RH - sh - below;
-          const float mn = (float)min(RW, RH);
-          up.l4 = 0.25f * (float)RW * (float)RH * mn * mn;
-          plan[buf] = up;
-        }
-        nbar_sync(kBarProd, kPipeProd);
-        region_sweeps<kPipeProd, kBarProd>(B, P, RW, RH, ghi, tid);
-        __threadfence_block();
-        nbar_arrive(kBarFull + buf, NB);
-        used[buf] = true;
-        buf ^= 1;
-      }
-    }
-    // end of work through the next buffer; balance the EMPTY arrivals
-    if (used[buf]) {
-      nbar_sync(kBarEmpty + buf, NB);
-      if (tid == 0) pipe_reclaim(plan[buf], &s_pw[buf], ovf_list, st);
-    }
-    if (tid == 0) plan[buf].nblk = -1;
-    __threadfence_block();
-    nbar_arrive(kBarFull + buf, NB);
-    if (used[buf ^ 1]) {
-      nbar_sync(kBarEmpty + (buf ^ 1), NB);
-      if (tid == 0) pipe_reclaim(plan[buf ^ 1], &s_pw[buf ^ 1], ovf_list, st);
-    }
-  } else {
-    // ================================================================ consumer
-    // the 4x8-pixel blocks of all units form one stream; consumer warp cw
-    // takes blocks cw, cw + 12, cw + 24, ... of it
-    constexpr int NCW = kPipeCons / 32;
-    const int cw = warp - kPipeProd / 32;
-    const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(S);
-    int buf = 0, cum = 0;
-    for (;;) {
-      nbar_sync(kBarFull + buf, NB);
-      const UnitPlan up = plan[buf];
-      if (up.nblk < 0) break;
-      const uint32_t Sb = sbase + (uint32_t)(buf * kPipeBuf) * 8u -
-                          (uint32_t)((up.rr0 * up.P + up.rc0) * 8);
-      int j = cum + (((cw - cum) % NCW) + NCW) % NCW;
-#pragma unroll 1
-      for (; j < cum + up.nblk; j += NCW) {
-        const int b = j - cum;
-        const int by = b / up.nbx, bx = b - by * up.nbx;
-        const int x = up.sx + 4 * bx + (lane & 3), y = up.sy + 8 * by + (lane >> 2);
-        if (x < up.sx + up.sw && y < up.sy + up.sh) {
-          const int n1 = D.pc_lo + x, n2 = D.pr_lo + y;
-          double a[4];
-          field_at<MODE>(F, n1, n2, a, flags);
-          pipe_precision_flag(up, a, &s_pw[buf]);
-          D.out[(int64_t)y * D.ld_out + x] = pixel_fd(Sb, up.P, n1, n2, a);
-        }
-      }
-      cum += up.nblk;
-      nbar_arrive(kBarEmpty + buf, NB);
-      buf ^= 1;
-    }
-  }
-  flush_status(st, ghi, flags);
-}
-
-// ---------------------------------------------------------------------------
 // Primary launch: 64 x 32-pixel tiles, two CTAs of 256 threads per SM.
 //
 // A wide tile halves the halo overhead of a 32 x 32 one at config-2 margins
@@ -1174,53 +901,17 @@ constexpr int kThreadsWide = RUBS_WIDE_THREADS;  // 2 CTAs per SM
 
 // Planning bounds of one pixel: read margins (left, right, below, above)
 // covering its taps, and an upper bound of w = 1 / (a1 a2 a3 a4).
+// Read margins and w = 1 / (a1 a2 a3 a4) of one pixel whose scale-vector
+// comes from a field or a uniform vector (LUT modes compute the exact
+// mapping in phase A and park it instead).
 template <int MODE>
 __device__ __forceinline__ void pixel_bound(const FieldSpec &F, int n1, int n2, int4 &m,
                                             float &w) {
-  if constexpr (MODE >= kModeLut) {
-    // the LUT mapping of lut_map in float32 (quarter index exact, in fp64:
-    // it is the one discontinuous choice), accurate to ~1e-6 relative
-    constexpr int PDT = MODE == kModeLut ? 1 : 0;
-    const int fc = min(max(n1, 0), F.FW - 1), fr = min(max(n2, 0), F.FH - 1) - F.fr_off;
-    const int64_t i = (int64_t)fr * F.pld + fc;
-    const double thd = load_px<PDT>(F.pt, i);
-    float sz = (float)load_px<PDT>(F.ps, i), rho = (float)load_px<PDT>(F.pr, i);
-    if (!(sz > 0.f && sz < INFINITY)) sz = 1.f;
-    if (!(rho >= 1.f && rho < INFINITY)) rho = 1.f;
-    const bool thok = thd >= 0.0 && thd < kPi;
-    const int q = thok ? quarter_index(thd) : 0;
-    const float phi = thok ? (float)(thd - (double)q * kQuarter) : 0.f;
-    const int nr = F.n_rho, np_ = F.n_phi;
-    float u = __logf(rho) * (float)F.inv_log_rho_max * (float)(nr - 1);
-    float v = phi * (float)(np_ / kQuarter) - 0.5f;
-    u = fminf(fmaxf(u, 0.f), (float)(nr - 1));
-    v = fminf(fmaxf(v, 0.f), (float)(np_ - 1));
-    const int i0 = min((int)u, nr - 2), j0 = min((int)v, np_ - 2);
-    const float fu = u - (float)i0, fv = v - (float)j0;
-    const float4 *e00 =
-        reinterpret_cast<const float4 *>(F.lutf) + ((int64_t)q * nr + i0) * np_ + j0;
-    const float4 A = __ldg(e00), C = __ldg(e00 + 1), B = __ldg(e00 + np_), Dd = __ldg(e00 + np_ + 1);
-    const float w00 = (1.f - fu) * (1.f - fv), w10 = fu * (1.f - fv), w01 = (1.f - fu) * fv,
-                w11 = fu * fv;
-    const float ss = sqrtf(sz), inv_div = (float)(1.0 / F.div);
-    float af[4] = {A.x * w00 + B.x * w10 + C.x * w01 + Dd.x * w11,
-                   A.y * w00 + B.y * w10 + C.y * w01 + Dd.y * w11,
-                   A.z * w00 + B.z * w10 + C.z * w01 + Dd.z * w11,
-                   A.w * w00 + B.w * w10 + C.w * w01 + Dd.w * w11};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) af[k] = fmaxf(af[k] * ss, (float)kScaleFloor) * inv_div;
-    const float d = (af[1] + af[3]) * 0.70710678f;
-    const float hx = 0.5f * (af[0] + d) * 1.00002f + 2e-4f;
-    const float hy = 0.5f * (af[2] + d) * 1.00002f + 2e-4f;
-    m = margins_from_extent(hx, hy);
-    w = 1.0002f / (af[0] * af[1] * af[2] * af[3]);
-  } else {
-    double a[4];
-    unsigned fl = 0;
-    field_at<MODE>(F, n1, n2, a, fl);
-    m = pixel_margins_fast(a);
-    w = 1.0f / (float)(a[0] * a[1] * a[2] * a[3]);
-  }
+  double a[4];
+  unsigned fl = 0;
+  field_at<MODE>(F, n1, n2, a, fl);
+  m = pixel_margins_fast(a);
+  w = 1.0f / (float)(a[0] * a[1] * a[2] * a[3]);
 }
 
 // Channels of a multi-channel launch: images (same geometry and dtype as
@@ -1851,9 +1542,6 @@ int ensure_scratch() {
   RUBS_CUDA_TRY(cudaFuncSetAttribute(tile_overflow_kernel<M, T>,                     \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                      kSmemLarge));                                  \
-  RUBS_CUDA_TRY(cudaFuncSetAttribute(pipe_filter_kernel<M, T>,                       \
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                     kPipeSmem));                                   \
   RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<M, T, kThreadsWide, 1>,                       \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,   \
                                      kSmemWide))
@@ -1993,7 +1681,7 @@ int kernel_choice() {
   static int choice = -1;
   if (choice < 0) {
     const char *e = std::getenv("RUBS_B200_KERNEL");
-    choice = (e && std::strcmp(e, "pipe") == 0) ? 0 : (e && std::strcmp(e, "tile") == 0) ? 1 : 2;
+    choice = (e && std::strcmp(e, "tile") == 0) ? 1 : 2;
   }
   return choice;
 }
@@ -2046,11 +1734,8 @@ void launch_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, c
   const int tiles_x = (D.pw + kTile - 1) / kTile, tiles_y = (D.ph + kTile - 1) / kTile;
   const int ntiles = tiles_x * tiles_y;
   cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s);
-  if (kernel_choice() == 2) {
+  if (kernel_choice() == 2)
     launch_wide_rows<M, T>(I, F, D, 0, (D.ph + kWideH - 1) / kWideH, s);
-  } else if (kernel_choice() == 0)
-    pipe_filter_kernel<M, T><<<std::min(ntiles, t_scr.sms), kPipeProd + kPipeCons, kPipeSmem, s>>>(
-        I, F, D, tiles_x, ntiles, t_scr.d_ovf, t_scr.d_status, tma_maps(I));
   else
     tile_filter_kernel<M, T><<<ntiles, kThreadsSmall, kSmemSmall, s>>>(
         I, F, D, tiles_x, kSmemSmall / 8, t_scr.d_ovf, t_scr.d_status, tma_maps(I));
@@ -2079,7 +1764,8 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
   RUBS_CUDA_TRY(cudaMemcpyAsync(raw.data(), t_scr.d_ovf, n_ovf * sizeof(OvfRec),
                                 cudaMemcpyDeviceToHost, s));
   RUBS_CUDA_TRY(cudaStreamSynchronize(s));
-  // one record per tile (the pipeline records a tile once per unit)
+  // one record per 32-pixel tile (the wide kernel records both halves of a
+  // 64 x 32 tile separately)
   std::sort(raw.begin(), raw.end(), [](const OvfRec &a, const OvfRec &b) { return a.tile < b.tile; });
   std::vector<OvfRec> recs;
   for (const OvfRec &r : raw) {
@@ -2217,7 +1903,7 @@ int run_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, in
 }
 
 // Overflow-record capacity for a pass over D: at most one record per tile
-// of the 32-pixel grid (tile kernel) or per unit (pipeline).
+// of the 32-pixel grid.
 int ensure_ovf(const DomainSpec &D) {
   const size_t ntiles = (size_t)((D.pw + kTile - 1) / kTile) * ((D.ph + kTile - 1) / kTile);
   if (4 * ntiles > t_scr.ovf_cap) {
@@ -2538,7 +2224,6 @@ bool streamable(int iterations, int64_t H, int64_t W) {
 
 struct rubs_lut {
   double *entries = nullptr;
-  float *lutf = nullptr;
   int n_rho = 0, n_phi = 0;
   double rho_max = 0.0;
 };
@@ -2554,7 +2239,6 @@ FieldSpec lut_field(const rubs_lut *lut, const void *size, const void *elong, co
   F.pdt = p_dtype;
   F.pld = ld_p;
   F.lut = lut->entries;
-  F.lutf = lut->lutf;
   F.n_rho = lut->n_rho;
   F.n_phi = lut->n_phi;
   F.rho_max = lut->rho_max;
@@ -2672,16 +2356,10 @@ int rubs_b200_lut_create(const double *rho_grid, const double *phi_grid, const d
     for (size_t e = 0; e < (size_t)n_rho * n_phi; ++e)
       for (int k = 0; k < 4; ++k) rolled[q * per + e * 4 + k] = entries[e * 4 + ((k - q + 4) & 3)];
   size_t bytes = rolled.size() * sizeof(double);
-  // float32 copy for the planning pass (float4 per entry, same layout)
-  std::vector<float> rolledf(rolled.begin(), rolled.end());
   cudaError_t e = cudaMalloc(&L->entries, bytes);
   if (e == cudaSuccess) e = cudaMemcpy(L->entries, rolled.data(), bytes, cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMalloc(&L->lutf, rolledf.size() * sizeof(float));
-  if (e == cudaSuccess)
-    e = cudaMemcpy(L->lutf, rolledf.data(), rolledf.size() * sizeof(float), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     if (L->entries) cudaFree(L->entries);
-    if (L->lutf) cudaFree(L->lutf);
     delete L;
     return set_error(RUBS_ECUDA, std::string("lut upload: ") + cudaGetErrorString(e));
   }
@@ -2692,7 +2370,6 @@ int rubs_b200_lut_create(const double *rho_grid, const double *phi_grid, const d
 void rubs_b200_lut_destroy(rubs_lut *lut) {
   if (!lut) return;
   if (lut->entries) cudaFree(lut->entries);
-  if (lut->lutf) cudaFree(lut->lutf);
   delete lut;
 }
 

@@ -58,7 +58,6 @@ struct FieldSpec {
   int pdt;  // 0 f32, 1 f64
   int64_t pld;
   const double *lut;  // (n_rho, n_phi, 4)
-  const float *lutf;  // float32 copy (planning pass)
   int n_rho, n_phi;
   double rho_max, log_rho_max, inv_log_rho_max;
   double phi_scale;  // n_phi / (pi / 4)
