@@ -156,12 +156,14 @@ __global__ void __launch_bounds__(256) global_margins_kernel(FieldSpec F, Domain
 // of the region is in flight at once.  float32 images: eight loads in flight
 // per thread, widened to fp64 on the way.
 
-// Synchronise the NT threads of a group: the whole CTA (BAR 0) or a named
-// barrier shared by a warp-specialised subset.
+// Synchronise the NT threads of a group: the whole CTA (BAR 0), one warp
+// (BAR -1) or a named barrier shared by a subset of warps.
 template <int NT, int BAR>
 __device__ __forceinline__ void group_sync() {
   if constexpr (BAR == 0)
     __syncthreads();
+  else if constexpr (BAR < 0)
+    __syncwarp();  // a one-warp group
   else
     asm volatile("bar.sync %0, %1;" ::"n"(BAR), "n"(NT) : "memory");
 }
@@ -646,6 +648,31 @@ __device__ __forceinline__ void pixel_fd_n(uint32_t Sb, int P8, int n1, int n2, 
 #endif
 constexpr float kPrecisionBudget = RUBS_PREC_BUDGET;  // w * L4 (see above)
 
+// Per-pixel precision fallback.  The overflow passes share one region among
+// many pixels; a pixel whose weight w = 1/(a1 a2 a3 a4) is large (a small,
+// partly floored kernel) next to huge kernels would exceed the precision
+// budget w L4 in that region.  Such pixels are listed and computed one per
+// warp, each with the region of its own taps (pixel_kernel).
+constexpr int kPixSlab = 3072;  // doubles of shared memory per warp (24 KB)
+
+__device__ __forceinline__ bool defer_pixel(const double a[4], float l4, int x, int y, int2 *pix,
+                                            int pix_cap, Status *st) {
+  const float w = 1.0f / (float)(a[0] * a[1] * a[2] * a[3]);
+  if (pix == nullptr || !(w * l4 > kPrecisionBudget)) return false;
+  // only if the pixel's own region fits a warp's slab (large w goes with a
+  // small kernel; a pixel that is neither stays in the shared region)
+  const int4 m = pixel_margins_fast(a);
+  if (region_pitch(1 + m.x + m.y) * (1 + m.z + m.w) > kPixSlab) return false;
+  const int i = atomicAdd(&st->pix_count, 1);
+  if (i < pix_cap) {
+    pix[i] = make_int2(x, y);
+  } else {
+    atomicOr(&st->flags, kFlagRegionTooLarge);  // cannot happen: cap = deferred tiles' pixels
+  }
+  return true;
+}
+
+
 struct PlanCtx {
   int m[16][4];     // per 8x8 cell: left, right, below, above
   float w[16];      // per 8x8 cell: max 1/(a1 a2 a3 a4)
@@ -684,10 +711,12 @@ __device__ __forceinline__ bool plan_unit(const PlanCtx &pc, const DomainSpec &D
 //   C. every pixel of the unit takes its finite difference from the region.
 template <int MODE, int DT, int NT>
 __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec &F,
-                                             const DomainSpec &D, int tile, int tiles_x,
-                                             int region_cap, int *ovf_list, Status *st,
-                                             double *S, unsigned &ghi, unsigned &flags,
-                                             const TmaMaps *tm, uint32_t mbar, uint32_t &phase) {
+                                             const DomainSpec &D, int tile, unsigned cmask,
+                                             int tiles_x, int region_cap, int *ovf_list,
+                                             Status *st, double *S, unsigned &ghi,
+                                             unsigned &flags, const TmaMaps *tm, uint32_t mbar,
+                                             uint32_t &phase, int2 *pix = nullptr,
+                                             int pix_cap = 0) {
   constexpr int PPT = 1024 / NT;   // pixels per thread
   constexpr int NW = NT / 32;      // warps
   __shared__ PlanCtx s_pc;
@@ -738,9 +767,9 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
     m.z = __reduce_max_sync(0xffffffffu, m.z);
     m.w = __reduce_max_sync(0xffffffffu, m.w);
     const int wi = __reduce_max_sync(0xffffffffu, __float_as_int(w));  // w >= 0
-    if (lane == 0) {
-      const int b = warp + NW * k;
-      const int c = (b >> 3) * 4 + ((b & 7) >> 1);
+    const int b = warp + NW * k;
+    const int c = (b >> 3) * 4 + ((b & 7) >> 1);
+    if (lane == 0 && ((cmask >> c) & 1u)) {  // cells outside the mask are not computed
       atomicMax(&s_pc.m[c][0], m.x);
       atomicMax(&s_pc.m[c][1], m.y);
       atomicMax(&s_pc.m[c][2], m.z);
@@ -777,6 +806,7 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
       if (ovf_list) {
         OvfRec r;
         r.tile = tile;
+        r.mask = cmask;
         r.m[0] = r.m[1] = r.m[2] = r.m[3] = 0;
         r.w = 0.f;
         for (int c = 0; c < 16; ++c) {
@@ -801,6 +831,8 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
     int left = s_plan[si][4], RW = s_plan[si][6];
     align_region<DT>(I, D.pc_lo + sx, left, RW);
     const int P = region_pitch(RW);
+    const float mnu = (float)min(RW, RH);
+    const float l4u = 0.25f * (float)RW * (float)RH * mnu * mnu;  // precision model
     // ---- B: region load + running sums
     const int rc0 = D.pc_lo + sx - left, rr0 = D.pr_lo + sy - below;
     load_region<DT, NT, 0>(S, P, I, rc0, rr0, RW, RH, tid, tm, mbar, phase);
@@ -812,7 +844,8 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
     for (int k = 0; k < PPT; ++k) {
       int x, y;
       px_of(k, x, y);
-      if (valid[k] && x >= sx && x < sx + sw && y >= sy && y < sy + sh) {
+      const int cb = warp + NW * k, cc = (cb >> 3) * 4 + ((cb & 7) >> 1);
+      if (valid[k] && ((cmask >> cc) & 1u) && x >= sx && x < sx + sw && y >= sy && y < sy + sh) {
         const int n1 = D.pc_lo + x, n2 = D.pr_lo + y;
         double ak[4];
 #pragma unroll
@@ -821,6 +854,7 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
 #pragma unroll
           for (int kk = 1; kk < PPT; ++kk) ak[j] = (k == kk) ? av[kk][j] : ak[j];
         }
+        if (defer_pixel(ak, l4u, x, y, pix, pix_cap, st)) continue;
         D.out[(int64_t)y * D.ld_out + x] = pixel_fd(Sb, P, n1, n2, ak);
       }
     }
@@ -850,8 +884,8 @@ __global__ void __launch_bounds__(kThreadsSmall, 2)
   __syncthreads();
   unsigned ghi = 0, flags = 0;
   uint32_t phase = 0;
-  process_tile<MODE, DT, kThreadsSmall>(I, F, D, blockIdx.x, tiles_x, region_cap, ovf_list, st,
-                                        S, ghi, flags, &tm, mbar, phase);
+  process_tile<MODE, DT, kThreadsSmall>(I, F, D, blockIdx.x, 0xffffu, tiles_x, region_cap,
+                                        ovf_list, st, S, ghi, flags, &tm, mbar, phase);
   flush_status(st, ghi, flags);
 }
 
@@ -860,7 +894,7 @@ __global__ void __launch_bounds__(kThreadsSmall, 2)
 template <int MODE, int DT>
 __global__ void __launch_bounds__(kThreadsLarge, 1)
     tile_overflow_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int region_cap,
-                         const int *ovf_list, int n, Status *st,
+                         const int2 *list, int n, Status *st, int2 *pix, int pix_cap,
                          const __grid_constant__ TmaMaps tm) {
   extern __shared__ __align__(128) double S[];
   __shared__ uint64_t s_mbar;
@@ -869,9 +903,12 @@ __global__ void __launch_bounds__(kThreadsLarge, 1)
   __syncthreads();
   unsigned ghi = 0, flags = 0;
   uint32_t phase = 0;
-  for (int i = blockIdx.x; i < n; i += gridDim.x)
-    process_tile<MODE, DT, kThreadsLarge>(I, F, D, ovf_list[i], tiles_x, region_cap, nullptr, st,
-                                          S, ghi, flags, &tm, mbar, phase);
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const int2 e = list[i];  // (tile, mask of its deferred 8x8 cells)
+    process_tile<MODE, DT, kThreadsLarge>(I, F, D, e.x, (unsigned)e.y, tiles_x, region_cap,
+                                          nullptr, st, S, ghi, flags, &tm, mbar, phase, pix,
+                                          pix_cap);
+  }
   flush_status(st, ghi, flags);
 }
 
@@ -1046,7 +1083,7 @@ __global__ void __launch_bounds__(NT, 2)
   //      (a tile of the overflow launches' 32-pixel grid) to the overflow pass
   if (tid == 0) {
     int n = 0;
-    unsigned ovf_half = 0;
+    unsigned ovf_cells = 0;  // bit cy * NCX + cx
     int stk[16][4];
     int sp = 0;
     stk[sp][0] = 0; stk[sp][1] = 0; stk[sp][2] = NCX; stk[sp][3] = NCY; ++sp;
@@ -1073,7 +1110,9 @@ __global__ void __launch_bounds__(NT, 2)
         continue;
       }
       if (ncx * ncy == 1) {
-        ovf_half |= 1u << (cx0 >> 2);
+        // a cell that still fails goes to the overflow pass; the rest of
+        // the tile keeps its (smaller, better-conditioned) units
+        ovf_cells |= 1u << (cy0 * NCX + cx0);
         continue;
       }
       if (ncx >= ncy) {
@@ -1086,31 +1125,24 @@ __global__ void __launch_bounds__(NT, 2)
         stk[sp][0] = cx0; stk[sp][1] = cy0 + h; stk[sp][2] = ncx; stk[sp][3] = ncy - h; ++sp;
       }
     }
-    if (ovf_half) {
-      // units never straddle the halves (the first split is the halves)
-      int k = 0;
-      for (int i = 0; i < n; ++i) {
-        const int hx = (s_unit[i][0] - x0) >> 5;
-        if (!((ovf_half >> hx) & 1u)) {
-          if (k != i)
-            for (int j = 0; j < 8; ++j) s_unit[k][j] = s_unit[i][j];
-          ++k;
-        }
-      }
-      n = k;
+    if (ovf_cells) {
+      // one record per 32 x 32 half with deferred cells (the overflow
+      // passes work on the 32-pixel grid), margins and w over those cells
       for (int h = 0; h < 2; ++h) {
-        if (!((ovf_half >> h) & 1u)) continue;
         OvfRec r;
         r.tile = ty * tiles_x32 + 2 * tx + h;
         r.m[0] = r.m[1] = r.m[2] = r.m[3] = 0;
         r.w = 0.f;
+        r.mask = 0;
         for (int cy = 0; cy < NCY; ++cy)
           for (int cx = 4 * h; cx < 4 * h + 4; ++cx) {
             const int c = cy * NCX + cx;
+            if (!((ovf_cells >> c) & 1u)) continue;
+            r.mask |= 1u << (cy * 4 + (cx - 4 * h));
             for (int j = 0; j < 4; ++j) r.m[j] = max(r.m[j], s_cm[c][j]);
             r.w = fmaxf(r.w, s_cw[c]);
           }
-        reinterpret_cast<OvfRec *>(ovf_list)[atomicAdd(&st->ovf_count, 1)] = r;
+        if (r.mask) reinterpret_cast<OvfRec *>(ovf_list)[atomicAdd(&st->ovf_count, 1)] = r;
       }
     }
     s_nu = n;
@@ -1222,13 +1254,55 @@ __global__ void __launch_bounds__(NT, 2)
 // taps through L1/L2.  Member tiles are gathered in block-raster order, so
 // neighbouring CTAs share the rows their vertices touch in L2.
 
+constexpr int kPixSmem = 8 * kPixSlab * 8;  // 8 warps per CTA
+
+template <int MODE, int DT>
+__global__ void __launch_bounds__(256) pixel_kernel(ImageSpec I, FieldSpec F, DomainSpec D,
+                                                    const int2 *pix, int n, Status *st) {
+  extern __shared__ __align__(16) double Sw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double *S = Sw + warp * kPixSlab;
+  unsigned flags = 0, ghi = 0;
+  for (int i = blockIdx.x * 8 + warp; i < n; i += gridDim.x * 8) {
+    const int2 p = pix[i];
+    const int n1 = D.pc_lo + p.x, n2 = D.pr_lo + p.y;
+    double a[4];
+    field_at<MODE>(F, n1, n2, a, flags);
+    const int4 m = pixel_margins_fast(a);
+    const int RW = 1 + m.x + m.y, RH = 1 + m.z + m.w;
+    const int P = region_pitch(RW);
+    if (P * RH > kPixSlab) {  // a large kernel never has a large w
+      if (lane == 0) atomicOr(&st->flags, kFlagRegionTooLarge);
+      continue;
+    }
+    const int rc0 = n1 - m.x, rr0 = n2 - m.z;
+    // region load (zero outside the image), then the four running sums
+    for (int e = lane; e < RW * RH; e += 32) {
+      const int r = e / RW, c = e - r * RW;
+      const int ir = rr0 + r - I.row0, ic = rc0 + c - I.col0;
+      S[r * P + c] = (ir >= 0 && ir < I.h && ic >= 0 && ic < I.w)
+                         ? load_px<DT>(I.f, (int64_t)ir * I.ld + ic) : 0.0;
+    }
+    __syncwarp();
+    region_sweeps<32, -1>(S, P, RW, RH, ghi, lane);
+    if (lane == 0) {
+      const uint32_t Sb = (uint32_t)__cvta_generic_to_shared(S) - (uint32_t)((rr0 * P + rc0) * 8);
+      D.out[(int64_t)p.y * D.ld_out + p.x] = pixel_fd(Sb, P, n1, n2, a);
+    }
+    __syncwarp();
+  }
+  flush_status(st, ghi, flags);
+}
+
 struct BigRegion {
   int64_t off;       // element offset of region element (0, 0) in scratch
   int rc0, rr0;      // lattice of region element (0, 0)
-  int RW, RH, P, pad;
+  int RW, RH, P;
+  float l4;          // RW RH min(RW, RH)^2 / 4 (precision model)
 };
 struct BigTile {
   int tile, region;
+  unsigned mask;  // 8x8 cells of the tile to compute
 };
 
 template <int DT>
@@ -1321,7 +1395,7 @@ template <int MODE>
 __global__ void __launch_bounds__(256) big_gather_kernel(FieldSpec F, DomainSpec D, int tiles_x,
                                                          const BigTile *tl, int nt,
                                                          const BigRegion *R, const double *scratch,
-                                                         Status *st) {
+                                                         Status *st, int2 *pix, int pix_cap) {
   unsigned flags = 0;
   const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
   for (int i = blockIdx.x; i < nt; i += gridDim.x) {
@@ -1334,10 +1408,14 @@ __global__ void __launch_bounds__(256) big_gather_kernel(FieldSpec F, DomainSpec
 #pragma unroll 1
     for (int k = 0; k < 4; ++k) {
       const int x = x0 + lx, y = y0 + ly + 8 * k;
-      if (x < D.pw && y < D.ph) {
+      const int c = (ly + 8 * k) / 8 * 4 + lx / 8;
+      if (x < D.pw && y < D.ph && ((bt.mask >> c) & 1u)) {
         const int n1 = D.pc_lo + x, n2 = D.pr_lo + y;
         double a[4];
         field_at<MODE>(F, n1, n2, a, flags);
+        // a small kernel sharing a tile with huge ones: its own region is
+        // small, the block's is not -- deferred to the per-pixel pass
+        if (defer_pixel(a, g.l4, x, y, pix, pix_cap, st)) continue;
         D.out[(int64_t)y * D.ld_out + x] = pixel_fd_t<const char *, int64_t>(Sb, P8, n1, n2, a);
       }
     }
@@ -1494,7 +1572,9 @@ struct Scratch {
   int sms = 148;
   int *d_ovf = nullptr;  // OvfRec records
   size_t ovf_cap = 0;
-  int *d_list = nullptr;
+  int2 *d_list = nullptr;  // (tile, cell mask) of the shared-memory overflow pass
+  int2 *d_pix = nullptr;   // pixels deferred to the per-pixel pass
+  size_t pix_cap = 0;
   size_t list_cap = 0;
   double *d_big = nullptr;
   size_t big_cap = 0;
@@ -1544,7 +1624,10 @@ int ensure_scratch() {
                                      kSmemLarge));                                  \
   RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<M, T, kThreadsWide, 1>,                       \
                                      cudaFuncAttributeMaxDynamicSharedMemorySize,   \
-                                     kSmemWide))
+                                     kSmemWide));                                   \
+  RUBS_CUDA_TRY(cudaFuncSetAttribute(pixel_kernel<M, T>,                             \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                                     kPixSmem))
     RUBS_SET_SMEM(kModeField, 0);
     RUBS_SET_SMEM(kModeField, 1);
     RUBS_SET_SMEM(kModeUniform, 0);
@@ -1758,7 +1841,7 @@ int upload(std::vector<V> &h, V *&d, size_t &cap, cudaStream_t s) {
 // 225 KB configuration go to the shared-memory overflow kernel, the rest to
 // the global-memory block path (see big_* kernels).
 template <int M, int T>
-int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int n_ovf,
+int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int n_ovf,
                     cudaStream_t s) {
   std::vector<OvfRec> raw(n_ovf);
   RUBS_CUDA_TRY(cudaMemcpyAsync(raw.data(), t_scr.d_ovf, n_ovf * sizeof(OvfRec),
@@ -1772,16 +1855,26 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
     if (!recs.empty() && recs.back().tile == r.tile) {
       for (int j = 0; j < 4; ++j) recs.back().m[j] = std::max(recs.back().m[j], r.m[j]);
       recs.back().w = std::max(recs.back().w, r.w);
+      recs.back().mask |= r.mask;
     } else {
       recs.push_back(r);
     }
   }
   const int tiles_x = (D.pw + kTile - 1) / kTile;
-  std::vector<int> smem_list;
+  // per-pixel fallback list: at most every pixel of the deferred tiles
+  const int pix_cap = (int)std::min<size_t>(recs.size() * kTile * kTile, 1u << 30);
+  if ((size_t)pix_cap > t_scr.pix_cap) {
+    if (t_scr.d_pix) cudaFree(t_scr.d_pix);
+    t_scr.d_pix = nullptr;
+    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_pix, (size_t)pix_cap * sizeof(int2)));
+    t_scr.pix_cap = pix_cap;
+  }
+  RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->pix_count, 0, sizeof(int), s));
+  std::vector<int2> smem_list;  // (tile, cell mask)
   struct Blk {
     int S = 0, x0 = 1 << 30, y0 = 1 << 30, x1 = 0, y1 = 0;
     int m[4] = {0, 0, 0, 0};
-    std::vector<int> tiles;
+    std::vector<int2> tiles;
   };
   std::map<std::tuple<int, int, int>, Blk> blocks;
   const int cap_large = kSmemLarge / 8;
@@ -1789,7 +1882,7 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
     const int x0 = (r.tile % tiles_x) * kTile, y0 = (r.tile / tiles_x) * kTile;
     const int tw = std::min(kTile, D.pw - x0), th = std::min(kTile, D.ph - y0);
     if (region_elems(std::min(8, tw) + r.m[0] + r.m[1] + 1, std::min(8, th) + r.m[2] + r.m[3]) <= cap_large) {
-      smem_list.push_back(r.tile);
+      smem_list.push_back(make_int2(r.tile, (int)r.mask));
       continue;
     }
     const int h = std::max(std::max(r.m[0], r.m[1]), std::max(r.m[2], r.m[3]));
@@ -1808,16 +1901,17 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
     b.x1 = std::max(b.x1, x0 + tw);
     b.y1 = std::max(b.y1, y0 + th);
     for (int j = 0; j < 4; ++j) b.m[j] = std::max(b.m[j], r.m[j]);
-    b.tiles.push_back(r.tile);
+    b.tiles.push_back(make_int2(r.tile, (int)r.mask));
   }
   int rc;
   if (!smem_list.empty()) {
-    std::sort(smem_list.begin(), smem_list.end());
+    std::sort(smem_list.begin(), smem_list.end(),
+              [](const int2 &a, const int2 &b) { return a.x < b.x; });
     if ((rc = upload(smem_list, t_scr.d_list, t_scr.list_cap, s))) return rc;
     tile_overflow_kernel<M, T><<<std::min((int)smem_list.size(), t_scr.sms), kThreadsLarge,
                                  kSmemLarge, s>>>(I, F, D, tiles_x, kSmemLarge / 8, t_scr.d_list,
                                                   (int)smem_list.size(), t_scr.d_status,
-                                                  tma_maps(I));
+                                                  t_scr.d_pix, pix_cap, tma_maps(I));
     ++t_launches;
     RUBS_CUDA_TRY(cudaGetLastError());
   }
@@ -1852,7 +1946,8 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
     big_line_kernel<4><<<dim3((maxL + 255) / 256, nreg), 256, 0, s>>>(t_scr.d_regs, t_scr.d_big,
                                                                        t_scr.d_status);
     big_gather_kernel<M><<<std::min((int)tl.size(), t_scr.sms * 8), 256, 0, s>>>(
-        F, D, tiles_x, t_scr.d_btiles, (int)tl.size(), t_scr.d_regs, t_scr.d_big, t_scr.d_status);
+        F, D, tiles_x, t_scr.d_btiles, (int)tl.size(), t_scr.d_regs, t_scr.d_big, t_scr.d_status,
+        t_scr.d_pix, pix_cap);
     t_launches += 5;
     RUBS_CUDA_TRY(cudaGetLastError());
     // the next batch reuses the scratch: wait for this one
@@ -1870,17 +1965,40 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
     g.P = g.RW;
     g.rc0 = D.pc_lo + b.x0 - b.m[0];
     g.rr0 = D.pr_lo + b.y0 - b.m[2];
-    g.pad = 0;
+    {
+      const double mn = std::min(g.RW, g.RH);
+      g.l4 = (float)(0.25 * g.RW * (double)g.RH * mn * mn);
+    }
     const int64_t n = (int64_t)g.P * g.RH;
     if (!regs.empty() && used + n > budget)
       if ((rc = flush())) return rc;
     g.off = used;
     used += n;
-    std::sort(b.tiles.begin(), b.tiles.end());
-    for (int t : b.tiles) tl.push_back(BigTile{t, (int)regs.size()});
+    std::sort(b.tiles.begin(), b.tiles.end(), [](const int2 &a, const int2 &c) { return a.x < c.x; });
+    for (const int2 &t : b.tiles) tl.push_back(BigTile{t.x, (int)regs.size(), (unsigned)t.y});
     regs.push_back(g);
   }
   return flush();
+}
+
+// The deferred tiles, then the pixels they deferred in turn (per-pixel pass).
+template <int M, int T>
+int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int n_ovf,
+                    cudaStream_t s) {
+  int rc = handle_overflow_tiles<M, T>(I, F, D, n_ovf, s);
+  if (rc) return rc;
+  int cnt = 0;
+  RUBS_CUDA_TRY(cudaMemcpyAsync(&cnt, &t_scr.d_status->pix_count, sizeof(int),
+                                cudaMemcpyDeviceToHost, s));
+  RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+  cnt = std::min<int64_t>(cnt, (int64_t)t_scr.pix_cap);
+  if (cnt > 0) {
+    pixel_kernel<M, T><<<std::min((cnt + 7) / 8, t_scr.sms * 4), 256, kPixSmem, s>>>(
+        I, F, D, t_scr.d_pix, cnt, t_scr.d_status);
+    ++t_launches;
+    RUBS_CUDA_TRY(cudaGetLastError());
+  }
+  return RUBS_OK;
 }
 
 template <int M, int T>

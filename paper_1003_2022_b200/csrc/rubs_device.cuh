@@ -36,16 +36,20 @@ struct Status {
   unsigned long long guard_bits;  // same for the global-canvas path, full bits
   int gm[4];                      // global margins left, right, below, above
   int ovf_count;                  // tiles deferred to the large-smem launch
-  int pad2;
+  int pix_count;                  // pixels deferred to the per-pixel pass
 };
 
 // A tile deferred by the primary launch (its regions exceed the primary
-// configuration's shared memory): tile index, tile-wide read margins
-// (left, right, below, above) and max 1/(a1 a2 a3 a4).
+// configuration's shared memory): tile index (32-pixel grid), the read
+// margins (left, right, below, above) and max 1/(a1 a2 a3 a4) over the
+// deferred cells, and which 8x8 cells are deferred -- the other cells of the
+// tile were computed by the primary launch with their own (smaller,
+// better-conditioned) regions and must not be overwritten.
 struct OvfRec {
   int tile;
   int m[4];
   float w;
+  unsigned mask;  // the tile's 8x8 cells (bit cy * 4 + cx) that need the overflow pass
 };
 
 // Where the per-pixel scale-vector comes from.

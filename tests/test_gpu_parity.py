@@ -346,6 +346,24 @@ def test_streamed_host_path_equals_device_path(cuda, rng):
     assert rel_err(host[pts[:, 0], pts[:, 1]], ref) < REL_TOL
 
 
+def test_streamed_host_path_float32_and_pageable(cuda, rng):
+    # float32 image, float64 parameters, no caller-provided result buffer
+    torch = cuda
+    H, W = 520, 480
+    f = rng.random((H, W)).astype(np.float32)
+    size = rng.uniform(2.0, 60.0, (H, W))
+    rho = rng.uniform(1.0, 3.5, (H, W))
+    th = rng.uniform(0.0, math.pi, (H, W))
+    host = rb.filter_space_variant_params(f, size, rho, th)
+    dev = rb.filter_space_variant_params(torch.from_numpy(f).cuda(), *(torch.from_numpy(v).cuda()
+                                                                        for v in (size, rho, th)))
+    assert host.dtype == np.float64 and np.array_equal(host, dev.cpu().numpy())
+    lut = rb.default_lut()
+    fld = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, size, rho, th)
+    pts = sample_points(rng, H, W, 16)
+    assert rel_err(host[pts[:, 0], pts[:, 1]], oracle.points(f.astype(np.float64), fld, pts)) < REL_TOL
+
+
 # --- BASELINE configs at full size ------------------------------------------
 
 

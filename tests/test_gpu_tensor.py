@@ -199,3 +199,16 @@ def test_multichannel_passes_equal_single_channel_calls(cuda):
         gain = rb.filter_space_variant_params(np.ones_like(img), m.size, rho, m.orientation, lut)
         want = np.where(np.abs(gain) > 1e-6, out / np.where(gain == 0.0, 1.0, gain), out)
         assert rel(tensor.adaptive_smooth(img, 0.1), want) < REL_TOL
+
+
+def test_adaptive_smooth_large_kernels_take_the_overflow_path(cuda):
+    # sizes up to 3000 (sigma ~ 39): the two-channel launch defers most
+    # tiles (half the shared memory per channel), which then run through
+    # the single-channel overflow path channel by channel
+    rng = np.random.default_rng(9)
+    img = tensor_port.stripe_image((160, 176), period=13.0, angle=0.9) + rng.normal(0.0, 0.1, (160, 176))
+    kw = dict(size_range=(0.5, 3000.0))
+    got = tensor.adaptive_smooth(img, 0.1, **kw)
+    j = tensor.structure_tensor(img, 1.5)
+    exact = tensor_port.adaptive_smooth(img, 0.1, lut_tuple(), j=j, **kw)
+    assert rel(got, exact) < REL_TOL
