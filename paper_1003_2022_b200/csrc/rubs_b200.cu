@@ -1255,6 +1255,13 @@ __global__ void __launch_bounds__(NT, 2)
 // neighbouring CTAs share the rows their vertices touch in L2.
 
 constexpr int kPixSmem = 8 * kPixSlab * 8;  // 8 warps per CTA
+// Doubles of big-block scratch per batch.  L2-sized batches (8M doubles)
+// were measured 2x slower on config 5: the line sweeps draw their
+// parallelism from the number of regions in a batch.
+#ifndef RUBS_BIG_BATCH
+#define RUBS_BIG_BATCH (1ll << 29)
+#endif
+constexpr int64_t kBigBatch = RUBS_BIG_BATCH;
 
 template <int MODE, int DT>
 __global__ void __launch_bounds__(256) pixel_kernel(ImageSpec I, FieldSpec F, DomainSpec D,
@@ -1916,46 +1923,28 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
     RUBS_CUDA_TRY(cudaGetLastError());
   }
   if (blocks.empty()) return RUBS_OK;
-  // batches of blocks under a scratch budget (elements)
-  const int64_t budget = (int64_t)1 << 29;  // 4 GiB of fp64
+  // Batches of blocks under a scratch budget.  A batch's kernels follow the
+  // previous batch's in stream order, so the scratch is reused without a
+  // host sync; region / tile lists of all batches are uploaded once.
+  const int64_t budget = kBigBatch;
+  struct Batch {
+    int r0, r1, t0, t1;
+    int64_t used;
+    int maxRH, maxL;
+  };
   std::vector<BigRegion> regs;
   std::vector<BigTile> tl;
-  int64_t used = 0;
-  auto flush = [&]() -> int {
-    if (regs.empty()) return RUBS_OK;
-    if (used > (int64_t)t_scr.big_cap) {
-      if (t_scr.d_big) cudaFree(t_scr.d_big);
-      t_scr.d_big = nullptr;
-      RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_big, (size_t)used * sizeof(double)));
-      t_scr.big_cap = (size_t)used;
+  std::vector<Batch> batches;
+  Batch cur{0, 0, 0, 0, 0, 0, 0};
+  int64_t max_used = 0;
+  auto close_batch = [&]() {
+    cur.r1 = (int)regs.size();
+    cur.t1 = (int)tl.size();
+    if (cur.r1 > cur.r0) {
+      batches.push_back(cur);
+      max_used = std::max(max_used, cur.used);
     }
-    int r2;
-    if ((r2 = upload(regs, t_scr.d_regs, t_scr.regs_cap, s))) return r2;
-    if ((r2 = upload(tl, t_scr.d_btiles, t_scr.btiles_cap, s))) return r2;
-    int maxRH = 0, maxL = 0;
-    for (const BigRegion &g : regs) {
-      maxRH = std::max(maxRH, g.RH);
-      maxL = std::max(maxL, g.RH + g.RW - 1);
-    }
-    const int nreg = (int)regs.size();
-    big_fill_rs1_kernel<T><<<dim3((maxRH + 7) / 8, nreg), 256, 0, s>>>(I, t_scr.d_regs, t_scr.d_big);
-    big_line_kernel<2><<<dim3((maxL + 255) / 256, nreg), 256, 0, s>>>(t_scr.d_regs, t_scr.d_big,
-                                                                       t_scr.d_status);
-    big_line_kernel<3><<<dim3((maxL + 255) / 256, nreg), 256, 0, s>>>(t_scr.d_regs, t_scr.d_big,
-                                                                       t_scr.d_status);
-    big_line_kernel<4><<<dim3((maxL + 255) / 256, nreg), 256, 0, s>>>(t_scr.d_regs, t_scr.d_big,
-                                                                       t_scr.d_status);
-    big_gather_kernel<M><<<std::min((int)tl.size(), t_scr.sms * 8), 256, 0, s>>>(
-        F, D, tiles_x, t_scr.d_btiles, (int)tl.size(), t_scr.d_regs, t_scr.d_big, t_scr.d_status,
-        t_scr.d_pix, pix_cap);
-    t_launches += 5;
-    RUBS_CUDA_TRY(cudaGetLastError());
-    // the next batch reuses the scratch: wait for this one
-    RUBS_CUDA_TRY(cudaStreamSynchronize(s));
-    regs.clear();
-    tl.clear();
-    used = 0;
-    return RUBS_OK;
+    cur = Batch{(int)regs.size(), 0, (int)tl.size(), 0, 0, 0, 0};
   };
   for (auto &kv : blocks) {
     Blk &b = kv.second;
@@ -1970,15 +1959,42 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
       g.l4 = (float)(0.25 * g.RW * (double)g.RH * mn * mn);
     }
     const int64_t n = (int64_t)g.P * g.RH;
-    if (!regs.empty() && used + n > budget)
-      if ((rc = flush())) return rc;
-    g.off = used;
-    used += n;
+    if (cur.used > 0 && cur.used + n > budget) close_batch();
+    g.off = cur.used;
+    cur.used += n;
+    cur.maxRH = std::max(cur.maxRH, g.RH);
+    cur.maxL = std::max(cur.maxL, g.RH + g.RW - 1);
     std::sort(b.tiles.begin(), b.tiles.end(), [](const int2 &a, const int2 &c) { return a.x < c.x; });
-    for (const int2 &t : b.tiles) tl.push_back(BigTile{t.x, (int)regs.size(), (unsigned)t.y});
+    for (const int2 &t : b.tiles)
+      tl.push_back(BigTile{t.x, (int)regs.size() - cur.r0, (unsigned)t.y});
     regs.push_back(g);
   }
-  return flush();
+  close_batch();
+  if (max_used > (int64_t)t_scr.big_cap) {
+    if (t_scr.d_big) cudaFree(t_scr.d_big);
+    t_scr.d_big = nullptr;
+    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_big, (size_t)max_used * sizeof(double)));
+    t_scr.big_cap = (size_t)max_used;
+  }
+  if ((rc = upload(regs, t_scr.d_regs, t_scr.regs_cap, s))) return rc;
+  if ((rc = upload(tl, t_scr.d_btiles, t_scr.btiles_cap, s))) return rc;
+  for (const Batch &bt : batches) {
+    const int nreg = bt.r1 - bt.r0, ntl = bt.t1 - bt.t0;
+    const BigRegion *R = t_scr.d_regs + bt.r0;
+    big_fill_rs1_kernel<T><<<dim3((bt.maxRH + 7) / 8, nreg), 256, 0, s>>>(I, R, t_scr.d_big);
+    big_line_kernel<2><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
+                                                                          t_scr.d_status);
+    big_line_kernel<3><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
+                                                                          t_scr.d_status);
+    big_line_kernel<4><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
+                                                                          t_scr.d_status);
+    big_gather_kernel<M><<<std::min(ntl, t_scr.sms * 8), 256, 0, s>>>(
+        F, D, tiles_x, t_scr.d_btiles + bt.t0, ntl, R, t_scr.d_big, t_scr.d_status, t_scr.d_pix,
+        pix_cap);
+    t_launches += 5;
+    RUBS_CUDA_TRY(cudaGetLastError());
+  }
+  return RUBS_OK;
 }
 
 // The deferred tiles, then the pixels they deferred in turn (per-pixel pass).
