@@ -14,6 +14,9 @@ Two oracles live here:
   independent area routine (polygon clipping instead of slice integration).
 * ``port.py``: a numpy restatement of the reference fast path (engine.py,
   zp.py, solver.lookup_many), used as the CPU baseline and as oracle "B".
+* ``dense_oracle_cuda.cu`` (``dense_cuda``): the same exact dense filter on
+  the GPU, for whole-image checks at the BASELINE sizes (tests only; pinned
+  to ``dense`` by tests/test_gpu_fullsize.py).
 
 Both are pinned against golden vectors generated from the reference itself
 (tests/golden/make_golden.py, tests/test_oracle_golden.py).
@@ -33,10 +36,48 @@ _LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
 _lib = None
 
 
+_CUDA_LIB_PATH = os.path.join(_HERE, "_build", "liboracle_cuda.so")
+_cuda_lib = None
+
+
 def build() -> str:
-    """Compile the C oracle (make in oracle/)."""
+    """Compile the C oracle (make in oracle/) and, where nvcc exists, its
+    GPU copy for whole-image checks (make cuda)."""
     subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    try:
+        subprocess.run(["make", "-s", "-C", _HERE, "cuda"], check=True)
+    except (OSError, subprocess.CalledProcessError):
+        pass
     return _LIB_PATH
+
+
+def dense_cuda(f, field, rows=None, cols=None):
+    """Exact dense filter (one pass) on the GPU: output rows x cols (ranges,
+    default the whole image) of the H x W image ``f``; inputs numpy or torch.
+    Same kernel geometry as ``dense`` (dense_oracle_cuda.cu)."""
+    global _cuda_lib
+    import torch
+    if _cuda_lib is None:
+        if not os.path.exists(_CUDA_LIB_PATH):
+            subprocess.run(["make", "-s", "-C", _HERE, "cuda"], check=True)
+        L = ctypes.CDLL(_CUDA_LIB_PATH)
+        vp, i = ctypes.c_void_p, ctypes.c_int
+        L.rubs_oracle_cuda_dense.restype = i
+        L.rubs_oracle_cuda_dense.argtypes = [vp, i, i, vp, i, i, i, i, i, vp]
+        _cuda_lib = L
+    ft = torch.as_tensor(f).to("cuda", torch.float64).contiguous()
+    fl = torch.as_tensor(field).to("cuda", torch.float64).contiguous()
+    H, W = ft.shape
+    uniform = int(fl.numel() == 4)
+    r0, r1 = rows if rows is not None else (0, H)
+    c0, c1 = cols if cols is not None else (0, W)
+    out = torch.empty((r1 - r0, c1 - c0), dtype=torch.float64, device="cuda")
+    rc = _cuda_lib.rubs_oracle_cuda_dense(ctypes.c_void_p(ft.data_ptr()), H, W,
+                                          ctypes.c_void_p(fl.data_ptr()), uniform, r0, c0,
+                                          r1 - r0, c1 - c0, ctypes.c_void_p(out.data_ptr()))
+    if rc:
+        raise RuntimeError(f"oracle cuda error {rc}")
+    return out
 
 
 def lib():

@@ -488,8 +488,9 @@ __device__ __forceinline__ double zp_read8(A c, S P8, double d1, double d2) {
 }
 
 // Per-pixel finite difference (engine.py:219-244) over a region plane,
-// 16 vertices x 7 ZP taps.  Sb = byte address such that
-// Sb + m2 * P8 + m1 * 8 is the region element at lattice (m1, m2).
+// 16 vertices x 7 ZP taps.  (n1, n2) = the pixel's lattice position relative
+// to the region origin; Sb = byte address of region element (0, 0), so
+// Sb + m2 * P8 + m1 * 8 is the element at local lattice (m1, m2).
 //
 // The 4 x 7 quadratic table of zp.py (exact multiples of 1/8)
 // folds into one canonical wedge: partition q (zp.py:82-86) only decides
@@ -839,7 +840,10 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
     __syncthreads();
     region_sweeps<NT, 0>(S, P, RW, RH, ghi, tid);
     // ---- C: finite differences
-    const uint32_t Sb = sbase - (uint32_t)((rr0 * P + rc0) * 8);
+    // positions relative to the region origin: small coordinates keep the
+    // vertex residuals exact to ~1e-14 (thin kernels difference vertices
+    // 0.05 apart; global coordinates up to 32768 would cost ~1e-12 each)
+    const uint32_t Sb = sbase;
 #pragma unroll 1
     for (int k = 0; k < PPT; ++k) {
       int x, y;
@@ -855,7 +859,7 @@ __device__ __forceinline__ void process_tile(const ImageSpec &I, const FieldSpec
           for (int kk = 1; kk < PPT; ++kk) ak[j] = (k == kk) ? av[kk][j] : ak[j];
         }
         if (defer_pixel(ak, l4u, x, y, pix, pix_cap, st)) continue;
-        D.out[(int64_t)y * D.ld_out + x] = pixel_fd(Sb, P, n1, n2, ak);
+        D.out[(int64_t)y * D.ld_out + x] = pixel_fd(Sb, P, n1 - rc0, n2 - rr0, ak);
       }
     }
     __syncthreads();
@@ -1172,7 +1176,7 @@ __global__ void __launch_bounds__(NT, 2)
     // ---- C: 4 x 8-pixel blocks of the unit, warp-strided; the exact
     //         scale-vector of the next block is fetched before this one's
     //         finite differences
-    const uint32_t Sb = sbase - (uint32_t)((rr0 * P + rc0) * 8);
+    const uint32_t Sb = sbase;  // local coordinates (see process_tile)
     const int nbx = (sw + 3) >> 2, nblk = nbx * ((sh + 7) >> 3);
     // block b = by * nbx + bx, walked in steps of NW without a division:
     // (cbx, cby) is the current block, (nbx_, nby_) the next one
@@ -1225,10 +1229,11 @@ __global__ void __launch_bounds__(NT, 2)
       if (x < sx + sw && y < sy + sh) {
         if constexpr (NCH == 1) {
           D.out[(int64_t)y * D.ld_out + x] =
-              RUBS_DEV_SKIP_GATHER ? ac[0] : pixel_fd(Sb, P, D.pc_lo + x, D.pr_lo + y, ac);
+              RUBS_DEV_SKIP_GATHER ? ac[0]
+                                   : pixel_fd(Sb, P, D.pc_lo + x - rc0, D.pr_lo + y - rr0, ac);
         } else {
           double o[NCH];
-          pixel_fd_n<NCH, CAP * 8>(Sb, P * 8, D.pc_lo + x, D.pr_lo + y, ac, o);
+          pixel_fd_n<NCH, CAP * 8>(Sb, P * 8, D.pc_lo + x - rc0, D.pr_lo + y - rr0, ac, o);
 #pragma unroll
           for (int ch = 0; ch < NCH; ++ch) mc.out[ch][(int64_t)y * D.ld_out + x] = o[ch];
         }
@@ -1293,8 +1298,8 @@ __global__ void __launch_bounds__(256) pixel_kernel(ImageSpec I, FieldSpec F, Do
     __syncwarp();
     region_sweeps<32, -1>(S, P, RW, RH, ghi, lane);
     if (lane == 0) {
-      const uint32_t Sb = (uint32_t)__cvta_generic_to_shared(S) - (uint32_t)((rr0 * P + rc0) * 8);
-      D.out[(int64_t)p.y * D.ld_out + p.x] = pixel_fd(Sb, P, n1, n2, a);
+      const uint32_t Sb = (uint32_t)__cvta_generic_to_shared(S);
+      D.out[(int64_t)p.y * D.ld_out + p.x] = pixel_fd(Sb, P, n1 - rc0, n2 - rr0, a);
     }
     __syncwarp();
   }
@@ -1409,8 +1414,7 @@ __global__ void __launch_bounds__(256) big_gather_kernel(FieldSpec F, DomainSpec
     const BigTile bt = tl[i];
     const BigRegion g = R[bt.region];
     const int x0 = (bt.tile % tiles_x) * kTile, y0 = (bt.tile / tiles_x) * kTile;
-    const char *Sb = reinterpret_cast<const char *>(scratch + g.off) -
-                     ((int64_t)g.rr0 * g.P + g.rc0) * 8;
+    const char *Sb = reinterpret_cast<const char *>(scratch + g.off);  // local coordinates
     const int64_t P8 = (int64_t)g.P * 8;
 #pragma unroll 1
     for (int k = 0; k < 4; ++k) {
@@ -1423,7 +1427,8 @@ __global__ void __launch_bounds__(256) big_gather_kernel(FieldSpec F, DomainSpec
         // a small kernel sharing a tile with huge ones: its own region is
         // small, the block's is not -- deferred to the per-pixel pass
         if (defer_pixel(a, g.l4, x, y, pix, pix_cap, st)) continue;
-        D.out[(int64_t)y * D.ld_out + x] = pixel_fd_t<const char *, int64_t>(Sb, P8, n1, n2, a);
+        D.out[(int64_t)y * D.ld_out + x] =
+            pixel_fd_t<const char *, int64_t>(Sb, P8, n1 - g.rc0, n2 - g.rr0, a);
       }
     }
   }

@@ -259,9 +259,12 @@ __device__ __forceinline__ int4 pixel_margins(const double a[4]) {
 // ZP taps within 1 of it, so the taps span columns n1 - floor(hx) - 2 ..
 // n1 + floor(hx) + 1 and rows n2 - floor(hy) - 3 .. n2 + floor(hy).  The
 // 1e-6 covers the rounding of the vertex arithmetic.
+#ifndef RUBS_MARGIN_SLACK
+#define RUBS_MARGIN_SLACK 0
+#endif
 __device__ __forceinline__ int4 margins_from_extent(double hx, double hy) {
-  const int fx = (int)floor(hx + 1e-6), fy = (int)floor(hy + 1e-6);
-  return make_int4(fx + 2, fx + 1, fy + 3, fy);
+  const int fx = (int)floor(hx + 1e-6), fy = (int)floor(hy + 1e-6), k = RUBS_MARGIN_SLACK;
+  return make_int4(fx + 2 + k, fx + 1 + k, fy + 3 + k, fy + k);
 }
 
 __device__ __forceinline__ int4 pixel_margins_fast(const double a[4]) {
