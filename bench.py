@@ -48,7 +48,7 @@ METRIC = "Gpixel/s filtered"
 UNIT = "Gpixel/s"
 # Algorithmic bytes per output pixel for the fused path: f64 image (8) +
 # three f32 params (12) + f64 output (8) = 28.
-BYTES_PER_PX = {"2": 28, "1": 48, "3": 24, "4": 52, "5": 24, "A": 16}
+BYTES_PER_PX = {"2": 28, "1": 48, "3": 24, "3n4": 24, "4": 52, "5": 24, "A": 16}
 
 
 def parse():
@@ -57,7 +57,7 @@ def parse():
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="2", choices=["1", "2", "3", "4", "5", "A"])
+    p.add_argument("--config", default="2", choices=["1", "2", "3", "3n4", "4", "5", "A"])
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     return p.parse_args()
@@ -147,8 +147,11 @@ def make_inputs(cfg: str, torch, device, copies: int, rank: int):
     elif cfg == "1":
         w = workloads.config1()
     elif cfg == "3":
-        w = workloads.config3(device=device, param_dtype=torch.float32)
+        w = workloads.config3_n3(device=device, param_dtype=torch.float32)
         copies = 1  # inputs alone exceed L2
+    elif cfg == "3n4":
+        w = workloads.config3(device=device, param_dtype=torch.float32)
+        copies = 1
     elif cfg == "5":
         w = workloads.config5(device=device, param_dtype=torch.float32, image_device=device)
         copies = 1
@@ -184,6 +187,7 @@ def run_ours(args, rank, world, local):
     L = _native.load()
     w, sets = make_inputs(args.config, torch, device, 4, rank)
     iters = int(w["iterations"])
+    n3 = w.get("directions") == 3
     H, W = w["f"].shape
     row_bands = args.config == "5" and world > 1
     if row_bands:
@@ -203,6 +207,8 @@ def run_ours(args, rank, world, local):
         s = sets[i % len(sets)]
         if "adaptive" in s:
             return rb.adaptive_smooth(s["f"], w["noise_sigma"])
+        if "p" in s and n3:
+            return rb.filter_space_variant3_params(s["f"], *s["p"], iterations=iters)
         if "p" in s:
             return rb.filter_space_variant_params(s["f"], *s["p"], iterations=iters)
         return rb.filter_space_variant(s["f"], s["field"], iters)
@@ -272,6 +278,8 @@ def run_ours(args, rank, world, local):
             hout = torch.empty((H, W), dtype=torch.float64, pin_memory=True).numpy()
 
             def e2e_step():
+                if n3:
+                    return rb.filter_space_variant3_params(hfn, *hp, iterations=iters, out=hout)
                 return rb.filter_space_variant_params(hfn, *hp, lut=lut, iterations=iters, out=hout)
             h2d = hf.numel() * hf.element_size() + sum(p.nbytes for p in hp)
         else:
@@ -338,12 +346,14 @@ def run_ours(args, rank, world, local):
             "config": {"workload": WORKLOADS[args.config], "image": [H, W], "iterations": iters,
                        "per_rank_images_per_step": 1,
                        "l2": "4 rotating input/output sets per rank (working set > 126 MB L2)",
-                       "path": "fused LUT mapping + filter (rubs_b200_filter_params)" if args.config != "1"
-                       else "drop-in (H,W,4) field (rubs_b200_filter)"},
+                       "path": ("fused closed-form N=3 mapping + exact N=3 filter (rubs_b200_filter3_params)"
+                                if n3 else "fused LUT mapping + filter (rubs_b200_filter_params)")
+                       if args.config != "1" else "drop-in (H,W,4) field (rubs_b200_filter)"},
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "traffic_unit": "bytes/launch (ncu)",
-                         "kernel": "wide_filter_kernel", "kernel_ms_avg": tile_avg_ms,
+                         "kernel": "n3_tile_kernel" if n3 else "wide_filter_kernel",
+                         "kernel_ms_avg": tile_avg_ms,
                          "algorithmic_bytes_per_px": bpp, "peak_source": peak_kind,
                          "binding_bound": "shared-memory wavefronts and issue (see smem, fp64)"},
             "fp64": fp64,
@@ -360,8 +370,11 @@ def run_ours(args, rank, world, local):
 
 
 WORKLOADS = {
-    "3": "config3 shapes: 8192^2 fp32 rectangles + N(0,0.05^2) noise; sigma [1,32], rho [1,6] "
-         "clamped, smooth theta; N=4 ZP element (the reference has no N=3 path)",
+    "3": "config3: 8192^2 fp32 rectangles + N(0,0.05^2) noise; N=3 directions (0/60/120 deg); "
+         "sigma [1,32], rho [1,6] clamped to 0.95 of the N=3 bound, smooth theta; exact N=3 path "
+         "(closed-form mapping fused, f32 params)",
+    "3n4": "config3 shapes with the N=4 ZP element: 8192^2 fp32 rectangles + N(0,0.05^2) noise; "
+           "sigma [1,32], rho [1,6] clamped, smooth theta (LUT mapping)",
     "5": "config5: 32768^2 fp32 uniform[0,1) (torch Philox seed 0); sigma [2,256], rho [1,8] "
          "clamped to the LUT, smooth theta; single GPU",
     "2": "config2: 2048^2 fp64 uniform[0,1) seed 0; N=4 ZP box spline; sigma [2,16], rho [1,4], "
@@ -397,6 +410,14 @@ def _adaptive_worker(k):
     crop = f[r0:r0 + c, :c]
     tensor_port.adaptive_smooth(crop, noise, lut, filt=lambda a, fld, m=1: port.filter_space_variant(a, fld, m))
     return c * c
+
+
+def _band3_worker(band):
+    """One N=3 row band (oracle/port3.py); returns pixels produced."""
+    from oracle import port3
+    lo, hi = band
+    port3.filter3_band(_PORT["f"], _PORT["field"], lo, hi)
+    return (hi - lo) * _PORT["f"].shape[1]
 
 
 def _band_worker(band):
@@ -437,6 +458,13 @@ class CpuPort:
             if cfg == "2":
                 w = workloads.config2()
             elif cfg == "3":
+                # N=3: a 2048^2 instance of config 3's recipe through the
+                # numpy restatement of the exact N=3 algorithm (no reference
+                # N=3 filter exists)
+                from oracle import port3
+                w = workloads.config3_n3(2048, 2048)
+                self.note = " (2048^2 instance of the config-3 N=3 recipe; oracle/port3.py)"
+            elif cfg == "3n4":
                 # a 2048^2 instance of config 3's recipe (same sigma / rho
                 # ranges; the full 8192^2 CPU run would take hours)
                 w = workloads.config3(2048, 2048)
@@ -446,15 +474,21 @@ class CpuPort:
                 self.note = " (2048^2 instance of the config-5 recipe)"
             else:
                 w = workloads.config4_image(0)
-            lut = default_lut()
-            field = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, w["size"].numpy(),
-                                     w["elong"].numpy(), w["orient"].numpy())
+            if cfg == "3":
+                field = port3.scales3_from_params(w["size"].numpy(), w["elong"].numpy(),
+                                                  w["orient"].numpy())
+            else:
+                lut = default_lut()
+                field = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, w["size"].numpy(),
+                                         w["elong"].numpy(), w["orient"].numpy())
         f = np.asarray(w["f"], dtype=np.float64)
         _PORT.update(f=f, field=field, iters=int(w["iterations"]))
         self.H, self.W = f.shape
         self.cfg = cfg
         self.cores = workers or os.cpu_count() or 1
         rows = max(min_rows, -(-self.H // self.cores))
+        if cfg == "3":
+            rows = 32  # bounded sample: the N=3 port costs O(kernel height) per pixel
         self.bands = [(lo, min(self.H, lo + rows)) for lo in range(0, self.H, rows)][: self.cores]
         self.cores = len(self.bands)
         os.environ["OMP_NUM_THREADS"] = "1"
@@ -466,7 +500,7 @@ class CpuPort:
         if self.cfg == "A":
             px = sum(self.pool.map(_adaptive_worker, self.jobs))
         else:
-            px = sum(self.pool.map(_band_worker, self.bands))
+            px = sum(self.pool.map(_band3_worker if self.cfg == "3" else _band_worker, self.bands))
         return px, time.perf_counter() - t0
 
     def sample(self):
@@ -477,8 +511,10 @@ class CpuPort:
         return (f"{len(self.bands)} row bands of {self.rows} rows x {self.W} cols "
                 f"({sum(h - l for l, h in self.bands)} of {self.H} rows) of {WORKLOADS[self.cfg].split(':')[0]}"
                 f"{self.note}, "
-                f"halo rows recomputed per band; numpy port of the reference fast path "
-                f"(oracle/port.py), {self.cores} processes x 1 thread")
+                f"halo rows recomputed per band; "
+                + ("numpy restatement of the exact N=3 row-profile algorithm (oracle/port3.py)"
+                   if self.cfg == "3" else "numpy port of the reference fast path (oracle/port.py)")
+                + f", {self.cores} processes x 1 thread")
 
     def close(self):
         self.pool.close()

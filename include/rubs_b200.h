@@ -27,6 +27,7 @@
  *   RUBS_EOUTOFGRID   3  -> OutOfGrid       (solver.py:304-307)
  *   RUBS_ECUDA        4  -> RuntimeError    (CUDA error / OOM)
  *   RUBS_EUNSUPPORTED 5  -> RuntimeError    (configuration not handled)
+ *   RUBS_EINFEASIBLE  6  -> Infeasible      (solver.py:64-82; N=3 mapping)
  */
 #ifndef RUBS_B200_H
 #define RUBS_B200_H
@@ -43,6 +44,7 @@ extern "C" {
 #define RUBS_EOUTOFGRID 3
 #define RUBS_ECUDA 4
 #define RUBS_EUNSUPPORTED 5
+#define RUBS_EINFEASIBLE 6
 
 #define RUBS_F32 0
 #define RUBS_F64 1
@@ -222,6 +224,45 @@ int rubs_b200_adaptive_smooth(const void *f, int f_dtype, int64_t H, int64_t W, 
                               const rubs_lut *lut, double bound_fraction,
                               const double *size_range, double iso_gain, double *out,
                               int64_t ld_out, void *stream);
+
+/*
+ * Three-direction (N=3) radially-uniform box spline: directions at 0, 60
+ * and 120 degrees (the reference's direction_vectors(3), geometry.py:76-81;
+ * covariance sum a_k^2/12 u_k u_k^T, covariance_general, geometry.py:102-106),
+ * BASELINE.json config 3.  The reference has no N=3 filter (SURVEY.md §0
+ * fact 6); these entry points extend engine.filter_space_variant
+ * (engine.py:265-324) with its semantics -- zero padding, floor 0.05 before
+ * the 1/sqrt(m) scaling, iterated passes on canvases extended by the global
+ * support with the field edge-clamped -- to the N=3 kernel, computed
+ * exactly (no interpolation of the image).
+ *   field    device (H, W, 3) float64, element (r, c, k) at
+ *            field[(r * ld_field + c) * 3 + k]; or, when field_is_uniform,
+ *            a HOST pointer to 3 doubles
+ */
+int rubs_b200_filter3(const void *f, int f_dtype, int64_t H, int64_t W, int64_t ld_f,
+                      const double *field, int field_is_uniform, int64_t ld_field,
+                      int iterations, double *out, int64_t ld_out, void *stream);
+int rubs_b200_filter3_host(const void *f, int f_dtype, int64_t H, int64_t W,
+                           const double *field, int field_is_uniform, int iterations,
+                           double *out);
+
+/*
+ * Fused N=3 mapping + filter: per-pixel (size, elongation, orientation) ->
+ * covariance (covariance_from_params, geometry.py:153-172) -> the unique
+ * N=3 scales matching it (closed form; RUBS_EINFEASIBLE beyond the N=3
+ * elongation bound, min 3 at 30/90/150 degrees) -> filter.
+ */
+int rubs_b200_filter3_params(const void *f, int f_dtype, int64_t H, int64_t W, int64_t ld_f,
+                             const void *size, const void *elong, const void *orient,
+                             int p_dtype, int64_t ld_p, int iterations, double *out,
+                             int64_t ld_out, void *stream);
+int rubs_b200_filter3_params_host(const void *f, int f_dtype, int64_t H, int64_t W,
+                                  const void *size, const void *elong, const void *orient,
+                                  int p_dtype, int iterations, double *out);
+
+/* The N=3 mapping alone: device arrays of n parameters -> device n x 3. */
+int rubs_b200_scales3(const void *size, const void *elong, const void *orient, int p_dtype,
+                      int64_t n, double *out, void *stream);
 
 #ifdef __cplusplus
 }

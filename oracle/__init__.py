@@ -168,3 +168,83 @@ def points(f, field, pts, iterations=1, threads=None):
     with ThreadPoolExecutor(threads) as ex:
         list(ex.map(run, chunks))
     return out
+
+
+# ---------------------------------------------------------------------------
+# Three-direction (N=3) kernel (dense3_oracle.c): exact, test side only.
+
+
+def _lib3():
+    L = lib()
+    if not getattr(L, "_n3_ready", False):
+        dp = ctypes.POINTER(ctypes.c_double)
+        L.rubs_oracle3_kernel_many.restype = None
+        L.rubs_oracle3_kernel_many.argtypes = [dp, dp, dp, ctypes.c_int64, dp]
+        L.rubs_oracle3_dense.restype = ctypes.c_int
+        L.rubs_oracle3_dense.argtypes = [dp, ctypes.c_int, ctypes.c_int, dp, ctypes.c_int, ctypes.c_int, dp]
+        L.rubs_oracle3_points.restype = ctypes.c_int
+        L.rubs_oracle3_points.argtypes = [dp, ctypes.c_int, ctypes.c_int, dp, ctypes.c_int,
+                                          ctypes.POINTER(ctypes.c_int64), ctypes.c_int64, dp]
+        L._n3_ready = True
+    return L
+
+
+def kernel3_values(a, x1, x2):
+    """Exact N=3 kernel (directions 0/60/120 degrees) at points (x1, x2)."""
+    a = np.ascontiguousarray(a, dtype=np.float64).reshape(3)
+    x1, x2 = np.broadcast_arrays(np.asarray(x1, np.float64), np.asarray(x2, np.float64))
+    shape = x1.shape
+    x1 = np.ascontiguousarray(x1).reshape(-1)
+    x2 = np.ascontiguousarray(x2).reshape(-1)
+    out = np.empty(x1.size)
+    _lib3().rubs_oracle3_kernel_many(_dp(a), _dp(x1), _dp(x2), x1.size, _dp(out))
+    return out.reshape(shape)
+
+
+def _field3_arg(field, shape):
+    field = np.asarray(field, dtype=np.float64)
+    if field.shape == (3,):
+        return np.ascontiguousarray(field), 1
+    if field.shape != (*shape, 3):
+        raise ValueError("field shape mismatch")
+    return np.ascontiguousarray(field), 0
+
+
+def dense3(f, field, iterations=1):
+    """Exact dense N=3 filter (whole image)."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    H, W = f.shape
+    fld, uni = _field3_arg(field, f.shape)
+    out = np.empty((H, W))
+    if _lib3().rubs_oracle3_dense(_dp(f), H, W, _dp(fld), uni, int(iterations), _dp(out)) != 0:
+        raise RuntimeError("oracle dense3 failed")
+    return out
+
+
+def points3(f, field, pts, threads=None):
+    """Exact one-pass N=3 filter at pixels pts = (N, 2) [row, col]; threaded."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    H, W = f.shape
+    fld, uni = _field3_arg(field, f.shape)
+    pts = np.ascontiguousarray(pts, dtype=np.int64).reshape(-1, 2)
+    out = np.empty(pts.shape[0])
+    n = pts.shape[0]
+    if n == 0:
+        return out
+    threads = threads or min(os.cpu_count() or 1, 64)
+    chunks = np.array_split(np.arange(n), min(threads * 4, n))
+    L = _lib3()
+
+    def run(idx):
+        if idx.size == 0:
+            return
+        p = np.ascontiguousarray(pts[idx])
+        o = np.empty(idx.size)
+        if L.rubs_oracle3_points(_dp(f), H, W, _dp(fld), uni,
+                                 p.ctypes.data_as(ctypes.POINTER(ctypes.c_int64)), idx.size, _dp(o)):
+            raise RuntimeError("oracle points3 failed")
+        out[idx] = o
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(run, chunks))
+    return out

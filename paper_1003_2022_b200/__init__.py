@@ -22,7 +22,10 @@ from .engine import (
     filter_space_invariant,
     filter_space_variant,
     filter_space_variant_params,
+    filter_space_variant3,
+    filter_space_variant3_params,
     interpolate,
+    scales3_many,
     lookup_many,
     preintegrate,
 )
@@ -30,8 +33,12 @@ from .geometry import (
     MIN_ELONGATION_BOUND,
     as_scale_vector,
     covariance_from_params,
+    covariance_general,
     covariance_of,
+    direction_vectors,
     elongation_bound,
+    elongation_bound3,
+    scales3_from_params,
     sigma_to_size,
 )
 from .solver import Infeasible, OutOfGrid, ScaleLut, build_lut, default_lut, optimize_scale_vector
@@ -64,6 +71,13 @@ __all__ = [
     "filter_space_invariant",
     "filter_space_variant",
     "filter_space_variant_params",
+    "filter_space_variant3",
+    "filter_space_variant3_params",
+    "scales3_many",
+    "scales3_from_params",
+    "covariance_general",
+    "direction_vectors",
+    "elongation_bound3",
     "interpolate",
     "lookup_many",
     "optimize_scale_vector",

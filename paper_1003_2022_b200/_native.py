@@ -26,7 +26,8 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-shared",
 ]
 
-RUBS_OK, RUBS_EVALUE, RUBS_EOVERFLOW, RUBS_EOUTOFGRID, RUBS_ECUDA, RUBS_EUNSUPPORTED = range(6)
+(RUBS_OK, RUBS_EVALUE, RUBS_EOVERFLOW, RUBS_EOUTOFGRID, RUBS_ECUDA, RUBS_EUNSUPPORTED,
+ RUBS_EINFEASIBLE) = range(7)
 RUBS_F32, RUBS_F64 = 0, 1
 
 
@@ -35,7 +36,7 @@ def build_native(verbose: bool = False, defines=(), out: str | None = None) -> s
     ``defines``/``out`` build a variant library for A/B runs."""
     os.makedirs(LIB_DIR, exist_ok=True)
     out = out or LIB_PATH
-    srcs = [os.path.join(CSRC, "rubs_b200.cu"), os.path.join(CSRC, "rubs_tensor.cu")]
+    srcs = [os.path.join(CSRC, n) for n in ("rubs_b200.cu", "rubs_tensor.cu", "rubs_n3.cu")]
     cmd = ["nvcc", *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", INCLUDE, "-o", out + ".tmp",
            *srcs]
     if verbose:
@@ -89,6 +90,12 @@ SIGNATURES = {
     "rubs_b200_anisotropy": (_int, [_vp, _i64, _i64, _dbl, _vp, _dbl, _dbl, _vp, _vp, _vp, _vp, _vp]),
     "rubs_b200_adaptive_smooth": (_int, [_vp, _int, _i64, _i64, _i64, _dbl, _dbl, _int, _vp, _dbl, _vp,
                                          _dbl, _vp, _i64, _vp]),
+    "rubs_b200_filter3": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _int, _i64, _int, _vp, _i64, _vp]),
+    "rubs_b200_filter3_host": (_int, [_vp, _int, _i64, _i64, _vp, _int, _int, _vp]),
+    "rubs_b200_filter3_params": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp, _int, _i64, _int,
+                                        _vp, _i64, _vp]),
+    "rubs_b200_filter3_params_host": (_int, [_vp, _int, _i64, _i64, _vp, _vp, _vp, _int, _int, _vp]),
+    "rubs_b200_scales3": (_int, [_vp, _vp, _vp, _int, _i64, _vp, _vp]),
 }
 
 
@@ -124,4 +131,7 @@ def check(rc: int) -> None:
     if rc == RUBS_EOUTOFGRID:
         from .solver import OutOfGrid
         raise OutOfGrid(msg)
+    if rc == RUBS_EINFEASIBLE:
+        from .solver import Infeasible
+        raise Infeasible(msg)
     raise RuntimeError(f"rubs_b200 error {rc}: {msg}")

@@ -2720,6 +2720,12 @@ int rubs_b200_interpolate(const double *plane, int64_t rows, int64_t cols, int64
 
 namespace rubs_internal {
 int set_error(int code, const std::string &msg) { return ::set_error(code, msg); }
+void count_launches(int n) { t_launches += n; }
+void *timed_begin(int kind, void *stream) {
+  return new TimedLaunch(kind, static_cast<cudaStream_t>(stream));
+}
+void timed_end(void *token) { delete static_cast<TimedLaunch *>(token); }
+void timer_collect() { ::timer_collect(); }
 double lut_rho_max(const rubs_lut *lut) { return lut->rho_max; }
 
 int filter_uniform_multi(const double *const *f, int nch, int64_t H, int64_t W, int64_t ld,

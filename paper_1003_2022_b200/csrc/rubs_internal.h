@@ -13,6 +13,15 @@ namespace rubs_internal {
 // `code`.
 int set_error(int code, const std::string &msg);
 
+// Launch accounting shared by the translation units: count `n` kernel
+// launches (rubs_b200_launch_count), and bracket the primary filter launch
+// of a pass with CUDA events when profiling is on (rubs_b200_kernel_time,
+// kind 0 = primary filter kernel); timer_collect() after the stream sync.
+void count_launches(int n);
+void *timed_begin(int kind, void *stream);
+void timed_end(void *token);
+void timer_collect();
+
 // Largest elongation of a LUT's rho grid.
 double lut_rho_max(const rubs_lut *lut);
 

@@ -1,0 +1,662 @@
+// rubs_n3.cu -- the three-direction (N=3) radially-uniform box-spline filter
+// on sm_100a: directions at 0, 60 and 120 degrees (BASELINE.json config 3;
+// the reference's direction_vectors(3), geometry.py:76-81, covariance
+// sum a_k^2/12 u_k u_k^T, geometry.py:102-106).
+//
+// The reference has no N=3 filter: the paper's O(1)
+// algorithm needs running sums along the box directions on the pixel
+// lattice, and 60/120 degrees are not lattice directions (PAPER.md:285,
+// 662).  Any interpolation there changes the kernel.  This path is EXACT
+// instead: only the on-lattice direction u1 = (1, 0) is
+// pre-integrated, and the rest of the kernel is taken row by row.
+//
+// Slicing the kernel at height y: box(u2) * box(u3) is uniform on a
+// parallelogram whose horizontal chord is [L(y), U(y)],
+//   L(y) = max(-a2/2 - y/sqrt3, y/sqrt3 - a3/2),
+//   U(y) = min( a2/2 - y/sqrt3, y/sqrt3 + a3/2),
+// so beta(x, y) = K |[x - a1/2, x + a1/2] n [L(y), U(y)]|, K = 2/(sqrt3 a1 a2 a3),
+// a trapezoid in x = four ramps.  With the row's double running sum
+// S_j(t) = sum_m f[j, m] max(t - m, 0) -- piecewise linear between integers,
+// so linear interpolation of its integer samples is exact --
+//   out(n) = K sum_d [S(n1+h-L) - S(n1+h-U) - S(n1-h-L) + S(n1-h-U)],  j = n2 - d.
+// Cost per pixel is O(kernel height), four interpolated reads per row.
+//
+// Layout: one 32x32 output tile per CTA (256 threads, 2 CTAs per SM).  The
+// tile's region -- the columns its pixels read, rows streamed in chunks --
+// holds per entry k the pair (S[k] + C[k]/2, C[k]) (C = inclusive running
+// sum), restarted at the region's left edge: a restart adds a linear
+// function of t to S, which the four-ramp difference cancels exactly.  A
+// read at real t is then one LDS.128 and one FMA: S(t) = M[k] + phi C[k]
+// with k = round(t - 1/2), phi = t - 1/2 - k.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <string>
+
+#include "../../include/rubs_b200.h"
+#include "rubs_device.cuh"
+#include "rubs_internal.h"
+
+using namespace rubs;
+using rubs_internal::set_error;
+
+namespace {
+
+#define RUBS3_CUDA_TRY(expr)                                                         \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      return set_error(RUBS_ECUDA, std::string(#expr ": ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+constexpr double kInvSqrt3 = 0.5773502691896258;
+constexpr double kQuarterSqrt3 = 0.4330127018922193;  // sqrt3 / 4
+constexpr double kRoundMagic = 6755399441055744.0;     // 1.5 * 2^52: round to nearest
+constexpr unsigned kFlagInfeasible = 16u;              // a_k^2 < 0: covariance out of reach
+
+// field modes
+constexpr int kM3Field = 0;     // (FH, FW, 3) float64
+constexpr int kM3Uniform = 1;   // one (3,) vector
+constexpr int kM3Params = 2;    // (size, elongation, orientation) float64
+constexpr int kM3Params32 = 3;  // same, float32
+
+constexpr int kTW = 32, kTH = 32, kNT = 256, kPx = kTH / (kNT / 32);
+constexpr int kSmem3 = 110 * 1024;
+
+struct Field3 {
+  int mode;
+  const double *a;
+  int64_t ld;  // field row stride in pixels
+  double u[3];
+  const void *ps, *pr, *pt;
+  int64_t pld;
+  int FH, FW;  // field grid (edge-clamped on iterated canvases)
+  double div;  // sqrt(iterations)
+  int scaled;
+};
+
+struct Status3 {
+  unsigned flags;
+  int rx, ry;  // global support radii (iterations > 1)
+};
+
+// (size, elongation, orientation) -> N=3 scales: C = sum_k a_k^2/12 u_k u_k^T
+// solved in closed form (u1 = (1,0), u2 = (1/2, sqrt3/2), u3 = (-1/2, sqrt3/2)):
+//   p1 = C11 - C22/3,  p2,3 = 2/3 C22 +- 2/sqrt3 C12,  a_k = sqrt(12 p_k).
+// Validation as solver.lookup_many (solver.py:298-303); p_k < -1e-12 size is
+// beyond the N=3 elongation bound -> Infeasible.
+__device__ __forceinline__ void params_to_scales3(double s, double rho, double th, double a[3],
+                                                  unsigned &flags) {
+  const bool s_ok = (s > 0.0) && (s < INFINITY);
+  const bool r_ok = (rho >= 1.0) && (rho < INFINITY);
+  const bool t_ok = (th >= 0.0) && (th < kPi);
+  if (!(s_ok && r_ok && t_ok)) {
+    flags |= kFlagParamInvalid;
+    s = 1.0;
+    rho = 1.0;
+    th = 0.0;
+  }
+  double sn, cs;
+  sincos(th, &sn, &cs);
+  const double inv = 1.0 / (1.0 + rho);
+  const double big = s * rho * inv, small = s * inv;
+  const double c11 = big * cs * cs + small * sn * sn;
+  const double c22 = big * sn * sn + small * cs * cs;
+  const double c12 = (big - small) * cs * sn;
+  double p[3];
+  p[0] = c11 - c22 * (1.0 / 3.0);
+  p[1] = c22 * (2.0 / 3.0) + c12 * (2.0 * kInvSqrt3);
+  p[2] = c22 * (2.0 / 3.0) - c12 * (2.0 * kInvSqrt3);
+  const double tol = -1e-12 * s;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (p[k] < tol) flags |= kFlagInfeasible;
+    a[k] = sqrt(12.0 * fmax(p[k], 0.0));
+  }
+}
+
+// Floored, pass-scaled scales of lattice pixel (gx, gy); field edge-clamped.
+template <int MODE>
+__device__ __forceinline__ void scales3_at(const Field3 &F, int gx, int gy, double a[3],
+                                           unsigned &flags) {
+  const int c = min(max(gx, 0), F.FW - 1), r = min(max(gy, 0), F.FH - 1);
+  if constexpr (MODE == kM3Field) {
+    const double *p = F.a + ((int64_t)r * F.ld + c) * 3;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      a[k] = __ldg(p + k);
+      if ((__double2hiint(a[k]) & 0x7ff00000) == 0x7ff00000) flags |= kFlagFieldNonFinite;
+    }
+  } else if constexpr (MODE == kM3Uniform) {
+    a[0] = F.u[0];
+    a[1] = F.u[1];
+    a[2] = F.u[2];
+  } else {
+    const int64_t i = (int64_t)r * F.pld + c;
+    const int dt = MODE == kM3Params ? 1 : 0;
+    params_to_scales3(load_scalar(F.ps, dt, i), load_scalar(F.pr, dt, i),
+                      load_scalar(F.pt, dt, i), a, flags);
+  }
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    double v = fmax(a[k], kScaleFloor);  // engine.py:292 (NaN -> flagged above)
+    a[k] = F.scaled ? v / F.div : v;     // engine.py:293
+  }
+}
+
+__device__ __forceinline__ double2 lds128(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr));
+  return v;
+}
+
+// S at entry coordinate t' + 1/2 of the row at shared address `row`.
+__device__ __forceinline__ double s_read(uint32_t row, double tp) {
+  const double r = __dadd_rn(tp, kRoundMagic);
+  const int k = __double2loint(r);
+  const double phi = __dsub_rn(tp, __dsub_rn(r, kRoundMagic));
+  const double2 e = lds128(row + 16u * (uint32_t)k);
+  return __fma_rn(phi, e.y, e.x);
+}
+
+template <int MODE, int DT>
+__global__ void __launch_bounds__(kNT, 2)
+    n3_tile_kernel(ImageSpec I, Field3 F, DomainSpec D, Status3 *st) {
+  extern __shared__ __align__(16) double2 E[];
+  __shared__ int s_ext[4];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tx0 = blockIdx.x * kTW, ty0 = blockIdx.y * kTH;
+  if (threadIdx.x == 0) {
+    s_ext[0] = INT_MAX;
+    s_ext[1] = INT_MIN;
+    s_ext[2] = INT_MAX;
+    s_ext[3] = INT_MIN;
+  }
+  __syncthreads();
+
+  // --- per-pixel scales and the tile's region extent
+  double A1[kPx], A2[kPx], A3[kPx];
+  bool live[kPx];
+  unsigned flags = 0;
+  int cmin = INT_MAX, cmax = INT_MIN, rmin = INT_MAX, rmax = INT_MIN;
+  const int X = D.pc_lo + tx0 + lane;
+#pragma unroll
+  for (int i = 0; i < kPx; ++i) {
+    const int px = tx0 + lane, py = ty0 + warp + 8 * i;
+    live[i] = px < D.pw && py < D.ph;
+    A1[i] = A2[i] = A3[i] = 1.0;
+    if (live[i]) {
+      const int Y = D.pr_lo + py;
+      double a[3];
+      scales3_at<MODE>(F, X, Y, a, flags);
+      A1[i] = a[0];
+      A2[i] = a[1];
+      A3[i] = a[2];
+      const double hx = 0.5 * a[0] + 0.25 * (a[1] + a[2]);
+      const double hy = kQuarterSqrt3 * (a[1] + a[2]);
+      cmin = min(cmin, (int)floor(X - hx));
+      cmax = max(cmax, (int)floor(X + hx));
+      rmin = min(rmin, (int)ceil(Y - hy));
+      rmax = max(rmax, (int)floor(Y + hy));
+    }
+  }
+  cmin = __reduce_min_sync(0xffffffffu, cmin);
+  cmax = __reduce_max_sync(0xffffffffu, cmax);
+  rmin = __reduce_min_sync(0xffffffffu, rmin);
+  rmax = __reduce_max_sync(0xffffffffu, rmax);
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if (lane == 0) {
+    atomicMin(&s_ext[0], cmin);
+    atomicMax(&s_ext[1], cmax);
+    atomicMin(&s_ext[2], rmin);
+    atomicMax(&s_ext[3], rmax);
+    if (flags) atomicOr(&st->flags, flags);
+  }
+  __syncthreads();
+  const int c0 = s_ext[0], c1 = s_ext[1], r0 = s_ext[2], r1 = s_ext[3];
+  if (c0 > c1) return;  // no live pixel
+  const int Wr = c1 - c0 + 2;  // entries k = c0 - 1 .. c1
+  const int Rc = min(r1 - r0 + 1, (int)(kSmem3 / (16 * Wr)));
+  if (Rc < 1) {
+    if (threadIdx.x == 0) atomicOr(&st->flags, kFlagRegionTooLarge);
+    return;
+  }
+
+  // --- per-pixel constants in entry coordinates (entry e <-> column c0 - 1 + e)
+  double X1[kPx], X3[kPx], acc[kPx], K[kPx];
+  int jlo[kPx], jhi[kPx];
+#pragma unroll
+  for (int i = 0; i < kPx; ++i) {
+    const int Y = D.pr_lo + ty0 + warp + 8 * i;
+    const double h = 0.5 * A1[i];
+    const double hy = kQuarterSqrt3 * (A2[i] + A3[i]);
+    const double xe = (double)(X - c0);  // entry coordinate of x, minus 1/2
+    X1[i] = xe + h;
+    X3[i] = xe - h;
+    K[i] = 2.0 * kInvSqrt3 / (A1[i] * A2[i] * A3[i]);
+    acc[i] = 0.0;
+    jlo[i] = live[i] ? (int)ceil(Y - hy) : INT_MAX;
+    jhi[i] = live[i] ? (int)floor(Y + hy) : INT_MIN;
+    A2[i] *= 0.5;  // half widths from here on
+    A3[i] *= 0.5;
+  }
+
+  const uint32_t Es = (uint32_t)__cvta_generic_to_shared(E);
+  for (int cr0 = r0; cr0 <= r1; cr0 += Rc) {
+    const int nrows = min(Rc, r1 - cr0 + 1);
+    __syncthreads();  // previous chunk's reads are done
+    // --- rows of the chunk: entry pairs (S + C/2, C), one warp per row
+    for (int rr = warp; rr < nrows; rr += kNT / 32) {
+      const int ir = cr0 + rr - I.row0;
+      const bool rin = ir >= 0 && ir < I.h;
+      double2 *row = E + (size_t)rr * Wr;
+      double carryC = 0.0, carryS = 0.0;
+      for (int e0 = 0; e0 < Wr; e0 += 32) {
+        const int e = e0 + lane;
+        double v = 0.0;
+        const int ic = c0 - 1 + e - I.col0;
+        if (rin && e >= 1 && e < Wr && ic >= 0 && ic < I.w)
+          v = load_px<DT>(I.f, (int64_t)ir * I.ld + ic);
+        double c = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double t = __shfl_up_sync(0xffffffffu, c, o);
+          if (lane >= o) c += t;
+        }
+        c += carryC;
+        double sc = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const double t = __shfl_up_sync(0xffffffffu, sc, o);
+          if (lane >= o) sc += t;
+        }
+        const double S = carryS + (sc - c);
+        if (e < Wr) row[e] = make_double2(__fma_rn(0.5, c, S), c);
+        carryC = __shfl_sync(0xffffffffu, c, 31);
+        carryS += __shfl_sync(0xffffffffu, sc, 31);
+      }
+    }
+    __syncthreads();
+    // --- rows of the chunk into every pixel's sum
+    const int cr1 = cr0 + nrows - 1;
+#pragma unroll 1
+    for (int i = 0; i < kPx; ++i) {
+      const int ja = max(jlo[i], cr0), jb = min(jhi[i], cr1);
+      const int Y = D.pr_lo + ty0 + warp + 8 * i;
+      const double ha = A2[i], hb = A3[i], x1 = X1[i], x3 = X3[i];
+      double s = 0.0;
+      uint32_t row = Es + 16u * (uint32_t)((ja - cr0) * Wr);
+      const uint32_t rstep = 16u * (uint32_t)Wr;
+#pragma unroll 2
+      for (int j = ja; j <= jb; ++j, row += rstep) {
+        const double yd = (double)(Y - j) * kInvSqrt3;
+        const double L = fmax(-ha - yd, yd - hb);
+        const double U = fmax(fmin(ha - yd, yd + hb), L);
+        const double e1 = s_read(row, x1 - L), e2 = s_read(row, x1 - U);
+        const double e3 = s_read(row, x3 - L), e4 = s_read(row, x3 - U);
+        s += (e1 - e2) - (e3 - e4);
+      }
+      acc[i] += s;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < kPx; ++i)
+    if (live[i]) {
+      const int px = tx0 + lane, py = ty0 + warp + 8 * i;
+      D.out[(int64_t)py * D.ld_out + px] = K[i] * acc[i];
+    }
+}
+
+// Global support radii of the (floored, scaled) field: canvases of iterated
+// passes (the N=3 counterpart of engine.py:295 + oracle.py:200-203).
+template <int MODE>
+__global__ void __launch_bounds__(256) n3_margins_kernel(Field3 F, Status3 *st) {
+  unsigned flags = 0;
+  int rx = 0, ry = 0;
+  const int64_t n = MODE == kM3Uniform ? 1 : (int64_t)F.FH * F.FW;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double a[3];
+    scales3_at<MODE>(F, (int)(i % F.FW), (int)(i / F.FW), a, flags);
+    rx = max(rx, (int)ceil(0.5 * a[0] + 0.25 * (a[1] + a[2])) + 1);
+    ry = max(ry, (int)ceil(kQuarterSqrt3 * (a[1] + a[2])) + 1);
+  }
+  rx = __reduce_max_sync(0xffffffffu, rx);
+  ry = __reduce_max_sync(0xffffffffu, ry);
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&st->rx, rx);
+    atomicMax(&st->ry, ry);
+    if (flags) atomicOr(&st->flags, flags);
+  }
+}
+
+// Standalone mapping (size, elongation, orientation) -> (n, 3) scales.
+template <int DT>
+__global__ void scales3_kernel(const void *ps, const void *pr, const void *pt, int64_t n,
+                               double *out, Status3 *st) {
+  unsigned flags = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    double a[3];
+    params_to_scales3(load_scalar(ps, DT, i), load_scalar(pr, DT, i), load_scalar(pt, DT, i), a,
+                      flags);
+    out[3 * i] = a[0];
+    out[3 * i + 1] = a[1];
+    out[3 * i + 2] = a[2];
+  }
+  flags = __reduce_or_sync(0xffffffffu, flags);
+  if ((threadIdx.x & 31) == 0 && flags) atomicOr(&st->flags, flags);
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+struct Scratch3 {
+  int device = -1;
+  Status3 *d_st = nullptr;
+  Status3 *h_st = nullptr;  // pinned
+  double *d_pass[2] = {nullptr, nullptr};
+  size_t pass_cap[2] = {0, 0};
+  bool attr = false;
+};
+thread_local Scratch3 t3;
+
+template <int M, int T>
+int set_attr() {
+  RUBS3_CUDA_TRY(cudaFuncSetAttribute(n3_tile_kernel<M, T>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem3));
+  return RUBS_OK;
+}
+
+int ensure3() {
+  int dev = 0;
+  RUBS3_CUDA_TRY(cudaGetDevice(&dev));
+  if (t3.device != dev) {
+    t3 = Scratch3();
+    t3.device = dev;
+    RUBS3_CUDA_TRY(cudaMalloc(&t3.d_st, sizeof(Status3)));
+    RUBS3_CUDA_TRY(cudaMallocHost(&t3.h_st, sizeof(Status3)));
+  }
+  if (!t3.attr) {
+    int rc;
+    if ((rc = set_attr<kM3Field, 0>()) || (rc = set_attr<kM3Field, 1>()) ||
+        (rc = set_attr<kM3Uniform, 0>()) || (rc = set_attr<kM3Uniform, 1>()) ||
+        (rc = set_attr<kM3Params, 0>()) || (rc = set_attr<kM3Params, 1>()) ||
+        (rc = set_attr<kM3Params32, 0>()) || (rc = set_attr<kM3Params32, 1>()))
+      return rc;
+    t3.attr = true;
+  }
+  return RUBS_OK;
+}
+
+int fetch3(cudaStream_t s, Status3 &out) {
+  RUBS3_CUDA_TRY(cudaMemcpyAsync(t3.h_st, t3.d_st, sizeof(Status3), cudaMemcpyDeviceToHost, s));
+  RUBS3_CUDA_TRY(cudaStreamSynchronize(s));
+  out = *t3.h_st;
+  rubs_internal::timer_collect();
+  return RUBS_OK;
+}
+
+int code3(const Status3 &st) {
+  if (st.flags & kFlagFieldNonFinite)
+    return set_error(RUBS_EVALUE, "scale field entries must be finite");
+  if (st.flags & kFlagParamInvalid)
+    return set_error(RUBS_EVALUE,
+                     "size must be positive and finite, elongation >= 1 and finite, "
+                     "orientation in [0, pi)");
+  if (st.flags & kFlagInfeasible)
+    return set_error(RUBS_EINFEASIBLE,
+                     "elongation beyond the three-direction bound at this orientation");
+  if (st.flags & kFlagRegionTooLarge)
+    return set_error(RUBS_EUNSUPPORTED,
+                     "kernel support exceeds the on-chip region capacity of this build");
+  return RUBS_OK;
+}
+
+template <int M, int T>
+void launch3(const ImageSpec &I, const Field3 &F, const DomainSpec &D, cudaStream_t s) {
+  dim3 grid((D.pw + kTW - 1) / kTW, (D.ph + kTH - 1) / kTH);
+  n3_tile_kernel<M, T><<<grid, kNT, kSmem3, s>>>(I, F, D, t3.d_st);
+}
+
+int launch_pass3(const ImageSpec &I, const Field3 &F, const DomainSpec &D, cudaStream_t s) {
+  void *tok = rubs_internal::timed_begin(0, s);
+  const int t = I.dt;
+  switch (F.mode) {
+    case kM3Field: t ? launch3<kM3Field, 1>(I, F, D, s) : launch3<kM3Field, 0>(I, F, D, s); break;
+    case kM3Uniform:
+      t ? launch3<kM3Uniform, 1>(I, F, D, s) : launch3<kM3Uniform, 0>(I, F, D, s);
+      break;
+    case kM3Params: t ? launch3<kM3Params, 1>(I, F, D, s) : launch3<kM3Params, 0>(I, F, D, s); break;
+    default: t ? launch3<kM3Params32, 1>(I, F, D, s) : launch3<kM3Params32, 0>(I, F, D, s);
+  }
+  rubs_internal::timed_end(tok);
+  rubs_internal::count_launches(1);
+  RUBS3_CUDA_TRY(cudaGetLastError());
+  return RUBS_OK;
+}
+
+int ensure_pass3(int k, size_t n) {
+  if (n > t3.pass_cap[k]) {
+    if (t3.d_pass[k]) cudaFree(t3.d_pass[k]);
+    t3.d_pass[k] = nullptr;
+    t3.pass_cap[k] = 0;
+    RUBS3_CUDA_TRY(cudaMalloc(&t3.d_pass[k], n * sizeof(double)));
+    t3.pass_cap[k] = n;
+  }
+  return RUBS_OK;
+}
+
+// filter_space_variant orchestration (engine.py:285-324) for N=3.
+int run3(const ImageSpec &img, Field3 F, int iterations, double *out, int64_t ld_out,
+         cudaStream_t s) {
+  if (img.h < 0 || img.w < 0) return set_error(RUBS_EVALUE, "image must be 2-D");
+  if (iterations < 1) return set_error(RUBS_EVALUE, "iterations must be >= 1");
+  int rc = ensure3();
+  if (rc) return rc;
+  if (img.h == 0 || img.w == 0) return RUBS_OK;
+  F.FH = img.h;
+  F.FW = img.w;
+  F.div = std::sqrt((double)iterations);
+  F.scaled = iterations > 1;
+  RUBS3_CUDA_TRY(cudaMemsetAsync(t3.d_st, 0, sizeof(Status3), s));
+  Status3 st;
+  if (iterations == 1) {
+    DomainSpec D{0, 0, img.w, img.h, out, ld_out};
+    if ((rc = launch_pass3(img, F, D, s))) return rc;
+    if ((rc = fetch3(s, st))) return rc;
+    return code3(st);
+  }
+  {
+    const int blocks = F.mode == kM3Uniform ? 1 : 4 * 148;
+    switch (F.mode) {
+      case kM3Field: n3_margins_kernel<kM3Field><<<blocks, 256, 0, s>>>(F, t3.d_st); break;
+      case kM3Uniform: n3_margins_kernel<kM3Uniform><<<blocks, 256, 0, s>>>(F, t3.d_st); break;
+      case kM3Params: n3_margins_kernel<kM3Params><<<blocks, 256, 0, s>>>(F, t3.d_st); break;
+      default: n3_margins_kernel<kM3Params32><<<blocks, 256, 0, s>>>(F, t3.d_st);
+    }
+    rubs_internal::count_launches(1);
+    RUBS3_CUDA_TRY(cudaGetLastError());
+  }
+  if ((rc = fetch3(s, st))) return rc;
+  if ((rc = code3(st))) return rc;
+  const int rx = st.rx, ry = st.ry;
+  ImageSpec cur = img;
+  for (int p = 0; p < iterations; ++p) {
+    const int remain = iterations - 1 - p;
+    DomainSpec Dp;
+    Dp.pc_lo = -remain * rx;
+    Dp.pr_lo = -remain * ry;
+    Dp.pw = img.w + 2 * remain * rx;
+    Dp.ph = img.h + 2 * remain * ry;
+    if (remain == 0) {
+      Dp.out = out;
+      Dp.ld_out = ld_out;
+    } else {
+      const int k = p & 1;
+      if ((rc = ensure_pass3(k, (size_t)Dp.pw * Dp.ph))) return rc;
+      Dp.out = t3.d_pass[k];
+      Dp.ld_out = Dp.pw;
+    }
+    if ((rc = launch_pass3(cur, F, Dp, s))) return rc;
+    cur = ImageSpec{Dp.out, 1, Dp.ld_out, Dp.ph, Dp.pw, Dp.pc_lo, Dp.pr_lo};
+  }
+  if ((rc = fetch3(s, st))) return rc;
+  return code3(st);
+}
+
+int check_image(int f_dtype, int64_t H, int64_t W) {
+  if (f_dtype != RUBS_F32 && f_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (H < 0 || W < 0) return set_error(RUBS_EVALUE, "image must be 2-D");
+  if (H > (1 << 30) || W > (1 << 30)) return set_error(RUBS_EUNSUPPORTED, "image too large");
+  return RUBS_OK;
+}
+
+int field3_of(const double *field, int uniform, int64_t ld_field, Field3 &F) {
+  F = Field3{};
+  if (uniform) {
+    F.mode = kM3Uniform;
+    for (int k = 0; k < 3; ++k) {
+      if (!std::isfinite(field[k])) return set_error(RUBS_EVALUE, "scale field entries must be finite");
+      F.u[k] = field[k];
+    }
+  } else {
+    F.mode = kM3Field;
+    F.a = field;
+    F.ld = ld_field;
+  }
+  return RUBS_OK;
+}
+
+Field3 params3_of(const void *size, const void *elong, const void *orient, int p_dtype,
+                  int64_t ld_p) {
+  Field3 F{};
+  F.mode = p_dtype == RUBS_F64 ? kM3Params : kM3Params32;
+  F.ps = size;
+  F.pr = elong;
+  F.pt = orient;
+  F.pld = ld_p;
+  return F;
+}
+
+// Host buffers: stage through device memory on a private stream.
+struct HostRun {
+  cudaStream_t s = nullptr;
+  void *buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  ~HostRun() {
+    for (void *b : buf)
+      if (b) cudaFreeAsync(b, s);
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int rubs_b200_filter3(const void *f, int f_dtype, int64_t H, int64_t W, int64_t ld_f,
+                      const double *field, int field_is_uniform, int64_t ld_field, int iterations,
+                      double *out, int64_t ld_out, void *stream) {
+  int rc;
+  if ((rc = check_image(f_dtype, H, W))) return rc;
+  Field3 F;
+  if ((rc = field3_of(field, field_is_uniform, ld_field, F))) return rc;
+  ImageSpec I{f, f_dtype, ld_f, (int)H, (int)W, 0, 0};
+  return run3(I, F, iterations, out, ld_out, static_cast<cudaStream_t>(stream));
+}
+
+int rubs_b200_filter3_params(const void *f, int f_dtype, int64_t H, int64_t W, int64_t ld_f,
+                             const void *size, const void *elong, const void *orient, int p_dtype,
+                             int64_t ld_p, int iterations, double *out, int64_t ld_out,
+                             void *stream) {
+  int rc;
+  if ((rc = check_image(f_dtype, H, W))) return rc;
+  if (p_dtype != RUBS_F32 && p_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  ImageSpec I{f, f_dtype, ld_f, (int)H, (int)W, 0, 0};
+  return run3(I, params3_of(size, elong, orient, p_dtype, ld_p), iterations, out, ld_out,
+              static_cast<cudaStream_t>(stream));
+}
+
+int rubs_b200_filter3_host(const void *f, int f_dtype, int64_t H, int64_t W, const double *field,
+                           int field_is_uniform, int iterations, double *out) {
+  int rc;
+  if ((rc = check_image(f_dtype, H, W))) return rc;
+  if (iterations < 1) return set_error(RUBS_EVALUE, "iterations must be >= 1");
+  if (H == 0 || W == 0) return RUBS_OK;
+  const size_t n = (size_t)H * W, fb = n * (f_dtype == RUBS_F64 ? 8 : 4);
+  HostRun h;
+  RUBS3_CUDA_TRY(cudaStreamCreateWithFlags(&h.s, cudaStreamNonBlocking));
+  RUBS3_CUDA_TRY(cudaMallocAsync(&h.buf[0], fb, h.s));
+  RUBS3_CUDA_TRY(cudaMallocAsync(&h.buf[1], n * 8, h.s));
+  RUBS3_CUDA_TRY(cudaMemcpyAsync(h.buf[0], f, fb, cudaMemcpyHostToDevice, h.s));
+  const double *fld = field;
+  if (!field_is_uniform) {
+    RUBS3_CUDA_TRY(cudaMallocAsync(&h.buf[2], n * 24, h.s));
+    RUBS3_CUDA_TRY(cudaMemcpyAsync(h.buf[2], field, n * 24, cudaMemcpyHostToDevice, h.s));
+    fld = static_cast<const double *>(h.buf[2]);
+  }
+  if ((rc = rubs_b200_filter3(h.buf[0], f_dtype, H, W, W, fld, field_is_uniform, W, iterations,
+                              static_cast<double *>(h.buf[1]), W, h.s)))
+    return rc;
+  RUBS3_CUDA_TRY(cudaMemcpyAsync(out, h.buf[1], n * 8, cudaMemcpyDeviceToHost, h.s));
+  RUBS3_CUDA_TRY(cudaStreamSynchronize(h.s));
+  return RUBS_OK;
+}
+
+int rubs_b200_filter3_params_host(const void *f, int f_dtype, int64_t H, int64_t W,
+                                  const void *size, const void *elong, const void *orient,
+                                  int p_dtype, int iterations, double *out) {
+  int rc;
+  if ((rc = check_image(f_dtype, H, W))) return rc;
+  if (p_dtype != RUBS_F32 && p_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (iterations < 1) return set_error(RUBS_EVALUE, "iterations must be >= 1");
+  if (H == 0 || W == 0) return RUBS_OK;
+  const size_t n = (size_t)H * W, fb = n * (f_dtype == RUBS_F64 ? 8 : 4),
+               pb = n * (p_dtype == RUBS_F64 ? 8 : 4);
+  HostRun h;
+  RUBS3_CUDA_TRY(cudaStreamCreateWithFlags(&h.s, cudaStreamNonBlocking));
+  RUBS3_CUDA_TRY(cudaMallocAsync(&h.buf[0], fb, h.s));
+  RUBS3_CUDA_TRY(cudaMallocAsync(&h.buf[1], n * 8, h.s));
+  RUBS3_CUDA_TRY(cudaMemcpyAsync(h.buf[0], f, fb, cudaMemcpyHostToDevice, h.s));
+  const void *src[3] = {size, elong, orient};
+  for (int k = 0; k < 3; ++k) {
+    RUBS3_CUDA_TRY(cudaMallocAsync(&h.buf[2 + k], pb, h.s));
+    RUBS3_CUDA_TRY(cudaMemcpyAsync(h.buf[2 + k], src[k], pb, cudaMemcpyHostToDevice, h.s));
+  }
+  if ((rc = rubs_b200_filter3_params(h.buf[0], f_dtype, H, W, W, h.buf[2], h.buf[3], h.buf[4],
+                                     p_dtype, W, iterations, static_cast<double *>(h.buf[1]), W,
+                                     h.s)))
+    return rc;
+  RUBS3_CUDA_TRY(cudaMemcpyAsync(out, h.buf[1], n * 8, cudaMemcpyDeviceToHost, h.s));
+  RUBS3_CUDA_TRY(cudaStreamSynchronize(h.s));
+  return RUBS_OK;
+}
+
+int rubs_b200_scales3(const void *size, const void *elong, const void *orient, int p_dtype,
+                      int64_t n, double *out, void *stream) {
+  if (p_dtype != RUBS_F32 && p_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (n < 0) return set_error(RUBS_EVALUE, "negative count");
+  int rc = ensure3();
+  if (rc) return rc;
+  if (n == 0) return RUBS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  RUBS3_CUDA_TRY(cudaMemsetAsync(t3.d_st, 0, sizeof(Status3), s));
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 8 * 148);
+  if (p_dtype == RUBS_F64)
+    scales3_kernel<1><<<blocks, 256, 0, s>>>(size, elong, orient, n, out, t3.d_st);
+  else
+    scales3_kernel<0><<<blocks, 256, 0, s>>>(size, elong, orient, n, out, t3.d_st);
+  rubs_internal::count_launches(1);
+  RUBS3_CUDA_TRY(cudaGetLastError());
+  Status3 st;
+  if ((rc = fetch3(s, st))) return rc;
+  return code3(st);
+}
+
+}  // extern "C"

@@ -404,3 +404,143 @@ def interpolate(image: IntegratedImage, x1, x2) -> np.ndarray:
         int(image.row0), ctypes.c_void_p(dx.data_ptr()), ctypes.c_void_p(dy.data_ptr()), xa.shape[0],
         ctypes.c_void_p(out.data_ptr()), _stream_handle()))
     return out.cpu().numpy().reshape(shape)
+
+
+# ---------------------------------------------------------------------------
+# Three-direction (N=3) box spline (BASELINE.json config 3).  Not in the
+# reference: these extend filter_space_variant's
+# semantics (engine.py:265-324) to the 0/60/120-degree kernel, computed
+# exactly on the device (csrc/rubs_n3.cu).
+
+
+def _host_field3(field, shape):
+    fld = np.asarray(field, dtype=np.float64)
+    if fld.shape == (3,):
+        if not np.isfinite(fld).all():
+            raise ValueError("scale field entries must be finite")
+        return np.ascontiguousarray(fld), True
+    if fld.shape != (*shape, 3):
+        raise ValueError(f"three-direction scale field shape {fld.shape} does not match image {shape}")
+    return np.ascontiguousarray(fld), False
+
+
+def _check_iterations(iterations) -> int:
+    if isinstance(iterations, bool) or int(iterations) != iterations:
+        raise ValueError("iterations must be an integer")
+    if int(iterations) < 1:
+        raise ValueError("iterations must be >= 1")
+    return int(iterations)
+
+
+def _torch_image(f):
+    torch = _torch()
+    if f.dim() != 2:
+        raise ValueError("image must be 2-D")
+    if not f.is_cuda:
+        raise ValueError("torch input must live on a CUDA device")
+    if f.dtype not in (torch.float32, torch.float64):
+        f = f.to(torch.float64)
+    return f.contiguous()
+
+
+def filter_space_variant3(f, field, iterations: int = 1, *, out=None):
+    """Three-direction filter: per-pixel scales (a1, a2, a3) along 0, 60 and
+    120 degrees.  ``field`` is (H, W, 3) or (3,); entries below SCALE_FLOOR
+    are clamped, passes use a / sqrt(iterations) like filter_space_variant.
+    Returns float64 of f's shape (numpy, or a CUDA tensor for CUDA input)."""
+    iterations = _check_iterations(iterations)
+    L = _native.load()
+    if _is_torch(f):
+        torch = _torch()
+        f = _torch_image(f)
+        H, W = f.shape
+        res = torch.empty((H, W), dtype=torch.float64, device=f.device)
+        fld = field.detach().cpu().numpy() if _is_torch(field) and tuple(field.shape) == (3,) else field
+        if _is_torch(fld):
+            if tuple(fld.shape) != (H, W, 3):
+                raise ValueError(f"three-direction scale field shape {tuple(fld.shape)} does not match image {(H, W)}")
+            dfl = fld.to(device=f.device, dtype=torch.float64).contiguous()
+            uniform, fptr = False, ctypes.c_void_p(dfl.data_ptr())
+        else:
+            arr, uniform = _host_field3(fld, (H, W))
+            if uniform:
+                fptr = _ptr(arr)
+            else:
+                dfl = torch.from_numpy(arr).to(f.device)
+                fptr = ctypes.c_void_p(dfl.data_ptr())
+        if H == 0 or W == 0:
+            return res
+        with torch.cuda.device(f.device):
+            _native.check(L.rubs_b200_filter3(
+                ctypes.c_void_p(f.data_ptr()), _native.RUBS_F32 if f.dtype == torch.float32 else _native.RUBS_F64,
+                H, W, W, fptr, int(uniform), W, iterations, ctypes.c_void_p(res.data_ptr()), W,
+                _stream_handle()))
+        return res
+    img = _host_image(f)
+    fld, uniform = _host_field3(field, img.shape)
+    H, W = img.shape
+    out = _host_out(out, (H, W))
+    if H == 0 or W == 0:
+        return out
+    _native.check(L.rubs_b200_filter3_host(_ptr(img), _img_dtype_code(img.dtype), H, W, _ptr(fld),
+                                           int(uniform), iterations, _ptr(out)))
+    return out
+
+
+def filter_space_variant3_params(f, size, elongation, orientation, iterations: int = 1, *, out=None):
+    """filter_space_variant3(f, scales3_from_params(size, elongation,
+    orientation), iterations) with the (closed-form) mapping fused into the
+    filter kernel.  Raises Infeasible beyond the N=3 elongation bound."""
+    iterations = _check_iterations(iterations)
+    L = _native.load()
+    if _is_torch(f):
+        torch = _torch()
+        f = _torch_image(f)
+        H, W = f.shape
+        ps = []
+        for v in (size, elongation, orientation):
+            v = v if _is_torch(v) else torch.as_tensor(np.asarray(v))
+            v = v.to(device=f.device)
+            if v.dtype not in (torch.float32, torch.float64):
+                v = v.to(torch.float64)
+            ps.append(v)
+        pdt = torch.float32 if all(p.dtype == torch.float32 for p in ps) else torch.float64
+        ps = [torch.broadcast_to(p.to(pdt), (H, W)).contiguous() for p in ps]
+        res = torch.empty((H, W), dtype=torch.float64, device=f.device)
+        if H == 0 or W == 0:
+            return res
+        with torch.cuda.device(f.device):
+            _native.check(L.rubs_b200_filter3_params(
+                ctypes.c_void_p(f.data_ptr()), _native.RUBS_F32 if f.dtype == torch.float32 else _native.RUBS_F64,
+                H, W, W, *(ctypes.c_void_p(p.data_ptr()) for p in ps),
+                _native.RUBS_F32 if pdt == torch.float32 else _native.RUBS_F64, W, iterations,
+                ctypes.c_void_p(res.data_ptr()), W, _stream_handle()))
+        return res
+    img = _host_image(f)
+    H, W = img.shape
+    (s, r, t), shape, dt = _params_host(size, elongation, orientation)
+    if shape != (H, W):
+        s, r, t = (np.ascontiguousarray(np.broadcast_to(v, (H, W))) for v in (s, r, t))
+    out = _host_out(out, (H, W))
+    if H == 0 or W == 0:
+        return out
+    _native.check(L.rubs_b200_filter3_params_host(
+        _ptr(img), _img_dtype_code(img.dtype), H, W, _ptr(s), _ptr(r), _ptr(t),
+        _native.RUBS_F32 if dt == np.float32 else _native.RUBS_F64, iterations, _ptr(out)))
+    return out
+
+
+def scales3_many(size, elongation, orientation):
+    """The N=3 mapping on the device: (..., 3) float64 numpy scales."""
+    (s, r, t), shape, dt = _params_host(size, elongation, orientation)
+    n = int(np.prod(shape)) if shape else 1
+    if n == 0:
+        return np.empty(shape + (3,))
+    torch = _torch()
+    ds, dr, dth = (torch.from_numpy(v.reshape(-1)).cuda() for v in (s, r, t))
+    res = torch.empty((n, 3), dtype=torch.float64, device="cuda")
+    _native.check(_native.load().rubs_b200_scales3(
+        ctypes.c_void_p(ds.data_ptr()), ctypes.c_void_p(dr.data_ptr()), ctypes.c_void_p(dth.data_ptr()),
+        _native.RUBS_F32 if dt == np.float32 else _native.RUBS_F64, n, ctypes.c_void_p(res.data_ptr()),
+        _stream_handle()))
+    return res.cpu().numpy().reshape(shape + (3,))

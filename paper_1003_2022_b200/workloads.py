@@ -11,8 +11,11 @@ Conventions (recorded in DESIGN.md):
   * rho is clamped to min(rho, 0.95 U(theta), 5.8 (1 - 1e-6)) like
     tensor.py:140 and tensor.py:216 (which use 1 - 1e-9; float32 parameters
     need the wider margin to stay inside the table after rounding).
-  * config 3's N=3 directions have no reference implementation; its shapes
-    run with the N=4 ZP element.
+  * config 3 names N=3 directions (0/60/120 degrees), which the reference
+    does not implement: ``config3_n3`` is that workload
+    for this repo's exact N=3 path (rho clamped to 0.95 of the N=3 bound,
+    min 3 at 30/90/150 degrees); ``config3`` keeps its shapes with the N=4
+    ZP element for the reference-anchored path.
 """
 
 from __future__ import annotations
@@ -122,6 +125,44 @@ def config3(H: int = 8192, W: int = 8192, device="cpu", param_dtype=None):
     f = rectangles_image(H, W)
     size, rho, theta = _param_fields(H, W, 1.0, 32.0, 6.0, (31, 32, 33), device, param_dtype)
     return {"name": "config3", "f": f, "size": size, "elong": rho, "orient": theta, "iterations": 1}
+
+
+def clamp_rho3(rho, theta):
+    """rho <- min(rho, 0.95 U3(theta)): the three-direction bound
+    (geometry.elongation_bound3), torch elementwise."""
+    torch = _torch()
+    c, s = torch.cos(theta), torch.sin(theta)
+    cc, ss, cs = c * c, s * s, c * s
+    r3 = 2.0 / math.sqrt(3.0)
+    alpha = [cc - ss / 3.0, 2.0 / 3.0 * ss + r3 * cs, 2.0 / 3.0 * ss - r3 * cs]
+    beta = [ss - cc / 3.0, 2.0 / 3.0 * cc - r3 * cs, 2.0 / 3.0 * cc + r3 * cs]
+    bound = torch.full_like(rho, float("inf"))
+    for al, be in zip(alpha, beta):
+        lim = torch.where(al < -1e-15, -be / al, torch.full_like(al, float("inf")))
+        bound = torch.minimum(bound, lim)
+    return torch.clamp(torch.minimum(rho, 0.95 * bound), min=1.0)
+
+
+def config3_n3(H: int = 8192, W: int = 8192, device="cpu", param_dtype=None):
+    """Config 3 as BASELINE.json names it: the 8192^2 float32 rectangles
+    image, N=3 directions (0/60/120 degrees), sigma in [1, 32], rho in
+    [1, 6] clamped to 0.95 of the N=3 bound, smooth theta; (size, rho,
+    theta) map to N=3 scales in closed form (filter_space_variant3_params)."""
+    torch = _torch()
+    f = rectangles_image(H, W)
+    sig = 1.0 + 31.0 * smooth(31, H, W, device)
+    size = 2.0 * sig * sig
+    theta = torch.remainder(2.0 * math.pi * smooth(33, H, W, device), math.pi)
+    theta = torch.where(theta >= math.pi, torch.zeros_like(theta), theta)
+    rho = clamp_rho3(1.0 + 5.0 * smooth(32, H, W, device), theta)
+    out = [size, rho, theta]
+    if param_dtype is not None:
+        out = [v.to(param_dtype) for v in out]
+        # the 0.95 margin dwarfs float32 rounding of (rho, theta)
+        out[2] = torch.where(out[2] >= math.pi, torch.zeros_like(out[2]), out[2])
+        out[1] = torch.clamp(out[1], min=1.0)
+    return {"name": "config3_n3", "f": f, "size": out[0], "elong": out[1], "orient": out[2],
+            "iterations": 1, "directions": 3}
 
 
 def config4_image(i: int, H: int = 4096, W: int = 4096, device="cpu", param_dtype=None):
