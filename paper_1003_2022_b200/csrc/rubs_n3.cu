@@ -232,7 +232,8 @@ __global__ void __launch_bounds__(kNT, 2)
     const int Y = D.pr_lo + ty0 + warp + 8 * i;
     const double h = 0.5 * A1[i];
     const double hy = kQuarterSqrt3 * (A2[i] + A3[i]);
-    const double xe = (double)(X - c0);  // entry coordinate of x, minus 1/2
+    // x's entry coordinate is X - c0 + 1; reads take t - 1/2 (s_read)
+    const double xe = (double)(X - c0) + 0.5;
     X1[i] = xe + h;
     X3[i] = xe - h;
     K[i] = 2.0 * kInvSqrt3 / (A1[i] * A2[i] * A3[i]);
