@@ -161,6 +161,131 @@ __device__ __forceinline__ double s_read(uint32_t row, double tp) {
   return __fma_rn(phi, e.y, e.x);
 }
 
+// Raw image values of one region entry into its .y slot (zero outside the
+// image and for the guard entry): cp.async, so a chunk's loads are all in
+// flight at once.
+template <int DT>
+__device__ __forceinline__ void fill_raw(uint32_t dst, const ImageSpec &I, int ir, int ic,
+                                         bool valid) {
+  if constexpr (DT == 1) {
+    const double *src = static_cast<const double *>(I.f) + (valid ? (int64_t)ir * I.ld + ic : 0);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst + 8u), "l"(src),
+                 "r"(valid ? 8 : 0)
+                 : "memory");
+  } else {
+    const float *src = static_cast<const float *>(I.f) + (valid ? (int64_t)ir * I.ld + ic : 0);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst + 8u), "l"(src),
+                 "r"(valid ? 4 : 0)
+                 : "memory");
+  }
+}
+
+template <int DT>
+__device__ __forceinline__ double raw_at(const double2 *e) {
+  if constexpr (DT == 1)
+    return e->y;
+  else
+    return (double)reinterpret_cast<const float *>(e)[2];
+}
+
+// One row of the region: raw values -> pairs (S + C/2, C) in place.  Each
+// lane owns 4 consecutive entries of a 128-entry pass; the lane blocks are
+// chained by a warp scan of the affine maps (C, S) -> (C + F, S + n C + G)
+// (F = block sum of f, G = block sum of its local running sums, n = length).
+template <int DT>
+__device__ __forceinline__ void scan_row(double2 *row, int Wr, int lane) {
+  double Cp = 0.0, Sp = 0.0;
+  for (int e0 = 0; e0 < Wr; e0 += 128) {
+    const int eb = e0 + 4 * lane;
+    double c[4], sl[4];
+    double acc = 0.0, sacc = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double v = (eb + i < Wr) ? raw_at<DT>(row + eb + i) : 0.0;
+      sl[i] = sacc;  // exclusive prefix of the local running sums
+      acc += v;
+      c[i] = acc;
+      sacc += acc;
+    }
+    double F = acc, G = sacc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double Fa = __shfl_up_sync(0xffffffffu, F, o);
+      const double Ga = __shfl_up_sync(0xffffffffu, G, o);
+      if (lane >= o) {
+        G = __fma_rn((double)(4 * o), Fa, G + Ga);
+        F += Fa;
+      }
+    }
+    double Fe = __shfl_up_sync(0xffffffffu, F, 1), Ge = __shfl_up_sync(0xffffffffu, G, 1);
+    if (lane == 0) Fe = Ge = 0.0;
+    const double Cin = Cp + Fe;
+    const double Sin = __fma_rn((double)(4 * lane), Cp, Sp) + Ge;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (eb + i < Wr) {
+        const double C = Cin + c[i];
+        const double S = __fma_rn((double)i, Cin, Sin) + sl[i];
+        row[eb + i] = make_double2(__fma_rn(0.5, C, S), C);
+      }
+    const double F31 = __shfl_sync(0xffffffffu, F, 31), G31 = __shfl_sync(0xffffffffu, G, 31);
+    Sp = __fma_rn(128.0, Cp, Sp) + G31;
+    Cp += F31;
+  }
+}
+
+// Rows [j0, j0 + n) of one pixel with the chord edges moving linearly:
+// per row t1, t3 (= x -/+ h - L) move by -sL, t2, t4 (= x -/+ h - U) by -sU.
+__device__ __forceinline__ double gather_seg(uint32_t row, uint32_t rstep, int n, double t1,
+                                             double t2, double t3, double t4, double sL,
+                                             double sU) {
+  double s = 0.0;
+#pragma unroll 2
+  for (int r = 0; r < n; ++r, row += rstep) {
+    const double e1 = s_read(row, t1), e2 = s_read(row, t2);
+    const double e3 = s_read(row, t3), e4 = s_read(row, t4);
+    s += (e1 - e2) - (e3 - e4);
+    t1 -= sL;
+    t3 -= sL;
+    t2 -= sU;
+    t4 -= sU;
+  }
+  return s;
+}
+
+// Pixel (x1, x3 = entry offsets, half widths ha, hb, lattice row Y) over the
+// rows [ja, jb] of the chunk starting at row cr0.  The chord edges are
+//   L = max(-ha - yd, yd - hb),  U = min(ha - yd, yd + hb),  yd = (Y - j)/sqrt3,
+// piecewise linear in j with breaks at yd = +-|hb - ha|/2: three segments
+// (A: yd >= |dl|, B: between, C: yd <= -|dl|), each initialised exactly and
+// then stepped by +-1/sqrt3 per row.
+__device__ __forceinline__ double gather_pixel(uint32_t Es, int Wr, int cr0, int ja, int jb,
+                                               int Y, double x1, double x3, double ha,
+                                               double hb) {
+  const double dl = 0.5 * (hb - ha);
+  const double w = fabs(dl) * 1.7320508075688772;
+  const int jA = (int)floor(Y - w), jB = (int)ceil(Y + w) - 1;
+  const uint32_t rstep = 16u * (uint32_t)Wr;
+  double s = 0.0;
+  // jB = jA - 1 when hb == ha (no middle segment): keep the bounds monotone
+  const int sA = min(jb, jA) + 1;
+  const int segs[4] = {ja, sA, max(sA, min(jb, jB) + 1), jb + 1};
+  const double c = kInvSqrt3;
+  const double sLs[3] = {-c, dl > 0.0 ? c : -c, c};
+  const double sUs[3] = {c, dl > 0.0 ? c : -c, -c};
+#pragma unroll
+  for (int g = 0; g < 3; ++g) {
+    const int j0 = max(segs[g], ja), j1 = segs[g + 1];
+    if (j1 <= j0) continue;
+    const double yd = (double)(Y - j0) * c;
+    const double L = fmax(-ha - yd, yd - hb);
+    const double U = fmax(fmin(ha - yd, yd + hb), L);
+    s += gather_seg(Es + (uint32_t)(j0 - cr0) * rstep, rstep, j1 - j0, x1 - L, x1 - U, x3 - L,
+                    x3 - U, sLs[g], sUs[g]);
+  }
+  return s;
+}
+
 template <int MODE, int DT>
 __global__ void __launch_bounds__(kNT, 2)
     n3_tile_kernel(ImageSpec I, Field3 F, DomainSpec D, Status3 *st) {
@@ -177,30 +302,35 @@ __global__ void __launch_bounds__(kNT, 2)
   __syncthreads();
 
   // --- per-pixel scales and the tile's region extent
-  double A1[kPx], A2[kPx], A3[kPx];
-  bool live[kPx];
+  double X1[kPx], X3[kPx], HA[kPx], HB[kPx], K[kPx], acc[kPx];
+  int jlo[kPx], jhi[kPx];
   unsigned flags = 0;
   int cmin = INT_MAX, cmax = INT_MIN, rmin = INT_MAX, rmax = INT_MIN;
   const int X = D.pc_lo + tx0 + lane;
+  const bool colok = tx0 + lane < D.pw;
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
-    const int px = tx0 + lane, py = ty0 + warp + 8 * i;
-    live[i] = px < D.pw && py < D.ph;
-    A1[i] = A2[i] = A3[i] = 1.0;
-    if (live[i]) {
-      const int Y = D.pr_lo + py;
-      double a[3];
+    const int py = ty0 + warp + 8 * i;
+    const int Y = D.pr_lo + py;
+    double a[3] = {1.0, 1.0, 1.0};
+    jlo[i] = INT_MAX;
+    jhi[i] = INT_MIN;
+    if (colok && py < D.ph) {
       scales3_at<MODE>(F, X, Y, a, flags);
-      A1[i] = a[0];
-      A2[i] = a[1];
-      A3[i] = a[2];
       const double hx = 0.5 * a[0] + 0.25 * (a[1] + a[2]);
       const double hy = kQuarterSqrt3 * (a[1] + a[2]);
       cmin = min(cmin, (int)floor(X - hx));
       cmax = max(cmax, (int)floor(X + hx));
-      rmin = min(rmin, (int)ceil(Y - hy));
-      rmax = max(rmax, (int)floor(Y + hy));
+      jlo[i] = (int)ceil(Y - hy);
+      jhi[i] = (int)floor(Y + hy);
+      rmin = min(rmin, jlo[i]);
+      rmax = max(rmax, jhi[i]);
     }
+    X1[i] = 0.5 * a[0];  // h for now
+    HA[i] = 0.5 * a[1];
+    HB[i] = 0.5 * a[2];
+    K[i] = 2.0 * kInvSqrt3 / (a[0] * a[1] * a[2]);
+    acc[i] = 0.0;
   }
   cmin = __reduce_min_sync(0xffffffffu, cmin);
   cmax = __reduce_max_sync(0xffffffffu, cmax);
@@ -223,91 +353,48 @@ __global__ void __launch_bounds__(kNT, 2)
     if (threadIdx.x == 0) atomicOr(&st->flags, kFlagRegionTooLarge);
     return;
   }
-
-  // --- per-pixel constants in entry coordinates (entry e <-> column c0 - 1 + e)
-  double X1[kPx], X3[kPx], acc[kPx], K[kPx];
-  int jlo[kPx], jhi[kPx];
+  // entry coordinates: x's entry is X - c0 + 1, and reads take t - 1/2
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
-    const int Y = D.pr_lo + ty0 + warp + 8 * i;
-    const double h = 0.5 * A1[i];
-    const double hy = kQuarterSqrt3 * (A2[i] + A3[i]);
-    // x's entry coordinate is X - c0 + 1; reads take t - 1/2 (s_read)
-    const double xe = (double)(X - c0) + 0.5;
+    const double xe = (double)(X - c0) + 0.5, h = X1[i];
     X1[i] = xe + h;
     X3[i] = xe - h;
-    K[i] = 2.0 * kInvSqrt3 / (A1[i] * A2[i] * A3[i]);
-    acc[i] = 0.0;
-    jlo[i] = live[i] ? (int)ceil(Y - hy) : INT_MAX;
-    jhi[i] = live[i] ? (int)floor(Y + hy) : INT_MIN;
-    A2[i] *= 0.5;  // half widths from here on
-    A3[i] *= 0.5;
   }
 
   const uint32_t Es = (uint32_t)__cvta_generic_to_shared(E);
   for (int cr0 = r0; cr0 <= r1; cr0 += Rc) {
     const int nrows = min(Rc, r1 - cr0 + 1);
     __syncthreads();  // previous chunk's reads are done
-    // --- rows of the chunk: entry pairs (S + C/2, C), one warp per row
+    // --- the warp's rows of the chunk: raw values (all of its loads in
+    // flight together), then the running sums
     for (int rr = warp; rr < nrows; rr += kNT / 32) {
       const int ir = cr0 + rr - I.row0;
       const bool rin = ir >= 0 && ir < I.h;
-      double2 *row = E + (size_t)rr * Wr;
-      double carryC = 0.0, carryS = 0.0;
-      for (int e0 = 0; e0 < Wr; e0 += 32) {
-        const int e = e0 + lane;
-        double v = 0.0;
+      const uint32_t rb = Es + 16u * (uint32_t)(rr * Wr);
+      for (int e = lane; e < Wr; e += 32) {
         const int ic = c0 - 1 + e - I.col0;
-        if (rin && e >= 1 && e < Wr && ic >= 0 && ic < I.w)
-          v = load_px<DT>(I.f, (int64_t)ir * I.ld + ic);
-        double c = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const double t = __shfl_up_sync(0xffffffffu, c, o);
-          if (lane >= o) c += t;
-        }
-        c += carryC;
-        double sc = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const double t = __shfl_up_sync(0xffffffffu, sc, o);
-          if (lane >= o) sc += t;
-        }
-        const double S = carryS + (sc - c);
-        if (e < Wr) row[e] = make_double2(__fma_rn(0.5, c, S), c);
-        carryC = __shfl_sync(0xffffffffu, c, 31);
-        carryS += __shfl_sync(0xffffffffu, sc, 31);
+        fill_raw<DT>(rb + 16u * (uint32_t)e, I, ir, ic, rin && e >= 1 && ic >= 0 && ic < I.w);
       }
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+    for (int rr = warp; rr < nrows; rr += kNT / 32) scan_row<DT>(E + (size_t)rr * Wr, Wr, lane);
     __syncthreads();
     // --- rows of the chunk into every pixel's sum
     const int cr1 = cr0 + nrows - 1;
-#pragma unroll 1
+#pragma unroll
     for (int i = 0; i < kPx; ++i) {
       const int ja = max(jlo[i], cr0), jb = min(jhi[i], cr1);
-      const int Y = D.pr_lo + ty0 + warp + 8 * i;
-      const double ha = A2[i], hb = A3[i], x1 = X1[i], x3 = X3[i];
-      double s = 0.0;
-      uint32_t row = Es + 16u * (uint32_t)((ja - cr0) * Wr);
-      const uint32_t rstep = 16u * (uint32_t)Wr;
-#pragma unroll 2
-      for (int j = ja; j <= jb; ++j, row += rstep) {
-        const double yd = (double)(Y - j) * kInvSqrt3;
-        const double L = fmax(-ha - yd, yd - hb);
-        const double U = fmax(fmin(ha - yd, yd + hb), L);
-        const double e1 = s_read(row, x1 - L), e2 = s_read(row, x1 - U);
-        const double e3 = s_read(row, x3 - L), e4 = s_read(row, x3 - U);
-        s += (e1 - e2) - (e3 - e4);
-      }
-      acc[i] += s;
+      if (ja <= jb)
+        acc[i] += gather_pixel(Es, Wr, cr0, ja, jb, D.pr_lo + ty0 + warp + 8 * i, X1[i], X3[i],
+                               HA[i], HB[i]);
     }
   }
 #pragma unroll
-  for (int i = 0; i < kPx; ++i)
-    if (live[i]) {
-      const int px = tx0 + lane, py = ty0 + warp + 8 * i;
-      D.out[(int64_t)py * D.ld_out + px] = K[i] * acc[i];
-    }
+  for (int i = 0; i < kPx; ++i) {
+    const int py = ty0 + warp + 8 * i;
+    if (colok && py < D.ph) D.out[(int64_t)py * D.ld_out + tx0 + lane] = K[i] * acc[i];
+  }
 }
 
 // Global support radii of the (floored, scaled) field: canvases of iterated
