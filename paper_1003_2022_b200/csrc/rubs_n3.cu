@@ -161,49 +161,84 @@ __device__ __forceinline__ double s_read(uint32_t row, double tp) {
   return __fma_rn(phi, e.y, e.x);
 }
 
-// Raw image values of one region entry into its .y slot (zero outside the
-// image and for the guard entry): cp.async, so a chunk's loads are all in
-// flight at once.
+// Region rows: Wr entries of 16 bytes (Wr a multiple of 4).  The raw image
+// values of a row are staged packed at the END of the row's own area
+// (float64: byte 8 Wr + 8 e; float32: 12 Wr + 4 e), then scanned into the
+// (S + C/2, C) pairs from the front: a pass writes entries below e0 + 128,
+// i.e. bytes below 16 (e0 + 128), while its unread raw values sit at or
+// above (8|12) Wr + (8|4)(e0 + 128) -- never clobbered while Wr >= e0 + 128.
+template <int DT>
+__host__ __device__ __forceinline__ uint32_t raw_offset(int Wr) {
+  return (DT == 1 ? 8u : 12u) * (uint32_t)Wr;
+}
+
+// One raw value into the staging area (zero outside the image and for the
+// guard entry): cp.async, so a chunk's loads are all in flight at once.
 template <int DT>
 __device__ __forceinline__ void fill_raw(uint32_t dst, const ImageSpec &I, int ir, int ic,
                                          bool valid) {
   if constexpr (DT == 1) {
     const double *src = static_cast<const double *>(I.f) + (valid ? (int64_t)ir * I.ld + ic : 0);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst + 8u), "l"(src),
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"(dst), "l"(src),
                  "r"(valid ? 8 : 0)
                  : "memory");
   } else {
     const float *src = static_cast<const float *>(I.f) + (valid ? (int64_t)ir * I.ld + ic : 0);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst + 8u), "l"(src),
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
                  "r"(valid ? 4 : 0)
                  : "memory");
   }
 }
 
-template <int DT>
-__device__ __forceinline__ double raw_at(const double2 *e) {
-  if constexpr (DT == 1)
-    return e->y;
-  else
-    return (double)reinterpret_cast<const float *>(e)[2];
+__device__ __forceinline__ float4 lds128f(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
 }
 
-// One row of the region: raw values -> pairs (S + C/2, C) in place.  Each
-// lane owns 4 consecutive entries of a 128-entry pass; the lane blocks are
-// chained by a warp scan of the affine maps (C, S) -> (C + F, S + n C + G)
-// (F = block sum of f, G = block sum of its local running sums, n = length).
+__device__ __forceinline__ void sts128(uint32_t addr, double x, double y) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(x), "d"(y) : "memory");
+}
+
+// One row of the region: raw values -> pairs (S + C/2, C).  Each lane owns
+// 4 consecutive entries of a 128-entry pass; the lane blocks are chained by
+// a warp scan of the affine maps (C, S) -> (C + F, S + n C + G) (F = block
+// sum of f, G = block sum of its local running sums, n = length).  Shared
+// accesses are rotated per lane so that every quarter-warp touches 8
+// distinct 16-byte bank groups (no conflicts).
 template <int DT>
-__device__ __forceinline__ void scan_row(double2 *row, int Wr, int lane) {
+__device__ __forceinline__ void scan_row(uint32_t rowS, int Wr, int lane) {
+  const uint32_t rawS = rowS + raw_offset<DT>(Wr);
   double Cp = 0.0, Sp = 0.0;
   for (int e0 = 0; e0 < Wr; e0 += 128) {
     const int eb = e0 + 4 * lane;
+    const bool in = eb < Wr;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    if (in) {
+      if constexpr (DT == 1) {
+        const uint32_t p = rawS + 8u * (uint32_t)eb;
+        const bool sw = (lane >> 2) & 1;
+        const double2 q0 = lds128(p + (sw ? 16u : 0u)), q1 = lds128(p + (sw ? 0u : 16u));
+        v[0] = sw ? q1.x : q0.x;
+        v[1] = sw ? q1.y : q0.y;
+        v[2] = sw ? q0.x : q1.x;
+        v[3] = sw ? q0.y : q1.y;
+      } else {
+        const float4 q = lds128f(rawS + 4u * (uint32_t)eb);
+        v[0] = q.x;
+        v[1] = q.y;
+        v[2] = q.z;
+        v[3] = q.w;
+      }
+    }
     double c[4], sl[4];
     double acc = 0.0, sacc = 0.0;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const double v = (eb + i < Wr) ? raw_at<DT>(row + eb + i) : 0.0;
       sl[i] = sacc;  // exclusive prefix of the local running sums
-      acc += v;
+      acc += v[i];
       c[i] = acc;
       sacc += acc;
     }
@@ -221,13 +256,21 @@ __device__ __forceinline__ void scan_row(double2 *row, int Wr, int lane) {
     if (lane == 0) Fe = Ge = 0.0;
     const double Cin = Cp + Fe;
     const double Sin = __fma_rn((double)(4 * lane), Cp, Sp) + Ge;
+    double M[4], Cv[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (eb + i < Wr) {
-        const double C = Cin + c[i];
-        const double S = __fma_rn((double)i, Cin, Sin) + sl[i];
-        row[eb + i] = make_double2(__fma_rn(0.5, C, S), C);
+    for (int i = 0; i < 4; ++i) {
+      Cv[i] = Cin + c[i];
+      M[i] = __fma_rn(0.5, Cv[i], __fma_rn((double)i, Cin, Sin) + sl[i]);
+    }
+    if (in) {
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = ((lane >> 1) + i) & 3;
+        const double m = r == 0 ? M[0] : r == 1 ? M[1] : r == 2 ? M[2] : M[3];
+        const double cc = r == 0 ? Cv[0] : r == 1 ? Cv[1] : r == 2 ? Cv[2] : Cv[3];
+        sts128(rowS + 16u * (uint32_t)(eb + r), m, cc);
       }
+    }
     const double F31 = __shfl_sync(0xffffffffu, F, 31), G31 = __shfl_sync(0xffffffffu, G, 31);
     Sp = __fma_rn(128.0, Cp, Sp) + G31;
     Cp += F31;
@@ -347,7 +390,7 @@ __global__ void __launch_bounds__(kNT, 2)
   __syncthreads();
   const int c0 = s_ext[0], c1 = s_ext[1], r0 = s_ext[2], r1 = s_ext[3];
   if (c0 > c1) return;  // no live pixel
-  const int Wr = c1 - c0 + 2;  // entries k = c0 - 1 .. c1
+  const int Wr = (c1 - c0 + 5) & ~3;  // entries k = c0 - 1 .. c1, padded to a multiple of 4
   const int Rc = min(r1 - r0 + 1, (int)(kSmem3 / (16 * Wr)));
   if (Rc < 1) {
     if (threadIdx.x == 0) atomicOr(&st->flags, kFlagRegionTooLarge);
@@ -370,15 +413,17 @@ __global__ void __launch_bounds__(kNT, 2)
     for (int rr = warp; rr < nrows; rr += kNT / 32) {
       const int ir = cr0 + rr - I.row0;
       const bool rin = ir >= 0 && ir < I.h;
-      const uint32_t rb = Es + 16u * (uint32_t)(rr * Wr);
+      const uint32_t rb = Es + 16u * (uint32_t)(rr * Wr) + raw_offset<DT>(Wr);
       for (int e = lane; e < Wr; e += 32) {
         const int ic = c0 - 1 + e - I.col0;
-        fill_raw<DT>(rb + 16u * (uint32_t)e, I, ir, ic, rin && e >= 1 && ic >= 0 && ic < I.w);
+        fill_raw<DT>(rb + (DT == 1 ? 8u : 4u) * (uint32_t)e, I, ir, ic,
+                     rin && e >= 1 && ic >= 0 && ic < I.w);
       }
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
-    for (int rr = warp; rr < nrows; rr += kNT / 32) scan_row<DT>(E + (size_t)rr * Wr, Wr, lane);
+    for (int rr = warp; rr < nrows; rr += kNT / 32)
+      scan_row<DT>(Es + 16u * (uint32_t)(rr * Wr), Wr, lane);
     __syncthreads();
     // --- rows of the chunk into every pixel's sum
     const int cr1 = cr0 + nrows - 1;
