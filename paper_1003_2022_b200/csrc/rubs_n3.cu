@@ -62,8 +62,19 @@ constexpr int kM3Uniform = 1;   // one (3,) vector
 constexpr int kM3Params = 2;    // (size, elongation, orientation) float64
 constexpr int kM3Params32 = 3;  // same, float32
 
-constexpr int kTW = 32, kTH = 32, kNT = 256, kPx = kTH / (kNT / 32);
-constexpr int kSmem3 = 110 * 1024;
+// tile geometry (dev A/B builds override with -D)
+#ifndef RUBS3_TH
+#define RUBS3_TH 64
+#endif
+#ifndef RUBS3_NT
+#define RUBS3_NT 512
+#endif
+#ifndef RUBS3_SMEM_KB
+#define RUBS3_SMEM_KB 220
+#endif
+constexpr int kTW = 32, kTH = RUBS3_TH, kNT = RUBS3_NT, kWarps = kNT / 32, kPx = kTH / kWarps;
+constexpr int kMinBlocks = (RUBS3_SMEM_KB <= 110) ? 2 : 1;
+constexpr int kSmem3 = RUBS3_SMEM_KB * 1024;
 
 struct Field3 {
   int mode;
@@ -330,7 +341,7 @@ __device__ __forceinline__ double gather_pixel(uint32_t Es, int Wr, int cr0, int
 }
 
 template <int MODE, int DT>
-__global__ void __launch_bounds__(kNT, 2)
+__global__ void __launch_bounds__(kNT, kMinBlocks)
     n3_tile_kernel(ImageSpec I, Field3 F, DomainSpec D, Status3 *st) {
   extern __shared__ __align__(16) double2 E[];
   __shared__ int s_ext[4];
@@ -353,7 +364,7 @@ __global__ void __launch_bounds__(kNT, 2)
   const bool colok = tx0 + lane < D.pw;
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
-    const int py = ty0 + warp + 8 * i;
+    const int py = ty0 + warp + kWarps * i;
     const int Y = D.pr_lo + py;
     double a[3] = {1.0, 1.0, 1.0};
     jlo[i] = INT_MAX;
@@ -410,7 +421,7 @@ __global__ void __launch_bounds__(kNT, 2)
     __syncthreads();  // previous chunk's reads are done
     // --- the warp's rows of the chunk: raw values (all of its loads in
     // flight together), then the running sums
-    for (int rr = warp; rr < nrows; rr += kNT / 32) {
+    for (int rr = warp; rr < nrows; rr += kWarps) {
       const int ir = cr0 + rr - I.row0;
       const bool rin = ir >= 0 && ir < I.h;
       const uint32_t rb = Es + 16u * (uint32_t)(rr * Wr) + raw_offset<DT>(Wr);
@@ -422,7 +433,7 @@ __global__ void __launch_bounds__(kNT, 2)
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
-    for (int rr = warp; rr < nrows; rr += kNT / 32)
+    for (int rr = warp; rr < nrows; rr += kWarps)
       scan_row<DT>(Es + 16u * (uint32_t)(rr * Wr), Wr, lane);
     __syncthreads();
     // --- rows of the chunk into every pixel's sum
@@ -431,13 +442,13 @@ __global__ void __launch_bounds__(kNT, 2)
     for (int i = 0; i < kPx; ++i) {
       const int ja = max(jlo[i], cr0), jb = min(jhi[i], cr1);
       if (ja <= jb)
-        acc[i] += gather_pixel(Es, Wr, cr0, ja, jb, D.pr_lo + ty0 + warp + 8 * i, X1[i], X3[i],
+        acc[i] += gather_pixel(Es, Wr, cr0, ja, jb, D.pr_lo + ty0 + warp + kWarps * i, X1[i], X3[i],
                                HA[i], HB[i]);
     }
   }
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
-    const int py = ty0 + warp + 8 * i;
+    const int py = ty0 + warp + kWarps * i;
     if (colok && py < D.ph) D.out[(int64_t)py * D.ld_out + tx0 + lane] = K[i] * acc[i];
   }
 }
