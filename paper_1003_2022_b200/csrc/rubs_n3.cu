@@ -340,10 +340,15 @@ __device__ __forceinline__ double gather_pixel(uint32_t Es, int Wr, int cr0, int
   return s;
 }
 
+// Per-pixel state kept in shared memory (h = a1/2, ha = a2/2, hb = a3/2),
+// so that registers go to loads in flight in the gather loop.
+constexpr int kStateBytes = 3 * 8 * kTW * kTH;
+
 template <int MODE, int DT>
 __global__ void __launch_bounds__(kNT, kMinBlocks)
     n3_tile_kernel(ImageSpec I, Field3 F, DomainSpec D, Status3 *st) {
-  extern __shared__ __align__(16) double2 E[];
+  extern __shared__ __align__(16) double SM[];
+  double *Ph = SM, *Pa = SM + kTW * kTH, *Pb = SM + 2 * kTW * kTH;
   __shared__ int s_ext[4];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx0 = blockIdx.x * kTW, ty0 = blockIdx.y * kTH;
@@ -356,8 +361,6 @@ __global__ void __launch_bounds__(kNT, kMinBlocks)
   __syncthreads();
 
   // --- per-pixel scales and the tile's region extent
-  double X1[kPx], X3[kPx], HA[kPx], HB[kPx], K[kPx], acc[kPx];
-  int jlo[kPx], jhi[kPx];
   unsigned flags = 0;
   int cmin = INT_MAX, cmax = INT_MIN, rmin = INT_MAX, rmax = INT_MIN;
   const int X = D.pc_lo + tx0 + lane;
@@ -366,25 +369,20 @@ __global__ void __launch_bounds__(kNT, kMinBlocks)
   for (int i = 0; i < kPx; ++i) {
     const int py = ty0 + warp + kWarps * i;
     const int Y = D.pr_lo + py;
-    double a[3] = {1.0, 1.0, 1.0};
-    jlo[i] = INT_MAX;
-    jhi[i] = INT_MIN;
+    double a[3] = {-2.0, -2.0, -2.0};  // dead pixel: empty row range
     if (colok && py < D.ph) {
       scales3_at<MODE>(F, X, Y, a, flags);
       const double hx = 0.5 * a[0] + 0.25 * (a[1] + a[2]);
       const double hy = kQuarterSqrt3 * (a[1] + a[2]);
       cmin = min(cmin, (int)floor(X - hx));
       cmax = max(cmax, (int)floor(X + hx));
-      jlo[i] = (int)ceil(Y - hy);
-      jhi[i] = (int)floor(Y + hy);
-      rmin = min(rmin, jlo[i]);
-      rmax = max(rmax, jhi[i]);
+      rmin = min(rmin, (int)ceil(Y - hy));
+      rmax = max(rmax, (int)floor(Y + hy));
     }
-    X1[i] = 0.5 * a[0];  // h for now
-    HA[i] = 0.5 * a[1];
-    HB[i] = 0.5 * a[2];
-    K[i] = 2.0 * kInvSqrt3 / (a[0] * a[1] * a[2]);
-    acc[i] = 0.0;
+    const int q = i * kNT + threadIdx.x;
+    Ph[q] = 0.5 * a[0];
+    Pa[q] = 0.5 * a[1];
+    Pb[q] = 0.5 * a[2];
   }
   cmin = __reduce_min_sync(0xffffffffu, cmin);
   cmax = __reduce_max_sync(0xffffffffu, cmax);
@@ -402,20 +400,18 @@ __global__ void __launch_bounds__(kNT, kMinBlocks)
   const int c0 = s_ext[0], c1 = s_ext[1], r0 = s_ext[2], r1 = s_ext[3];
   if (c0 > c1) return;  // no live pixel
   const int Wr = (c1 - c0 + 5) & ~3;  // entries k = c0 - 1 .. c1, padded to a multiple of 4
-  const int Rc = min(r1 - r0 + 1, (int)(kSmem3 / (16 * Wr)));
+  const int Rc = min(r1 - r0 + 1, (int)((kSmem3 - kStateBytes) / (16 * Wr)));
   if (Rc < 1) {
     if (threadIdx.x == 0) atomicOr(&st->flags, kFlagRegionTooLarge);
     return;
   }
   // entry coordinates: x's entry is X - c0 + 1, and reads take t - 1/2
+  const double xe = (double)(X - c0) + 0.5;
+  double acc[kPx];
 #pragma unroll
-  for (int i = 0; i < kPx; ++i) {
-    const double xe = (double)(X - c0) + 0.5, h = X1[i];
-    X1[i] = xe + h;
-    X3[i] = xe - h;
-  }
+  for (int i = 0; i < kPx; ++i) acc[i] = 0.0;
 
-  const uint32_t Es = (uint32_t)__cvta_generic_to_shared(E);
+  const uint32_t Es = (uint32_t)__cvta_generic_to_shared(SM) + kStateBytes;
   for (int cr0 = r0; cr0 <= r1; cr0 += Rc) {
     const int nrows = min(Rc, r1 - cr0 + 1);
     __syncthreads();  // previous chunk's reads are done
@@ -438,18 +434,23 @@ __global__ void __launch_bounds__(kNT, kMinBlocks)
     __syncthreads();
     // --- rows of the chunk into every pixel's sum
     const int cr1 = cr0 + nrows - 1;
-#pragma unroll
+#pragma unroll 1
     for (int i = 0; i < kPx; ++i) {
-      const int ja = max(jlo[i], cr0), jb = min(jhi[i], cr1);
-      if (ja <= jb)
-        acc[i] += gather_pixel(Es, Wr, cr0, ja, jb, D.pr_lo + ty0 + warp + kWarps * i, X1[i], X3[i],
-                               HA[i], HB[i]);
+      const int q = i * kNT + threadIdx.x;
+      const double h = Ph[q], ha = Pa[q], hb = Pb[q];
+      const int Y = D.pr_lo + ty0 + warp + kWarps * i;
+      const double hy = kQuarterSqrt3 * (2.0 * ha + 2.0 * hb);  // == phase A's bound
+      const int ja = max((int)ceil(Y - hy), cr0), jb = min((int)floor(Y + hy), cr1);
+      if (ja <= jb) acc[i] += gather_pixel(Es, Wr, cr0, ja, jb, Y, xe + h, xe - h, ha, hb);
     }
   }
 #pragma unroll
   for (int i = 0; i < kPx; ++i) {
     const int py = ty0 + warp + kWarps * i;
-    if (colok && py < D.ph) D.out[(int64_t)py * D.ld_out + tx0 + lane] = K[i] * acc[i];
+    const int q = i * kNT + threadIdx.x;
+    if (colok && py < D.ph)
+      D.out[(int64_t)py * D.ld_out + tx0 + lane] =
+          (0.25 * kInvSqrt3 / (Ph[q] * Pa[q] * Pb[q])) * acc[i];
   }
 }
 
