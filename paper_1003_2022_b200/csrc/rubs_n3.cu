@@ -30,6 +30,7 @@
 // with k = round(t - 1/2), phi = t - 1/2 - k.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cmath>
 #include <cstring>
@@ -687,19 +688,95 @@ Field3 params3_of(const void *size, const void *elong, const void *orient, int p
   return F;
 }
 
-// Host buffers: stage through device memory on a private stream.
-struct HostRun {
-  cudaStream_t s = nullptr;
+// Host-buffer calls: device staging buffers (kept across calls) and, for
+// one pass, a pipeline over bands of output rows on three streams -- the
+// image goes up whole (a band's rows read the image beyond the band), then
+// each band's per-pixel inputs; a band's tiles launch once its inputs have
+// landed and its rows go back while later bands are still in flight (the
+// N=4 path's scheme, rubs_b200.cu run_streamed).
+struct Stage3 {
+  int device = -1;
   void *buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
-  ~HostRun() {
-    for (void *b : buf)
-      if (b) cudaFreeAsync(b, s);
-    if (s) {
-      cudaStreamSynchronize(s);
-      cudaStreamDestroy(s);
-    }
-  }
+  size_t cap[5] = {0, 0, 0, 0, 0};
+  cudaStream_t h2d = nullptr, cmp = nullptr, d2h = nullptr;
+  cudaEvent_t ev[32];
 };
+thread_local Stage3 t_st3;
+
+int stage3(int k, size_t bytes, void **out) {
+  int dev = 0;
+  RUBS3_CUDA_TRY(cudaGetDevice(&dev));
+  if (t_st3.device != dev) {
+    t_st3 = Stage3();
+    t_st3.device = dev;
+    RUBS3_CUDA_TRY(cudaStreamCreateWithFlags(&t_st3.h2d, cudaStreamNonBlocking));
+    RUBS3_CUDA_TRY(cudaStreamCreateWithFlags(&t_st3.cmp, cudaStreamNonBlocking));
+    RUBS3_CUDA_TRY(cudaStreamCreateWithFlags(&t_st3.d2h, cudaStreamNonBlocking));
+    for (auto &e : t_st3.ev) RUBS3_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  if (bytes > t_st3.cap[k]) {
+    if (t_st3.buf[k]) cudaFree(t_st3.buf[k]);
+    t_st3.buf[k] = nullptr;
+    t_st3.cap[k] = 0;
+    RUBS3_CUDA_TRY(cudaMalloc(&t_st3.buf[k], bytes));
+    t_st3.cap[k] = bytes;
+  }
+  *out = t_st3.buf[k];
+  return RUBS_OK;
+}
+
+struct Plane3 {
+  const void *host;
+  void *dev;
+  size_t row_bytes;
+};
+
+// One pass from host buffers: image f_host (already described by I, whose
+// .f is the device copy), per-pixel planes (uploaded by row band), result
+// into out_host.
+int run3_streamed(ImageSpec I, Field3 F, const void *f_host, const Plane3 *planes, int np,
+                  double *dout, double *out_host) {
+  int rc = ensure3();
+  if (rc) return rc;
+  const int H = I.h, W = I.w;
+  F.FH = H;
+  F.FW = W;
+  F.div = 1.0;
+  F.scaled = 0;
+  const cudaStream_t h2d = t_st3.h2d, cmp = t_st3.cmp, d2h = t_st3.d2h;
+  const int ty = (H + kTH - 1) / kTH;
+  const int nb = std::max(1, std::min(8, ty));
+  const int per = (ty + nb - 1) / nb;
+  RUBS3_CUDA_TRY(cudaMemsetAsync(t3.d_st, 0, sizeof(Status3), cmp));
+  RUBS3_CUDA_TRY(cudaMemcpyAsync(const_cast<void *>(I.f), f_host,
+                                 (size_t)H * W * (I.dt ? 8 : 4), cudaMemcpyHostToDevice, h2d));
+  int bands = 0;
+  for (int b = 0; b < nb; ++b, ++bands) {
+    const int r0 = b * per * kTH, r1 = std::min(H, (b + 1) * per * kTH);
+    if (r0 >= r1) break;
+    for (int k = 0; k < np; ++k)
+      RUBS3_CUDA_TRY(cudaMemcpyAsync(static_cast<char *>(planes[k].dev) + r0 * planes[k].row_bytes,
+                                     static_cast<const char *>(planes[k].host) + r0 * planes[k].row_bytes,
+                                     (size_t)(r1 - r0) * planes[k].row_bytes, cudaMemcpyHostToDevice,
+                                     h2d));
+    RUBS3_CUDA_TRY(cudaEventRecord(t_st3.ev[2 * b], h2d));
+    RUBS3_CUDA_TRY(cudaStreamWaitEvent(cmp, t_st3.ev[2 * b], 0));
+    DomainSpec D{0, r0, W, r1 - r0, dout + (size_t)r0 * W, W};
+    if ((rc = launch_pass3(I, F, D, cmp))) return rc;
+    RUBS3_CUDA_TRY(cudaEventRecord(t_st3.ev[2 * b + 1], cmp));
+  }
+  // returns last: a copy into pageable memory blocks the host until it ran
+  for (int b = 0; b < bands; ++b) {
+    const int r0 = b * per * kTH, r1 = std::min(H, (b + 1) * per * kTH);
+    RUBS3_CUDA_TRY(cudaStreamWaitEvent(d2h, t_st3.ev[2 * b + 1], 0));
+    RUBS3_CUDA_TRY(cudaMemcpyAsync(out_host + (size_t)r0 * W, dout + (size_t)r0 * W,
+                                   (size_t)(r1 - r0) * W * 8, cudaMemcpyDeviceToHost, d2h));
+  }
+  RUBS3_CUDA_TRY(cudaStreamSynchronize(d2h));
+  Status3 st;
+  if ((rc = fetch3(cmp, st))) return rc;
+  return code3(st);
+}
 
 }  // namespace
 
@@ -733,24 +810,28 @@ int rubs_b200_filter3_host(const void *f, int f_dtype, int64_t H, int64_t W, con
   int rc;
   if ((rc = check_image(f_dtype, H, W))) return rc;
   if (iterations < 1) return set_error(RUBS_EVALUE, "iterations must be >= 1");
+  Field3 F;
+  if ((rc = field3_of(field, field_is_uniform, W, F))) return rc;
   if (H == 0 || W == 0) return RUBS_OK;
-  const size_t n = (size_t)H * W, fb = n * (f_dtype == RUBS_F64 ? 8 : 4);
-  HostRun h;
-  RUBS3_CUDA_TRY(cudaStreamCreateWithFlags(&h.s, cudaStreamNonBlocking));
-  RUBS3_CUDA_TRY(cudaMallocAsync(&h.buf[0], fb, h.s));
-  RUBS3_CUDA_TRY(cudaMallocAsync(&h.buf[1], n * 8, h.s));
-  RUBS3_CUDA_TRY(cudaMemcpyAsync(h.buf[0], f, fb, cudaMemcpyHostToDevice, h.s));
-  const double *fld = field;
-  if (!field_is_uniform) {
-    RUBS3_CUDA_TRY(cudaMallocAsync(&h.buf[2], n * 24, h.s));
-    RUBS3_CUDA_TRY(cudaMemcpyAsync(h.buf[2], field, n * 24, cudaMemcpyHostToDevice, h.s));
-    fld = static_cast<const double *>(h.buf[2]);
+  const size_t n = (size_t)H * W, esz = f_dtype == RUBS_F64 ? 8 : 4;
+  void *df, *dout, *dfl = nullptr;
+  if ((rc = stage3(0, n * esz, &df)) || (rc = stage3(1, n * 8, &dout))) return rc;
+  if (!field_is_uniform && (rc = stage3(2, n * 24, &dfl))) return rc;
+  ImageSpec I{df, f_dtype, W, (int)H, (int)W, 0, 0};
+  if (iterations == 1) {
+    if (!field_is_uniform) F.a = static_cast<const double *>(dfl);
+    Plane3 pl{field, dfl, (size_t)W * 24};
+    return run3_streamed(I, F, f, &pl, field_is_uniform ? 0 : 1, static_cast<double *>(dout), out);
   }
-  if ((rc = rubs_b200_filter3(h.buf[0], f_dtype, H, W, W, fld, field_is_uniform, W, iterations,
-                              static_cast<double *>(h.buf[1]), W, h.s)))
-    return rc;
-  RUBS3_CUDA_TRY(cudaMemcpyAsync(out, h.buf[1], n * 8, cudaMemcpyDeviceToHost, h.s));
-  RUBS3_CUDA_TRY(cudaStreamSynchronize(h.s));
+  const cudaStream_t s = t_st3.cmp;
+  RUBS3_CUDA_TRY(cudaMemcpyAsync(df, f, n * esz, cudaMemcpyHostToDevice, s));
+  if (!field_is_uniform) {
+    RUBS3_CUDA_TRY(cudaMemcpyAsync(dfl, field, n * 24, cudaMemcpyHostToDevice, s));
+    F.a = static_cast<const double *>(dfl);
+  }
+  if ((rc = run3(I, F, iterations, static_cast<double *>(dout), W, s))) return rc;
+  RUBS3_CUDA_TRY(cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDeviceToHost, s));
+  RUBS3_CUDA_TRY(cudaStreamSynchronize(s));
   return RUBS_OK;
 }
 
@@ -762,24 +843,27 @@ int rubs_b200_filter3_params_host(const void *f, int f_dtype, int64_t H, int64_t
   if (p_dtype != RUBS_F32 && p_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
   if (iterations < 1) return set_error(RUBS_EVALUE, "iterations must be >= 1");
   if (H == 0 || W == 0) return RUBS_OK;
-  const size_t n = (size_t)H * W, fb = n * (f_dtype == RUBS_F64 ? 8 : 4),
-               pb = n * (p_dtype == RUBS_F64 ? 8 : 4);
-  HostRun h;
-  RUBS3_CUDA_TRY(cudaStreamCreateWithFlags(&h.s, cudaStreamNonBlocking));
-  RUBS3_CUDA_TRY(cudaMallocAsync(&h.buf[0], fb, h.s));
-  RUBS3_CUDA_TRY(cudaMallocAsync(&h.buf[1], n * 8, h.s));
-  RUBS3_CUDA_TRY(cudaMemcpyAsync(h.buf[0], f, fb, cudaMemcpyHostToDevice, h.s));
+  const size_t n = (size_t)H * W, esz = f_dtype == RUBS_F64 ? 8 : 4,
+               psz = p_dtype == RUBS_F64 ? 8 : 4;
+  void *df, *dout, *dp[3];
+  if ((rc = stage3(0, n * esz, &df)) || (rc = stage3(1, n * 8, &dout))) return rc;
+  for (int k = 0; k < 3; ++k)
+    if ((rc = stage3(2 + k, n * psz, &dp[k]))) return rc;
+  ImageSpec I{df, f_dtype, W, (int)H, (int)W, 0, 0};
+  Field3 F = params3_of(dp[0], dp[1], dp[2], p_dtype, W);
   const void *src[3] = {size, elong, orient};
-  for (int k = 0; k < 3; ++k) {
-    RUBS3_CUDA_TRY(cudaMallocAsync(&h.buf[2 + k], pb, h.s));
-    RUBS3_CUDA_TRY(cudaMemcpyAsync(h.buf[2 + k], src[k], pb, cudaMemcpyHostToDevice, h.s));
+  if (iterations == 1) {
+    Plane3 pl[3];
+    for (int k = 0; k < 3; ++k) pl[k] = Plane3{src[k], dp[k], (size_t)W * psz};
+    return run3_streamed(I, F, f, pl, 3, static_cast<double *>(dout), out);
   }
-  if ((rc = rubs_b200_filter3_params(h.buf[0], f_dtype, H, W, W, h.buf[2], h.buf[3], h.buf[4],
-                                     p_dtype, W, iterations, static_cast<double *>(h.buf[1]), W,
-                                     h.s)))
-    return rc;
-  RUBS3_CUDA_TRY(cudaMemcpyAsync(out, h.buf[1], n * 8, cudaMemcpyDeviceToHost, h.s));
-  RUBS3_CUDA_TRY(cudaStreamSynchronize(h.s));
+  const cudaStream_t s = t_st3.cmp;
+  RUBS3_CUDA_TRY(cudaMemcpyAsync(df, f, n * esz, cudaMemcpyHostToDevice, s));
+  for (int k = 0; k < 3; ++k)
+    RUBS3_CUDA_TRY(cudaMemcpyAsync(dp[k], src[k], n * psz, cudaMemcpyHostToDevice, s));
+  if ((rc = run3(I, F, iterations, static_cast<double *>(dout), W, s))) return rc;
+  RUBS3_CUDA_TRY(cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDeviceToHost, s));
+  RUBS3_CUDA_TRY(cudaStreamSynchronize(s));
   return RUBS_OK;
 }
 

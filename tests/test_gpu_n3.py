@@ -189,3 +189,24 @@ def test_config3_n3_sampled_exact(cuda, rng):
         ref[i] = oracle.points3(f64, a, p[None, :], threads=1)[0]
     got = out[pts[:, 0], pts[:, 1]].cpu().numpy()
     assert np.abs(got - ref).max() < REL_TOL * np.abs(ref).max()
+
+
+def test_streamed_host_path_equals_device_path(cuda, rng):
+    """Host buffers go through the banded H2D / compute / D2H pipeline; the
+    tiles are the device path's tiles, so the result is bitwise the same."""
+    torch = cuda
+    H, W = 700, 333
+    f = rng.random((H, W)).astype(np.float32)
+    s = smooth_random_field(rng, (H, W), 2.0, 800.0)
+    th = smooth_random_field(rng, (H, W), 0.0, math.pi - 1e-9)
+    r = np.minimum(smooth_random_field(rng, (H, W), 1.0, 5.0), 0.95 * rb.elongation_bound3(th))
+    host = rb.filter_space_variant3_params(f, s, r, th)
+    dev = rb.filter_space_variant3_params(torch.from_numpy(f).cuda(), *(torch.from_numpy(v).cuda() for v in (s, r, th)))
+    assert np.array_equal(host, dev.cpu().numpy())
+    field = rb.scales3_from_params(s, r, th)
+    hf = rb.filter_space_variant3(f, field)
+    df = rb.filter_space_variant3(torch.from_numpy(f).cuda(), torch.from_numpy(field).cuda())
+    assert np.array_equal(hf, df.cpu().numpy())
+    pts = np.array([[0, 0], [699, 332], [128, 10], [127, 300], [400, 200]])
+    ref = oracle.points3(f.astype(np.float64), field, pts)
+    assert np.abs(hf[pts[:, 0], pts[:, 1]] - ref).max() < REL_TOL * np.abs(ref).max()
