@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -1403,6 +1404,63 @@ __global__ void __launch_bounds__(256) big_line_kernel(const BigRegion *R, doubl
   }
 }
 
+// RS2, RS3 and RS4 of a region in ONE top-down pass (one CTA per region).
+// Row r of each sweep needs only row r of the previous sweep and row r - 1
+// of its own, so three previous-row vectors carry the state (double-
+// buffered in shared memory, one barrier per row); every element is read
+// once (RS1, from big_fill_rs1_kernel) and written once (final).  The three
+// separate line sweeps read and wrote the region three times.  Same adds in
+// the same order per element as the line sweeps.
+constexpr int kRsThreads = 512, kRsCols = 9;  // regions up to 4608 columns
+constexpr int kRsSmem = 6 * (kRsThreads * kRsCols + 2) * 8;
+__global__ void __launch_bounds__(kRsThreads, 1)
+    big_rs234_kernel(const BigRegion *R, double *scratch, Status *st) {
+  extern __shared__ double prow[];
+  const BigRegion g = R[blockIdx.x];
+  const int W2 = g.RW + 2;  // entry c + 1 holds column c; 0 and RW + 1 stay zero
+  double *A = prow, *B = prow + 3 * W2;
+  for (int i = threadIdx.x; i < 6 * W2; i += kRsThreads) prow[i] = 0.0;
+  double *base = scratch + g.off;
+  double nxt[kRsCols];
+#pragma unroll
+  for (int k = 0; k < kRsCols; ++k) {
+    const int c = threadIdx.x + k * kRsThreads;
+    nxt[k] = (c < g.RW && g.RH > 0) ? base[c] : 0.0;
+  }
+  __syncthreads();
+  unsigned gh = 0;
+  for (int r = 0; r < g.RH; ++r) {
+    double *row = base + (int64_t)r * g.P;
+    double cur[kRsCols];
+#pragma unroll
+    for (int k = 0; k < kRsCols; ++k) {
+      cur[k] = nxt[k];
+      const int c = threadIdx.x + k * kRsThreads;
+      nxt[k] = (c < g.RW && r + 1 < g.RH) ? row[g.P + c] : 0.0;  // prefetch row r + 1
+    }
+#pragma unroll
+    for (int k = 0; k < kRsCols; ++k) {
+      const int c = threadIdx.x + k * kRsThreads;
+      if (c < g.RW) {
+        const double v2 = cur[k] + A[c];              // RS2: + row r-1 at c-1
+        const double v3 = v2 + A[W2 + c + 1];         // RS3: + row r-1 at c
+        const double v4 = v3 + A[2 * W2 + c + 2];     // RS4: + row r-1 at c+1
+        B[c + 1] = v2;
+        B[W2 + c + 1] = v3;
+        B[2 * W2 + c + 1] = v4;
+        row[c] = v4;
+        gh = max(gh, (unsigned)__double2hiint(v4) & 0x7fffffffu);
+      }
+    }
+    __syncthreads();
+    double *t = A;
+    A = B;
+    B = t;
+  }
+  gh = __reduce_max_sync(0xffffffffu, gh);
+  if ((threadIdx.x & 31) == 0 && gh) atomicMax(&st->guard_hi, gh);
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) big_gather_kernel(FieldSpec F, DomainSpec D, int tiles_x,
                                                          const BigTile *tl, int nt,
@@ -1412,6 +1470,7 @@ __global__ void __launch_bounds__(256) big_gather_kernel(FieldSpec F, DomainSpec
   const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
   for (int i = blockIdx.x; i < nt; i += gridDim.x) {
     const BigTile bt = tl[i];
+    if (bt.tile < 0) continue;  // a gap of the block's tile raster
     const BigRegion g = R[bt.region];
     const int x0 = (bt.tile % tiles_x) * kTile, y0 = (bt.tile / tiles_x) * kTile;
     const char *Sb = reinterpret_cast<const char *>(scratch + g.off);  // local coordinates
@@ -1656,6 +1715,8 @@ int ensure_scratch() {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWide));
     RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<kModeLut, 0, kThreadsWide, 2>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWide));
+    RUBS_CUDA_TRY(cudaFuncSetAttribute(big_rs234_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kRsSmem));
     t_scr.attr_set = true;
   }
   return RUBS_OK;
@@ -1852,29 +1913,213 @@ int upload(std::vector<V> &h, V *&d, size_t &cap, cudaStream_t s) {
 // Tiles deferred by the primary launch: those whose 8x8 regions fit the
 // 225 KB configuration go to the shared-memory overflow kernel, the rest to
 // the global-memory block path (see big_* kernels).
+// dev: RUBS_B200_HOST_TIMING=1 prints the host planning phases
+struct HostClock {
+  bool on = std::getenv("RUBS_B200_HOST_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char *what) {
+    if (!on) return;
+    auto n = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[host] %-22s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(n - t).count());
+    t = n;
+  }
+};
+
+// ---- planning of the deferred tiles, on the device ----------------------
+// The primary launch appends one OvfRec per deferred 32-pixel tile.  Each
+// record either goes to the shared-memory overflow pass, or to a block of
+// side S = 2^k >= 2h (shrunk for the precision budget) whose region lives
+// in global scratch.  Blocks are cells of a per-S grid; the records are
+// classified and the cells aggregated by kernels (one thread per record /
+// cell), so only the few used cells travel to the host, which orders them,
+// cuts the scratch batches and uploads the regions.  (A host-side sort and
+// merge of ~1M records cost ~60 ms on config 5 with the GPU idle.)
+constexpr int kPlanLevels = 9;  // block sides 32 << lv, lv = 0..8 (32 .. 8192)
+struct PlanGrid {
+  int gx[kPlanLevels], gy[kPlanLevels], base[kPlanLevels + 1];
+};
+struct CellAgg {
+  int x0, y0, x1, y1;
+  int m[4];
+  int count;
+};
+
+// 0: shared-memory overflow pass; else the block side S.
+__host__ __device__ inline int plan_side(const OvfRec &r, int tw, int th) {
+  if (region_elems(min(8, tw) + r.m[0] + r.m[1] + 1, min(8, th) + r.m[2] + r.m[3]) <=
+      kSmemLarge / 8)
+    return 0;
+  const int h = max(max(r.m[0], r.m[1]), max(r.m[2], r.m[3]));
+  int S = 64;
+  while (S < 2 * h && S < 8192) S *= 2;
+  while (S > kTile) {
+    const double RW = S + r.m[0] + r.m[1], RH = S + r.m[2] + r.m[3];
+    const double mn = RW < RH ? RW : RH;
+    if ((double)r.w * 0.25 * RW * RH * mn * mn <= (double)kPrecisionBudget) break;
+    S /= 2;
+  }
+  return S;
+}
+
+__global__ void plan_init_kernel(CellAgg *c, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    c[i] = CellAgg{INT_MAX, INT_MAX, 0, 0, {0, 0, 0, 0}, 0};
+}
+
+// counters: [0] records for the shared-memory pass, [1] used cells
+__global__ void plan_classify_kernel(const OvfRec *rec, int n, PlanGrid G, int tiles_x, int pw,
+                                     int ph, CellAgg *cells, int *rec_cell, int2 *smem_list,
+                                     int *counters) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const OvfRec r = rec[i];
+    const int x0 = (r.tile % tiles_x) * kTile, y0 = (r.tile / tiles_x) * kTile;
+    const int tw = min(kTile, pw - x0), th = min(kTile, ph - y0);
+    const int S = plan_side(r, tw, th);
+    if (S == 0) {
+      smem_list[atomicAdd(&counters[0], 1)] = make_int2(r.tile, (int)r.mask);
+      rec_cell[i] = -1;
+      continue;
+    }
+    const int lv = __ffs(S) - 6;  // S = 32 << lv
+    const int cell = G.base[lv] + (x0 / S) * G.gy[lv] + (y0 / S);
+    rec_cell[i] = cell;
+    CellAgg *c = cells + cell;
+    atomicMin(&c->x0, x0);
+    atomicMin(&c->y0, y0);
+    atomicMax(&c->x1, x0 + tw);
+    atomicMax(&c->y1, y0 + th);
+    for (int j = 0; j < 4; ++j) atomicMax(&c->m[j], r.m[j]);
+    atomicAdd(&c->count, 1);
+  }
+}
+
+__global__ void plan_compact_kernel(const CellAgg *cells, int n, int *used, CellAgg *agg,
+                                    int *counters) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (cells[i].count > 0) {
+      const int k = atomicAdd(&counters[1], 1);
+      used[k] = i;
+      agg[k] = cells[i];
+    }
+}
+
+// per cell: region index relative to its batch, first tile slot
+// per used cell: (batch-relative region, first slot, tile x0, tile y0, row
+// width in tiles); the block's tiles take slots in raster order of its tile
+// bounding box (gaps stay tile = -1), so the gather walks each block row by
+// row, neighbouring CTAs sharing the region rows in L2
+struct CellMap {
+  int region, slot0, tx0, ty0, bw;
+};
+__global__ void plan_map_kernel(const int *cells, const CellMap *cm, int n, CellMap *cell_map) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    cell_map[cells[i]] = cm[i];
+}
+
+__global__ void plan_assign_kernel(const OvfRec *rec, int n, const int *rec_cell,
+                                   const CellMap *cell_map, int tiles_x, BigTile *out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int cell = rec_cell[i];
+    if (cell < 0) continue;
+    const CellMap m = cell_map[cell];
+    const OvfRec r = rec[i];
+    const int tx = r.tile % tiles_x, ty = r.tile / tiles_x;
+    out[m.slot0 + (ty - m.ty0) * m.bw + (tx - m.tx0)] = BigTile{r.tile, m.region, r.mask};
+  }
+}
+
+struct PlanScratch {
+  size_t ncell_cap = 0, nrec_cap = 0;
+  CellAgg *cells = nullptr, *agg = nullptr;
+  int *used = nullptr, *rec_cell = nullptr, *counters = nullptr;
+  CellMap *cell_map = nullptr;
+  int *h_counters = nullptr;  // pinned
+  CellMap *d_cm = nullptr;
+  int *d_cm_cell = nullptr;
+  size_t cm_cap = 0, cmc_cap = 0;
+};
+thread_local PlanScratch t_plan;
+
+int plan_buffers(size_t ncell, size_t nrec) {
+  if (!t_plan.h_counters) RUBS_CUDA_TRY(cudaMallocHost(&t_plan.h_counters, 2 * sizeof(int)));
+  if (!t_plan.counters) RUBS_CUDA_TRY(cudaMalloc(&t_plan.counters, 2 * sizeof(int)));
+  if (ncell > t_plan.ncell_cap) {
+    for (void *p : {(void *)t_plan.cells, (void *)t_plan.agg, (void *)t_plan.used,
+                    (void *)t_plan.cell_map})
+      if (p) cudaFree(p);
+    t_plan.cells = t_plan.agg = nullptr;
+    t_plan.used = nullptr;
+    t_plan.cell_map = nullptr;
+    t_plan.ncell_cap = 0;
+    RUBS_CUDA_TRY(cudaMalloc(&t_plan.cells, ncell * sizeof(CellAgg)));
+    RUBS_CUDA_TRY(cudaMalloc(&t_plan.agg, ncell * sizeof(CellAgg)));
+    RUBS_CUDA_TRY(cudaMalloc(&t_plan.used, ncell * sizeof(int)));
+    RUBS_CUDA_TRY(cudaMalloc(&t_plan.cell_map, ncell * sizeof(CellMap)));
+    t_plan.ncell_cap = ncell;
+  }
+  if (nrec > t_plan.nrec_cap) {
+    if (t_plan.rec_cell) cudaFree(t_plan.rec_cell);
+    t_plan.rec_cell = nullptr;
+    t_plan.nrec_cap = 0;
+    RUBS_CUDA_TRY(cudaMalloc(&t_plan.rec_cell, nrec * sizeof(int)));
+    t_plan.nrec_cap = nrec;
+  }
+  return RUBS_OK;
+}
+
 template <int M, int T>
 int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int n_ovf,
                     cudaStream_t s) {
-  std::vector<OvfRec> raw(n_ovf);
-  RUBS_CUDA_TRY(cudaMemcpyAsync(raw.data(), t_scr.d_ovf, n_ovf * sizeof(OvfRec),
+  HostClock hc;
+  const int tiles_x = (D.pw + kTile - 1) / kTile;
+  PlanGrid G;
+  G.base[0] = 0;
+  for (int lv = 0; lv < kPlanLevels; ++lv) {
+    const int S = kTile << lv;
+    G.gx[lv] = (D.pw + S - 1) / S;
+    G.gy[lv] = (D.ph + S - 1) / S;
+    G.base[lv + 1] = G.base[lv] + G.gx[lv] * G.gy[lv];
+  }
+  const int ncell = G.base[kPlanLevels];
+  int rc;
+  if ((rc = plan_buffers(ncell, n_ovf))) return rc;
+  // shared-memory overflow list: at most one entry per record
+  if ((size_t)n_ovf > t_scr.list_cap) {
+    if (t_scr.d_list) cudaFree(t_scr.d_list);
+    t_scr.d_list = nullptr;
+    t_scr.list_cap = 0;
+    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_list, (size_t)n_ovf * sizeof(int2)));
+    t_scr.list_cap = n_ovf;
+  }
+  const OvfRec *rec = reinterpret_cast<const OvfRec *>(t_scr.d_ovf);
+  const int gb = std::min((ncell + 255) / 256, 4 * t_scr.sms);
+  const int rb = std::min((n_ovf + 255) / 256, 4 * t_scr.sms);
+  RUBS_CUDA_TRY(cudaMemsetAsync(t_plan.counters, 0, 2 * sizeof(int), s));
+  plan_init_kernel<<<gb, 256, 0, s>>>(t_plan.cells, ncell);
+  plan_classify_kernel<<<rb, 256, 0, s>>>(rec, n_ovf, G, tiles_x, D.pw, D.ph, t_plan.cells,
+                                          t_plan.rec_cell, t_scr.d_list, t_plan.counters);
+  plan_compact_kernel<<<gb, 256, 0, s>>>(t_plan.cells, ncell, t_plan.used, t_plan.agg,
+                                         t_plan.counters);
+  t_launches += 3;
+  RUBS_CUDA_TRY(cudaGetLastError());
+  RUBS_CUDA_TRY(cudaMemcpyAsync(t_plan.h_counters, t_plan.counters, 2 * sizeof(int),
                                 cudaMemcpyDeviceToHost, s));
   RUBS_CUDA_TRY(cudaStreamSynchronize(s));
-  // one record per 32-pixel tile (the wide kernel records both halves of a
-  // 64 x 32 tile separately)
-  std::sort(raw.begin(), raw.end(), [](const OvfRec &a, const OvfRec &b) { return a.tile < b.tile; });
-  std::vector<OvfRec> recs;
-  for (const OvfRec &r : raw) {
-    if (!recs.empty() && recs.back().tile == r.tile) {
-      for (int j = 0; j < 4; ++j) recs.back().m[j] = std::max(recs.back().m[j], r.m[j]);
-      recs.back().w = std::max(recs.back().w, r.w);
-      recs.back().mask |= r.mask;
-    } else {
-      recs.push_back(r);
-    }
+  const int n_smem = t_plan.h_counters[0], n_used = t_plan.h_counters[1];
+  std::vector<int> used(n_used);
+  std::vector<CellAgg> agg(n_used);
+  if (n_used > 0) {
+    RUBS_CUDA_TRY(cudaMemcpyAsync(used.data(), t_plan.used, n_used * sizeof(int),
+                                  cudaMemcpyDeviceToHost, s));
+    RUBS_CUDA_TRY(cudaMemcpyAsync(agg.data(), t_plan.agg, n_used * sizeof(CellAgg),
+                                  cudaMemcpyDeviceToHost, s));
+    RUBS_CUDA_TRY(cudaStreamSynchronize(s));
   }
-  const int tiles_x = (D.pw + kTile - 1) / kTile;
+  hc.lap("device plan");
+  if (hc.on) std::fprintf(stderr, "[host] %d records: %d shared-memory tiles, %d blocks\n", n_ovf, n_smem, n_used);
   // per-pixel fallback list: at most every pixel of the deferred tiles
-  const int pix_cap = (int)std::min<size_t>(recs.size() * kTile * kTile, 1u << 30);
+  const int pix_cap = (int)std::min<size_t>((size_t)n_ovf * kTile * kTile, 1u << 30);
   if ((size_t)pix_cap > t_scr.pix_cap) {
     if (t_scr.d_pix) cudaFree(t_scr.d_pix);
     t_scr.d_pix = nullptr;
@@ -1882,52 +2127,28 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
     t_scr.pix_cap = pix_cap;
   }
   RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->pix_count, 0, sizeof(int), s));
-  std::vector<int2> smem_list;  // (tile, cell mask)
-  struct Blk {
-    int S = 0, x0 = 1 << 30, y0 = 1 << 30, x1 = 0, y1 = 0;
-    int m[4] = {0, 0, 0, 0};
-    std::vector<int2> tiles;
-  };
-  std::map<std::tuple<int, int, int>, Blk> blocks;
-  const int cap_large = kSmemLarge / 8;
-  for (const OvfRec &r : recs) {
-    const int x0 = (r.tile % tiles_x) * kTile, y0 = (r.tile / tiles_x) * kTile;
-    const int tw = std::min(kTile, D.pw - x0), th = std::min(kTile, D.ph - y0);
-    if (region_elems(std::min(8, tw) + r.m[0] + r.m[1] + 1, std::min(8, th) + r.m[2] + r.m[3]) <= cap_large) {
-      smem_list.push_back(make_int2(r.tile, (int)r.mask));
-      continue;
-    }
-    const int h = std::max(std::max(r.m[0], r.m[1]), std::max(r.m[2], r.m[3]));
-    int S = 64;
-    while (S < 2 * h && S < 8192) S *= 2;
-    while (S > kTile) {
-      const double RW = S + r.m[0] + r.m[1], RH = S + r.m[2] + r.m[3];
-      const double mn = std::min(RW, RH);
-      if ((double)r.w * 0.25 * RW * RH * mn * mn <= (double)kPrecisionBudget) break;
-      S /= 2;
-    }
-    Blk &b = blocks[std::make_tuple(S, x0 / S, y0 / S)];
-    b.S = S;
-    b.x0 = std::min(b.x0, x0);
-    b.y0 = std::min(b.y0, y0);
-    b.x1 = std::max(b.x1, x0 + tw);
-    b.y1 = std::max(b.y1, y0 + th);
-    for (int j = 0; j < 4; ++j) b.m[j] = std::max(b.m[j], r.m[j]);
-    b.tiles.push_back(make_int2(r.tile, (int)r.mask));
-  }
-  int rc;
-  if (!smem_list.empty()) {
-    std::sort(smem_list.begin(), smem_list.end(),
-              [](const int2 &a, const int2 &b) { return a.x < b.x; });
-    if ((rc = upload(smem_list, t_scr.d_list, t_scr.list_cap, s))) return rc;
-    tile_overflow_kernel<M, T><<<std::min((int)smem_list.size(), t_scr.sms), kThreadsLarge,
+  if (n_smem > 0) {
+    // tile order (the classify kernel appended them in arbitrary order):
+    // neighbouring persistent-CTA tiles then share their region rows in L2
+    std::vector<int2> sl(n_smem);
+    RUBS_CUDA_TRY(cudaMemcpyAsync(sl.data(), t_scr.d_list, n_smem * sizeof(int2),
+                                  cudaMemcpyDeviceToHost, s));
+    RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+    std::sort(sl.begin(), sl.end(), [](const int2 &a, const int2 &b) { return a.x < b.x; });
+    RUBS_CUDA_TRY(cudaMemcpyAsync(t_scr.d_list, sl.data(), n_smem * sizeof(int2),
+                                  cudaMemcpyHostToDevice, s));
+    tile_overflow_kernel<M, T><<<std::min(n_smem, t_scr.sms), kThreadsLarge,
                                  kSmemLarge, s>>>(I, F, D, tiles_x, kSmemLarge / 8, t_scr.d_list,
-                                                  (int)smem_list.size(), t_scr.d_status,
+                                                  n_smem, t_scr.d_status,
                                                   t_scr.d_pix, pix_cap, tma_maps(I));
     ++t_launches;
     RUBS_CUDA_TRY(cudaGetLastError());
   }
-  if (blocks.empty()) return RUBS_OK;
+  if (n_used == 0) return RUBS_OK;
+  // blocks in cell order = (S, x0 / S, y0 / S): deterministic
+  std::vector<int> order(n_used);
+  for (int i = 0; i < n_used; ++i) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](int a, int b) { return used[a] < used[b]; });
   // Batches of blocks under a scratch budget.  A batch's kernels follow the
   // previous batch's in stream order, so the scratch is reused without a
   // host sync; region / tile lists of all batches are uploaded once.
@@ -1935,24 +2156,26 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   struct Batch {
     int r0, r1, t0, t1;
     int64_t used;
-    int maxRH, maxL;
+    int maxRH, maxL, maxRW;
   };
   std::vector<BigRegion> regs;
-  std::vector<BigTile> tl;
+  std::vector<CellMap> cm;
+  std::vector<int> cm_cell;
   std::vector<Batch> batches;
-  Batch cur{0, 0, 0, 0, 0, 0, 0};
+  int ntl = 0;
+  Batch cur{0, 0, 0, 0, 0, 0, 0, 0};
   int64_t max_used = 0;
   auto close_batch = [&]() {
     cur.r1 = (int)regs.size();
-    cur.t1 = (int)tl.size();
+    cur.t1 = ntl;
     if (cur.r1 > cur.r0) {
       batches.push_back(cur);
       max_used = std::max(max_used, cur.used);
     }
-    cur = Batch{(int)regs.size(), 0, (int)tl.size(), 0, 0, 0, 0};
+    cur = Batch{(int)regs.size(), 0, ntl, 0, 0, 0, 0, 0};
   };
-  for (auto &kv : blocks) {
-    Blk &b = kv.second;
+  for (int k : order) {
+    const CellAgg &b = agg[k];
     BigRegion g;
     g.RW = (b.x1 - b.x0) + b.m[0] + b.m[1];
     g.RH = (b.y1 - b.y0) + b.m[2] + b.m[3];
@@ -1969,9 +2192,12 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
     cur.used += n;
     cur.maxRH = std::max(cur.maxRH, g.RH);
     cur.maxL = std::max(cur.maxL, g.RH + g.RW - 1);
-    std::sort(b.tiles.begin(), b.tiles.end(), [](const int2 &a, const int2 &c) { return a.x < c.x; });
-    for (const int2 &t : b.tiles)
-      tl.push_back(BigTile{t.x, (int)regs.size() - cur.r0, (unsigned)t.y});
+    cur.maxRW = std::max(cur.maxRW, g.RW);
+    const int tx0 = b.x0 / kTile, ty0 = b.y0 / kTile;
+    const int bw = (b.x1 + kTile - 1) / kTile - tx0, bh = (b.y1 + kTile - 1) / kTile - ty0;
+    cm.push_back(CellMap{(int)regs.size() - cur.r0, ntl, tx0, ty0, bw});
+    cm_cell.push_back(used[k]);
+    ntl += bw * bh;
     regs.push_back(g);
   }
   close_batch();
@@ -1982,17 +2208,39 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
     t_scr.big_cap = (size_t)max_used;
   }
   if ((rc = upload(regs, t_scr.d_regs, t_scr.regs_cap, s))) return rc;
-  if ((rc = upload(tl, t_scr.d_btiles, t_scr.btiles_cap, s))) return rc;
+  if ((rc = upload(cm, t_plan.d_cm, t_plan.cm_cap, s))) return rc;
+  if ((rc = upload(cm_cell, t_plan.d_cm_cell, t_plan.cmc_cap, s))) return rc;
+  if ((size_t)ntl > t_scr.btiles_cap) {
+    if (t_scr.d_btiles) cudaFree(t_scr.d_btiles);
+    t_scr.d_btiles = nullptr;
+    t_scr.btiles_cap = 0;
+    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_btiles, (size_t)ntl * sizeof(BigTile)));
+    t_scr.btiles_cap = ntl;
+  }
+  RUBS_CUDA_TRY(cudaMemsetAsync(t_scr.d_btiles, 0xff, (size_t)ntl * sizeof(BigTile), s));  // tile -1
+  plan_map_kernel<<<std::min((n_used + 255) / 256, t_scr.sms), 256, 0, s>>>(
+      t_plan.d_cm_cell, t_plan.d_cm, n_used, t_plan.cell_map);
+  plan_assign_kernel<<<rb, 256, 0, s>>>(rec, n_ovf, t_plan.rec_cell, t_plan.cell_map, tiles_x,
+                                        t_scr.d_btiles);
+  t_launches += 2;
+  RUBS_CUDA_TRY(cudaGetLastError());
+  hc.lap("regions + upload");
   for (const Batch &bt : batches) {
     const int nreg = bt.r1 - bt.r0, ntl = bt.t1 - bt.t0;
     const BigRegion *R = t_scr.d_regs + bt.r0;
     big_fill_rs1_kernel<T><<<dim3((bt.maxRH + 7) / 8, nreg), 256, 0, s>>>(I, R, t_scr.d_big);
-    big_line_kernel<2><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
-                                                                          t_scr.d_status);
-    big_line_kernel<3><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
-                                                                          t_scr.d_status);
-    big_line_kernel<4><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
-                                                                          t_scr.d_status);
+    if (bt.maxRW <= kRsThreads * kRsCols && !std::getenv("RUBS_B200_LINE_SWEEPS")) {
+      big_rs234_kernel<<<nreg, kRsThreads, 6 * (bt.maxRW + 2) * 8, s>>>(R, t_scr.d_big,
+                                                                         t_scr.d_status);
+      t_launches -= 2;
+    } else {
+      big_line_kernel<2><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
+                                                                            t_scr.d_status);
+      big_line_kernel<3><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
+                                                                            t_scr.d_status);
+      big_line_kernel<4><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
+                                                                            t_scr.d_status);
+    }
     big_gather_kernel<M><<<std::min(ntl, t_scr.sms * 8), 256, 0, s>>>(
         F, D, tiles_x, t_scr.d_btiles + bt.t0, ntl, R, t_scr.d_big, t_scr.d_status, t_scr.d_pix,
         pix_cap);
@@ -2008,10 +2256,12 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
                     cudaStream_t s) {
   int rc = handle_overflow_tiles<M, T>(I, F, D, n_ovf, s);
   if (rc) return rc;
+  HostClock hc;
   int cnt = 0;
   RUBS_CUDA_TRY(cudaMemcpyAsync(&cnt, &t_scr.d_status->pix_count, sizeof(int),
                                 cudaMemcpyDeviceToHost, s));
   RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+  hc.lap("overflow kernels (sync)");
   cnt = std::min<int64_t>(cnt, (int64_t)t_scr.pix_cap);
   if (cnt > 0) {
     pixel_kernel<M, T><<<std::min((cnt + 7) / 8, t_scr.sms * 4), 256, kPixSmem, s>>>(
