@@ -1461,8 +1461,11 @@ __global__ void __launch_bounds__(kRsThreads, 1)
   if ((threadIdx.x & 31) == 0 && gh) atomicMax(&st->guard_hi, gh);
 }
 
+#ifndef RUBS_BG_MINB
+#define RUBS_BG_MINB 4  // 64 registers, 4 CTAs per SM: more loads in flight (config 5: -15 %)
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(256) big_gather_kernel(FieldSpec F, DomainSpec D, int tiles_x,
+__global__ void __launch_bounds__(256, RUBS_BG_MINB) big_gather_kernel(FieldSpec F, DomainSpec D, int tiles_x,
                                                          const BigTile *tl, int nt,
                                                          const BigRegion *R, const double *scratch,
                                                          Status *st, int2 *pix, int pix_cap) {
