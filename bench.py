@@ -189,12 +189,12 @@ def run_ours(args, rank, world, local):
     iters = int(w["iterations"])
     n3 = w.get("directions") == 3
     H, W = w["f"].shape
-    row_bands = args.config == "5" and world > 1
+    row_bands = args.config in ("5", "3") and world > 1
     if row_bands:
         # one image, sharded by output-row bands; each step exchanges halo
         # rows with the neighbours (NCCL) and filters the own band
         from paper_1003_2022_b200 import sharding
-        band = sharding.band_bounds(H, world)[rank]
+        band = sharding.band_bounds(H, world, sharding.TILE3 if n3 else sharding.TILE)[rank]
         s0 = sets[0]
         own = s0["f"][band[0]:band[1]].contiguous()
         pb = [p[band[0]:band[1]].contiguous() for p in s0["p"]]
@@ -202,6 +202,8 @@ def run_ours(args, rank, world, local):
         torch.cuda.empty_cache()
 
     def step(i):
+        if row_bands and n3:
+            return sharding.filter3_row_band(own, band, H, *pb)
         if row_bands:
             return sharding.filter_row_band(own, band, H, *pb)
         s = sets[i % len(sets)]
@@ -249,7 +251,7 @@ def run_ours(args, rank, world, local):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     # weak scaling: every rank filters a whole image per step; row bands
-    # (config 5 on N > 1): the ranks share one image per step
+    # (configs 5 and 3 on N > 1): the ranks share one image per step
     px_total = float(H * W) * args.steps * (1 if row_bands else world)
     value = px_total / (ms_max * 1e-3) / 1e9
 

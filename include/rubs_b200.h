@@ -260,6 +260,24 @@ int rubs_b200_filter3_params_host(const void *f, int f_dtype, int64_t H, int64_t
                                   const void *size, const void *elong, const void *orient,
                                   int p_dtype, int iterations, double *out);
 
+/*
+ * N=3 row bands (multi-GPU sharding of config 3's single image, as the N=4
+ * rubs_b200_filter_params_rows): output rows [out_row0, out_row0 +
+ * out_rows) from image rows [f_row0, f_row0 + f_rows) (rows outside read as
+ * zero, so the halo must cover the band's reach) and parameter rows from
+ * p_row0 on.  rubs_b200_read_margins3_params gives the reach of a band's
+ * parameter rows: out2 = {columns, rows} = max over its pixels of
+ * ceil(a1/2 + (a2 + a3)/4) + 1 and ceil((a2 + a3) sqrt3 / 4) + 1.
+ */
+int rubs_b200_read_margins3_params(const void *size, const void *elong, const void *orient,
+                                   int p_dtype, int64_t rows, int64_t W, int64_t ld_p,
+                                   int *out2, void *stream);
+int rubs_b200_filter3_params_rows(const void *f, int f_dtype, int64_t f_row0, int64_t f_rows,
+                                  int64_t W, int64_t ld_f, int64_t H_total, const void *size,
+                                  const void *elong, const void *orient, int p_dtype,
+                                  int64_t p_row0, int64_t ld_p, int64_t out_row0,
+                                  int64_t out_rows, double *out, int64_t ld_out, void *stream);
+
 /* The N=3 mapping alone: device arrays of n parameters -> device n x 3. */
 int rubs_b200_scales3(const void *size, const void *elong, const void *orient, int p_dtype,
                       int64_t n, double *out, void *stream);

@@ -96,6 +96,10 @@ SIGNATURES = {
                                         _vp, _i64, _vp]),
     "rubs_b200_filter3_params_host": (_int, [_vp, _int, _i64, _i64, _vp, _vp, _vp, _int, _int, _vp]),
     "rubs_b200_scales3": (_int, [_vp, _vp, _vp, _int, _i64, _vp, _vp]),
+    "rubs_b200_read_margins3_params": (_int, [_vp, _vp, _vp, _int, _i64, _i64, _i64,
+                                              ctypes.POINTER(_int), _vp]),
+    "rubs_b200_filter3_params_rows": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp,
+                                             _int, _i64, _i64, _i64, _i64, _vp, _i64, _vp]),
 }
 
 

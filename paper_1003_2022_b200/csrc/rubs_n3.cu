@@ -85,6 +85,7 @@ struct Field3 {
   const void *ps, *pr, *pt;
   int64_t pld;
   int FH, FW;  // field grid (edge-clamped on iterated canvases)
+  int fr_off;  // global row of the first row held in the arrays (row bands)
   double div;  // sqrt(iterations)
   int scaled;
 };
@@ -133,7 +134,7 @@ __device__ __forceinline__ void params_to_scales3(double s, double rho, double t
 template <int MODE>
 __device__ __forceinline__ void scales3_at(const Field3 &F, int gx, int gy, double a[3],
                                            unsigned &flags) {
-  const int c = min(max(gx, 0), F.FW - 1), r = min(max(gy, 0), F.FH - 1);
+  const int c = min(max(gx, 0), F.FW - 1), r = min(max(gy, 0), F.FH - 1) - F.fr_off;
   if constexpr (MODE == kM3Field) {
     const double *p = F.a + ((int64_t)r * F.ld + c) * 3;
 #pragma unroll
@@ -865,6 +866,62 @@ int rubs_b200_filter3_params_host(const void *f, int f_dtype, int64_t H, int64_t
   RUBS3_CUDA_TRY(cudaMemcpyAsync(out, dout, n * 8, cudaMemcpyDeviceToHost, s));
   RUBS3_CUDA_TRY(cudaStreamSynchronize(s));
   return RUBS_OK;
+}
+
+int rubs_b200_read_margins3_params(const void *size, const void *elong, const void *orient,
+                                   int p_dtype, int64_t rows, int64_t W, int64_t ld_p,
+                                   int *out2, void *stream) {
+  if (p_dtype != RUBS_F32 && p_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (rows < 0 || W < 0) return set_error(RUBS_EVALUE, "negative size");
+  int rc = ensure3();
+  if (rc) return rc;
+  out2[0] = out2[1] = 0;
+  if (rows == 0 || W == 0) return RUBS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Field3 F = params3_of(size, elong, orient, p_dtype, ld_p);
+  F.FH = (int)rows;
+  F.FW = (int)W;
+  F.div = 1.0;
+  RUBS3_CUDA_TRY(cudaMemsetAsync(t3.d_st, 0, sizeof(Status3), s));
+  if (p_dtype == RUBS_F64)
+    n3_margins_kernel<kM3Params><<<4 * 148, 256, 0, s>>>(F, t3.d_st);
+  else
+    n3_margins_kernel<kM3Params32><<<4 * 148, 256, 0, s>>>(F, t3.d_st);
+  rubs_internal::count_launches(1);
+  RUBS3_CUDA_TRY(cudaGetLastError());
+  Status3 st;
+  if ((rc = fetch3(s, st))) return rc;
+  out2[0] = st.rx;
+  out2[1] = st.ry;
+  return code3(st);
+}
+
+int rubs_b200_filter3_params_rows(const void *f, int f_dtype, int64_t f_row0, int64_t f_rows,
+                                  int64_t W, int64_t ld_f, int64_t H_total, const void *size,
+                                  const void *elong, const void *orient, int p_dtype,
+                                  int64_t p_row0, int64_t ld_p, int64_t out_row0,
+                                  int64_t out_rows, double *out, int64_t ld_out, void *stream) {
+  int rc;
+  if ((rc = check_image(f_dtype, H_total, W))) return rc;
+  if (p_dtype != RUBS_F32 && p_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (out_row0 < 0 || out_rows < 0 || out_row0 + out_rows > H_total || p_row0 > out_row0 ||
+      f_row0 < 0 || f_rows < 0 || f_row0 + f_rows > H_total)
+    return set_error(RUBS_EVALUE, "row ranges out of the image");
+  if ((rc = ensure3())) return rc;
+  if (out_rows == 0 || W == 0) return RUBS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ImageSpec I{f, f_dtype, ld_f, (int)f_rows, (int)W, 0, (int)f_row0};
+  Field3 F = params3_of(size, elong, orient, p_dtype, ld_p);
+  F.FH = (int)H_total;
+  F.FW = (int)W;
+  F.fr_off = (int)p_row0;
+  F.div = 1.0;
+  RUBS3_CUDA_TRY(cudaMemsetAsync(t3.d_st, 0, sizeof(Status3), s));
+  DomainSpec D{0, (int)out_row0, (int)W, (int)out_rows, out, ld_out};
+  if ((rc = launch_pass3(I, F, D, s))) return rc;
+  Status3 st;
+  if ((rc = fetch3(s, st))) return rc;
+  return code3(st);
 }
 
 int rubs_b200_scales3(const void *size, const void *elong, const void *orient, int p_dtype,

@@ -5,7 +5,7 @@ gloo on CPU for the tests):
 
 * batches (BASELINE config 4): images are independent -- each rank filters
   its own images, there is no data-path collective (``batch_indices``);
-* row bands (config 5): one large image is split into horizontal bands of
+* row bands (configs 5 and, with three directions, 3): one large image is split into horizontal bands of
   output rows.  A rank needs the input rows its outputs read -- its band
   grown by the read margins (engine.py:247-262) -- so the one exchange step
   is a halo exchange of image rows with the neighbouring ranks
@@ -171,3 +171,71 @@ def filter_row_band(f_own, band, H: int, size, elong, orient, lut=None, group=No
     f_need = exchange_rows(f_own, band, bands, needs, rank, group)
     return filter_rows_params(f_need, needs[rank][0], H, size, elong, orient, band[0], band[0],
                               band[1] - band[0], lut)
+
+
+# --- three directions (config 3) -------------------------------------------
+# Same decomposition; the N=3 kernel's tiles are 64 rows tall, so band edges
+# sit on the 64-row grid (bitwise equal to the whole-image result), and a
+# band's reach is the vertical half-extent of its kernels
+# (rubs_b200_read_margins3_params).
+
+TILE3 = 64
+
+
+def read_margins3_params(size, elong, orient):
+    """(columns, rows) reach of the N=3 kernels of these parameter rows."""
+    import torch
+    from . import _native
+    from .engine import _stream_handle
+    ps = [v.contiguous() for v in (size, elong, orient)]
+    pdt = _native.RUBS_F32 if ps[0].dtype == torch.float32 else _native.RUBS_F64
+    out2 = (ctypes.c_int * 2)()
+    _native.check(_native.load().rubs_b200_read_margins3_params(
+        *(ctypes.c_void_p(p.data_ptr()) for p in ps), pdt, ps[0].shape[0], ps[0].shape[1],
+        ps[0].stride(0), out2, _stream_handle()))
+    return tuple(out2)
+
+
+def needed_rows3(band, reach_rows: int, H: int):
+    """Image rows an N=3 band reads."""
+    r0, r1 = band
+    if r1 <= r0:
+        return (r0, r0)
+    return (max(0, r0 - reach_rows), min(H, r1 + reach_rows))
+
+
+def filter3_rows_params(f_rows, f_row0: int, H: int, size, elong, orient, p_row0: int,
+                        out_row0: int, out_rows: int, out=None):
+    """N=3 output rows [out_row0, out_row0 + out_rows) of the H-row image whose
+    rows [f_row0, f_row0 + len(f_rows)) are given (rubs_b200_filter3_params_rows)."""
+    import torch
+    from . import _native
+    from .engine import _stream_handle
+    f_rows = f_rows.contiguous()
+    ps = [v.contiguous() for v in (size, elong, orient)]
+    W = f_rows.shape[1]
+    if out is None:
+        out = torch.empty((out_rows, W), dtype=torch.float64, device=f_rows.device)
+    pdt = _native.RUBS_F32 if ps[0].dtype == torch.float32 else _native.RUBS_F64
+    fdt = _native.RUBS_F32 if f_rows.dtype == torch.float32 else _native.RUBS_F64
+    _native.check(_native.load().rubs_b200_filter3_params_rows(
+        ctypes.c_void_p(f_rows.data_ptr()), fdt, f_row0, f_rows.shape[0], W, f_rows.stride(0), H,
+        *(ctypes.c_void_p(p.data_ptr()) for p in ps), pdt, p_row0, ps[0].stride(0),
+        out_row0, out_rows, ctypes.c_void_p(out.data_ptr()), out.stride(0), _stream_handle()))
+    return out
+
+
+def filter3_row_band(f_own, band, H: int, size, elong, orient, group=None):
+    """One rank's share of an N=3 row-band filter (band = band_bounds(H,
+    world, TILE3)[rank]); collective over the group (needs all-gather +
+    halo exchange), like filter_row_band."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    rank = dist.get_rank(group)
+    bands = band_bounds(H, world, TILE3)
+    assert tuple(band) == bands[rank], "band must match band_bounds(H, world, TILE3)[rank]"
+    reach = read_margins3_params(size, elong, orient)[1]
+    needs = gather_needs(needed_rows3(band, reach, H), group, device=f_own.device)
+    f_need = exchange_rows(f_own, band, bands, needs, rank, group)
+    return filter3_rows_params(f_need, needs[rank][0], H, size, elong, orient, band[0], band[0],
+                               band[1] - band[0])

@@ -210,3 +210,27 @@ def test_streamed_host_path_equals_device_path(cuda, rng):
     pts = np.array([[0, 0], [699, 332], [128, 10], [127, 300], [400, 200]])
     ref = oracle.points3(f.astype(np.float64), field, pts)
     assert np.abs(hf[pts[:, 0], pts[:, 1]] - ref).max() < REL_TOL * np.abs(ref).max()
+
+
+def test_row_bands_reproduce_whole_image_bitwise(cuda):
+    """Multi-GPU row bands of one N=3 image (each band computed from the
+    image rows its reach needs): bitwise equal to the whole-image call."""
+    torch = cuda
+    from paper_1003_2022_b200 import sharding
+    H, W = 1000, 640
+    w = workloads.config3_n3(H, W, device="cuda", param_dtype=torch.float32)
+    f = torch.from_numpy(w["f"]).cuda()
+    params = (w["size"], w["elong"], w["orient"])
+    whole = rb.filter_space_variant3_params(f, *params)
+    for world in (2, 3, 8):
+        parts = []
+        for band in sharding.band_bounds(H, world, sharding.TILE3):
+            pb = [p[band[0]:band[1]] for p in params]
+            reach = sharding.read_margins3_params(*pb)[1]
+            field = np.maximum(port3.scales3_from_params(*(p.double().cpu().numpy() for p in pb)), 0.05)
+            hy = 0.25 * math.sqrt(3.0) * (field[..., 1] + field[..., 2])
+            assert reach == int(np.ceil(hy).max()) + 1
+            n0, n1 = sharding.needed_rows3(band, reach, H)
+            parts.append(sharding.filter3_rows_params(f[n0:n1], n0, H, *pb, band[0], band[0],
+                                                      band[1] - band[0]))
+        assert torch.equal(torch.cat(parts), whole)

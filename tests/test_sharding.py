@@ -91,3 +91,46 @@ def test_row_bands_with_halo_exchange_reproduce_whole_image():
     whole = cpu.filter_space_variant(f, field)
     assert banded.shape == whole.shape
     assert np.abs(banded - whole).max() < 1e-9
+
+
+def _worker3(rank, world, port, f, field, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import port3
+        H, W = f.shape
+        bands = sharding.band_bounds(H, world, sharding.TILE3)
+        band = bands[rank]
+        own = torch.from_numpy(f[band[0]:band[1]].copy())
+        _, ry = port3.support3(np.maximum(field[band[0]:band[1]], 0.05))
+        needs = sharding.gather_needs(sharding.needed_rows3(band, ry, H))
+        rows = sharding.exchange_rows(own, band, bands, needs, rank)
+        n0, n1 = needs[rank]
+        assert np.array_equal(rows.numpy(), f[n0:n1])
+        a = np.maximum(field[band[0]:band[1]], 0.05)
+        out = port3.pass3(rows.numpy(), 0, n0, a, 0, band[0], W, band[1] - band[0])
+        parts = [None] * world
+        dist.all_gather_object(parts, out)
+        if rank == 0:
+            ret.put(np.concatenate(parts))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_three_direction_row_bands_reproduce_whole_image():
+    """N=3 bands (64-row grid, reach = vertical kernel half-extent) with the
+    halo exchange at world size 2; the band filter is the numpy restatement."""
+    from oracle import port3
+    rng = np.random.default_rng(5)
+    H, W = 200, 40
+    f = rng.random((H, W))
+    field = np.stack([np.full((H, W), 3.0), np.linspace(1.0, 60.0, H)[:, None] * np.ones((1, W)),
+                      np.full((H, W), 2.5)], axis=-1)
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    procs = mp.start_processes(_worker3, args=(2, _free_port(), f, field, ret), nprocs=2,
+                               join=False, start_method="spawn")
+    banded = ret.get(timeout=120)
+    procs.join()
+    whole = port3.filter3(f, field)
+    assert np.abs(banded - whole).max() < 1e-11
