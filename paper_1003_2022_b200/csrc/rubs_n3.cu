@@ -68,10 +68,10 @@ constexpr int kM3Params32 = 3;  // same, float32
 #define RUBS3_TH 64
 #endif
 #ifndef RUBS3_NT
-#define RUBS3_NT 512
+#define RUBS3_NT 256
 #endif
 #ifndef RUBS3_SMEM_KB
-#define RUBS3_SMEM_KB 220
+#define RUBS3_SMEM_KB 110
 #endif
 constexpr int kTW = 32, kTH = RUBS3_TH, kNT = RUBS3_NT, kWarps = kNT / 32, kPx = kTH / kWarps;
 constexpr int kMinBlocks = (RUBS3_SMEM_KB <= 110) ? 2 : 1;
