@@ -1289,7 +1289,7 @@ constexpr int kPixSmem = 8 * kPixSlab * 8;  // 8 warps per CTA
 // were measured 2x slower on config 5: the line sweeps draw their
 // parallelism from the number of regions in a batch.
 #ifndef RUBS_BIG_BATCH
-#define RUBS_BIG_BATCH (1ll << 29)
+#define RUBS_BIG_BATCH (1ll << 31)
 #endif
 constexpr int64_t kBigBatch = RUBS_BIG_BATCH;
 
@@ -2252,6 +2252,15 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   t_launches += 2;
   RUBS_CUDA_TRY(cudaGetLastError());
   hc.lap("regions + upload");
+  if (hc.on) {
+    int64_t area = 0;
+    for (const BigRegion &g : regs) area += (int64_t)g.RW * g.RH;
+    std::fprintf(stderr, "[host] %zu regions, %zu batches, region area %.3g elements\n", regs.size(),
+                 batches.size(), (double)area);
+    for (const Batch &bt : batches)
+      std::fprintf(stderr, "[host]   batch: %d regions, %d tile slots, max %d x %d, %.3g doubles\n",
+                   bt.r1 - bt.r0, bt.t1 - bt.t0, bt.maxRW, bt.maxRH, (double)bt.used);
+  }
   for (const Batch &bt : batches) {
     const int nreg = bt.r1 - bt.r0, ntl = bt.t1 - bt.t0;
     const BigRegion *R = t_scr.d_regs + bt.r0;
