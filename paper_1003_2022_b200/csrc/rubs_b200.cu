@@ -1285,9 +1285,10 @@ __global__ void __launch_bounds__(NT, 2)
 // neighbouring CTAs share the rows their vertices touch in L2.
 
 constexpr int kPixSmem = 8 * kPixSlab * 8;  // 8 warps per CTA
-// Doubles of big-block scratch per batch.  L2-sized batches (8M doubles)
-// were measured 2x slower on config 5: the line sweeps draw their
-// parallelism from the number of regions in a batch.
+// Doubles of big-block scratch per batch (16 GB of the 180 GB HBM).
+// L2-sized batches (8M doubles) were measured 2x slower on config 5: the
+// region sweeps draw their parallelism from the number of regions in a
+// batch (2^29 -> 2^31 doubles: config 5 180 -> 173 ms).
 #ifndef RUBS_BIG_BATCH
 #define RUBS_BIG_BATCH (1ll << 31)
 #endif
