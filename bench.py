@@ -393,10 +393,10 @@ WORKLOADS = {
 # per output pixel (DADD + DFMA + DMUL + DSETP, thread level), shared-memory
 # wavefronts per output pixel, and DRAM bytes per launch
 # (dram__bytes_read.sum + dram__bytes_write.sum).
-# Config 3 (N=3, n3_tile_kernel): profiles/ncu_r01_n3_summary.md.
-DP_INST_PER_PX = {"2": 602, "3": 2113}
-SMEM_WF_PER_PX = {"2": 15.55, "3": 55.4}
-TRAFFIC_PER_LAUNCH = {"2": 105.07e6, "3": 1.5906e9}
+# Config 3 (N=3, n3_tile_kernel): profiles/ncu_r01b_summary.md.
+DP_INST_PER_PX = {"2": 602, "3": 2147}
+SMEM_WF_PER_PX = {"2": 15.55, "3": 53.9}
+TRAFFIC_PER_LAUNCH = {"2": 105.07e6, "3": 1.588e9}
 
 
 # ---------------------------------------------------------------------------
