@@ -1974,10 +1974,10 @@ struct CellAgg {
 };
 
 // 0: shared-memory overflow pass; else the block side S.
+#ifndef RUBS_BIG_K
+#define RUBS_BIG_K 3.0
+#endif
 __host__ __device__ inline int plan_side(const OvfRec &r, int tw, int th) {
-  if (region_elems(min(8, tw) + r.m[0] + r.m[1] + 1, min(8, th) + r.m[2] + r.m[3]) <=
-      kSmemLarge / 8)
-    return 0;
   const int h = max(max(r.m[0], r.m[1]), max(r.m[2], r.m[3]));
   int S = 64;
   while (S < 2 * h && S < 8192) S *= 2;
@@ -1986,6 +1986,16 @@ __host__ __device__ inline int plan_side(const OvfRec &r, int tw, int th) {
     const double mn = RW < RH ? RW : RH;
     if ((double)r.w * 0.25 * RW * RH * mn * mn <= (double)kPrecisionBudget) break;
     S /= 2;
+  }
+  if (region_elems(min(8, tw) + r.m[0] + r.m[1] + 1, min(8, th) + r.m[2] + r.m[3]) <=
+      kSmemLarge / 8) {
+    // both paths can take the tile: region elements per tile pixel, the
+    // global-scratch ones weighted by RUBS_BIG_K (a shared-memory region of
+    // the 32 x 32 tile grows as (32 + 2h)^2, a block region as (S + 2h)^2)
+    const double mx = r.m[0] + r.m[1], my = r.m[2] + r.m[3];
+    const double smem = (kTile + mx) * (kTile + my) / (double)(kTile * kTile);
+    const double big = RUBS_BIG_K * (S + mx) * (S + my) / ((double)S * S);
+    if (S <= kTile || smem <= big) return 0;
   }
   return S;
 }
