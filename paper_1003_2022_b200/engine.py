@@ -280,6 +280,28 @@ def device_lut(lut: ScaleLut | None = None) -> DeviceLut:
     return hit
 
 
+def _fast_device_args(f, params):
+    """(image dtype code, parameter dtype code) when f and the three
+    parameter planes are contiguous float32/float64 CUDA tensors of f's shape
+    on f's device, which is the current device, the parameters sharing one
+    dtype; else None (the general path converts)."""
+    torch = _torch()
+    if not f.is_cuda or not f.is_contiguous() or f.dtype not in (torch.float32, torch.float64):
+        return None
+    if f.device.index != torch.cuda.current_device():
+        return None
+    p0 = params[0]
+    for p in params:
+        if (not _is_torch(p) or p.device != f.device or p.dtype != p0.dtype or p.shape != f.shape
+                or not p.is_contiguous()):
+            return None
+    if p0.dtype not in (torch.float32, torch.float64):
+        return None
+    f32 = _native.RUBS_F32
+    return (f32 if f.dtype == torch.float32 else _native.RUBS_F64,
+            f32 if p0.dtype == torch.float32 else _native.RUBS_F64)
+
+
 def _params_host(size, elongation, orientation):
     s = np.asarray(size)
     r = np.asarray(elongation)
@@ -321,6 +343,17 @@ def filter_space_variant_params(f, size, elongation, orientation, lut: ScaleLut 
         if iterations < 1:
             raise ValueError("iterations must be >= 1")
         H, W = f.shape
+        fast = _fast_device_args(f, (size, elongation, orientation))
+        if fast is not None:
+            # already-placed contiguous CUDA tensors: no conversions (the
+            # wrapper's own cost is part of every call's step time)
+            fdt, pdt = fast
+            out = torch.empty((H, W), dtype=torch.float64, device=f.device)
+            _native.check(L.rubs_b200_filter_params(
+                f.data_ptr(), fdt, H, W, W, size.data_ptr(), elongation.data_ptr(),
+                orientation.data_ptr(), pdt, W, dl.handle, iterations, out.data_ptr(), W,
+                torch.cuda.current_stream(f.device).cuda_stream))
+            return out
         ps = []
         for v in (size, elongation, orientation):
             v = v if _is_torch(v) else torch.as_tensor(np.asarray(v))
@@ -495,6 +528,17 @@ def filter_space_variant3_params(f, size, elongation, orientation, iterations: i
     L = _native.load()
     if _is_torch(f):
         torch = _torch()
+        if f.dim() == 2:
+            fast = _fast_device_args(f, (size, elongation, orientation))
+            if fast is not None:
+                H, W = f.shape
+                res = torch.empty((H, W), dtype=torch.float64, device=f.device)
+                if H and W:
+                    _native.check(L.rubs_b200_filter3_params(
+                        f.data_ptr(), fast[0], H, W, W, size.data_ptr(), elongation.data_ptr(),
+                        orientation.data_ptr(), fast[1], W, iterations, res.data_ptr(), W,
+                        torch.cuda.current_stream(f.device).cuda_stream))
+                return res
         f = _torch_image(f)
         H, W = f.shape
         ps = []
