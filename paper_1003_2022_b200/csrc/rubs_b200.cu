@@ -122,6 +122,27 @@ int set_error(int code, const std::string &msg) {
 // ---------------------------------------------------------------------------
 // Kernels
 
+// Largest LUT size parameter over the field grid (positive finite values;
+// anything else is left to the passes' validation).  Bounds the iterated
+// canvases in LUT modes without mapping every pixel (see run_filter).
+__global__ void __launch_bounds__(256) size_max_kernel(FieldSpec F, Status *st) {
+  double m = 0.0;
+  const int64_t n = (int64_t)F.FH * F.FW;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / F.FW, c = i - r * F.FW;
+    const double v = load_scalar(F.ps, F.pdt, r * F.pld + c);
+    if (v > m && v < INFINITY) m = v;
+  }
+  unsigned long long b = (unsigned long long)__double_as_longlong(m);
+  b = max(b, __shfl_xor_sync(0xffffffffu, b, 16));
+  b = max(b, __shfl_xor_sync(0xffffffffu, b, 8));
+  b = max(b, __shfl_xor_sync(0xffffffffu, b, 4));
+  b = max(b, __shfl_xor_sync(0xffffffffu, b, 2));
+  b = max(b, __shfl_xor_sync(0xffffffffu, b, 1));
+  if ((threadIdx.x & 31) == 0) atomicMax(&st->smax_bits, b);
+}
+
 // Whole-field margins (the reference's _read_margins, engine.py:247-262),
 // needed before launch only when iterations > 1 (they size the extended
 // pass canvases).  One CTA per 16x16 cell, exact reference arithmetic.
@@ -2407,12 +2428,45 @@ int run_filter(const ImageSpec &img, FieldSpec F, int iterations, double *out, i
     if ((rc = finish_pass(img, F, D, s, st))) return rc;
     return status_to_code(st);
   } else {
-    // whole-field margins (engine.py:295) decide the pass canvases
-    if ((rc = launch_global_margins(F, D, s))) return rc;
-    Status st;
-    if ((rc = fetch_status(s, st))) return rc;
-    if ((rc = status_to_code(st))) return rc;
-    const int left = st.gm[0], right = st.gm[1], below = st.gm[2], above = st.gm[3];
+    // whole-field margins (engine.py:295) decide the pass canvases.  In LUT
+    // modes a bound replaces them: every mapped component is a convex blend
+    // of table entries times sqrt(size) <= amax sqrt(max size), and the
+    // margins grow with each component.  A larger pass canvas changes
+    // nothing: the final pass only reads the previous pass within its own
+    // margins (the passes' results differ from exact-canvas ones only by
+    // rounding).  Mapping every pixel for exact margins cost ~1/4 of a
+    // two-pass config-4 step.
+    int left, right, below, above;
+    bool bounded = false;
+    if (F.mode >= kModeLut && F.lut_amax > 0.0) {
+      size_max_kernel<<<4 * t_scr.sms, 256, 0, s>>>(F, t_scr.d_status);
+      ++t_launches;
+      RUBS_CUDA_TRY(cudaGetLastError());
+      Status st;
+      if ((rc = fetch_status(s, st))) return rc;
+      double smax;
+      std::memcpy(&smax, &st.smax_bits, sizeof(smax));
+      if (smax > 0.0 && std::isfinite(smax)) {
+        const double A = std::max(F.lut_amax * std::sqrt(smax), kScaleFloor) / F.div;
+        const double p = A / kSqrt2;
+        const double hx = 0.5 * A + p + 0.5;  // >= -(t1 - a1 - p2) and >= t1 + p4 (+1)
+        const double hy = 0.5 * A + p + 1.5;  // >= -(t2 - a3 - p2 - p4) and >= t2 (+3)
+        left = right = (int)std::ceil(hx) + 3;
+        below = above = (int)std::ceil(hy) + 3;
+        bounded = true;
+      }
+    }
+    if (!bounded) {
+      RUBS_CUDA_TRY(cudaMemsetAsync(t_scr.d_status, 0, sizeof(Status), s));
+      if ((rc = launch_global_margins(F, D, s))) return rc;
+      Status st;
+      if ((rc = fetch_status(s, st))) return rc;
+      if ((rc = status_to_code(st))) return rc;
+      left = st.gm[0];
+      right = st.gm[1];
+      below = st.gm[2];
+      above = st.gm[3];
+    }
     ImageSpec cur = img;
     for (int p = 0; p < iterations; ++p) {
       const int remain = iterations - 1 - p;
@@ -2662,6 +2716,7 @@ struct rubs_lut {
   double *entries = nullptr;
   int n_rho = 0, n_phi = 0;
   double rho_max = 0.0;
+  double amax = 0.0;  // largest component of any entry
 };
 
 namespace {
@@ -2682,6 +2737,7 @@ FieldSpec lut_field(const rubs_lut *lut, const void *size, const void *elong, co
   F.inv_log_rho_max = 1.0 / F.log_rho_max;
   F.phi_scale = (double)lut->n_phi / kQuarter;
   F.rho_lim = lut->rho_max * (1.0 + 1e-12);
+  F.lut_amax = lut->amax;
   return F;
 }
 }  // namespace
@@ -2785,6 +2841,7 @@ int rubs_b200_lut_create(const double *rho_grid, const double *phi_grid, const d
   L->n_rho = n_rho;
   L->n_phi = n_phi;
   L->rho_max = rho_grid[n_rho - 1];
+  for (size_t e = 0; e < (size_t)n_rho * n_phi * 4; ++e) L->amax = std::max(L->amax, entries[e]);
   // four copies, copy q rolled by q quarter turns: out[k] = mix[(k - q) mod 4]
   const size_t per = (size_t)n_rho * n_phi * 4;
   std::vector<double> rolled(4 * per);

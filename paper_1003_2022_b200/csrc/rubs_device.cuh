@@ -37,6 +37,7 @@ struct Status {
   int gm[4];                      // global margins left, right, below, above
   int ovf_count;                  // tiles deferred to the large-smem launch
   int pix_count;                  // pixels deferred to the per-pixel pass
+  unsigned long long smax_bits;   // max LUT size parameter (bits of a positive double)
 };
 
 // A tile deferred by the primary launch (its regions exceed the primary
@@ -65,6 +66,7 @@ struct FieldSpec {
   int n_rho, n_phi;
   double rho_max, log_rho_max, inv_log_rho_max;
   double phi_scale;  // n_phi / (pi / 4)
+  double lut_amax;   // largest component of any table entry (canvas bounds)
   double rho_lim;  // rho_max * (1 + 1e-12)
   int FH, FW;      // field grid, edge-clamped (np.pad mode="edge", engine.py:306-314)
   int fr_off;      // global row of the first row held in the arrays (row bands)
