@@ -131,10 +131,11 @@ inline double key_value(uint64_t k) {
   return v;
 }
 
-struct SelectPass {
-  uint64_t prefix[4];
-  int nr;
-  int shift;  // bits below the byte being counted
+// Radix-select state, on the device: the selected key prefix and the
+// remaining rank of each of the (up to 4) wanted order statistics.
+struct SelectState {
+  unsigned long long prefix[4];
+  long long left[4];
 };
 
 // tr = J11 + J22 (tensor.py:117), compacted once for the select passes
@@ -144,56 +145,74 @@ __global__ void trace_kernel(const double *j, int64_t n, double *tr) {
     tr[i] = j[3 * i] + j[3 * i + 2];
 }
 
-__global__ void select_hist_kernel(const double *tr, int64_t n, SelectPass sp, unsigned *hist) {
+// One 8-bit digit: counts of the keys that match each rank's prefix above
+// the digit (bits >= shift + 8).
+__global__ void select_hist_kernel(const double *tr, int64_t n, int nr, int shift,
+                                   const SelectState *ss, unsigned *hist) {
   __shared__ unsigned h[4][256];
+  __shared__ unsigned long long pre[4];
   for (int t = threadIdx.x; t < 4 * 256; t += blockDim.x) (&h[0][0])[t] = 0;
+  if (threadIdx.x < 4) pre[threadIdx.x] = ss->prefix[threadIdx.x];
   __syncthreads();
-  const int hi = sp.shift + 8;
+  const int hi = shift + 8;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t k = order_key(tr[i]);
-    const unsigned byte = (unsigned)(k >> sp.shift) & 255u;
-    for (int r = 0; r < sp.nr; ++r)
-      if (hi >= 64 || (k >> hi) == (sp.prefix[r] >> hi)) atomicAdd(&h[r][byte], 1u);
+    const unsigned byte = (unsigned)(k >> shift) & 255u;
+    for (int r = 0; r < nr; ++r)
+      if (hi >= 64 || (k >> hi) == (pre[r] >> hi)) atomicAdd(&h[r][byte], 1u);
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < sp.nr * 256; t += blockDim.x) {
+  for (int t = threadIdx.x; t < nr * 256; t += blockDim.x) {
     const unsigned v = (&h[0][0])[t];
     if (v) atomicAdd(hist + t, v);
   }
+}
+
+// Pick each rank's bucket of this digit (thread r), extend its prefix, and
+// clear the histogram for the next digit -- no host round trip per digit.
+__global__ void select_pick_kernel(int nr, int shift, SelectState *ss, unsigned *hist) {
+  const int r = threadIdx.x;
+  if (r < nr) {
+    const unsigned *h = hist + r * 256;
+    long long left = ss->left[r];
+    int b = 0;
+    while (b < 255 && left >= (long long)h[b]) left -= h[b++];
+    ss->left[r] = left;
+    ss->prefix[r] |= (unsigned long long)b << shift;
+  }
+  __syncthreads();
+  for (int t = threadIdx.x; t < nr * 256; t += blockDim.x) hist[t] = 0u;
 }
 
 // values[r] = the element of rank ranks[r] (0-based, ascending) of tr
 int select_trace(const double *tr, int64_t n, const int64_t *ranks, int nr, double *values,
                  cudaStream_t s) {
   if (!t_ts.d_hist) {
-    RT_CUDA_TRY(cudaMalloc(&t_ts.d_hist, 4 * 256 * sizeof(unsigned)));
-    RT_CUDA_TRY(cudaMallocHost(&t_ts.h_hist, 4 * 256 * sizeof(unsigned)));
+    RT_CUDA_TRY(cudaMalloc(&t_ts.d_hist, 4 * 256 * sizeof(unsigned) + sizeof(SelectState)));
+    RT_CUDA_TRY(cudaMallocHost(&t_ts.h_hist, sizeof(SelectState)));
+    RT_CUDA_TRY(cudaMemsetAsync(t_ts.d_hist, 0, 4 * 256 * sizeof(unsigned), s));
   }
-  SelectPass sp{};
-  sp.nr = nr;
-  int64_t left[4];
-  for (int r = 0; r < nr; ++r) left[r] = ranks[r];
+  SelectState *ss = reinterpret_cast<SelectState *>(t_ts.d_hist + 4 * 256);
+  SelectState *hs = reinterpret_cast<SelectState *>(t_ts.h_hist);
+  for (int r = 0; r < 4; ++r) {
+    hs->prefix[r] = 0;
+    hs->left[r] = r < nr ? ranks[r] : 0;
+  }
+  RT_CUDA_TRY(cudaMemcpyAsync(ss, hs, sizeof(SelectState), cudaMemcpyHostToDevice, s));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = (int)std::min<int64_t>((n + 255) / 256, 4 * sms);
   for (int shift = 56; shift >= 0; shift -= 8) {
-    sp.shift = shift;
-    RT_CUDA_TRY(cudaMemsetAsync(t_ts.d_hist, 0, 4 * 256 * sizeof(unsigned), s));
-    select_hist_kernel<<<grid, 256, 0, s>>>(tr, n, sp, t_ts.d_hist);
+    select_hist_kernel<<<grid, 256, 0, s>>>(tr, n, nr, shift, ss, t_ts.d_hist);
+    select_pick_kernel<<<1, 256, 0, s>>>(nr, shift, ss, t_ts.d_hist);
+    rubs_internal::count_launches(2);
     RT_CUDA_TRY(cudaGetLastError());
-    RT_CUDA_TRY(cudaMemcpyAsync(t_ts.h_hist, t_ts.d_hist, nr * 256 * sizeof(unsigned),
-                                cudaMemcpyDeviceToHost, s));
-    RT_CUDA_TRY(cudaStreamSynchronize(s));
-    for (int r = 0; r < nr; ++r) {
-      const unsigned *h = t_ts.h_hist + r * 256;
-      int b = 0;
-      while (b < 255 && left[r] >= (int64_t)h[b]) left[r] -= h[b++];
-      sp.prefix[r] |= (uint64_t)b << shift;
-    }
   }
-  for (int r = 0; r < nr; ++r) values[r] = key_value(sp.prefix[r]);
+  RT_CUDA_TRY(cudaMemcpyAsync(hs, ss, sizeof(SelectState), cudaMemcpyDeviceToHost, s));
+  RT_CUDA_TRY(cudaStreamSynchronize(s));
+  for (int r = 0; r < nr; ++r) values[r] = key_value(hs->prefix[r]);
   return RUBS_OK;
 }
 
@@ -316,6 +335,7 @@ int anisotropy_impl(const double *j, int64_t H, int64_t W, double noise_sigma,
   int rc = tbuf(0, n * sizeof(double), &trb);
   if (rc) return rc;
   trace_kernel<<<grid_for(n), 256, 0, s>>>(j, n, static_cast<double *>(trb));
+  rubs_internal::count_launches(1);
   RT_CUDA_TRY(cudaGetLastError());
   if ((rc = select_trace(static_cast<const double *>(trb), n, ranks, 4, v, s))) return rc;
   p.q05 = lerp_np(v[0], v[1], t5);
@@ -328,6 +348,7 @@ int anisotropy_impl(const double *j, int64_t H, int64_t W, double noise_sigma,
   p.size_iso = sigma_iso * sigma_iso / 3.0;
   p.rho_cap = rho_cap;
   anisotropy_kernel<<<grid_for(n), 256, 0, s>>>(j, n, p, size, rho, theta, iso);
+  rubs_internal::count_launches(1);
   RT_CUDA_TRY(cudaGetLastError());
   return RUBS_OK;
 }
@@ -347,6 +368,7 @@ int structure_tensor_impl(const void *f, int f_dtype, int64_t H, int64_t W, int6
     grad_tensor_kernel<1><<<grid_for(n), 256, 0, s>>>(f, (int)H, (int)W, ld_f, g[0], g[1], g[2]);
   else
     grad_tensor_kernel<0><<<grid_for(n), 256, 0, s>>>(f, (int)H, (int)W, ld_f, g[0], g[1], g[2]);
+  rubs_internal::count_launches(1);
   RT_CUDA_TRY(cudaGetLastError());
   const double *src[3] = {g[0], g[1], g[2]};
   if (window_sigma > 0.0) {
@@ -360,6 +382,7 @@ int structure_tensor_impl(const void *f, int f_dtype, int64_t H, int64_t W, int6
     for (int k = 0; k < 3; ++k) src[k] = dst[k];
   }
   interleave3_kernel<<<grid_for(n), 256, 0, s>>>(src[0], src[1], src[2], n, j);
+  rubs_internal::count_launches(1);
   RT_CUDA_TRY(cudaGetLastError());
   return RUBS_OK;
 }
@@ -424,6 +447,7 @@ int rubs_b200_adaptive_smooth(const void *f, int f_dtype, int64_t H, int64_t W, 
     fill_kernel<float><<<grid_for(n), 256, 0, s>>>(reinterpret_cast<float *>(ones), n, 1.0f);
   else
     fill_kernel<double><<<grid_for(n), 256, 0, s>>>(ones, n, 1.0);
+  rubs_internal::count_launches(1);
   RT_CUDA_TRY(cudaGetLastError());
   if (iterations == 1 && ld_f == W && ld_out == W) {
     const void *chans[2] = {f, ones};
@@ -440,6 +464,7 @@ int rubs_b200_adaptive_smooth(const void *f, int f_dtype, int64_t H, int64_t W, 
       return rc;
   }
   gain_correct_kernel<<<grid_for(n), 256, 0, s>>>(out, ld_out, gain, (int)H, (int)W);
+  rubs_internal::count_launches(1);
   RT_CUDA_TRY(cudaGetLastError());
   return RUBS_OK;
 }
