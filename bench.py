@@ -376,8 +376,12 @@ def run_ours(args, rank, world, local):
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "traffic_unit": "bytes/launch (ncu)",
-                         "kernel": "n3_tile_kernel" if n3 else "wide_filter_kernel",
+                         "kernel": ("n3_tile_kernel" if n3 else
+                                    "wide_filter_kernel" if launches_per_step <= iters else
+                                    "filter kernels of the pass: wide_filter_kernel + the deferred-tile "
+                                    "passes (tile_overflow / big_* kernels; split in profiles/)"),
                          "kernel_ms_avg": tile_avg_ms,
+                         "kernel_ms_per_step": max(tile_ms.value, 0.0) / max(1, args.steps),
                          "algorithmic_bytes_per_px": bpp, "peak_source": peak_kind,
                          "binding_bound": "shared-memory wavefronts and issue (see smem, fp64)"},
             "fp64": fp64,

@@ -2400,7 +2400,11 @@ int finish_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cud
   int rc;
   if ((rc = fetch_status(s, st))) return rc;
   if (st.ovf_count > 0 && !(st.flags & (kFlagFieldNonFinite | kFlagParamInvalid))) {
-    if ((rc = run_overflow(I, F, D, st.ovf_count, s))) return rc;
+    {
+      // the deferred-tile passes are part of the pass's filter work (kind 0)
+      TimedLaunch tl(0, s);
+      if ((rc = run_overflow(I, F, D, st.ovf_count, s))) return rc;
+    }
     RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s));
     if ((rc = fetch_status(s, st))) return rc;
   }
