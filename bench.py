@@ -342,7 +342,8 @@ def run_ours(args, rank, world, local):
         tile_avg_ms = tile_ms.value / max(1, tile_n.value)
         launches_per_step = tile_n.value / max(1, args.steps)
         kern_s = max(tile_ms.value, 1e-9) / max(1, args.steps) * 1e-3
-        achieved = bpp * H * W * iters / kern_s / 1e9
+        # bpp counts every pass (config 4: both passes' bytes per output pixel)
+        achieved = bpp * H * W / kern_s / 1e9
         # fp64 issue bound: B200 has 64 fp64 lanes per SM; DP instructions
         # per pixel measured with ncu (profiles/ncu_r01_summary.md)
         dp_per_px = DP_INST_PER_PX.get(args.config)
