@@ -32,6 +32,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 #include <string>
 #include <vector>
 
@@ -1068,8 +1069,24 @@ __global__ void __launch_bounds__(NT, 2)
       acc = make_int4(0, 0, 0, 0);
       wacc = 0.f;
     };
+    constexpr int NK = (kWideH + RS - 1) / RS;
+    // LUT modes: all of this thread's parameter loads in flight at once
+    using PT = typename std::conditional<MODE == kModeLut, double, float>::type;
+    PT pre[kPark ? NK : 1][3];
+    if constexpr (kPark) {
 #pragma unroll
-    for (int k = 0; k < (kWideH + RS - 1) / RS; ++k) {
+      for (int k = 0; k < NK; ++k) {
+        const int ty_ = py + RS * k;
+        const int fc = min(max(D.pc_lo + x0 + px, 0), F.FW - 1);
+        const int fr = min(max(D.pr_lo + y0 + min(ty_, kWideH - 1), 0), F.FH - 1) - F.fr_off;
+        const int64_t i = (int64_t)fr * F.pld + fc;
+        pre[k][0] = __ldg(static_cast<const PT *>(F.ps) + i);
+        pre[k][1] = __ldg(static_cast<const PT *>(F.pr) + i);
+        pre[k][2] = __ldg(static_cast<const PT *>(F.pt) + i);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < NK; ++k) {
       const int ty_ = py + RS * k;  // tile row (warp-uniform)
       if (ty_ < kWideH) {
         if ((ty_ >> 3) != cur) {
@@ -1082,7 +1099,7 @@ __global__ void __launch_bounds__(NT, 2)
           float w;
           if constexpr (kPark) {
             double a[4];
-            field_at<MODE>(F, D.pc_lo + x, D.pr_lo + y, a, flags);
+            field_from_params(F, (double)pre[k][0], (double)pre[k][1], (double)pre[k][2], a, flags);
             m = pixel_margins_fast(a);
             w = 1.0f / (float)(a[0] * a[1] * a[2] * a[3]);
             double2 *dst = reinterpret_cast<double2 *>(apark + (ty_ * kWideW + px) * 4);

@@ -228,6 +228,20 @@ __device__ __forceinline__ void field_at(const FieldSpec &F, int n1, int n2, dou
   }
 }
 
+// LUT modes with the three parameters already loaded (the primary kernel
+// issues all of a thread's parameter loads up front): lut_map, floor, scale
+// exactly as field_at.
+__device__ __forceinline__ void field_from_params(const FieldSpec &F, double s, double r, double t,
+                                                  double a[4], unsigned &flags) {
+  lut_map(F, s, r, t, a, flags);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) a[k] = fmax(a[k], kScaleFloor);
+  if (F.scaled) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) a[k] = __ddiv_rn(a[k], F.div);
+  }
+}
+
 // Runtime-mode dispatch (pre-pass kernels, not on the hot path).
 __device__ __forceinline__ void field_at_rt(const FieldSpec &F, int n1, int n2, double a[4],
                                             unsigned &flags) {
