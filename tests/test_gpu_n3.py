@@ -234,3 +234,14 @@ def test_row_bands_reproduce_whole_image_bitwise(cuda):
             parts.append(sharding.filter3_rows_params(f[n0:n1], n0, H, *pb, band[0], band[0],
                                                       band[1] - band[0]))
         assert torch.equal(torch.cat(parts), whole)
+
+
+def test_kernel_wider_than_the_region_buffer_fails_loudly(cuda):
+    """A kernel whose row reach exceeds the shared-memory row buffer (about
+    4000 columns) is refused with an error, never computed wrongly."""
+    f = np.ones((16, 16))
+    with pytest.raises(RuntimeError):
+        rb.filter_space_variant3(f, np.array([9000.0, 1.0, 1.0]))
+    out = rb.filter_space_variant3(f, np.array([3000.0, 1.0, 1.0]))  # fits
+    ref = oracle.dense3(f, np.array([3000.0, 1.0, 1.0]))
+    assert np.abs(out - ref).max() < 1e-9 * np.abs(ref).max()
