@@ -956,7 +956,11 @@ __global__ void __launch_bounds__(kThreadsLarge, 1)
 #define RUBS_DEV_SKIP_GATHER 0
 #endif
 constexpr int kWideW = 64, kWideH = 32;
-constexpr int kSmemWide = 110 * 1024;  // x2 CTAs + static + reserved <= 228 KB
+#ifndef RUBS_WIDE_CTAS
+#define RUBS_WIDE_CTAS 2  // CTAs per SM of the primary kernel (dev A/B: 3)
+#endif
+constexpr int kWideCtas = RUBS_WIDE_CTAS;
+constexpr int kSmemWide = (kWideCtas == 3 ? 72 : 110) * 1024;  // x CTAs + static <= 228 KB
 constexpr int kMaxSmId = 256;          // bound of %smid (scale-vector slots)
 #ifndef RUBS_WIDE_THREADS
 #define RUBS_WIDE_THREADS 384
@@ -995,7 +999,7 @@ __host__ __device__ constexpr int wide_cap() {
 }
 
 template <int MODE, int DT, int NT, int NCH>
-__global__ void __launch_bounds__(NT, 2)
+__global__ void __launch_bounds__(NT, kWideCtas)
     wide_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int tiles_x32,
                        int region_cap, int *ovf_list, Status *st, double *aslots,
                        unsigned *slotmask, int tile_base, MultiChan mc,
@@ -1023,8 +1027,8 @@ __global__ void __launch_bounds__(NT, 2)
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       int slot = -1;
       while (slot < 0) {
-        for (int b = 0; b < 2 && slot < 0; ++b)
-          if (!(atomicOr(&slotmask[smid], 1u << b) & (1u << b))) slot = (int)smid * 2 + b;
+        for (int b = 0; b < kWideCtas && slot < 0; ++b)
+          if (!(atomicOr(&slotmask[smid], 1u << b) & (1u << b))) slot = (int)smid * kWideCtas + b;
       }
       s_slot = slot;
     }
@@ -1304,7 +1308,7 @@ __global__ void __launch_bounds__(NT, 2)
     }
     __syncthreads();
   }
-  if (kPark && tid == 0) atomicAnd(&slotmask[smid], ~(1u << (s_slot & 1)));
+  if (kPark && tid == 0) atomicAnd(&slotmask[smid], ~(1u << (s_slot % kWideCtas)));
   flush_status(st, ghi, flags);
 }
 
@@ -1738,7 +1742,7 @@ int ensure_scratch() {
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_status, sizeof(Status)));
     RUBS_CUDA_TRY(cudaMallocHost(&t_scr.h_status, sizeof(Status)));
     RUBS_CUDA_TRY(cudaDeviceGetAttribute(&t_scr.sms, cudaDevAttrMultiProcessorCount, dev));
-    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_aslot, (size_t)kMaxSmId * 2 * kWideW * kWideH * 4 *
+    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_aslot, (size_t)kMaxSmId * kWideCtas * kWideW * kWideH * 4 *
                                                  sizeof(double)));
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_slotmask, kMaxSmId * sizeof(unsigned)));
     RUBS_CUDA_TRY(cudaMemset(t_scr.d_slotmask, 0, kMaxSmId * sizeof(unsigned)));
