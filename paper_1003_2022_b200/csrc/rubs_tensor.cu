@@ -169,20 +169,37 @@ __global__ void select_hist_kernel(const double *tr, int64_t n, int nr, int shif
   }
 }
 
-// Pick each rank's bucket of this digit (thread r), extend its prefix, and
-// clear the histogram for the next digit -- no host round trip per digit.
-__global__ void select_pick_kernel(int nr, int shift, SelectState *ss, unsigned *hist) {
-  const int r = threadIdx.x;
-  if (r < nr) {
-    const unsigned *h = hist + r * 256;
-    long long left = ss->left[r];
-    int b = 0;
-    while (b < 255 && left >= (long long)h[b]) left -= h[b++];
-    ss->left[r] = left;
-    ss->prefix[r] |= (unsigned long long)b << shift;
+// Pick each rank's bucket of this digit, extend its prefix, and clear the
+// histogram for the next digit -- no host round trip per digit.  One CTA of
+// 256 threads: an inclusive scan of the 256 counts in shared memory, then the
+// bin whose [exclusive, inclusive) count range holds the remaining rank.
+__global__ void __launch_bounds__(256) select_pick_kernel(int nr, int shift, SelectState *ss,
+                                                          unsigned *hist) {
+  __shared__ unsigned long long c[256];
+  __shared__ long long s_left;
+  const int t = threadIdx.x;
+  for (int r = 0; r < nr; ++r) {
+    const unsigned long long own = hist[r * 256 + t];
+    c[t] = own;
+    if (t == 0) s_left = ss->left[r];  // read before the selected thread rewrites it
+    __syncthreads();
+    for (int o = 1; o < 256; o <<= 1) {  // Hillis-Steele inclusive scan
+      const unsigned long long v = t >= o ? c[t - o] : 0ull;
+      __syncthreads();
+      c[t] += v;
+      __syncthreads();
+    }
+    const long long left = s_left;
+    const long long inc = (long long)c[t], exc = inc - (long long)own;
+    // the first bin whose inclusive count exceeds the rank (bin 255 takes
+    // any remainder) -- the host loop's `while (left >= h[b]) left -= h[b++]`
+    if (exc <= left && (left < inc || t == 255)) {
+      ss->left[r] = left - exc;
+      ss->prefix[r] |= (unsigned long long)t << shift;
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  for (int t = threadIdx.x; t < nr * 256; t += blockDim.x) hist[t] = 0u;
+  for (int i = t; i < nr * 256; i += blockDim.x) hist[i] = 0u;
 }
 
 // values[r] = the element of rank ranks[r] (0-based, ascending) of tr
