@@ -956,16 +956,20 @@ __global__ void __launch_bounds__(kThreadsLarge, 1)
 #define RUBS_DEV_SKIP_GATHER 0
 #endif
 constexpr int kWideW = 64, kWideH = 32;
-#ifndef RUBS_WIDE_CTAS
-#define RUBS_WIDE_CTAS 2  // CTAs per SM of the primary kernel (dev A/B: 3)
-#endif
-constexpr int kWideCtas = RUBS_WIDE_CTAS;
-constexpr int kSmemWide = (kWideCtas == 3 ? 72 : 110) * 1024;  // x CTAs + static <= 228 KB
+// CTAs per SM of a wide-kernel launch: 2 (110 KB regions, 384 threads) by
+// default; 3 (72 KB, 256 threads) for the two-channel LUT launch of the
+// adaptive_smooth pipeline, where it measured faster (1.22 -> 0.95 ms).
+constexpr int kSlotsPerSm = 3;  // parked scale-vector slots per SM (any CT)
+template <int CT>
+__host__ __device__ constexpr int wide_smem() { return (CT == 3 ? 72 : 110) * 1024; }
+constexpr int kSmemWide = wide_smem<2>();
 constexpr int kMaxSmId = 256;          // bound of %smid (scale-vector slots)
 #ifndef RUBS_WIDE_THREADS
 #define RUBS_WIDE_THREADS 384
 #endif
 constexpr int kThreadsWide = RUBS_WIDE_THREADS;  // 2 CTAs per SM
+template <int CT>
+__host__ __device__ constexpr int wide_threads() { return CT == 3 ? 256 : kThreadsWide; }
 
 // Planning bounds of one pixel: read margins (left, right, below, above)
 // covering its taps, and an upper bound of w = 1 / (a1 a2 a3 a4).
@@ -993,18 +997,18 @@ struct TmaMapsN {
   TmaMaps m[NCH];
 };
 // shared memory per channel region (doubles, 128-byte multiple)
-template <int NCH>
+template <int NCH, int CT = 2>
 __host__ __device__ constexpr int wide_cap() {
-  return (kSmemWide / 8 / NCH) & ~15;
+  return (wide_smem<CT>() / 8 / NCH) & ~15;
 }
 
-template <int MODE, int DT, int NT, int NCH>
-__global__ void __launch_bounds__(NT, kWideCtas)
+template <int MODE, int DT, int NT, int NCH, int CT = 2>
+__global__ void __launch_bounds__(NT, CT)
     wide_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int tiles_x32,
                        int region_cap, int *ovf_list, Status *st, double *aslots,
                        unsigned *slotmask, int tile_base, MultiChan mc,
                        const __grid_constant__ TmaMapsN<NCH> tm) {
-  constexpr int CAP = wide_cap<NCH>();
+  constexpr int CAP = wide_cap<NCH, CT>();
   constexpr int NW = NT / 32;
   constexpr int NCX = kWideW / 8, NCY = kWideH / 8;  // 8 x 4 cells of 8 x 8
   extern __shared__ __align__(128) double S[];
@@ -1027,8 +1031,8 @@ __global__ void __launch_bounds__(NT, kWideCtas)
       asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
       int slot = -1;
       while (slot < 0) {
-        for (int b = 0; b < kWideCtas && slot < 0; ++b)
-          if (!(atomicOr(&slotmask[smid], 1u << b) & (1u << b))) slot = (int)smid * kWideCtas + b;
+        for (int b = 0; b < CT && slot < 0; ++b)
+          if (!(atomicOr(&slotmask[smid], 1u << b) & (1u << b))) slot = (int)smid * kSlotsPerSm + b;
       }
       s_slot = slot;
     }
@@ -1308,7 +1312,7 @@ __global__ void __launch_bounds__(NT, kWideCtas)
     }
     __syncthreads();
   }
-  if (kPark && tid == 0) atomicAnd(&slotmask[smid], ~(1u << (s_slot % kWideCtas)));
+  if (kPark && tid == 0) atomicAnd(&slotmask[smid], ~(1u << (s_slot % kSlotsPerSm)));
   flush_status(st, ghi, flags);
 }
 
@@ -1742,7 +1746,7 @@ int ensure_scratch() {
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_status, sizeof(Status)));
     RUBS_CUDA_TRY(cudaMallocHost(&t_scr.h_status, sizeof(Status)));
     RUBS_CUDA_TRY(cudaDeviceGetAttribute(&t_scr.sms, cudaDevAttrMultiProcessorCount, dev));
-    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_aslot, (size_t)kMaxSmId * kWideCtas * kWideW * kWideH * 4 *
+    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_aslot, (size_t)kMaxSmId * kSlotsPerSm * kWideW * kWideH * 4 *
                                                  sizeof(double)));
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_slotmask, kMaxSmId * sizeof(unsigned)));
     RUBS_CUDA_TRY(cudaMemset(t_scr.d_slotmask, 0, kMaxSmId * sizeof(unsigned)));
@@ -1781,10 +1785,10 @@ int ensure_scratch() {
     // multi-channel instantiations (adaptive_smooth pipeline)
     RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<kModeUniform, 1, kThreadsWide, 3>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWide));
-    RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<kModeLut, 1, kThreadsWide, 2>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWide));
-    RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<kModeLut, 0, kThreadsWide, 2>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWide));
+    RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<kModeLut, 1, wide_threads<3>(), 2, 3>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, wide_smem<3>()));
+    RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<kModeLut, 0, wide_threads<3>(), 2, 3>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, wide_smem<3>()));
     RUBS_CUDA_TRY(cudaFuncSetAttribute(big_rs234_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kRsSmem));
     t_scr.attr_set = true;
@@ -1913,7 +1917,7 @@ int kernel_choice() {
 }
 
 // Wide-kernel tiles of rows [wy0, wy1) of the 64 x 32 grid over domain D.
-template <int M, int T, int NCH = 1>
+template <int M, int T, int NCH = 1, int CT = 2>
 void launch_wide_rows(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int wy0,
                       int wy1, cudaStream_t s, const MultiChan *mcp = nullptr) {
   const int tiles_x = (D.pw + kTile - 1) / kTile;
@@ -1932,8 +1936,9 @@ void launch_wide_rows(const ImageSpec &I, const FieldSpec &F, const DomainSpec &
     Ic.f = mc.f[ch];
     tm.m[ch] = tma_maps(Ic);
   }
-  wide_filter_kernel<M, T, kThreadsWide, NCH><<<wx * (wy1 - wy0), kThreadsWide, kSmemWide, s>>>(
-      I, F, D, wx, tiles_x, wide_cap<NCH>(), t_scr.d_ovf, t_scr.d_status, t_scr.d_aslot,
+  wide_filter_kernel<M, T, wide_threads<CT>(), NCH, CT>
+      <<<wx * (wy1 - wy0), wide_threads<CT>(), wide_smem<CT>(), s>>>(
+      I, F, D, wx, tiles_x, wide_cap<NCH, CT>(), t_scr.d_ovf, t_scr.d_status, t_scr.d_aslot,
       t_scr.d_slotmask, wy0 * wx, mc, tm);
 }
 
@@ -2558,9 +2563,9 @@ int run_multi(const ImageSpec &I, const MultiChan &mc, int nch, FieldSpec F, int
     if (F.mode == kModeUniform)
       launch_wide_rows<kModeUniform, 1, 3>(I, F, D, 0, wy, s, &mc);
     else if (I.dt == 1)
-      launch_wide_rows<kModeLut, 1, 2>(I, F, D, 0, wy, s, &mc);
+      launch_wide_rows<kModeLut, 1, 2, 3>(I, F, D, 0, wy, s, &mc);
     else
-      launch_wide_rows<kModeLut, 0, 2>(I, F, D, 0, wy, s, &mc);
+      launch_wide_rows<kModeLut, 0, 2, 3>(I, F, D, 0, wy, s, &mc);
   }
   ++t_launches;
   RUBS_CUDA_TRY(cudaGetLastError());
