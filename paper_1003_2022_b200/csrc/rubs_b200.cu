@@ -1339,6 +1339,7 @@ constexpr int kPixSmem = 8 * kPixSlab * 8;  // 8 warps per CTA
 #define RUBS_BIG_BATCH (1ll << 31)
 #endif
 constexpr int64_t kBigBatch = RUBS_BIG_BATCH;
+constexpr int64_t kBigMinBatch = 1ll << 24;  // smallest budget tried after allocation failures
 
 template <int MODE, int DT>
 __global__ void __launch_bounds__(256) pixel_kernel(ImageSpec I, FieldSpec F, DomainSpec D,
@@ -2237,7 +2238,15 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   // Batches of blocks under a scratch budget.  A batch's kernels follow the
   // previous batch's in stream order, so the scratch is reused without a
   // host sync; region / tile lists of all batches are uploaded once.
-  const int64_t budget = kBigBatch;
+  // The budget is capped at half the free device memory (the scratch is kept
+  // for later calls) and quartered on an allocation failure.
+  int64_t budget = kBigBatch;
+  {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
+      budget = std::min<int64_t>(budget, (int64_t)((free_b + t_scr.big_cap * sizeof(double)) / 2 /
+                                                   sizeof(double)));
+  }
   struct Batch {
     int r0, r1, t0, t1;
     int64_t used;
@@ -2250,6 +2259,14 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   int ntl = 0;
   Batch cur{0, 0, 0, 0, 0, 0, 0, 0};
   int64_t max_used = 0;
+ replan:
+  regs.clear();
+  cm.clear();
+  cm_cell.clear();
+  batches.clear();
+  ntl = 0;
+  cur = Batch{0, 0, 0, 0, 0, 0, 0, 0};
+  max_used = 0;
   auto close_batch = [&]() {
     cur.r1 = (int)regs.size();
     cur.t1 = ntl;
@@ -2289,7 +2306,14 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   if (max_used > (int64_t)t_scr.big_cap) {
     if (t_scr.d_big) cudaFree(t_scr.d_big);
     t_scr.d_big = nullptr;
-    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_big, (size_t)max_used * sizeof(double)));
+    t_scr.big_cap = 0;
+    const cudaError_t e = cudaMalloc(&t_scr.d_big, (size_t)max_used * sizeof(double));
+    if (e == cudaErrorMemoryAllocation && budget > 4 * (int64_t)kBigMinBatch) {
+      (void)cudaGetLastError();  // clear, plan smaller batches
+      budget /= 4;
+      goto replan;
+    }
+    RUBS_CUDA_TRY(e);
     t_scr.big_cap = (size_t)max_used;
   }
   if ((rc = upload(regs, t_scr.d_regs, t_scr.regs_cap, s))) return rc;
