@@ -1340,6 +1340,9 @@ constexpr int kPixSmem = 8 * kPixSlab * 8;  // 8 warps per CTA
 #endif
 constexpr int64_t kBigBatch = RUBS_BIG_BATCH;
 constexpr int64_t kBigMinBatch = 1ll << 24;  // smallest budget tried after allocation failures
+// fewer than SMs / kRsFewDiv regions in a batch: line sweeps (flat-cost table:
+// 4 regions 3.8 -> 1.6 ms; 64 regions keep the fused sweep, 1.05 vs 1.44 ms)
+constexpr int kRsFewDiv = 8;
 
 template <int MODE, int DT>
 __global__ void __launch_bounds__(256) pixel_kernel(ImageSpec I, FieldSpec F, DomainSpec D,
@@ -2347,7 +2350,10 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
     const int nreg = bt.r1 - bt.r0, ntl = bt.t1 - bt.t0;
     const BigRegion *R = t_scr.d_regs + bt.r0;
     big_fill_rs1_kernel<T><<<dim3((bt.maxRH + 7) / 8, nreg), 256, 0, s>>>(I, R, t_scr.d_big);
-    if (bt.maxRW <= kRsThreads * kRsCols && !std::getenv("RUBS_B200_LINE_SWEEPS")) {
+    // the fused sweep runs one CTA per region: with few regions in the batch
+    // the three line sweeps (parallel over every line of every region) win
+    if (bt.maxRW <= kRsThreads * kRsCols && nreg * kRsFewDiv >= t_scr.sms &&
+        !std::getenv("RUBS_B200_LINE_SWEEPS")) {
       big_rs234_kernel<<<nreg, kRsThreads, 6 * (bt.maxRW + 2) * 8, s>>>(R, t_scr.d_big,
                                                                          t_scr.d_status);
       t_launches -= 2;
