@@ -1496,22 +1496,25 @@ __global__ void __launch_bounds__(kRsThreads, 1)
   double *A = prow, *B = prow + 3 * W2;
   for (int i = threadIdx.x; i < 6 * W2; i += kRsThreads) prow[i] = 0.0;
   double *base = scratch + g.off;
-  double nxt[kRsCols];
+  // RS1 rows are prefetched two rows ahead (one row of lead did not cover
+  // the load latency: the per-row time is a barrier plus a few shared ops)
+  double na[kRsCols], nb[kRsCols];
 #pragma unroll
   for (int k = 0; k < kRsCols; ++k) {
     const int c = threadIdx.x + k * kRsThreads;
-    nxt[k] = (c < g.RW && g.RH > 0) ? base[c] : 0.0;
+    na[k] = (c < g.RW && g.RH > 0) ? base[c] : 0.0;
+    nb[k] = (c < g.RW && g.RH > 1) ? base[g.P + c] : 0.0;
   }
   __syncthreads();
   unsigned gh = 0;
-  for (int r = 0; r < g.RH; ++r) {
+  auto row_step = [&](int r, double (&buf)[kRsCols]) {
     double *row = base + (int64_t)r * g.P;
     double cur[kRsCols];
 #pragma unroll
     for (int k = 0; k < kRsCols; ++k) {
-      cur[k] = nxt[k];
+      cur[k] = buf[k];
       const int c = threadIdx.x + k * kRsThreads;
-      nxt[k] = (c < g.RW && r + 1 < g.RH) ? row[g.P + c] : 0.0;  // prefetch row r + 1
+      buf[k] = (c < g.RW && r + 2 < g.RH) ? row[2 * (int64_t)g.P + c] : 0.0;  // row r + 2
     }
 #pragma unroll
     for (int k = 0; k < kRsCols; ++k) {
@@ -1531,6 +1534,10 @@ __global__ void __launch_bounds__(kRsThreads, 1)
     double *t = A;
     A = B;
     B = t;
+  };
+  for (int r = 0; r < g.RH; r += 2) {
+    row_step(r, na);
+    if (r + 1 < g.RH) row_step(r + 1, nb);
   }
   gh = __reduce_max_sync(0xffffffffu, gh);
   if ((threadIdx.x & 31) == 0 && gh) atomicMax(&st->guard_hi, gh);
