@@ -1975,7 +1975,8 @@ template <int M, int T>
 void launch_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cudaStream_t s) {
   const int tiles_x = (D.pw + kTile - 1) / kTile, tiles_y = (D.ph + kTile - 1) / kTile;
   const int ntiles = tiles_x * tiles_y;
-  cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s);
+  // ovf_count is zero here: every caller clears the status before its first
+  // pass and finish_pass clears the count after the deferred tiles
   if (kernel_choice() == 2)
     launch_wide_rows<M, T>(I, F, D, 0, (D.ph + kWideH - 1) / kWideH, s);
   else
