@@ -20,6 +20,7 @@ determinism, which this partition keeps.
 from __future__ import annotations
 
 import ctypes
+import math
 
 import numpy as np
 
@@ -157,6 +158,22 @@ def filter_rows_params(f_rows, f_row0: int, H: int, size, elong, orient, p_row0:
     return out
 
 
+def halo_bound_params(size, lut=None) -> tuple:
+    """Read-margin bound (left, right, below, above) of LUT-mapped kernels
+    with sizes up to size.max(): every mapped component is a convex blend of
+    table entries times sqrt(size) (solver.py:289-335), and the margins of
+    engine.py:247-262 grow with each component.  One reduction over the
+    band's size plane instead of mapping every pixel (the exact
+    read_margins_params costs about half a band's filter time at 8 ranks);
+    a wider halo changes nothing but the rows exchanged."""
+    from .solver import default_lut
+    lut = lut or default_lut()
+    smax = float(size.max().item()) if hasattr(size, "max") else float(np.max(size))
+    A = max(float(np.max(lut.entries)) * math.sqrt(max(smax, 0.0)), 0.05)
+    m = int(math.ceil(0.5 * A + A / math.sqrt(2.0) + 1.5)) + 3
+    return (m, m, m, m)
+
+
 def filter_row_band(f_own, band, H: int, size, elong, orient, lut=None, group=None):
     """One rank's share of a row-band filter: this rank holds image rows
     ``band`` (f_own) and the parameter rows of the same band; returns its
@@ -166,7 +183,7 @@ def filter_row_band(f_own, band, H: int, size, elong, orient, lut=None, group=No
     rank = dist.get_rank(group)
     bands = band_bounds(H, world)
     assert tuple(band) == bands[rank], "band must match band_bounds(H, world)[rank]"
-    margins = read_margins_params(size, elong, orient, band[0], H, lut)
+    margins = halo_bound_params(size, lut)
     needs = gather_needs(needed_rows(band, margins, H), group, device=f_own.device)
     f_need = exchange_rows(f_own, band, bands, needs, rank, group)
     return filter_rows_params(f_need, needs[rank][0], H, size, elong, orient, band[0], band[0],
@@ -225,6 +242,15 @@ def filter3_rows_params(f_rows, f_row0: int, H: int, size, elong, orient, p_row0
     return out
 
 
+def reach3_bound_params(size) -> int:
+    """Row reach bound of N=3 kernels with sizes up to size.max(): the
+    closed-form scales satisfy a_k^2 = 12 p_k <= 15 size (p_k <= (2/3 +
+    1/sqrt3) size), and the reach is ceil((a2 + a3) sqrt3 / 4) + 1."""
+    smax = float(size.max().item()) if hasattr(size, "max") else float(np.max(size))
+    a = max(math.sqrt(15.0 * max(smax, 0.0)), 0.05)
+    return int(math.ceil(0.5 * math.sqrt(3.0) * a)) + 2
+
+
 def filter3_row_band(f_own, band, H: int, size, elong, orient, group=None):
     """One rank's share of an N=3 row-band filter (band = band_bounds(H,
     world, TILE3)[rank]); collective over the group (needs all-gather +
@@ -234,7 +260,7 @@ def filter3_row_band(f_own, band, H: int, size, elong, orient, group=None):
     rank = dist.get_rank(group)
     bands = band_bounds(H, world, TILE3)
     assert tuple(band) == bands[rank], "band must match band_bounds(H, world, TILE3)[rank]"
-    reach = read_margins3_params(size, elong, orient)[1]
+    reach = reach3_bound_params(size)
     needs = gather_needs(needed_rows3(band, reach, H), group, device=f_own.device)
     f_need = exchange_rows(f_own, band, bands, needs, rank, group)
     return filter3_rows_params(f_need, needs[rank][0], H, size, elong, orient, band[0], band[0],

@@ -233,6 +233,10 @@ def test_row_bands_reproduce_whole_image_bitwise(cuda):
             n0, n1 = sharding.needed_rows3(band, reach, H)
             parts.append(sharding.filter3_rows_params(f[n0:n1], n0, H, *pb, band[0], band[0],
                                                       band[1] - band[0]))
+            b0, b1 = sharding.needed_rows3(band, sharding.reach3_bound_params(pb[0]), H)
+            assert b0 <= n0 and b1 >= n1
+            assert torch.equal(sharding.filter3_rows_params(f[b0:b1], b0, H, *pb, band[0], band[0],
+                                                            band[1] - band[0]), parts[-1])
         assert torch.equal(torch.cat(parts), whole)
 
 

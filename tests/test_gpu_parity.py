@@ -518,4 +518,9 @@ def test_row_bands_reproduce_whole_image_bitwise(cuda):
             n0, n1 = sharding.needed_rows(band, m, H)
             parts.append(sharding.filter_rows_params(f[n0:n1], n0, H, *pb, band[0], band[0],
                                                      band[1] - band[0]))
+            # the cheap halo bound the multi-GPU path uses: more rows, same result
+            b0, b1 = sharding.needed_rows(band, sharding.halo_bound_params(pb[0], lut), H)
+            assert b0 <= n0 and b1 >= n1
+            assert torch.equal(sharding.filter_rows_params(f[b0:b1], b0, H, *pb, band[0], band[0],
+                                                           band[1] - band[0]), parts[-1])
         assert torch.equal(torch.cat(parts), whole)

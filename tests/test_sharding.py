@@ -134,3 +134,24 @@ def test_three_direction_row_bands_reproduce_whole_image():
     procs.join()
     whole = port3.filter3(f, field)
     assert np.abs(banded - whole).max() < 1e-11
+
+
+def test_halo_bounds_cover_the_exact_margins(rng):
+    """The cheap halo bounds used by the row-band filters are >= the exact
+    per-pixel margins (N=4 LUT mapping, N=3 closed form)."""
+    import math
+    from oracle import port, port3
+    from paper_1003_2022_b200 import default_lut
+    lut = default_lut()
+    n = 4000
+    size = rng.uniform(0.1, 2.0e5, n)
+    th = rng.uniform(0.0, math.pi, n)
+    rho = rng.uniform(1.0, 5.79, n)
+    a = np.maximum(port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, size, rho, th), 0.05)
+    exact = port.read_margins(a)
+    bound = sharding.halo_bound_params(size, lut)
+    assert all(b >= e for b, e in zip(bound, exact))
+    from paper_1003_2022_b200 import elongation_bound3
+    rho3 = 1.0 + (np.minimum(elongation_bound3(th), 40.0) - 1.0) * rng.uniform(0.0, 0.95, n)
+    a3 = np.maximum(port3.scales3_from_params(size, rho3, th), 0.05)
+    assert sharding.reach3_bound_params(size) >= port3.support3(a3)[1]
