@@ -3,21 +3,28 @@
 // (pkg/src/rubs/engine.py:265-324).
 //
 // Design (DESIGN.md has the full story):
-//   * The output domain is cut into 32x32 tiles (16x16 cells for the margin
-//     pre-pass).  Every tile pre-integrates ITS OWN region -- the tile grown
-//     by the read margins of its own pixels -- in shared memory, with the
-//     running sums restarted at the region edge.  This is exact: the filter
-//     is linear and zero-padded, so cropping f to the region changes nothing
-//     for the tile's pixels, and restarting a sweep on a rectangle only adds
-//     ridge functions (constant along one of the four box directions) that
-//     the 16-vertex finite difference annihilates.  No canvas widening
-//     (engine.py:177) is needed and the sums stay O(region^4) instead of
-//     O(image^4), which is what keeps every config inside 1e-9.
+//   * The output domain is cut into 64x32 tiles (wide_filter_kernel, two CTAs
+//     per SM).  Every tile pre-integrates ITS OWN region -- the tile grown by
+//     the read margins of its own pixels -- in shared memory (TMA loads), with
+//     the running sums restarted at the region edge.  This is exact: the
+//     filter is linear and zero-padded, so cropping f to the region changes
+//     nothing for the tile's pixels, and restarting a sweep on a rectangle
+//     only adds ridge functions (constant along one of the four box
+//     directions) that the 16-vertex finite difference annihilates.  No
+//     canvas widening (engine.py:177) is needed and the sums stay
+//     O(region^4) instead of O(image^4), which is what keeps every config
+//     inside 1e-9.  A tile whose region is too large or too ill-conditioned
+//     is split into smaller units, down to 8x8 cells.
 //   * The four sweeps (engine.py:186-193) run in shared memory, one thread
 //     per row / diagonal / column / anti-diagonal.
 //   * Each pixel then takes its 16-vertex finite difference (engine.py:232-244)
 //     reading the region through the 7-tap ZP interpolant (zp.py:186-228) in
-//     one canonical-wedge form (rubs_device.cuh: zp_read8).
+//     one canonical-wedge form (zp_read8).
+//   * Cells whose regions exceed the shared memory are deferred: planned on
+//     the device (plan_* kernels) into the 225 KB shared-memory overflow pass
+//     or into power-of-two blocks whose regions live in global scratch
+//     (big_fill_rs1 / big_rs234 or the line sweeps / big_gather); pixels
+//     whose own precision budget fails go to a per-pixel pass.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
