@@ -249,3 +249,19 @@ def test_kernel_wider_than_the_region_buffer_fails_loudly(cuda):
     out = rb.filter_space_variant3(f, np.array([3000.0, 1.0, 1.0]))  # fits
     ref = oracle.dense3(f, np.array([3000.0, 1.0, 1.0]))
     assert np.abs(out - ref).max() < 1e-9 * np.abs(ref).max()
+
+
+def test_params_path_two_passes(cuda, rng):
+    """Fused N=3 mapping with iterated passes (global reach from the mapped
+    field, edge-clamped canvases) against the exact two-pass oracle."""
+    H, W = 36, 40
+    f = rng.random((H, W))
+    s = smooth_random_field(rng, (H, W), 2.0, 120.0)
+    th = rng.uniform(0.0, math.pi, (H, W))
+    rho = 1.0 + (0.9 * np.minimum(rb.elongation_bound3(th), 8.0) - 1.0) * rng.random((H, W))
+    ref = oracle.dense3(f, port3.scales3_from_params(s, rho, th), 2)
+    got = rb.filter_space_variant3_params(f, s, rho, th, iterations=2)
+    assert rel_err(got, ref) < REL_TOL
+    dev = rb.filter_space_variant3_params(cuda.from_numpy(f).cuda(), *(cuda.from_numpy(v).cuda() for v in (s, rho, th)),
+                                          iterations=2)
+    assert np.array_equal(dev.cpu().numpy(), got)
