@@ -177,3 +177,47 @@ def default_lut() -> ScaleLut:
     if "lut" not in _DEFAULT:
         _DEFAULT["lut"] = build_lut()
     return _DEFAULT["lut"]
+
+
+# ---------------------------------------------------------------------------
+# Table files (the reference's save_lut / load_lut, solver.py:351-395):
+# magic "RUBS", then little-endian u32 version 1, n_rho, n_phi, the two grids
+# and the entries (n_rho, n_phi, 4) as little-endian f64, orientation
+# fastest, components innermost.  Written atomically.
+
+LUT_MAGIC = b"RUBS"
+LUT_VERSION = 1
+
+
+def save_lut(lut: ScaleLut, path) -> None:
+    import struct
+    from .pgmio import atomic_write_bytes
+    rg = np.asarray(lut.rho_grid, dtype="<f8")
+    pg = np.asarray(lut.phi_grid, dtype="<f8")
+    en = np.ascontiguousarray(lut.entries, dtype="<f8")
+    if en.shape != (rg.shape[0], pg.shape[0], 4):
+        raise ValueError("table entries must be (n_rho, n_phi, 4)")
+    atomic_write_bytes(path, LUT_MAGIC + struct.pack("<III", LUT_VERSION, rg.shape[0], pg.shape[0])
+                       + rg.tobytes() + pg.tobytes() + en.tobytes())
+
+
+def load_lut(path) -> ScaleLut:
+    import struct
+    with open(path, "rb") as fh:
+        data = fh.read()
+    if len(data) < 16 or data[:4] != LUT_MAGIC:
+        raise ValueError("not a scale lookup table (bad magic)")
+    version, n_rho, n_phi = struct.unpack_from("<III", data, 4)
+    if version != LUT_VERSION:
+        raise ValueError(f"unsupported table version {version}")
+    need = 16 + 8 * (n_rho + n_phi + 4 * n_rho * n_phi)
+    if len(data) != need:
+        raise ValueError(f"truncated table: {len(data)} bytes, expected {need}")
+    vals = np.frombuffer(data, "<f8", (need - 16) // 8, 16).astype(np.float64)
+    rho_grid, phi_grid = vals[:n_rho].copy(), vals[n_rho:n_rho + n_phi].copy()
+    entries = vals[n_rho + n_phi:].reshape(n_rho, n_phi, 4).copy()
+    if (np.diff(rho_grid) <= 0.0).any() or (np.diff(phi_grid) <= 0.0).any():
+        raise ValueError("table grids must be strictly increasing")
+    if not (np.isfinite(entries).all() and (entries > 0.0).all()):
+        raise ValueError("table entries must be positive and finite")
+    return ScaleLut(rho_grid, phi_grid, entries)

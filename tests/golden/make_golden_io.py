@@ -9,7 +9,10 @@ Recorded (pkg/src/rubs/pgmio.py, cli.py):
   * quantize on edge values;
   * `rubs filter` and `rubs adapt` outputs (.f64) for a small noisy stripe
     PGM (the reference test's recipe, test_io_cli.py:108-114), and the
-    exit codes of its failure cases.
+    exit codes of its failure cases;
+  * (lut_file.npz) the bytes `rubs lut-build` writes for an 8 x 6 table up
+    to elongation 4.5, the table it loads back, and `rubs lut-inspect`'s
+    report of it (solver.py:351-395, cli.py:142-176).
 """
 
 from __future__ import annotations
@@ -72,5 +75,24 @@ def main():
     np.savez_compressed(os.path.join(OUT, "io_cli.npz"), **g)
 
 
+def lut_file():
+    import contextlib
+    import io
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "t.lut")
+        assert cli.main(["lut-build", "--out", p, "--rho-points", "8", "--phi-points", "6",
+                         "--rho-max", "4.5"]) == 0
+        buf = io.StringIO()
+        with contextlib.redirect_stdout(buf):
+            assert cli.main(["lut-inspect", "--in", p]) == 0
+        from rubs import solver
+        lut = solver.load_lut(p)
+        np.savez_compressed(os.path.join(OUT, "lut_file.npz"),
+                            lut_bytes=np.frombuffer(open(p, "rb").read(), np.uint8),
+                            rho_grid=lut.rho_grid, phi_grid=lut.phi_grid, entries=lut.entries,
+                            inspect=np.array(buf.getvalue()))
+
+
 if __name__ == "__main__":
     main()
+    lut_file()

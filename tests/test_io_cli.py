@@ -127,3 +127,68 @@ def test_cli_filter_three_directions_and_bench(cuda, tmp_path, g, capsys):
     assert cli.main(["bench", "--n", "256", "--scales", "1,16,256", "--runs", "2"]) == 0
     out = capsys.readouterr().out
     assert "size_s\tmean_s" in out and "max/min mean ratio" in out
+
+
+# --- lookup-table files (solver.save_lut / load_lut, cli lut-build / lut-inspect)
+
+
+def test_lut_file_round_trip_matches_reference_bytes(tmp_path):
+    from paper_1003_2022_b200 import solver
+    g = golden("lut_file.npz")
+    p = tmp_path / "ref.lut"
+    p.write_bytes(g["lut_bytes"].tobytes())
+    lut = solver.load_lut(p)
+    assert np.array_equal(lut.rho_grid, g["rho_grid"]) and np.array_equal(lut.phi_grid, g["phi_grid"])
+    assert np.array_equal(lut.entries, g["entries"])
+    q = tmp_path / "ours.lut"
+    solver.save_lut(lut, q)
+    assert q.read_bytes() == p.read_bytes()
+    # lut-build here: the same table to the host solver's accuracy
+    r = tmp_path / "built.lut"
+    assert cli.main(["lut-build", "--out", str(r), "--rho-points", "8", "--phi-points", "6",
+                     "--rho-max", "4.5"]) == 0
+    built = solver.load_lut(r)
+    assert np.array_equal(built.rho_grid, g["rho_grid"])
+    assert np.abs(built.entries - g["entries"]).max() < 1e-13
+
+
+def test_lut_file_errors(tmp_path):
+    from paper_1003_2022_b200 import solver
+    g = golden("lut_file.npz")
+    good = g["lut_bytes"].tobytes()
+    cases = [b"XXXX" + good[4:], good[:4] + (2).to_bytes(4, "little") + good[8:], good[:-8]]
+    bad_grid = bytearray(good)
+    bad_grid[16:24] = bad_grid[24:32]  # rho_grid[0] == rho_grid[1]
+    cases.append(bytes(bad_grid))
+    for i, body in enumerate(cases):
+        p = tmp_path / f"bad{i}.lut"
+        p.write_bytes(body)
+        with pytest.raises(ValueError):
+            solver.load_lut(p)
+    assert cli.main(["lut-inspect", "--in", str(tmp_path / "missing.lut")]) == 4
+    assert cli.main(["lut-inspect", "--in", str(tmp_path / "bad0.lut")]) == 5
+
+
+@pytest.mark.gpu
+def test_lut_inspect_and_adapt_with_a_table_file(cuda, tmp_path, g, capsys):
+    from paper_1003_2022_b200 import default_lut, solver
+    lg = golden("lut_file.npz")
+    p = tmp_path / "ref.lut"
+    p.write_bytes(lg["lut_bytes"].tobytes())
+    assert cli.main(["lut-inspect", "--in", str(p)]) == 0
+    ours = capsys.readouterr().out.splitlines()
+    ref = str(lg["inspect"]).splitlines()
+    assert ours[:3] == ref[:3]  # table size, elongation and orientation ranges
+    assert float(ours[3].split(":")[1]) < 1e-12 and float(ref[3].split(":")[1]) < 1e-12
+    num = lambda line: np.array([float(v) for v in line.split("[")[1].rstrip("]").split()])  # noqa: E731
+    assert np.abs(num(ours[4]) - num(ref[4])).max() < 1e-12
+    # adapt with the default table written to a file == adapt with the default table
+    t = tmp_path / "default.lut"
+    solver.save_lut(default_lut(), t)
+    src = tmp_path / "in.pgm"
+    src.write_bytes(g["cli_in"].tobytes())
+    a, b = tmp_path / "a.f64", tmp_path / "b.f64"
+    assert cli.main(["adapt", "--in", str(src), "--out", str(a), "--noise-sigma", "10"]) == 0
+    assert cli.main(["adapt", "--in", str(src), "--out", str(b), "--noise-sigma", "10", "--lut", str(t)]) == 0
+    from paper_1003_2022_b200 import pgmio
+    assert np.array_equal(pgmio.read_raw_plane(a), pgmio.read_raw_plane(b))
