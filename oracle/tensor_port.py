@@ -116,6 +116,12 @@ def stripe_image(shape=(160, 160), period=8.0, angle=0.3, contrast=1.0):
     return (0.5 * contrast) * (np.sin(2.0 * math.pi * phase / period) + 1.0)
 
 
+def add_gaussian_noise(image, target_psnr_db, peak=1.0, seed=0):
+    """oracle.py:366-372 (white noise sized for a target PSNR)."""
+    sigma = peak / 10.0 ** (target_psnr_db / 20.0)
+    return image + np.random.default_rng(seed).normal(0.0, sigma, size=np.shape(image))
+
+
 def psnr(reference, estimate, peak=1.0):
     """oracle.py:375-383."""
     mse = float(np.mean((np.asarray(reference, float) - np.asarray(estimate, float)) ** 2))

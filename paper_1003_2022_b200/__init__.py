@@ -28,6 +28,7 @@ from .engine import (
     scales3_many,
     lookup_many,
     preintegrate,
+    thread_cap,
 )
 from .geometry import (
     MIN_ELONGATION_BOUND,
@@ -83,5 +84,6 @@ __all__ = [
     "optimize_scale_vector",
     "preintegrate",
     "sigma_to_size",
+    "thread_cap",
     "__version__",
 ]

@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass
 from typing import NamedTuple
 
@@ -89,6 +90,22 @@ class IntegratedImage:
     plane: np.ndarray
     col0: int = 0
     row0: int = 0
+
+
+def thread_cap() -> int:
+    """Worker cap from RUBS_THREADS, validated as the reference does
+    (engine.py:128-142): unset or 0 means automatic, a negative or
+    non-integer value raises ValueError.  The device path is deterministic
+    for any value (one launch geometry per shape), so the cap only
+    documents the caller's intent; the CPU side here is single-threaded."""
+    raw = os.environ.get("RUBS_THREADS", "0")
+    try:
+        cap = int(raw)
+    except ValueError:
+        raise ValueError(f"RUBS_THREADS must be an integer, got {raw!r}") from None
+    if cap < 0:
+        raise ValueError(f"RUBS_THREADS must be >= 0, got {cap}")
+    return cap
 
 
 # ---------------------------------------------------------------------------

@@ -30,6 +30,18 @@ def test_field_shape_validated():
         rb.filter_space_variant(np.ones((4, 4)), np.ones(3))
 
 
+def test_thread_cap_env(monkeypatch):
+    # test_engine.py:180-187
+    monkeypatch.delenv("RUBS_THREADS", raising=False)
+    assert rb.thread_cap() == 0
+    monkeypatch.setenv("RUBS_THREADS", "4")
+    assert rb.thread_cap() == 4
+    for bad in ("junk", "-1"):
+        monkeypatch.setenv("RUBS_THREADS", bad)
+        with pytest.raises(ValueError):
+            rb.thread_cap()
+
+
 def test_uniform_nonfinite_rejected():
     with pytest.raises(ValueError):
         rb.filter_space_variant(np.ones((4, 4)), [1.0, np.nan, 1.0, 1.0])
