@@ -241,6 +241,25 @@ def test_acceptance_07_gaussian_correlation_of_the_device_kernel(cuda):
                 assert abs(mass - 1.0) < 0.02 and np.abs(cov - c).max() < 0.01 * np.abs(c).max() + 0.3
 
 
+def test_acceptance_08_l2_error_decreases_with_passes(cuda):
+    # test_acceptance.py:183-189 on the device: more passes of a / sqrt(m)
+    # move the discrete kernel strictly closer to its Gaussian limit
+    # (the reference engine: 0.0208, 0.0072, 0.0045, 0.0034 for m = 1..4)
+    n = 161
+    f = np.zeros((n, n))
+    f[n // 2, n // 2] = 1.0
+    y, x = np.mgrid[: n, : n].astype(float) - n // 2
+    a = 4.0 * np.array([1.5, 1.0, 2.0, 1.2])
+    c = rb.covariance_of(a)
+    ci = np.linalg.inv(c)
+    g = np.exp(-0.5 * (ci[0, 0] * x * x + 2.0 * ci[0, 1] * x * y + ci[1, 1] * y * y))
+    g /= 2.0 * math.pi * math.sqrt(np.linalg.det(c))
+    errs = [math.sqrt(float(((rb.filter_space_invariant(f, a, iterations=m) - g) ** 2).sum()))
+            for m in (1, 2, 3, 4)]
+    assert all(later < earlier for earlier, later in zip(errs, errs[1:])), errs
+    assert errs[0] < 0.025 and errs[-1] < 0.004, errs
+
+
 # --- ZP interpolation and global pre-integration (API parity) --------------
 
 
