@@ -1741,6 +1741,7 @@ struct Scratch {
   size_t list_cap = 0;
   double *d_big = nullptr;
   size_t big_cap = 0;
+  int64_t big_budget = 0;  // batch budget the scratch was sized for (0: none yet)
   BigRegion *d_regs = nullptr;
   size_t regs_cap = 0;
   BigTile *d_btiles = nullptr;
@@ -2256,15 +2257,13 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   // Batches of blocks under a scratch budget.  A batch's kernels follow the
   // previous batch's in stream order, so the scratch is reused without a
   // host sync; region / tile lists of all batches are uploaded once.
-  // The budget is capped at half the free device memory (the scratch is kept
-  // for later calls) and quartered on an allocation failure.
-  int64_t budget = kBigBatch;
-  {
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess)
-      budget = std::min<int64_t>(budget, (int64_t)((free_b + t_scr.big_cap * sizeof(double)) / 2 /
-                                                   sizeof(double)));
-  }
+  // When the scratch has to grow, the budget is capped at half the free
+  // device memory (the scratch is kept for later calls; the cap is
+  // remembered, so steady-state calls skip cudaMemGetInfo, which measured
+  // 1-13 ms of host time with the GPU idle) and quartered on an allocation
+  // failure.
+  int64_t budget = t_scr.big_budget > 0 ? t_scr.big_budget : kBigBatch;
+  bool capped = false;
   struct Batch {
     int r0, r1, t0, t1;
     int64_t used;
@@ -2321,6 +2320,18 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
     regs.push_back(g);
   }
   close_batch();
+  hc.lap("regions");
+  if (max_used > (int64_t)t_scr.big_cap && !capped) {
+    capped = true;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+      const int64_t cap = (int64_t)((free_b + t_scr.big_cap * sizeof(double)) / 2 / sizeof(double));
+      if (cap < budget) {
+        budget = std::max<int64_t>(cap, kBigMinBatch);
+        goto replan;
+      }
+    }
+  }
   if (max_used > (int64_t)t_scr.big_cap) {
     if (t_scr.d_big) cudaFree(t_scr.d_big);
     t_scr.d_big = nullptr;
@@ -2333,7 +2344,9 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
     }
     RUBS_CUDA_TRY(e);
     t_scr.big_cap = (size_t)max_used;
+    t_scr.big_budget = budget;
   }
+  hc.lap("scratch");
   if ((rc = upload(regs, t_scr.d_regs, t_scr.regs_cap, s))) return rc;
   if ((rc = upload(cm, t_plan.d_cm, t_plan.cm_cap, s))) return rc;
   if ((rc = upload(cm_cell, t_plan.d_cm_cell, t_plan.cmc_cap, s))) return rc;
