@@ -1139,95 +1139,94 @@ __global__ void __launch_bounds__(NT, CT)
   //      budget, else split the longer side recursively down to 8 x 8
   //      cells; a cell that still fails sends its 32 x 32 half of the tile
   //      (a tile of the overflow launches' 32-pixel grid) to the overflow pass.
-  //      A node's region contains each of its cells' regions, so if no cell
-  //      fits alone, no node does: warp 0 checks the cells in parallel first
-  //      and skips the (single-thread) split tree for such tiles -- on
-  //      config 5 the tree was 2/3 of this kernel's time.
-  static_assert(NCX * NCY == 32, "one lane per cell");
-  __shared__ unsigned s_nofit;  // all in-domain cells (no cell fits), or 0
+  //      The split rule depends only on a node's shape, so the tree is
+  //      fixed: 8x4 -> 4x4 -> 2x4 -> 2x2 -> 1x2 -> 1x1 cells.  Warp 0 plans
+  //      it with one lane per cell: node aggregates by butterfly max over
+  //      the lanes of each level's node, and a node becomes a unit iff it
+  //      fits and no ancestor does (exactly the depth-first split's units;
+  //      only their order differs, which no result depends on).  The
+  //      single-thread tree walk this replaces was ~6 % of the kernel's
+  //      stall samples on large kernels (config 3n4), every other warp
+  //      waiting at the barrier.
+  static_assert(NCX == 8 && NCY == 4, "one lane per cell, fixed split tree");
   if (warp == 0) {
-    const int cx = lane % NCX, cy = lane / NCX;
-    const int sx = x0 + 8 * cx, sy = y0 + 8 * cy;
-    const bool in = sx < D.pw && sy < D.ph;
-    bool fit = false;
-    if (in) {
-      const int sw = min(8, D.pw - sx), sh = min(8, D.ph - sy);
-      const int RW = sw + s_cm[lane][0] + s_cm[lane][1], RH = sh + s_cm[lane][2] + s_cm[lane][3];
-      const float mn = (float)min(RW + 1, RH);
-      const float l4 = 0.25f * (float)(RW + 1) * (float)RH * mn * mn;
-      fit = region_elems(RW + 1, RH) <= region_cap && s_cw[lane] * l4 <= kPrecisionBudget;
-    }
-    const unsigned inb = __ballot_sync(0xffffffffu, in), fitb = __ballot_sync(0xffffffffu, fit);
-    if (lane == 0) s_nofit = fitb ? 0u : inb;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int n = 0;
-    unsigned ovf_cells = s_nofit;  // bit cy * NCX + cx
-    int stk[16][4];
-    int sp = 0;
-    if (!ovf_cells) {
-      stk[sp][0] = 0; stk[sp][1] = 0; stk[sp][2] = NCX; stk[sp][3] = NCY; ++sp;
-    }
-    while (sp > 0) {
-      --sp;
-      const int cx0 = stk[sp][0], cy0 = stk[sp][1], ncx = stk[sp][2], ncy = stk[sp][3];
+    constexpr int kLv = 6;  // leaf (1x1) first
+    constexpr int kLw[kLv] = {1, 1, 2, 2, 4, 8}, kLh[kLv] = {1, 2, 2, 4, 4, 4};
+    constexpr int kXor[kLv] = {0, 8, 1, 16, 2, 4};  // lane = cy * 8 + cx
+    const int cx = lane & 7, cy = lane >> 3;
+    // a node's fit test (as the tree walk did it): region within the
+    // buffer and the precision budget met
+    auto node = [&](int L, const int *u, float wm, int *d) -> bool {
+      const int cx0 = cx & ~(kLw[L] - 1), cy0 = cy & ~(kLh[L] - 1);
       const int sx = x0 + 8 * cx0, sy = y0 + 8 * cy0;
-      if (sx >= D.pw || sy >= D.ph) continue;
-      const int sw = min(8 * ncx, D.pw - sx), sh = min(8 * ncy, D.ph - sy);
-      int u[4] = {0, 0, 0, 0};
-      float wm = 0.f;
-      for (int cy = cy0; cy < cy0 + ncy; ++cy)
-        for (int cx = cx0; cx < cx0 + ncx; ++cx) {
-          const int c = cy * NCX + cx;
-          for (int j = 0; j < 4; ++j) u[j] = max(u[j], s_cm[c][j]);
-          wm = fmaxf(wm, s_cw[c]);
-        }
+      if (sx >= D.pw || sy >= D.ph) return false;
+      const int sw = min(8 * kLw[L], D.pw - sx), sh = min(8 * kLh[L], D.ph - sy);
       const int RW = sw + u[0] + u[1], RH = sh + u[2] + u[3];
       const float mn = (float)min(RW + 1, RH);
       const float l4 = 0.25f * (float)(RW + 1) * (float)RH * mn * mn;
-      if (region_elems(RW + 1, RH) <= region_cap && wm * l4 <= kPrecisionBudget) {
-        int *d = s_unit[n++];
-        d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
-        continue;
-      }
-      if (ncx * ncy == 1) {
-        // a cell that still fails goes to the overflow pass; the rest of
-        // the tile keeps its (smaller, better-conditioned) units
-        ovf_cells |= 1u << (cy0 * NCX + cx0);
-        continue;
-      }
-      if (ncx >= ncy) {
-        const int h = ncx >> 1;
-        stk[sp][0] = cx0; stk[sp][1] = cy0; stk[sp][2] = h; stk[sp][3] = ncy; ++sp;
-        stk[sp][0] = cx0 + h; stk[sp][1] = cy0; stk[sp][2] = ncx - h; stk[sp][3] = ncy; ++sp;
-      } else {
-        const int h = ncy >> 1;
-        stk[sp][0] = cx0; stk[sp][1] = cy0; stk[sp][2] = ncx; stk[sp][3] = h; ++sp;
-        stk[sp][0] = cx0; stk[sp][1] = cy0 + h; stk[sp][2] = ncx; stk[sp][3] = ncy - h; ++sp;
-      }
-    }
-    if (ovf_cells) {
-      // one record per 32 x 32 half with deferred cells (the overflow
-      // passes work on the 32-pixel grid), margins and w over those cells
-      for (int h = 0; h < 2; ++h) {
-        OvfRec r;
-        r.tile = ty * tiles_x32 + 2 * tx + h;
-        r.m[0] = r.m[1] = r.m[2] = r.m[3] = 0;
-        r.w = 0.f;
-        r.mask = 0;
-        for (int cy = 0; cy < NCY; ++cy)
-          for (int cx = 4 * h; cx < 4 * h + 4; ++cx) {
-            const int c = cy * NCX + cx;
-            if (!((ovf_cells >> c) & 1u)) continue;
-            r.mask |= 1u << (cy * 4 + (cx - 4 * h));
-            for (int j = 0; j < 4; ++j) r.m[j] = max(r.m[j], s_cm[c][j]);
-            r.w = fmaxf(r.w, s_cw[c]);
-          }
-        if (r.mask) reinterpret_cast<OvfRec *>(ovf_list)[atomicAdd(&st->ovf_count, 1)] = r;
+      d[0] = sx; d[1] = sy; d[2] = sw; d[3] = sh; d[4] = u[0]; d[5] = u[2]; d[6] = RW; d[7] = RH;
+      return region_elems(RW + 1, RH) <= region_cap && wm * l4 <= kPrecisionBudget;
+    };
+    int u[4], d[8];
+    float wm;
+    unsigned fitm = 0;  // bit L: this lane's level-L node fits
+#pragma unroll
+    for (int pass = 0; pass < 2; ++pass) {
+      // pass 0 finds the levels that fit; pass 1 rebuilds the aggregates of
+      // the topmost fitting level (all lanes take part in the shuffles)
+      const int top = fitm ? 31 - __clz(fitm) : -1;
+      for (int j = 0; j < 4; ++j) u[j] = s_cm[lane][j];
+      wm = s_cw[lane];
+#pragma unroll
+      for (int L = 0; L < kLv; ++L) {
+        if (L > 0) {
+          for (int j = 0; j < 4; ++j) u[j] = max(u[j], __shfl_xor_sync(0xffffffffu, u[j], kXor[L]));
+          wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, kXor[L]));
+        }
+        if (pass == 0) {
+          int dd[8];
+          if (node(L, u, wm, dd)) fitm |= 1u << L;
+        } else if (L == top) {
+          node(L, u, wm, d);
+        }
       }
     }
-    s_nu = n;
+    const int top = fitm ? 31 - __clz(fitm) : -1;
+    // the unit is written by its node's first lane
+    const bool writer =
+        top >= 0 && cx == (cx & ~(kLw[top] - 1)) && cy == (cy & ~(kLh[top] - 1));
+    const unsigned wb = __ballot_sync(0xffffffffu, writer);
+    if (writer) {
+      int *dst = s_unit[__popc(wb & ((1u << lane) - 1u))];
+      for (int j = 0; j < 8; ++j) dst[j] = d[j];
+    }
+    // a cell no node fits goes to the overflow pass; the rest of the tile
+    // keeps its (smaller, better-conditioned) units
+    const bool in = x0 + 8 * cx < D.pw && y0 + 8 * cy < D.ph;
+    const unsigned ovf_cells = __ballot_sync(0xffffffffu, in && top < 0);
+    if (lane == 0) {
+      if (ovf_cells) {
+        // one record per 32 x 32 half with deferred cells (the overflow
+        // passes work on the 32-pixel grid), margins and w over those cells
+        for (int h = 0; h < 2; ++h) {
+          OvfRec r;
+          r.tile = ty * tiles_x32 + 2 * tx + h;
+          r.m[0] = r.m[1] = r.m[2] = r.m[3] = 0;
+          r.w = 0.f;
+          r.mask = 0;
+          for (int ccy = 0; ccy < NCY; ++ccy)
+            for (int ccx = 4 * h; ccx < 4 * h + 4; ++ccx) {
+              const int c = ccy * NCX + ccx;
+              if (!((ovf_cells >> c) & 1u)) continue;
+              r.mask |= 1u << (ccy * 4 + (ccx - 4 * h));
+              for (int j = 0; j < 4; ++j) r.m[j] = max(r.m[j], s_cm[c][j]);
+              r.w = fmaxf(r.w, s_cw[c]);
+            }
+          if (r.mask) reinterpret_cast<OvfRec *>(ovf_list)[atomicAdd(&st->ovf_count, 1)] = r;
+        }
+      }
+      s_nu = __popc(wb);
+    }
   }
   __syncthreads();
 
