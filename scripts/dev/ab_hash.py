@@ -24,7 +24,15 @@ add("4", lambda: rb.filter_space_variant_params(f4, *p4, iterations=2))
 w = workloads.config5(8192, 8192, device=dev, param_dtype=torch.float32, image_device=dev)
 f5 = torch.as_tensor(w["f"]).to(dev); p5 = [w["size"], w["elong"], w["orient"]]
 add("5@8192", lambda: rb.filter_space_variant_params(f5, *p5))
+wa = workloads.adaptive_image()
+fa = torch.as_tensor(wa["f"]).to(dev)
+add("A", lambda: rb.adaptive_smooth(fa, wa["noise_sigma"]))
+fc = torch.full((1024, 1024), 0.3, dtype=torch.float64, device=dev)
+add("A-flat", lambda: rb.adaptive_smooth(fc, 0.1))
+only = sys.argv[1].split(",") if len(sys.argv) > 1 else None
 for name, fn in runs.items():
+    if only and name not in only:
+        continue
     out = fn()
     torch.cuda.synchronize()
     h = hashlib.sha1(out.double().cpu().numpy().tobytes()).hexdigest()[:16]
