@@ -419,14 +419,14 @@ WORKLOADS = {
 }
 # From the committed ncu captures of the primary kernel (wide_filter_kernel)
 # on config 2 (profiles/ncu_r01_final_summary.md; wavefronts and traffic
-# re-measured in profiles/ncu_r01b_summary.md): fp64 instructions executed
+# re-measured in profiles/ncu_r01b_summary.md, final build): fp64 instructions executed
 # per output pixel (DADD + DFMA + DMUL + DSETP, thread level), shared-memory
 # wavefronts per output pixel, and DRAM bytes per launch
 # (dram__bytes_read.sum + dram__bytes_write.sum).
 # Config 3 (N=3, n3_tile_kernel): profiles/ncu_r01b_summary.md.
 DP_INST_PER_PX = {"2": 602, "3": 2147}
-SMEM_WF_PER_PX = {"2": 16.43, "3": 53.9}
-TRAFFIC_PER_LAUNCH = {"2": 104.32e6, "3": 1.588e9}
+SMEM_WF_PER_PX = {"2": 16.39, "3": 53.9}
+TRAFFIC_PER_LAUNCH = {"2": 105.45e6, "3": 1.588e9}
 
 
 # ---------------------------------------------------------------------------
