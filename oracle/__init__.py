@@ -55,16 +55,8 @@ def dense_cuda(f, field, rows=None, cols=None):
     """Exact dense filter (one pass) on the GPU: output rows x cols (ranges,
     default the whole image) of the H x W image ``f``; inputs numpy or torch.
     Same kernel geometry as ``dense`` (dense_oracle_cuda.cu)."""
-    global _cuda_lib
     import torch
-    if _cuda_lib is None:
-        if not os.path.exists(_CUDA_LIB_PATH):
-            subprocess.run(["make", "-s", "-C", _HERE, "cuda"], check=True)
-        L = ctypes.CDLL(_CUDA_LIB_PATH)
-        vp, i = ctypes.c_void_p, ctypes.c_int
-        L.rubs_oracle_cuda_dense.restype = i
-        L.rubs_oracle_cuda_dense.argtypes = [vp, i, i, vp, i, i, i, i, i, vp]
-        _cuda_lib = L
+    _cuda()
     ft = torch.as_tensor(f).to("cuda", torch.float64).contiguous()
     fl = torch.as_tensor(field).to("cuda", torch.float64).contiguous()
     H, W = ft.shape
@@ -77,6 +69,83 @@ def dense_cuda(f, field, rows=None, cols=None):
                                           r1 - r0, c1 - c0, ctypes.c_void_p(out.data_ptr()))
     if rc:
         raise RuntimeError(f"oracle cuda error {rc}")
+    return out
+
+
+def _cuda():
+    global _cuda_lib
+    if _cuda_lib is None:
+        if not os.path.exists(_CUDA_LIB_PATH):
+            subprocess.run(["make", "-s", "-C", _HERE, "cuda"], check=True)
+        L = ctypes.CDLL(_CUDA_LIB_PATH)
+        vp, i = ctypes.c_void_p, ctypes.c_int
+        L.rubs_oracle_cuda_dense.restype = i
+        L.rubs_oracle_cuda_dense.argtypes = [vp, i, i, vp, i, i, i, i, i, vp]
+        L.rubs_oracle_cuda_points.restype = i
+        L.rubs_oracle_cuda_points.argtypes = [vp, i, i, i, vp, ctypes.c_double, vp, i, vp]
+        _cuda_lib = L
+    return _cuda_lib
+
+
+def points_cuda(f, field, pts, div=1.0):
+    """Exact one-pass output at lattice points pts = (n, 2) [row, col] on
+    the GPU (dense_oracle_cuda.cu points_kernel): ``f`` is the H x W image
+    (torch f32 / f64, any device, zero outside), ``field`` the (n, 4) RAW
+    scale-vectors of the points (floored at 0.05, then divided by ``div`` =
+    sqrt(iterations), as in dense_oracle.c field_at).  Points may lie
+    outside the image (intermediate passes).  Returns numpy (n,)."""
+    import torch
+    ft = torch.as_tensor(f)
+    if ft.dtype not in (torch.float32, torch.float64):
+        ft = ft.double()
+    ft = ft.to("cuda").contiguous()
+    H, W = ft.shape
+    fl = torch.as_tensor(np.ascontiguousarray(field, np.float64).reshape(-1, 4)).to("cuda")
+    pt = torch.as_tensor(np.ascontiguousarray(pts, np.int64).reshape(-1, 2)).to("cuda")
+    n = pt.shape[0]
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    rc = _cuda().rubs_oracle_cuda_points(ctypes.c_void_p(ft.data_ptr()), int(ft.dtype == torch.float32),
+                                         H, W, ctypes.c_void_p(fl.data_ptr()), float(div),
+                                         ctypes.c_void_p(pt.data_ptr()), n, ctypes.c_void_p(out.data_ptr()))
+    if rc:
+        raise RuntimeError(f"oracle cuda error {rc}")
+    return out.cpu().numpy()
+
+
+def support_radius(a):
+    """(rx, ry) of dense_oracle.c support_radius for PREPARED vectors a (n, 4)."""
+    a = np.asarray(a, np.float64).reshape(-1, 4)
+    diag = (a[:, 1] + a[:, 3]) / np.sqrt(2.0)
+    return (np.ceil(0.5 * (a[:, 0] + diag)).astype(np.int64) + 1,
+            np.ceil(0.5 * (a[:, 2] + diag)).astype(np.int64) + 1)
+
+
+def points2_cuda(f, field_of, pts):
+    """Exact TWO-pass output (iterations=2: dense_oracle.c passp_at, the
+    reference's oracle.py:205-241 semantics) at pixels pts (n, 2).
+    ``field_of(rows, cols)`` returns the raw (k, 4) scale-vectors at image
+    pixels (already edge-clamped indices are passed).  Pass 1 is evaluated
+    on the GPU at every lattice point of the union window of the points'
+    pass-2 supports (edge-clamped field, zero-padded image); pass 2 sums
+    exact kernel values times those on the host."""
+    f_t = f
+    H, W = int(f_t.shape[0]), int(f_t.shape[1])
+    pts = np.asarray(pts, np.int64).reshape(-1, 2)
+    div = np.sqrt(2.0)
+    a2 = np.maximum(np.asarray(field_of(pts[:, 0], pts[:, 1]), np.float64), 0.05) / div
+    rx, ry = support_radius(a2)
+    r0, r1 = int((pts[:, 0] - ry).min()), int((pts[:, 0] + ry).max())
+    c0, c1 = int((pts[:, 1] - rx).min()), int((pts[:, 1] + rx).max())
+    rr, cc = np.mgrid[r0:r1 + 1, c0:c1 + 1]
+    q = np.stack([rr.ravel(), cc.ravel()], axis=1)
+    fq = field_of(np.clip(q[:, 0], 0, H - 1), np.clip(q[:, 1], 0, W - 1))
+    p1 = points_cuda(f_t, fq, q, div).reshape(rr.shape)
+    out = np.empty(len(pts))
+    for i, (r, c) in enumerate(pts):
+        ys = np.arange(r - ry[i], r + ry[i] + 1)
+        xs = np.arange(c - rx[i], c + rx[i] + 1)
+        k = kernel_values(a2[i], (c - xs)[None, :].astype(np.float64), (r - ys)[:, None].astype(np.float64))
+        out[i] = float((k * p1[ys[0] - r0:ys[-1] - r0 + 1, xs[0] - c0:xs[-1] - c0 + 1]).sum())
     return out
 
 

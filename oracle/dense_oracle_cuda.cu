@@ -96,6 +96,56 @@ __global__ void dense_kernel(const double *f, int H, int W, const double *field,
   }
 }
 
+
+// One CTA per query point: the exact one-pass output at lattice point
+// (row, col) (which may lie outside the image: iterated passes evaluate the
+// intermediate on extended canvases), the point's own raw scale-vector
+// floored at 0.05 and divided by div = sqrt(iterations).  The image is f32
+// or f64 (zero outside).  The taps of the support window are split over the
+// CTA's threads and summed by a fixed-order tree: deterministic.  Used for
+// the BASELINE-size samples of configs 4 and 5 (tests/test_gpu_fullsize.py),
+// where one point's support holds up to ~10^6 taps.
+__global__ void __launch_bounds__(256) points_kernel(const void *f, int f32, int H, int W,
+                                                     const double *field, double div,
+                                                     const int64_t *pts, int n, double *out) {
+  __shared__ double red[256];
+  for (int p = blockIdx.x; p < n; p += gridDim.x) {
+    const int row = (int)pts[2 * p], col = (int)pts[2 * p + 1];
+    double a[4];
+    for (int k = 0; k < 4; ++k) {
+      const double v = field[4 * p + k];
+      a[k] = (v < 0.05 ? 0.05 : v) / div;
+    }
+    const double diag = (a[1] + a[3]) / SQRT2;
+    const int rx = (int)ceil(0.5 * (a[0] + diag)) + 1;
+    const int ry = (int)ceil(0.5 * (a[2] + diag)) + 1;
+    const int r0 = max(0, row - ry), r1 = min(H - 1, row + ry);
+    const int c0 = max(0, col - rx), c1 = min(W - 1, col + rx);
+    double acc = 0.0;
+    if (r1 >= r0 && c1 >= c0) {
+      const int nc = c1 - c0 + 1;
+      const int64_t nt = (int64_t)(r1 - r0 + 1) * nc;
+      for (int64_t t = threadIdx.x; t < nt; t += blockDim.x) {
+        const int r = r0 + (int)(t / nc), c = c0 + (int)(t % nc);
+        const double k = kernel_value(a, (double)(col - c), (double)(row - r));
+        if (k != 0.0) {
+          const int64_t i = (int64_t)r * W + c;
+          const double v = f32 ? (double)((const float *)f)[i] : ((const double *)f)[i];
+          acc += k * v;
+        }
+      }
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if ((int)threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) out[p] = red[0];
+    __syncthreads();
+  }
+}
+
 extern "C" {
 
 // Device pointers; one pass.  Returns 0 or a cudaError_t.
@@ -105,6 +155,19 @@ int rubs_oracle_cuda_dense(const double *f, int H, int W, const double *field, i
   if (n <= 0) return 0;
   const int grid = (int)((n + 127) / 128);
   dense_kernel<<<grid, 128>>>(f, H, W, field, uniform, r_lo, c_lo, rows, cols, out);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  return (int)e;
+}
+
+
+// Device pointers: f (H x W, f32 if f32 != 0 else f64), field (n x 4 raw
+// scale-vectors, one per point), pts (n x 2 int64 row, col), out (n).
+// Returns 0 or a cudaError_t.
+int rubs_oracle_cuda_points(const void *f, int f32, int H, int W, const double *field,
+                            double div, const int64_t *pts, int n, double *out) {
+  if (n <= 0) return 0;
+  points_kernel<<<n < 65535 ? n : 65535, 256>>>(f, f32, H, W, field, div, pts, n, out);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaDeviceSynchronize();
   return (int)e;
