@@ -2,40 +2,54 @@
 """Benchmark of the B200 space-variant filter path (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 2|1|4]
+                    [--config 5|2|1|3|3n4|4|A]
 
-One step = one filter pass over one synthetic image of the chosen
-BASELINE.json config (default: config 2, 2048^2 fp64 image, LUT-mapped
-smooth (size, elongation, orientation) fields in float32, one pass; the
-fused params path, i.e. rubs_b200_filter_params).  With N GPUs (torchrun)
-every rank filters its own image per step (weak scaling, no collective on
-the data path); value = all pixels / max-over-ranks device time.
+Default workload: BASELINE.json config 5 -- ONE 32768^2 float32 image,
+N=4 ZP box spline, sigma up to 256 (the largest configuration that runs on
+one GPU), LUT-mapped (size, elongation, orientation) fields in float32, one
+pass, fused params path (rubs_b200_filter_params).  One step = one filter
+of the whole image.
+  N = 1   the whole image on one GPU;
+  N > 1   the image is split into N row bands (sharding.RowBandPlan): each
+          rank exchanges halo rows with its neighbours over NCCL and filters
+          its band (strong scaling: the N ranks share one image per step).
+Config 4 is the 64-image batch: each rank filters its 64/N images per step
+(two passes each; weak in per-rank work, the batch is fixed).  Other
+configs: one image per rank per step (configs 3 with N=3 shard by row bands
+like config 5).
+
+``--gpus N`` with no torchrun environment re-launches itself under
+``torch.distributed.run`` with N processes (one per GPU); under torchrun,
+WORLD_SIZE must equal N.
 
 Printed JSON (rank 0, one line) carries the driver's keys plus
   e2e          the same metric through the public API with HOST buffers
-               (H2D of image + params and D2H of the result inside the
-               timed region; wall clock around calls that return only when
-               the result is on the host)
-  roofline     dominant kernel (wide_filter_kernel): algorithmic bytes per
-               launch / CUDA-event kernel time, against MEASURED_PEAKS.json
-  fp64         the same kernel against the fp64 pipe rate
-  smem         the same kernel against the shared-memory wavefront rate
-               (1 per SM per clock) -- with issue, the bounds that bind
-               (DESIGN.md)
+               (pinned H2D of every input and D2H of the result inside the
+               timed region; N > 1 row bands: each rank's band and halo rows
+               in, its band out)
+  roofline     the pass's filter kernels (primary tile kernel + the
+               deferred-tile passes, bracketed by CUDA events on the launch
+               stream): algorithmic bytes / that time, against
+               MEASURED_PEAKS.json; ``traffic`` = ncu DRAM bytes of the same
+               kernels (profiles/)
+  fp64, smem   the primary kernel against the fp64 pipe and shared-memory
+               wavefront rates (configs 2, 3: the bounds that bind there)
   cpu_baseline the reference algorithm (oracle/port.py, numpy) on a bounded
                sample of the same workload, all host cores, rank 0 at N=1
-  parity       (same CPU leg, as the checker) max relative error of the
-               GPU output at sampled pixels of the workload against the exact
+  parity       (same leg, as the checker) max relative error of the GPU
+               output at sampled pixels of the workload against the exact
                dense oracle -- BASELINE.json's "max rel err vs oracle"
-`--impl reference` prints the same line for the CPU port alone.
+`--impl reference` prints the same line for the CPU port alone (rank 0).
 """
 
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -49,21 +63,26 @@ if ROOT not in sys.path:
 
 METRIC = "Gpixel/s filtered"
 UNIT = "Gpixel/s"
-# Algorithmic bytes per output pixel for the fused path: f64 image (8) +
-# three f32 params (12) + f64 output (8) = 28.
+CONFIGS = ["5", "2", "1", "3", "3n4", "4", "A"]
+BATCH4 = 64  # config 4: images per step (all ranks together)
+# Algorithmic bytes per output pixel: image + per-pixel
+# parameters + f64 output, per pass (config 4: both passes, intermediate
+# ignored; config 1: the drop-in (H,W,4) f64 field).
 BYTES_PER_PX = {"2": 28, "1": 48, "3": 24, "3n4": 24, "4": 52, "5": 24, "A": 16}
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="2", choices=["1", "2", "3", "3n4", "4", "5", "A"])
+    p.add_argument("--config", default="5", choices=CONFIGS)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
-    return p.parse_args()
+    p.add_argument("--probe-launch", action="store_true",
+                   help="start the ranks, all-gather them, print one JSON line, exit (launcher test)")
+    return p.parse_args(argv)
 
 
 def dist_env():
@@ -71,6 +90,20 @@ def dist_env():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return rank, world, local
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch(args_n: int) -> int:
+    """Re-run this script under torch.distributed.run with N processes."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args_n}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def measured_peaks():
@@ -141,46 +174,229 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-def make_inputs(cfg: str, torch, device, copies: int, rank: int):
-    """Device-resident inputs (rotating copies so the working set of
-    consecutive steps exceeds L2) plus one host copy for the e2e leg."""
-    from paper_1003_2022_b200 import workloads
-    if cfg == "2":
-        w = workloads.config2(device=device, param_dtype=torch.float32)
-    elif cfg == "1":
-        w = workloads.config1()
-    elif cfg == "3":
-        w = workloads.config3_n3(device=device, param_dtype=torch.float32)
-        copies = 1  # inputs alone exceed L2
-    elif cfg == "3n4":
-        w = workloads.config3(device=device, param_dtype=torch.float32)
-        copies = 1
-    elif cfg == "5":
-        w = workloads.config5(device=device, param_dtype=torch.float32, image_device=device)
-        copies = 1
-    elif cfg == "A":
-        w = workloads.adaptive_image()
-        f = torch.as_tensor(w["f"]).to(device)
-        return w, [{"f": f.clone(), "adaptive": True} for _ in range(copies)]
+WORKLOADS = {
+    "5": "config5: 32768^2 fp32 uniform[0,1) (torch Philox seed 0); N=4 ZP; sigma [2,256] smooth, "
+         "rho [1,8] clamped to the LUT, smooth theta (LUT mapping fused, f32 params); one pass",
+    "3": "config3: 8192^2 fp32 rectangles + N(0,0.05^2) noise; N=3 directions (0/60/120 deg); "
+         "sigma [1,32], rho [1,6] clamped to 0.95 of the N=3 bound, smooth theta; exact N=3 path "
+         "(closed-form mapping fused, f32 params)",
+    "3n4": "config3 shapes with the N=4 ZP element: 8192^2 fp32 rectangles + N(0,0.05^2) noise; "
+           "sigma [1,32], rho [1,6] clamped, smooth theta (LUT mapping)",
+    "2": "config2: 2048^2 fp64 uniform[0,1) seed 0; N=4 ZP box spline; sigma [2,16], rho [1,4], "
+         "theta [0,pi) smooth fields (LUT mapping, f32 params)",
+    "1": "config1: 256^2 fp64 uniform[0,1) seed 0; sigma 2->8 along x, rho 1->3 radial, "
+         "theta=atan2 mod pi; exact optimiser field",
+    "4": "config4: batch of 64 4096^2 fp32 uniform[0,1) images (seeds 1000+i); sigma [2,24], rho [1,4], "
+         "smooth theta (per-image seeds); N=4 ZP applied twice (iterations=2)",
+    "A": "adaptive_smooth pipeline (tensor.py; SURVEY 8f): 2048^2 fp64 stripes + N(0,0.1^2), "
+         "noise_sigma 0.1, window 1.5; structure tensor (3 window filters), percentiles, anisotropy, "
+         "LUT filter of image and flat image, gain correction",
+}
+SHAPES = {"5": (32768, 32768), "3": (8192, 8192), "3n4": (8192, 8192), "2": (2048, 2048),
+          "1": (256, 256), "4": (4096, 4096), "A": (2048, 2048)}
+ITERS = {"4": 2}
+
+
+def row_banded(cfg: str, world: int) -> bool:
+    return cfg in ("5", "3") and world > 1
+
+
+def bench_config(cfg: str, world: int) -> dict:
+    """The ``config`` object of the JSON line -- identical for both arms."""
+    H, W = SHAPES[cfg]
+    d = {"workload": WORKLOADS[cfg], "image": [H, W], "iterations": ITERS.get(cfg, 1)}
+    if cfg == "4":
+        d.update(batch=BATCH4, images_per_rank_per_step=-(-BATCH4 // world),
+                 parallelism=f"batch sharded over {world} rank(s), no data-path collective")
+    elif row_banded(cfg, world):
+        d.update(parallelism=f"one image in {world} row bands, NCCL halo exchange overlapped with "
+                             f"the band interior")
     else:
-        w = workloads.config4_image(rank, device=device, param_dtype=torch.float32)
-    f = torch.as_tensor(w["f"]).to(device)
-    if copies == 1:
-        return w, [{"f": f, "p": [w["size"], w["elong"], w["orient"]]}]
-    sets = []
-    for _ in range(copies):
-        if "field" in w:
+        d.update(parallelism="one image per rank per step" + (" (replicas)" if world > 1 else ""))
+    if cfg in ("5", "3", "3n4", "4"):
+        d["l2"] = "inputs + output per step exceed the 126 MB L2 (no flush needed)"
+    elif cfg != "1":
+        d["l2"] = "4 rotating input/output sets per rank (working set > 126 MB L2)"
+    else:
+        d["l2"] = "4 rotating input sets (working set < L2: launch-bound config)"
+    d["path"] = {"1": "drop-in (H,W,4) f64 field (rubs_b200_filter)",
+                 "3": "fused closed-form N=3 mapping + exact N=3 filter (rubs_b200_filter3_params)",
+                 "A": "rubs_b200_adaptive_smooth"}.get(
+        cfg, "fused LUT mapping + filter (rubs_b200_filter_params)")
+    return d
+
+
+def _load_workload(cfg, torch, device, rank=0, image=None):
+    from paper_1003_2022_b200 import workloads
+    f32 = torch.float32
+    if cfg == "2":
+        return workloads.config2(device=device, param_dtype=f32)
+    if cfg == "1":
+        return workloads.config1()
+    if cfg == "3":
+        return workloads.config3_n3(device=device, param_dtype=f32)
+    if cfg == "3n4":
+        return workloads.config3(device=device, param_dtype=f32)
+    if cfg == "5":
+        return workloads.config5(device=device, param_dtype=f32, image_device=device)
+    if cfg == "A":
+        return workloads.adaptive_image()
+    return workloads.config4_image(rank if image is None else image, device=device, param_dtype=f32)
+
+
+class Work:
+    """One rank's workload: device-resident inputs and the step function."""
+
+    def __init__(self, cfg, torch, device, rank, world):
+        import paper_1003_2022_b200 as rb
+        from paper_1003_2022_b200 import sharding
+        self.cfg, self.torch, self.rb = cfg, torch, rb
+        self.rank, self.world = rank, world
+        self.H, self.W = SHAPES[cfg]
+        self.iters = ITERS.get(cfg, 1)
+        self.n3 = cfg == "3"
+        self.row_bands = row_banded(cfg, world)
+        self.sets = []
+        self.lut = rb.default_lut()
+        if cfg == "4":
+            # the batch: this rank's 64/N images, all resident
+            self.images = sharding.batch_indices(BATCH4, world, rank)
+            for i in self.images:
+                w = _load_workload(cfg, torch, device, image=i)
+                self.sets.append({"f": torch.as_tensor(w["f"]).to(device),
+                                  "p": [w["size"], w["elong"], w["orient"]]})
+            self.px_per_step = float(self.H * self.W) * BATCH4  # all ranks together
+            return
+        w = _load_workload(cfg, torch, device, rank)
+        self.w = w
+        if cfg == "A":
+            f = torch.as_tensor(w["f"]).to(device)
+            self.sets = [{"f": f.clone(), "adaptive": True} for _ in range(4)]
+        elif cfg == "1":
+            f = torch.as_tensor(w["f"]).to(device)
             fld = torch.as_tensor(w["field"]).to(device)
-            sets.append({"f": f.clone(), "field": fld.clone()})
+            self.sets = [{"f": f.clone(), "field": fld.clone()} for _ in range(4)]
+        elif cfg == "2":
+            f = torch.as_tensor(w["f"]).to(device)
+            self.sets = [{"f": f.clone(), "p": [v.clone() for v in (w["size"], w["elong"], w["orient"])]}
+                         for _ in range(4)]
         else:
-            sets.append({"f": f.clone(), "p": [v.clone() for v in (w["size"], w["elong"], w["orient"])]})
-    return w, sets
+            self.sets = [{"f": torch.as_tensor(w["f"]).to(device), "p": [w["size"], w["elong"], w["orient"]]}]
+        if self.row_bands:
+            align = sharding.TILE3 if self.n3 else sharding.TILE
+            self.band = sharding.band_bounds(self.H, world, align)[rank]
+            s0 = self.sets[0]
+            b0, b1 = self.band
+            self.own = s0["f"][b0:b1].contiguous()
+            self.pb = [p[b0:b1].contiguous() for p in s0["p"]]
+            self.plan = (sharding.row_band_plan3(self.band, self.H, self.pb[0]) if self.n3 else
+                         sharding.row_band_plan(self.band, self.H, self.pb[0], self.lut))
+            self.sets = []
+            torch.cuda.empty_cache()
+            self.px_per_step = float(self.H * self.W)  # the ranks share one image
+        else:
+            self.px_per_step = float(self.H * self.W) * world
+
+    def step(self, i):
+        rb, sharding = self.rb, __import__("paper_1003_2022_b200.sharding", fromlist=["x"])
+        if self.row_bands and self.n3:
+            return sharding.filter3_row_band(self.own, self.band, self.H, *self.pb, plan=self.plan)
+        if self.row_bands:
+            return sharding.filter_row_band(self.own, self.band, self.H, *self.pb, lut=self.lut,
+                                            plan=self.plan)
+        if self.cfg == "4":
+            out = None
+            for s in self.sets:
+                out = rb.filter_space_variant_params(s["f"], *s["p"], lut=self.lut, iterations=2)
+            return out
+        s = self.sets[i % len(self.sets)]
+        if "adaptive" in s:
+            return rb.adaptive_smooth(s["f"], self.w["noise_sigma"])
+        if "p" in s and self.n3:
+            return rb.filter_space_variant3_params(s["f"], *s["p"], iterations=self.iters)
+        if "p" in s:
+            return rb.filter_space_variant_params(s["f"], *s["p"], lut=self.lut, iterations=self.iters)
+        return rb.filter_space_variant(s["f"], s["field"], self.iters)
+
+    # ---- end to end through the public API with host buffers ------------
+    def e2e_setup(self):
+        """(call, h2d bytes, d2h bytes, pixels per call) on pinned host
+        buffers; every call copies its inputs in and its result out."""
+        torch, rb = self.torch, self.rb
+
+        def pinned(t, dtype=None):
+            h = torch.empty(t.shape, dtype=dtype or t.dtype, pin_memory=True)
+            h.copy_(t)
+            return h
+
+        if self.row_bands:
+            from paper_1003_2022_b200 import sharding
+            # this rank's share as the host scatters it: its band's
+            # parameter rows and its band + halo image rows; the band's
+            # output rows come back (no exchange: the host holds the rows)
+            n0, n1 = self.plan.needs[self.rank]
+            b0, b1 = self.band
+            # the halo rows live on the neighbours: fetch them once here
+            # (setup), as the host scatter would hand them out
+            full = sharding.exchange_rows(self.own, self.band, self.plan.bands, self.plan.needs, self.rank)
+            hf = pinned(full)
+            hp = [pinned(p) for p in self.pb]
+            hout = torch.empty((b1 - b0, self.W), dtype=torch.float64, pin_memory=True)
+            dev = self.own.device
+
+            def call():
+                f_rows = hf.to(dev, non_blocking=True)
+                ps = [p.to(dev, non_blocking=True) for p in hp]
+                if self.n3:
+                    out = sharding.filter3_rows_params(f_rows, n0, self.H, *ps, b0, b0, b1 - b0)
+                else:
+                    out = sharding.filter_rows_params(f_rows, n0, self.H, *ps, b0, b0, b1 - b0, self.lut)
+                hout.copy_(out, non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+                return hout
+            h2d = hf.numel() * hf.element_size() + sum(p.numel() * p.element_size() for p in hp)
+            return call, h2d, hout.numel() * 8, float((b1 - b0) * self.W)
+        if self.cfg == "4":
+            # the rank's images as pinned host arrays (up to 8 distinct sets,
+            # rotating over the rank's 64/N images: every image is copied in
+            # and out on every call)
+            k = min(len(self.sets), 8)
+            hsets = [(pinned(s["f"]).numpy(), [pinned(p).numpy() for p in s["p"]]) for s in self.sets[:k]]
+            houts = [torch.empty((self.H, self.W), dtype=torch.float64, pin_memory=True).numpy()
+                     for _ in range(2)]
+
+            def call():
+                for j in range(len(self.sets)):
+                    hf, hp = hsets[j % k]
+                    rb.filter_space_variant_params(hf, *hp, lut=self.lut, iterations=2, out=houts[j % 2])
+                return houts[0]
+            one = hsets[0][0].nbytes + sum(p.nbytes for p in hsets[0][1])
+            return call, one * len(self.sets), self.H * self.W * 8 * len(self.sets), \
+                float(self.H * self.W) * len(self.sets)
+        s = self.sets[0]
+        hout = torch.empty((self.H, self.W), dtype=torch.float64, pin_memory=True).numpy()
+        if "adaptive" in s:
+            hf = pinned(s["f"]).numpy()
+            return (lambda: rb.adaptive_smooth(hf, self.w["noise_sigma"], out=hout)), hf.nbytes, \
+                hout.nbytes, float(self.H * self.W)
+        if "p" in s:
+            hf = pinned(s["f"]).numpy()
+            hp = [pinned(p).numpy() for p in s["p"]]
+            if self.n3:
+                call = lambda: rb.filter_space_variant3_params(hf, *hp, iterations=self.iters, out=hout)  # noqa: E731
+            else:
+                call = lambda: rb.filter_space_variant_params(hf, *hp, lut=self.lut,  # noqa: E731
+                                                              iterations=self.iters, out=hout)
+            return call, hf.nbytes + sum(p.nbytes for p in hp), hout.nbytes, float(self.H * self.W)
+        hf = pinned(s["f"]).numpy()
+        hfl = pinned(s["field"], torch.float64).numpy()
+        return (lambda: rb.filter_space_variant(hf, hfl, self.iters, out=hout)), hf.nbytes + hfl.nbytes, \
+            hout.nbytes, float(self.H * self.W)
 
 
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist
-    import paper_1003_2022_b200 as rb
     from paper_1003_2022_b200 import _native
 
     torch.cuda.set_device(local)
@@ -188,38 +404,12 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
     L = _native.load()
-    w, sets = make_inputs(args.config, torch, device, 4, rank)
-    iters = int(w["iterations"])
-    n3 = w.get("directions") == 3
-    H, W = w["f"].shape
-    row_bands = args.config in ("5", "3") and world > 1
-    if row_bands:
-        # one image, sharded by output-row bands; each step exchanges halo
-        # rows with the neighbours (NCCL) and filters the own band
-        from paper_1003_2022_b200 import sharding
-        band = sharding.band_bounds(H, world, sharding.TILE3 if n3 else sharding.TILE)[rank]
-        s0 = sets[0]
-        own = s0["f"][band[0]:band[1]].contiguous()
-        pb = [p[band[0]:band[1]].contiguous() for p in s0["p"]]
-        del sets[:]
-        torch.cuda.empty_cache()
-
-    def step(i):
-        if row_bands and n3:
-            return sharding.filter3_row_band(own, band, H, *pb)
-        if row_bands:
-            return sharding.filter_row_band(own, band, H, *pb)
-        s = sets[i % len(sets)]
-        if "adaptive" in s:
-            return rb.adaptive_smooth(s["f"], w["noise_sigma"])
-        if "p" in s and n3:
-            return rb.filter_space_variant3_params(s["f"], *s["p"], iterations=iters)
-        if "p" in s:
-            return rb.filter_space_variant_params(s["f"], *s["p"], iterations=iters)
-        return rb.filter_space_variant(s["f"], s["field"], iters)
+    wk = Work(args.config, torch, device, rank, world)
+    if rank == 0 and world == 1:
+        _WK_FOR_CPU["wk"] = wk
 
     for i in range(args.warmup):
-        step(i)
+        wk.step(i)
     torch.cuda.synchronize()
 
     clocks = ClockSampler(local)
@@ -234,7 +424,7 @@ def run_ours(args, rank, world, local):
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record()
     for i in range(args.steps):
-        step(i)
+        wk.step(i)
     ev1.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -242,9 +432,8 @@ def run_ours(args, rank, world, local):
     L.rubs_b200_set_profiling(0)
     ms_total = ev0.elapsed_time(ev1)
     launches = int(L.rubs_b200_launch_count())
-    import ctypes
-    tile_ms, tile_n = ctypes.c_double(), ctypes.c_int64()
-    L.rubs_b200_kernel_time(0, ctypes.byref(tile_ms), ctypes.byref(tile_n))
+    pass_ms, pass_n = ctypes.c_double(), ctypes.c_int64()
+    L.rubs_b200_kernel_time(0, ctypes.byref(pass_ms), ctypes.byref(pass_n))
     all_ms, all_n = ctypes.c_double(), ctypes.c_int64()
     L.rubs_b200_kernel_time(2, ctypes.byref(all_ms), ctypes.byref(all_n))
     clk = clocks.stop() if rank == 0 else None
@@ -253,183 +442,230 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
-    # weak scaling: every rank filters a whole image per step; row bands
-    # (configs 5 and 3 on N > 1): the ranks share one image per step
-    px_total = float(H * W) * args.steps * (1 if row_bands else world)
-    value = px_total / (ms_max * 1e-3) / 1e9
+    value = wk.px_per_step * args.steps / (ms_max * 1e-3) / 1e9
 
     # ---- end to end through the public API with host buffers ----
     e2e = None
-    if not args.no_e2e and not row_bands:
-        if "adaptive" in sets[0]:
-            hf = torch.empty((H, W), dtype=torch.float64, pin_memory=True)
-            hf.copy_(sets[0]["f"].cpu())
-            hfn = hf.numpy()
-            hout = torch.empty((H, W), dtype=torch.float64, pin_memory=True).numpy()
-
-            def e2e_step():
-                return rb.adaptive_smooth(hfn, w["noise_sigma"], out=hout)
-            h2d = hfn.nbytes
-        elif "p" in sets[0]:
-            hf = torch.empty((H, W), dtype=sets[0]["f"].dtype, pin_memory=True)
-            hf.copy_(sets[0]["f"].cpu())
-            hp = []
-            for v in sets[0]["p"]:
-                t_ = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
-                t_.copy_(v.cpu())
-                hp.append(t_.numpy())
-            hfn = hf.numpy()
-            lut = rb.default_lut()
-            hout = torch.empty((H, W), dtype=torch.float64, pin_memory=True).numpy()
-
-            def e2e_step():
-                if n3:
-                    return rb.filter_space_variant3_params(hfn, *hp, iterations=iters, out=hout)
-                return rb.filter_space_variant_params(hfn, *hp, lut=lut, iterations=iters, out=hout)
-            h2d = hf.numel() * hf.element_size() + sum(p.nbytes for p in hp)
-        else:
-            hf = torch.empty((H, W), dtype=sets[0]["f"].dtype, pin_memory=True)
-            hf.copy_(sets[0]["f"].cpu())
-            hfl = torch.empty(sets[0]["field"].shape, dtype=torch.float64, pin_memory=True)
-            hfl.copy_(sets[0]["field"].cpu())
-            hfn, hfln = hf.numpy(), hfl.numpy()
-            hout = torch.empty((H, W), dtype=torch.float64, pin_memory=True).numpy()
-
-            def e2e_step():
-                return rb.filter_space_variant(hfn, hfln, iters, out=hout)
-            h2d = hfn.nbytes + hfln.nbytes
+    if not args.no_e2e:
+        call, h2d, d2h, px_call = wk.e2e_setup()
         for _ in range(max(2, args.warmup // 2)):
-            e2e_step()
+            call()
         if world > 1:
             dist.barrier()
+        ksteps = max(3, args.steps // 2) if args.config != "4" else max(2, args.steps // 4)
         t0 = time.perf_counter()
-        ksteps = max(3, args.steps // 2)
         for _ in range(ksteps):
-            e2e_step()
+            call()
         el = time.perf_counter() - t0
         te = torch.tensor([el], dtype=torch.float64, device=device)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(H * W) * ksteps * world / float(te.item()) / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(H * W * 8),
+        px_all = wk.px_per_step if (wk.row_bands or args.config == "4") else px_call * world
+        e2e = {"value": px_all * ksteps / float(te.item()) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "steps": ksteps, "host_buffers": "pinned (inputs and result)",
-               "timing": "wall clock around blocking API calls, max over ranks"}
+               "timing": "wall clock around blocking API calls, max over ranks"
+                         + ("; per rank: its band + halo rows in, its band out" if wk.row_bands else "")}
 
     # one more call outside the timed region: the output at sampled pixels for
     # the parity line (checked against the exact oracle in the CPU leg)
-    parity_in = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config in PARITY_PX:
-        out = step(0)
+    pin = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out = wk.step(0)
         torch.cuda.synchronize()
-        rng = np.random.default_rng(7)
-        n = PARITY_PX[args.config]
-        pts = np.stack([rng.integers(0, H, n), rng.integers(0, W, n)], axis=1)
-        pts = np.concatenate([pts, [[0, 0], [H - 1, W - 1]]])
-        idx = torch.as_tensor(pts, device=out.device)
-        got = out[idx[:, 0], idx[:, 1]].double().cpu().numpy()
-        s0 = sets[0]
-        if "field" in s0:
-            par = s0["field"][idx[:, 0], idx[:, 1]].double().cpu().numpy()
-        else:
-            par = np.stack([v[idx[:, 0], idx[:, 1]].double().cpu().numpy() for v in s0["p"]], axis=1)
-        parity_in = {"pts": pts, "got": got, "par": par, "n3": n3, "f": s0["f"]}
+        pin = parity_sample(args.config, wk, out)
 
     result = None
     if rank == 0:
         hbm, sm_max, peak_kind = measured_peaks()
         bpp = BYTES_PER_PX[args.config]
-        per_launch_px = H * W  # final pass covers H x W (iterations > 1 adds extended passes)
-        tile_avg_ms = tile_ms.value / max(1, tile_n.value)
-        launches_per_step = tile_n.value / max(1, args.steps)
-        kern_s = max(tile_ms.value, 1e-9) / max(1, args.steps) * 1e-3
-        # bpp counts every pass (config 4: both passes' bytes per output pixel)
-        achieved = bpp * H * W / kern_s / 1e9
-        # fp64 issue bound: B200 has 64 fp64 lanes per SM; DP instructions
-        # per pixel measured with ncu (profiles/ncu_r01_summary.md)
+        px_rank_step = wk.px_per_step / (1 if wk.row_bands or args.config == "4" else world)
+        if wk.row_bands:
+            px_rank_step = float((wk.band[1] - wk.band[0]) * wk.W)
+        elif args.config == "4":
+            px_rank_step = float(wk.H * wk.W * len(wk.sets))
+        kern_s = max(pass_ms.value, 1e-9) / max(1, args.steps) * 1e-3  # filter kernels per step
+        achieved = bpp * px_rank_step / kern_s / 1e9
+        passes_per_step = pass_n.value / max(1, args.steps)
+        fp64 = smem = None
         dp_per_px = DP_INST_PER_PX.get(args.config)
-        fp64 = None
         if dp_per_px:
             peak_dp = 148 * 64 * sm_max * 1e6  # DP lane-ops / s at max clock
-            got_dp = dp_per_px * H * W * iters / kern_s
+            got_dp = dp_per_px * px_rank_step * wk.iters / kern_s
             fp64 = {"achieved_dp_ops_per_s": got_dp, "peak_dp_ops_per_s": peak_dp,
                     "frac": got_dp / peak_dp, "dp_inst_per_px": dp_per_px,
                     "peak_at_clock_mhz": sm_max, "source": "ncu sm__sass_thread_inst_executed_op_fp64 per px"}
-        smem = None
         wf_per_px = SMEM_WF_PER_PX.get(args.config)
         if wf_per_px:
             peak_wf = 148 * sm_max * 1e6  # wavefronts / s at max clock
-            got_wf = wf_per_px * H * W * iters / kern_s
+            got_wf = wf_per_px * px_rank_step * wk.iters / kern_s
             smem = {"achieved_wavefronts_per_s": got_wf, "peak_wavefronts_per_s": peak_wf,
                     "frac": got_wf / peak_wf, "wavefronts_per_px": wf_per_px,
                     "source": "ncu l1tex__data_pipe_lsu_wavefronts_mem_shared.sum per px"}
-        traffic = TRAFFIC_PER_LAUNCH.get(args.config)
+        traffic = TRAFFIC_PER_PASS.get(args.config)
         result = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "strong" if row_bands else "weak", "vs_baseline": None, "dtype": "f64",
+            "scaling": "strong" if wk.row_bands else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": WORKLOADS[args.config], "image": [H, W], "iterations": iters,
-                       "per_rank_images_per_step": 1,
-                       "l2": "4 rotating input/output sets per rank (working set > 126 MB L2)",
-                       "path": ("fused closed-form N=3 mapping + exact N=3 filter (rubs_b200_filter3_params)"
-                                if n3 else "fused LUT mapping + filter (rubs_b200_filter_params)")
-                       if args.config != "1" else "drop-in (H,W,4) field (rubs_b200_filter)"},
+            "config": bench_config(args.config, world),
             "e2e": e2e,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": traffic, "traffic_unit": "bytes/launch (ncu)",
-                         "kernel": ("n3_tile_kernel" if n3 else
-                                    "wide_filter_kernel" if launches_per_step <= iters else
-                                    "filter kernels of the pass: wide_filter_kernel + the deferred-tile "
-                                    "passes (tile_overflow / big_* kernels; split in profiles/)"),
-                         "kernel_ms_avg": tile_avg_ms,
-                         "kernel_ms_per_step": max(tile_ms.value, 0.0) / max(1, args.steps),
+                         "frac": achieved / hbm,
+                         "traffic": traffic[0] if traffic else None,
+                         "traffic_note": traffic[1] if traffic else None,
+                         "kernel": KERNEL_NOTE.get(args.config, "wide_filter_kernel (the pass's one launch)"),
+                         "kernel_ms_per_step": max(pass_ms.value, 0.0) / max(1, args.steps),
+                         "passes_per_step": passes_per_step,
                          "algorithmic_bytes_per_px": bpp, "peak_source": peak_kind,
-                         "binding_bound": "shared-memory wavefronts and issue (see smem, fp64)"},
+                         "binding_bound": BINDING.get(args.config, "shared-memory wavefronts and issue")},
             "fp64": fp64,
             "smem": smem,
             "gpu_launches": launches,
             "launches_per_step": launches / max(1, args.steps),
-            "tile_kernel_launches_per_step": launches_per_step,
             "kernel_share_of_step": all_ms.value / max(ms_total, 1e-9),
             "clocks": clk,
         }
-        if parity_in is not None:
-            result["_parity_in"] = parity_in
+        if pin is not None:
+            result["_parity_in"] = pin
     if world > 1:
         dist.destroy_process_group()
     return result
 
 
-WORKLOADS = {
-    "3": "config3: 8192^2 fp32 rectangles + N(0,0.05^2) noise; N=3 directions (0/60/120 deg); "
-         "sigma [1,32], rho [1,6] clamped to 0.95 of the N=3 bound, smooth theta; exact N=3 path "
-         "(closed-form mapping fused, f32 params)",
-    "3n4": "config3 shapes with the N=4 ZP element: 8192^2 fp32 rectangles + N(0,0.05^2) noise; "
-           "sigma [1,32], rho [1,6] clamped, smooth theta (LUT mapping)",
-    "5": "config5: 32768^2 fp32 uniform[0,1) (torch Philox seed 0); sigma [2,256], rho [1,8] "
-         "clamped to the LUT, smooth theta; single GPU",
-    "2": "config2: 2048^2 fp64 uniform[0,1) seed 0; N=4 ZP box spline; sigma [2,16], rho [1,4], "
-         "theta [0,pi) smooth fields (LUT mapping, f32 params)",
-    "1": "config1: 256^2 fp64 uniform[0,1) seed 0; sigma 2->8 along x, rho 1->3 radial, "
-         "theta=atan2 mod pi; exact optimiser field",
-    "4": "config4 image: 4096^2 fp32 uniform[0,1); sigma [2,24], rho [1,4], smooth theta; 2 passes",
-    "A": "adaptive_smooth pipeline (tensor.py; SURVEY 8f): 2048^2 fp64 stripes + N(0,0.1^2), "
-         "noise_sigma 0.1, window 1.5; structure tensor (3 window filters), percentiles, anisotropy, "
-         "LUT filter of image and flat image, gain correction",
+KERNEL_NOTE = {
+    "5": "the pass's filter kernels: wide_filter_kernel (mapping, plan, small kernels) + the "
+         "large-halo block passes (big_* kernels); per-kernel split in profiles/",
+    "3n4": "the pass's filter kernels: wide_filter_kernel + the large-halo block passes",
+    "4": "the filter kernels of both passes of each image",
+    "3": "n3_tile_kernel",
+    "A": "the pipeline's filter launches",
+}
+BINDING = {
+    "5": "on-chip: the 16-vertex gather (L1) and the block regions' scratch traffic (see traffic)",
+    "3": "shared-memory wavefronts (see smem)",
 }
 # From the committed ncu captures of the primary kernel (wide_filter_kernel)
-# on config 2 (profiles/ncu_r01_final_summary.md; wavefronts and traffic
-# re-measured in profiles/ncu_r01b_summary.md, final build): fp64 instructions executed
-# per output pixel (DADD + DFMA + DMUL + DSETP, thread level), shared-memory
-# wavefronts per output pixel, and DRAM bytes per launch
-# (dram__bytes_read.sum + dram__bytes_write.sum).
-# Config 3 (N=3, n3_tile_kernel): profiles/ncu_r01b_summary.md.
-DP_INST_PER_PX = {"2": 602, "3": 2147}
+# on config 2 (profiles/ncu_r01b_summary.md, final build): fp64 instructions
+# executed per output pixel (DADD + DFMA + DMUL, thread level), shared-memory
+# wavefronts per output pixel.  Config 3 (N=3, n3_tile_kernel): same file.
+DP_INST_PER_PX = {"2": 524, "3": 2147}
 SMEM_WF_PER_PX = {"2": 16.39, "3": 53.9}
-TRAFFIC_PER_LAUNCH = {"2": 105.45e6, "3": 1.588e9}
+# DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) per pass, summed
+# over the pass's kernels, from the ncu launch lists in profiles/.
+TRAFFIC_PER_PASS = {
+    "2": (105.45e6, "ncu, wide_filter_kernel, profiles/ncu_r01b_summary.md"),
+    "3": (1.588e9, "ncu, n3_tile_kernel, profiles/ncu_r01b_summary.md"),
+    "5": (270.3e9, "ncu launch list of one step, sum over the pass's kernels "
+                   "(profiles/ncu_r02_c5_launches.md; algorithmic 25.8 GB)"),
+}
 
 
 # ---------------------------------------------------------------------------
+# Parity leg (checker only, after the timed region): the GPU output at
+# sampled pixels against the exact dense oracle.
+
+PARITY_PX = {"1": 256, "2": 256, "3": 256, "3n4": 128}
+
+
+def parity_sample(cfg, wk, out):
+    """GPU outputs (and inputs) at the sampled pixels of the workload."""
+    torch = wk.torch
+    H, W = wk.H, wk.W
+    rng = np.random.default_rng(7)
+    if cfg == "A":
+        return None
+    if cfg == "4":
+        # 8 x 8 blocks of the last image filtered (two passes), corners incl.
+        blocks = [(0, 0), (H - 8, W - 8), (0, W - 8), (H - 8, 0)] + \
+                 [(int(rng.integers(0, H - 8)), int(rng.integers(0, W - 8))) for _ in range(4)]
+        pts = np.concatenate([np.stack(np.mgrid[y:y + 8, x:x + 8], -1).reshape(-1, 2) for y, x in blocks])
+        s = wk.sets[-1]
+    else:
+        n = PARITY_PX.get(cfg, 2000)
+        pts = np.stack([rng.integers(0, H, n), rng.integers(0, W, n)], axis=1)
+        pts = np.concatenate([pts, [[0, 0], [H - 1, W - 1], [0, W - 1], [H - 1, 0]]])
+        s = wk.sets[0]
+    idx = torch.as_tensor(pts, device=out.device)
+    got = out[idx[:, 0], idx[:, 1]].double().cpu().numpy()
+    if "field" in s:
+        par = s["field"][idx[:, 0], idx[:, 1]].double().cpu().numpy()
+    else:
+        par = np.stack([v[idx[:, 0], idx[:, 1]].double().cpu().numpy() for v in s["p"]], axis=1)
+    return {"pts": pts, "got": got, "par": par, "n3": wk.n3, "f": s["f"], "p": s.get("p")}
+
+
+def parity_check(cfg: str, pin) -> dict:
+    """Max relative error of the GPU output at sampled pixels of the bench
+    workload against the exact dense oracle (oracle/dense_oracle.c,
+    dense3_oracle.c; configs 4 and 5: its GPU copy dense_oracle_cuda.cu,
+    pinned to it by tests/test_gpu_baseline_size.py -- the checker, pinned to
+    the reference by tests/test_oracle_golden.py, test_oracle_n3.py).  Each
+    pixel is evaluated on the crop of the image its kernel reaches (exact:
+    zero padding), with its own scale-vector."""
+    import math as _m
+    import oracle
+    from oracle import port, port3
+    from paper_1003_2022_b200 import default_lut
+    pts, got, par = pin["pts"], pin["got"], pin["par"]
+    f = pin["f"]
+    lut = default_lut()
+    if cfg == "1" or par.shape[1] == 4:
+        field = par
+    elif pin["n3"]:
+        field = port3.scales3_from_params(par[:, 0], par[:, 1], par[:, 2])
+    else:
+        field = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, par[:, 0], par[:, 1], par[:, 2])
+    if cfg in ("4", "5"):
+        if cfg == "5":
+            ref = oracle.points_cuda(f, field, pts)
+            how = "exact dense filter per pixel on the GPU (oracle/dense_oracle_cuda.cu points_kernel)"
+        else:
+            import torch
+            params = pin["p"]
+
+            def field_of(rows, cols):
+                r = torch.as_tensor(np.asarray(rows, np.int64), device=params[0].device)
+                c = torch.as_tensor(np.asarray(cols, np.int64), device=params[0].device)
+                v = [p[r, c].double().cpu().numpy() for p in params]
+                return port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, *v)
+            ref = np.concatenate([oracle.points2_cuda(f, field_of, pts[i:i + 64])
+                                  for i in range(0, len(pts), 64)])
+            how = ("exact two-pass dense filter (pass 1 on the GPU over each 8x8 block's window, "
+                   "oracle/dense_oracle_cuda.cu; pass 2 exact kernel sums)")
+        scale = max(float(np.abs(ref).max()), 1e-300)
+        return {"max_rel_err": float(np.abs(got - ref).max() / scale), "pixels": int(len(pts)),
+                "oracle": how, "tolerance": 1e-9}
+    H, W = f.shape
+    ref = np.empty(len(pts))
+    for i, ((r, c), a) in enumerate(zip(pts, field)):
+        a = np.maximum(a, 0.05)
+        if pin["n3"]:
+            rx = int(_m.ceil(0.5 * a[0] + 0.25 * (a[1] + a[2]))) + 1
+            ry = int(_m.ceil(0.25 * _m.sqrt(3.0) * (a[1] + a[2]))) + 1
+        else:
+            diag = (a[1] + a[3]) / _m.sqrt(2.0)
+            rx = int(_m.ceil(0.5 * (a[0] + diag))) + 1
+            ry = int(_m.ceil(0.5 * (a[2] + diag))) + 1
+        r0, r1, c0, c1 = max(0, r - ry), min(H, r + ry + 1), max(0, c - rx), min(W, c + rx + 1)
+        crop = f[r0:r1, c0:c1]
+        crop = (crop.double().cpu().numpy() if hasattr(crop, "cpu") else np.asarray(crop, np.float64))
+        q = np.array([[r - r0, c - c0]])
+        ref[i] = (oracle.points3(crop, a, q, threads=1) if pin["n3"] else
+                  oracle.points(crop, a, q, threads=1))[0]
+    scale = max(float(np.abs(ref).max()), 1e-300)
+    return {"max_rel_err": float(np.abs(got - ref).max() / scale), "pixels": int(len(pts)),
+            "oracle": "exact dense filter per pixel (oracle/dense" + ("3" if pin["n3"] else "") +
+                      "_oracle.c) on the crop its kernel reaches",
+            "tolerance": 1e-9}
+
+
+# ---------------------------------------------------------------------------
+# CPU leg: the reference algorithm on the host cores (cpu_baseline and the
+# --impl reference arm).  Units are independent windows of the workload,
+# exact by linearity + zero padding; a unit's halo costs pre-integration
+# only (port.filter_window), not mesh work.
+
 _PORT = {}
 
 
@@ -462,89 +698,126 @@ def _band_worker(band):
     return (hi - lo) * f.shape[1]
 
 
+def _window_worker(k):
+    """One pre-cut 2-D window of config 5 (crop + window field); returns pixels."""
+    import oracle.port as port
+    crop, cr0, cc0, fld, r0, c0 = _PORT["windows"][k]
+    port.filter_window(crop, cr0, cc0, fld, r0, c0)
+    return fld.shape[0] * fld.shape[1]
+
+
 class CpuPort:
     """The reference algorithm (oracle/port.py, a numpy restatement of the
-    reference fast path) on row bands of the config's image, one process per
-    host core (exact by linearity + zero padding)."""
+    reference fast path, pinned to it at 1e-14) on independent units of the
+    config's workload, one process per host core."""
 
-    def __init__(self, cfg: str, workers: int | None = None, min_rows: int = 64):
+    def __init__(self, cfg: str, workers: int | None = None, wk=None):
         import multiprocessing as mp
         from oracle import port
         from paper_1003_2022_b200 import default_lut, workloads
         self.cfg = cfg
         self.cores = workers or os.cpu_count() or 1
+        os.environ["OMP_NUM_THREADS"] = "1"
+        lut = default_lut()
+        self.H, self.W = SHAPES[cfg]
+        self.note = ""
         if cfg == "A":
             w = workloads.adaptive_image()
-            lut = default_lut()
             _PORT.update(f=w["f"], lut=(lut.rho_grid, lut.phi_grid, lut.entries),
                          noise=w["noise_sigma"], crop=256)
-            self.H, self.W = w["f"].shape
             self.jobs = list(range(self.cores))
-            os.environ["OMP_NUM_THREADS"] = "1"
-            self.pool = mp.get_context("fork").Pool(self.cores)
-            return
-        self.note = ""
-        if cfg == "1":
-            w = workloads.config1()
-            field = w["field"]
+            self.kind = "adaptive"
+        elif cfg == "5":
+            # 1024 x 1024 output windows of the real 32768^2 workload (the
+            # device-resident image and fields), spread over the image; each
+            # window's crop carries its read margins
+            self._config5_windows(wk, lut)
+            self.kind = "window"
         else:
-            if cfg == "2":
+            if cfg == "1":
+                w = workloads.config1()
+                field = w["field"]
+            elif cfg == "2":
                 w = workloads.config2()
             elif cfg == "3":
-                # N=3: a 2048^2 instance of config 3's recipe through the
-                # numpy restatement of the exact N=3 algorithm (no reference
-                # N=3 filter exists)
                 from oracle import port3
                 w = workloads.config3_n3(2048, 2048)
                 self.note = " (2048^2 instance of the config-3 N=3 recipe; oracle/port3.py)"
             elif cfg == "3n4":
-                # a 2048^2 instance of config 3's recipe (same sigma / rho
-                # ranges; the full 8192^2 CPU run would take hours)
                 w = workloads.config3(2048, 2048)
                 self.note = " (2048^2 instance of the config-3 recipe)"
-            elif cfg == "5":
-                w = workloads.config5(2048, 2048)
-                self.note = " (2048^2 instance of the config-5 recipe)"
             else:
                 w = workloads.config4_image(0)
+                self.note = " (image 0 of the batch; two passes: each band's pass 1 covers its halo rows)"
             if cfg == "3":
-                field = port3.scales3_from_params(w["size"].numpy(), w["elong"].numpy(),
-                                                  w["orient"].numpy())
-            else:
-                lut = default_lut()
+                field = port3.scales3_from_params(w["size"].numpy(), w["elong"].numpy(), w["orient"].numpy())
+            elif cfg != "1":
                 field = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, w["size"].numpy(),
                                          w["elong"].numpy(), w["orient"].numpy())
-        f = np.asarray(w["f"], dtype=np.float64)
-        _PORT.update(f=f, field=field, iters=int(w["iterations"]))
-        self.H, self.W = f.shape
-        self.cfg = cfg
-        self.cores = workers or os.cpu_count() or 1
-        rows = max(min_rows, -(-self.H // self.cores))
-        if cfg == "3":
-            rows = 32  # bounded sample: the N=3 port costs O(kernel height) per pixel
-        self.bands = [(lo, min(self.H, lo + rows)) for lo in range(0, self.H, rows)][: self.cores]
-        self.cores = len(self.bands)
-        os.environ["OMP_NUM_THREADS"] = "1"
+            f = np.asarray(w["f"], dtype=np.float64)
+            _PORT.update(f=f, field=field, iters=int(w["iterations"]))
+            self.H, self.W = f.shape
+            rows = max(64 if cfg != "4" else 128, -(-self.H // self.cores))
+            if cfg == "3":
+                rows = 32  # bounded sample: the N=3 port costs O(kernel height) per pixel
+            self.bands = [(lo, min(self.H, lo + rows)) for lo in range(0, self.H, rows)][: self.cores]
+            self.rows = rows
+            self.jobs = self.bands
+            self.kind = "band3" if cfg == "3" else "band"
+        self.cores = len(self.jobs)
         self.pool = mp.get_context("fork").Pool(self.cores)
-        self.rows = rows
+
+    def _config5_windows(self, wk, lut):
+        import torch
+        from oracle import port
+        if wk is None:  # the reference arm: the same workload, generated on the device
+            dev = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cpu"
+            w = _load_workload("5", torch, dev)
+            f, params = w["f"], [w["size"], w["elong"], w["orient"]]
+        else:
+            f, params = wk.sets[0]["f"] if wk.sets else None, None
+            if f is None:
+                raise RuntimeError("config-5 CPU windows need the whole-image workload (N=1)")
+            params = wk.sets[0]["p"]
+        H, W = f.shape
+        T = 1024
+        n = self.cores
+        rng = np.random.default_rng(5)
+        wins = []
+        for k in range(n):
+            r0 = int(rng.integers(0, H // T)) * T
+            c0 = int(rng.integers(0, W // T)) * T
+            par = [p[r0:r0 + T, c0:c0 + T].double().cpu().numpy() for p in params]
+            fld = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, *par)
+            left, right, below, above = port.read_margins(np.maximum(fld, port.SCALE_FLOOR))
+            cr0, cr1 = max(0, r0 - below - 1), min(H, r0 + T + above + 1)
+            cc0, cc1 = max(0, c0 - left - 1), min(W, c0 + T + right + 1)
+            crop = f[cr0:cr1, cc0:cc1].double().cpu().numpy()
+            wins.append((crop, cr0, cc0, fld, r0, c0))
+        _PORT["windows"] = wins
+        self.jobs = list(range(n))
+        self.T = T
 
     def step(self):
+        worker = {"adaptive": _adaptive_worker, "window": _window_worker, "band3": _band3_worker,
+                  "band": _band_worker}[self.kind]
         t0 = time.perf_counter()
-        if self.cfg == "A":
-            px = sum(self.pool.map(_adaptive_worker, self.jobs))
-        else:
-            px = sum(self.pool.map(_band3_worker if self.cfg == "3" else _band_worker, self.bands))
+        px = sum(self.pool.map(worker, self.jobs))
         return px, time.perf_counter() - t0
 
     def sample(self):
-        if self.cfg == "A":
+        if self.kind == "adaptive":
             return (f"{self.cores} independent adaptive_smooth pipelines on 256x256 crops of the "
                     f"workload image (numpy restatement of tensor.py with the reference fast-path "
                     f"port as filter, oracle/tensor_port.py), {self.cores} processes x 1 thread")
+        if self.kind == "window":
+            return (f"{self.cores} output windows of {self.T}x{self.T} px at seeded random places of the "
+                    f"config-5 32768^2 image and fields, each from its crop with read margins "
+                    f"(halo pre-integrated only); numpy port of the reference fast path "
+                    f"(oracle/port.py filter_window), {self.cores} processes x 1 thread")
         return (f"{len(self.bands)} row bands of {self.rows} rows x {self.W} cols "
                 f"({sum(h - l for l, h in self.bands)} of {self.H} rows) of {WORKLOADS[self.cfg].split(':')[0]}"
-                f"{self.note}, "
-                f"halo rows recomputed per band; "
+                f"{self.note}, halo rows pre-integrated only; "
                 + ("numpy restatement of the exact N=3 row-profile algorithm (oracle/port3.py)"
                    if self.cfg == "3" else "numpy port of the reference fast path (oracle/port.py)")
                 + f", {self.cores} processes x 1 thread")
@@ -554,8 +827,8 @@ class CpuPort:
         self.pool.join()
 
 
-def cpu_port_throughput(cfg: str, steps: int = 1, warmup: int = 1):
-    cp = CpuPort(cfg)
+def cpu_port_throughput(cfg: str, steps: int = 1, warmup: int = 1, wk=None):
+    cp = CpuPort(cfg, wk=wk)
     try:
         for _ in range(warmup):
             cp.step()
@@ -572,72 +845,50 @@ def cpu_port_throughput(cfg: str, steps: int = 1, warmup: int = 1):
 def run_reference(args, rank, world):
     if rank != 0:
         return None
-    mpx, cores, sample, el = cpu_port_throughput(args.config, steps=args.steps, warmup=args.warmup)
+    # bounded: a few steps of the CPU sample (each step is a full pass over
+    # the sample, ~10-30 s of host work)
+    steps = max(1, min(args.steps, 2))
+    mpx, cores, sample, el = cpu_port_throughput(args.config, steps=steps, warmup=0)
     v = mpx / 1e3  # Gpixel/s
-    H = 2048 if args.config in ("2", "A") else (256 if args.config == "1" else 4096)
     return {
-        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": steps, "warmup": 0,
+        "ms_per_step": el / steps * 1e3, "higher_is_better": True,
+        "scaling": "strong" if row_banded(args.config, world) else "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": WORKLOADS[args.config], "image": [H, H]},
+        "config": bench_config(args.config, world),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
-# pixels checked against the exact oracle per bench run (configs whose
-# per-pixel exact cost is bounded; config 4's two passes and the pipeline
-# are covered by the tests)
-PARITY_PX = {"1": 256, "2": 256, "3": 256, "3n4": 128, "5": 12}
-
-
-def parity_check(cfg: str, pin) -> dict:
-    """Max relative error of the GPU output at sampled pixels of the bench
-    workload against the exact dense oracle (oracle/dense_oracle.c,
-    dense3_oracle.c -- the checker, pinned to the reference by
-    tests/test_oracle_golden.py, test_oracle_n3.py).  Each pixel is
-    evaluated on the crop of the image its kernel reaches (exact: zero
-    padding), with its own scale-vector."""
-    import math as _m
-    import oracle
-    from oracle import port, port3
-    from paper_1003_2022_b200 import default_lut
-    pts, got, par = pin["pts"], pin["got"], pin["par"]
-    f = pin["f"]
-    if cfg == "1" or par.shape[1] == 4:
-        field = par
-    elif pin["n3"]:
-        field = port3.scales3_from_params(par[:, 0], par[:, 1], par[:, 2])
+def probe_launch(rank, world, local):
+    """Launcher check: every rank joins a process group and reports."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+        got = [None] * world
+        dist.all_gather_object(got, {"rank": rank, "local": local, "pid": os.getpid()})
+        dist.destroy_process_group()
     else:
-        lut = default_lut()
-        field = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, par[:, 0], par[:, 1], par[:, 2])
-    H, W = f.shape
-    ref = np.empty(len(pts))
-    for i, ((r, c), a) in enumerate(zip(pts, field)):
-        a = np.maximum(a, 0.05)
-        if pin["n3"]:
-            rx = int(_m.ceil(0.5 * a[0] + 0.25 * (a[1] + a[2]))) + 1
-            ry = int(_m.ceil(0.25 * _m.sqrt(3.0) * (a[1] + a[2]))) + 1
-        else:
-            diag = (a[1] + a[3]) / _m.sqrt(2.0)
-            rx = int(_m.ceil(0.5 * (a[0] + diag))) + 1
-            ry = int(_m.ceil(0.5 * (a[2] + diag))) + 1
-        r0, r1, c0, c1 = max(0, r - ry), min(H, r + ry + 1), max(0, c - rx), min(W, c + rx + 1)
-        crop = f[r0:r1, c0:c1]
-        crop = (crop.double().cpu().numpy() if hasattr(crop, "cpu") else np.asarray(crop, np.float64))
-        q = np.array([[r - r0, c - c0]])
-        ref[i] = (oracle.points3(crop, a, q, threads=1) if pin["n3"] else
-                  oracle.points(crop, a, q, threads=1))[0]
-    scale = max(float(np.abs(ref).max()), 1e-300)
-    return {"max_rel_err": float(np.abs(got - ref).max() / scale), "pixels": int(len(pts)),
-            "oracle": "exact dense filter per pixel (oracle/dense" + ("3" if pin["n3"] else "") +
-                      "_oracle.c) on the crop its kernel reaches",
-            "tolerance": 1e-9}
+        got = [{"rank": 0, "local": 0, "pid": os.getpid()}]
+    if rank == 0:
+        print(json.dumps({"probe": True, "n_gpus": world, "ranks": got}), flush=True)
 
 
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args.gpus))
     rank, world, local = dist_env()
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.probe_launch:
+        probe_launch(rank, world, local)
+        return
     if args.impl == "reference":
         res = run_reference(args, rank, world)
         if res is not None:
@@ -647,13 +898,19 @@ def main():
     if rank == 0 and res is not None:
         pin = res.pop("_parity_in", None)
         if world == 1 and not args.no_cpu_baseline:
-            mpx, cores, sample, el = cpu_port_throughput(args.config, steps=1, warmup=0)
+            wk = None
+            if args.config == "5":
+                # the CPU windows are cut from the device-resident workload
+                wk = _WK_FOR_CPU.get("wk")
+            mpx, cores, sample, el = cpu_port_throughput(args.config, steps=1, warmup=0, wk=wk)
             res["cpu_baseline"] = {"value": mpx / 1e3, "unit": UNIT, "cores": cores, "kind": "port",
                                    "sample": sample, "wall_s": el}
             if pin is not None:
                 res["parity"] = parity_check(args.config, pin)
         print(json.dumps(res), flush=True)
 
+
+_WK_FOR_CPU: dict = {}
 
 if __name__ == "__main__":
     main()

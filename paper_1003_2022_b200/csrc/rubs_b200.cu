@@ -685,6 +685,16 @@ constexpr float kPrecisionBudget = RUBS_PREC_BUDGET;  // w * L4 (see above)
 // budget w L4 in that region.  Such pixels are listed and computed one per
 // warp, each with the region of its own taps (pixel_kernel).
 constexpr int kPixSlab = 3072;  // doubles of shared memory per warp (24 KB)
+// initial deferred-pixel list entries (grown on demand); the environment
+// variable RUBS_B200_PIX_LIST_INIT overrides it (tests of the regrow path)
+size_t pix_list_init() {
+  static const size_t v = [] {
+    const char *e = std::getenv("RUBS_B200_PIX_LIST_INIT");
+    const long long n = e ? std::atoll(e) : 0;
+    return n > 0 ? (size_t)n : (size_t)1 << 22;
+  }();
+  return v;
+}
 
 __device__ __forceinline__ bool defer_pixel(const double a[4], float l4, int x, int y, int2 *pix,
                                             int pix_cap, Status *st) {
@@ -694,12 +704,10 @@ __device__ __forceinline__ bool defer_pixel(const double a[4], float l4, int x, 
   // small kernel; a pixel that is neither stays in the shared region)
   const int4 m = pixel_margins_fast(a);
   if (region_pitch(1 + m.x + m.y) * (1 + m.z + m.w) > kPixSlab) return false;
+  // beyond the list's capacity the pixel is only counted: the host grows
+  // the list to the count and runs the deferred-tile passes again
   const int i = atomicAdd(&st->pix_count, 1);
-  if (i < pix_cap) {
-    pix[i] = make_int2(x, y);
-  } else {
-    atomicOr(&st->flags, kFlagRegionTooLarge);  // cannot happen: cap = deferred tiles' pixels
-  }
+  if (i < pix_cap) pix[i] = make_int2(x, y);
   return true;
 }
 
@@ -1753,13 +1761,17 @@ struct Scratch {
   unsigned *d_slotmask = nullptr;
   bool attr_set = false;
 };
-thread_local Scratch t_scr;
+thread_local Scratch t_scr_dev[rubs_internal::kMaxDevices];
+thread_local int t_dev = 0;  // set by ensure_scratch(), which every entry calls first
+#define t_scr (t_scr_dev[t_dev])
 
 int ensure_scratch() {
   int dev = 0;
   RUBS_CUDA_TRY(cudaGetDevice(&dev));
-  if (t_scr.device != dev) {
-    t_scr = Scratch();
+  if (dev < 0 || dev >= rubs_internal::kMaxDevices)
+    return set_error(RUBS_ECUDA, "device index beyond the per-device state table");
+  t_dev = dev;
+  if (t_scr.device != dev) {  // first call on this device
     t_scr.device = dev;
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_status, sizeof(Status)));
     RUBS_CUDA_TRY(cudaMallocHost(&t_scr.h_status, sizeof(Status)));
@@ -2143,7 +2155,8 @@ struct PlanScratch {
   int *d_cm_cell = nullptr;
   size_t cm_cap = 0, cmc_cap = 0;
 };
-thread_local PlanScratch t_plan;
+thread_local PlanScratch t_plan_dev[rubs_internal::kMaxDevices];
+#define t_plan (t_plan_dev[t_dev])
 
 int plan_buffers(size_t ncell, size_t nrec) {
   if (!t_plan.h_counters) RUBS_CUDA_TRY(cudaMallocHost(&t_plan.h_counters, 2 * sizeof(int)));
@@ -2222,14 +2235,19 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   }
   hc.lap("device plan");
   if (hc.on) std::fprintf(stderr, "[host] %d records: %d shared-memory tiles, %d blocks\n", n_ovf, n_smem, n_used);
-  // per-pixel fallback list: at most every pixel of the deferred tiles
-  const int pix_cap = (int)std::min<size_t>((size_t)n_ovf * kTile * kTile, 1u << 30);
-  if ((size_t)pix_cap > t_scr.pix_cap) {
-    if (t_scr.d_pix) cudaFree(t_scr.d_pix);
-    t_scr.d_pix = nullptr;
-    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_pix, (size_t)pix_cap * sizeof(int2)));
-    t_scr.pix_cap = pix_cap;
+  // per-pixel fallback list: grown on demand (handle_overflow), starting
+  // at min(the deferred tiles' pixels, 4M entries = 32 MB)
+  {
+    const size_t want = std::min<size_t>((size_t)n_ovf * kTile * kTile, pix_list_init());
+    if (want > t_scr.pix_cap) {
+      if (t_scr.d_pix) cudaFree(t_scr.d_pix);
+      t_scr.d_pix = nullptr;
+      t_scr.pix_cap = 0;
+      RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_pix, want * sizeof(int2)));
+      t_scr.pix_cap = want;
+    }
   }
+  const int pix_cap = (int)t_scr.pix_cap;
   RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->pix_count, 0, sizeof(int), s));
   if (n_smem > 0) {
     // tile order (the classify kernel appended them in arbitrary order):
@@ -2413,6 +2431,21 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
                                 cudaMemcpyDeviceToHost, s));
   RUBS_CUDA_TRY(cudaStreamSynchronize(s));
   hc.lap("overflow kernels (sync)");
+  if ((size_t)cnt > t_scr.pix_cap) {
+    // more precision-deferred pixels than the list holds (rare: fields with
+    // many small kernels inside huge-kernel blocks): grow the list to the
+    // count and run the deferred-tile passes again (same outputs, the
+    // skipped pixels now listed)
+    cudaFree(t_scr.d_pix);
+    t_scr.d_pix = nullptr;
+    t_scr.pix_cap = 0;
+    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_pix, (size_t)cnt * sizeof(int2)));
+    t_scr.pix_cap = (size_t)cnt;
+    if ((rc = handle_overflow_tiles<M, T>(I, F, D, n_ovf, s))) return rc;
+    RUBS_CUDA_TRY(cudaMemcpyAsync(&cnt, &t_scr.d_status->pix_count, sizeof(int),
+                                  cudaMemcpyDeviceToHost, s));
+    RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+  }
   cnt = std::min<int64_t>(cnt, (int64_t)t_scr.pix_cap);
   if (cnt > 0) {
     pixel_kernel<M, T><<<std::min((cnt + 7) / 8, t_scr.sms * 4), 256, kPixSmem, s>>>(
@@ -2668,7 +2701,8 @@ struct HostStage {
   cudaStream_t stream = nullptr;
   int device = -1;
 };
-thread_local HostStage t_stage;
+thread_local HostStage t_stage_dev[rubs_internal::kMaxDevices];
+#define t_stage (t_stage_dev[t_dev])
 
 int stage_buf(int k, size_t bytes, void **out) {
   if (bytes > t_stage.cap[k]) {
@@ -2682,11 +2716,10 @@ int stage_buf(int k, size_t bytes, void **out) {
 }
 
 int stage_stream(cudaStream_t *s) {
-  int dev = 0;
-  RUBS_CUDA_TRY(cudaGetDevice(&dev));
-  if (t_stage.device != dev || !t_stage.stream) {
-    t_stage = HostStage();
-    t_stage.device = dev;
+  int rc = ensure_scratch();  // selects the device's slot
+  if (rc) return rc;
+  if (!t_stage.stream) {
+    t_stage.device = t_dev;
     RUBS_CUDA_TRY(cudaStreamCreateWithFlags(&t_stage.stream, cudaStreamNonBlocking));
   }
   *s = t_stage.stream;
@@ -2710,14 +2743,14 @@ struct StreamSet {
   cudaStream_t h2d = nullptr, cmp = nullptr, d2h = nullptr;
   std::vector<cudaEvent_t> ev;
 };
-thread_local StreamSet t_ss;
+thread_local StreamSet t_ss_dev[rubs_internal::kMaxDevices];
+#define t_ss (t_ss_dev[t_dev])
 
 int stream_set(size_t nev) {
-  int dev = 0;
-  RUBS_CUDA_TRY(cudaGetDevice(&dev));
-  if (t_ss.device != dev) {
-    t_ss = StreamSet();
-    t_ss.device = dev;
+  int rc = ensure_scratch();  // selects the device's slot
+  if (rc) return rc;
+  if (t_ss.device != t_dev) {
+    t_ss.device = t_dev;
     RUBS_CUDA_TRY(cudaStreamCreateWithFlags(&t_ss.h2d, cudaStreamNonBlocking));
     RUBS_CUDA_TRY(cudaStreamCreateWithFlags(&t_ss.cmp, cudaStreamNonBlocking));
     RUBS_CUDA_TRY(cudaStreamCreateWithFlags(&t_ss.d2h, cudaStreamNonBlocking));

@@ -9,6 +9,13 @@ struct rubs_lut;
 
 namespace rubs_internal {
 
+// Thread-local host state (scratch buffers, streams, events) is kept per
+// CUDA device: a single-process caller that alternates devices keeps each
+// device's buffers and streams instead of dropping (leaking) them, and no
+// kernel is handed another device's memory.  Index = the current device,
+// checked against the bound by each translation unit's ensure function.
+constexpr int kMaxDevices = 16;
+
 // Record the thread's last error message (rubs_b200_last_error) and return
 // `code`.
 int set_error(int code, const std::string &msg);

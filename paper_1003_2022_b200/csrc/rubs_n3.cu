@@ -509,7 +509,9 @@ struct Scratch3 {
   size_t pass_cap[2] = {0, 0};
   bool attr = false;
 };
-thread_local Scratch3 t3;
+thread_local Scratch3 t3_dev[rubs_internal::kMaxDevices];
+thread_local int t3_cur = 0;  // set by ensure3() / stage3()
+#define t3 (t3_dev[t3_cur])
 
 template <int M, int T>
 int set_attr() {
@@ -521,8 +523,10 @@ int set_attr() {
 int ensure3() {
   int dev = 0;
   RUBS3_CUDA_TRY(cudaGetDevice(&dev));
-  if (t3.device != dev) {
-    t3 = Scratch3();
+  if (dev < 0 || dev >= rubs_internal::kMaxDevices)
+    return set_error(RUBS_ECUDA, "device index beyond the per-device state table");
+  t3_cur = dev;
+  if (t3.device != dev) {  // first call on this device
     t3.device = dev;
     RUBS3_CUDA_TRY(cudaMalloc(&t3.d_st, sizeof(Status3)));
     RUBS3_CUDA_TRY(cudaMallocHost(&t3.h_st, sizeof(Status3)));
@@ -702,13 +706,16 @@ struct Stage3 {
   cudaStream_t h2d = nullptr, cmp = nullptr, d2h = nullptr;
   cudaEvent_t ev[32];
 };
-thread_local Stage3 t_st3;
+thread_local Stage3 t_st3_dev[rubs_internal::kMaxDevices];
+#define t_st3 (t_st3_dev[t3_cur])
 
 int stage3(int k, size_t bytes, void **out) {
   int dev = 0;
   RUBS3_CUDA_TRY(cudaGetDevice(&dev));
-  if (t_st3.device != dev) {
-    t_st3 = Stage3();
+  if (dev < 0 || dev >= rubs_internal::kMaxDevices)
+    return set_error(RUBS_ECUDA, "device index beyond the per-device state table");
+  t3_cur = dev;
+  if (t_st3.device != dev) {  // first call on this device
     t_st3.device = dev;
     RUBS3_CUDA_TRY(cudaStreamCreateWithFlags(&t_st3.h2d, cudaStreamNonBlocking));
     RUBS3_CUDA_TRY(cudaStreamCreateWithFlags(&t_st3.cmp, cudaStreamNonBlocking));

@@ -49,15 +49,17 @@ struct TScratch {
   unsigned *d_hist = nullptr;      // 4 x 256 radix-select histograms
   unsigned *h_hist = nullptr;      // pinned
 };
-thread_local TScratch t_ts;
+thread_local TScratch t_ts_dev[rubs_internal::kMaxDevices];
+thread_local int t_ts_cur = 0;  // set by tbuf()
+#define t_ts (t_ts_dev[t_ts_cur])
 
 int tbuf(int k, size_t bytes, void **out) {
   int dev = 0;
   RT_CUDA_TRY(cudaGetDevice(&dev));
-  if (t_ts.device != dev) {
-    t_ts = TScratch();
-    t_ts.device = dev;
-  }
+  if (dev < 0 || dev >= rubs_internal::kMaxDevices)
+    return set_error(RUBS_ECUDA, "device index beyond the per-device state table");
+  t_ts_cur = dev;
+  t_ts.device = dev;
   if (bytes > t_ts.cap[k]) {
     if (t_ts.buf[k]) cudaFree(t_ts.buf[k]);
     t_ts.buf[k] = nullptr;
@@ -205,6 +207,13 @@ __global__ void __launch_bounds__(256) select_pick_kernel(int nr, int shift, Sel
 // values[r] = the element of rank ranks[r] (0-based, ascending) of tr
 int select_trace(const double *tr, int64_t n, const int64_t *ranks, int nr, double *values,
                  cudaStream_t s) {
+  {
+    int dev = 0;
+    RT_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= rubs_internal::kMaxDevices)
+      return set_error(RUBS_ECUDA, "device index beyond the per-device state table");
+    t_ts_cur = dev;
+  }
   if (!t_ts.d_hist) {
     RT_CUDA_TRY(cudaMalloc(&t_ts.d_hist, 4 * 256 * sizeof(unsigned) + sizeof(SelectState)));
     RT_CUDA_TRY(cudaMallocHost(&t_ts.h_hist, sizeof(SelectState)));
@@ -437,7 +446,13 @@ int rubs_b200_adaptive_smooth(const void *f, int f_dtype, int64_t H, int64_t W, 
   int rc;
   // buffers 0-5 are used by structure_tensor_impl; the pipeline's own go in
   // dedicated allocations of the same grow-only kind
-  static thread_local std::vector<std::pair<void *, size_t>> own(4, {nullptr, 0});
+  static thread_local std::vector<std::pair<void *, size_t>> own_dev[rubs_internal::kMaxDevices];
+  int dev = 0;
+  RT_CUDA_TRY(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= rubs_internal::kMaxDevices)
+    return set_error(RUBS_ECUDA, "device index beyond the per-device state table");
+  auto &own = own_dev[dev];
+  if (own.empty()) own.assign(4, {nullptr, 0});
   auto obuf = [&](int k, size_t bytes, double **o) -> int {
     if (bytes > own[k].second) {
       if (own[k].first) cudaFree(own[k].first);

@@ -139,9 +139,21 @@ def _host_image(f):
     return np.ascontiguousarray(arr)
 
 
-def _host_field(field, shape):
+def _unwrap_field(field):
+    """A ScaleField -- this package's or the reference's own ``rubs.ScaleField``
+    (callers of the shimmed reference pass theirs) -- is used through its
+    ``scales`` array; arrays and tensors pass through."""
     if isinstance(field, ScaleField):
-        field = field.scales
+        return field.scales
+    if not isinstance(field, np.ndarray) and not _is_torch(field):
+        scales = getattr(field, "scales", None)
+        if scales is not None:
+            return scales
+    return field
+
+
+def _host_field(field, shape):
+    field = _unwrap_field(field)
     fld = np.asarray(field, dtype=np.float64)
     if fld.shape == (4,):
         if not np.isfinite(fld).all():
@@ -207,8 +219,7 @@ def _filter_torch(f, field, iterations):
         f = f.contiguous()
     H, W = f.shape
     out = torch.empty((H, W), dtype=torch.float64, device=f.device)
-    if isinstance(field, ScaleField):
-        field = field.scales
+    field = _unwrap_field(field)
     uniform = False
     if _is_torch(field):
         fld = field.to(device=f.device, dtype=torch.float64)
@@ -263,10 +274,17 @@ def filter_space_invariant(f, a, iterations: int = 1):
 
 
 class DeviceLut:
-    """A ScaleLut uploaded to the current CUDA device (rubs_lut handle)."""
+    """A ScaleLut uploaded to one CUDA device (rubs_lut handle; the table
+    lives in that device's memory, so a handle serves that device only)."""
 
-    def __init__(self, lut: ScaleLut):
+    def __init__(self, lut: ScaleLut, device: int | None = None):
         self.lut = lut
+        torch = _torch()
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        with torch.cuda.device(self.device):
+            self._create(lut)
+
+    def _create(self, lut):
         L = _native.load()
         h = ctypes.c_void_p()
         rg = np.ascontiguousarray(lut.rho_grid, dtype=np.float64)
@@ -287,12 +305,25 @@ class DeviceLut:
 _LUT_CACHE: dict = {}
 
 
-def device_lut(lut: ScaleLut | None = None) -> DeviceLut:
+def _device_index(device) -> int:
+    torch = _torch()
+    if device is None:
+        return torch.cuda.current_device()
+    if isinstance(device, int):
+        return device
+    d = torch.device(device)
+    return d.index if d.index is not None else torch.cuda.current_device()
+
+
+def device_lut(lut: ScaleLut | None = None, device=None) -> DeviceLut:
+    """The device copy of ``lut`` on ``device`` (default: the current CUDA
+    device), cached per (table, device)."""
     lut = lut or default_lut()
-    key = id(lut)
+    dev = _device_index(device)
+    key = (id(lut), dev)
     hit = _LUT_CACHE.get(key)
     if hit is None or hit.lut is not lut:
-        hit = DeviceLut(lut)
+        hit = DeviceLut(lut, dev)
         _LUT_CACHE[key] = hit
     return hit
 
@@ -351,7 +382,7 @@ def filter_space_variant_params(f, size, elongation, orientation, lut: ScaleLut 
     """filter_space_variant(f, lookup_many(lut, size, elongation, orientation),
     iterations) with the lookup fused into the filter kernel."""
     iterations = int(iterations)
-    dl = device_lut(lut)
+    dl = device_lut(lut, f.device if _is_torch(f) and f.is_cuda else None)
     L = _native.load()
     if _is_torch(f):
         torch = _torch()

@@ -117,6 +117,78 @@ def exchange_rows(own, band, bands, needs, rank: int, group=None):
     return out
 
 
+class RowBandPlan:
+    """One rank's share of a row-band filter, planned once per field.
+
+    The halo reach (below, above) and the all-gather of every rank's needed
+    rows happen at construction, not per call.  ``run`` posts the halo
+    exchange (batched isend / irecv: NCCL runs it on its own stream), then
+    computes the band's INTERIOR output rows -- those whose reads lie inside
+    the rank's own rows -- while the transfer is in flight, and only then
+    waits for the halo and computes the rows next to the band edges.  The
+    output rows are split on the tile grid (``align``), so the shared-memory
+    tiles are the ones a single call would use.
+
+    ``filt(f_rows, f_row0, out_row0, out_rows, out)`` computes output rows
+    [out_row0, out_row0 + out_rows) into ``out`` from image rows
+    [f_row0, f_row0 + len(f_rows)) (the product: ``filter_rows_params``; the
+    gloo tests pass the CPU port)."""
+
+    def __init__(self, band, H: int, reach, group=None, align: int = TILE, device=None):
+        import torch.distributed as dist
+        world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.group = group
+        self.H = H
+        self.bands = band_bounds(H, world, align)
+        self.band = tuple(band)
+        assert self.band == self.bands[self.rank], "band must match band_bounds(H, world)[rank]"
+        below, above = int(reach[0]), int(reach[1])
+        self.needs = gather_needs(needed_rows(self.band, (0, 0, below, above), H), group, device)
+        self.sends, self.recvs = transfers(self.bands, self.needs, self.rank)
+        b0, b1 = self.band
+        lo = b0 if b0 == 0 else b0 + below + 1  # needed_rows' one-row slack
+        hi = b1 if b1 == H else b1 - above - 1
+        i0 = b0 + -(-(lo - b0) // align) * align
+        i1 = hi if hi == H else b0 + ((hi - b0) // align) * align
+        self.interior = (i0, i1) if i1 > i0 else None
+
+    def run(self, own, filt):
+        import torch
+        import torch.distributed as dist
+        b0, b1 = self.band
+        n0, n1 = self.needs[self.rank]
+        W = own.shape[1]
+        ops, bufs = [], []
+        for peer, s0, s1 in self.sends:
+            ops.append(dist.P2POp(dist.isend, own[s0 - b0:s1 - b0].contiguous(), peer, self.group))
+        for peer, r0, r1 in self.recvs:
+            buf = torch.empty((r1 - r0, W), dtype=own.dtype, device=own.device)
+            bufs.append((r0, r1, buf))
+            ops.append(dist.P2POp(dist.irecv, buf, peer, self.group))
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        out = torch.empty((b1 - b0, W), dtype=torch.float64, device=own.device)
+        if self.interior is not None:
+            i0, i1 = self.interior
+            filt(own, b0, i0, i1 - i0, out[i0 - b0:i1 - b0])
+        for req in reqs:
+            req.wait()
+        if self.interior is not None and not bufs and (n0, n1) == (b0, b1):
+            f_need = own
+        else:
+            f_need = torch.empty((n1 - n0, W), dtype=own.dtype, device=own.device)
+            lo, hi = max(b0, n0), min(b1, n1)
+            if lo < hi:
+                f_need[lo - n0:hi - n0] = own[lo - b0:hi - b0]
+            for r0, r1, buf in bufs:
+                f_need[r0 - n0:r1 - n0] = buf
+        parts = [(b0, b1)] if self.interior is None else [(b0, self.interior[0]), (self.interior[1], b1)]
+        for r0, r1 in parts:
+            if r1 > r0:
+                filt(f_need, n0, r0, r1 - r0, out[r0 - b0:r1 - b0])
+        return out
+
+
 # --- device calls (C ABI) --------------------------------------------------
 
 
@@ -126,13 +198,14 @@ def read_margins_params(size, elong, orient, row0: int, H: int, lut=None, iterat
     import torch
     from . import _native
     from .engine import _stream_handle, device_lut
-    dl = device_lut(lut)
+    dl = device_lut(lut, size.device)
     ps = [v.contiguous() for v in (size, elong, orient)]
     pdt = _native.RUBS_F32 if ps[0].dtype == torch.float32 else _native.RUBS_F64
     out4 = (ctypes.c_int * 4)()
-    _native.check(_native.load().rubs_b200_read_margins_params(
-        *(ctypes.c_void_p(p.data_ptr()) for p in ps), pdt, ps[0].shape[0], ps[0].shape[1],
-        ps[0].stride(0), H, row0, dl.handle, iterations, out4, _stream_handle()))
+    with torch.cuda.device(ps[0].device):
+        _native.check(_native.load().rubs_b200_read_margins_params(
+            *(ctypes.c_void_p(p.data_ptr()) for p in ps), pdt, ps[0].shape[0], ps[0].shape[1],
+            ps[0].stride(0), H, row0, dl.handle, iterations, out4, _stream_handle()))
     return tuple(out4)
 
 
@@ -143,7 +216,7 @@ def filter_rows_params(f_rows, f_row0: int, H: int, size, elong, orient, p_row0:
     import torch
     from . import _native
     from .engine import _stream_handle, device_lut
-    dl = device_lut(lut)
+    dl = device_lut(lut, f_rows.device)
     f_rows = f_rows.contiguous()
     ps = [v.contiguous() for v in (size, elong, orient)]
     W = f_rows.shape[1]
@@ -151,10 +224,11 @@ def filter_rows_params(f_rows, f_row0: int, H: int, size, elong, orient, p_row0:
         out = torch.empty((out_rows, W), dtype=torch.float64, device=f_rows.device)
     pdt = _native.RUBS_F32 if ps[0].dtype == torch.float32 else _native.RUBS_F64
     fdt = _native.RUBS_F32 if f_rows.dtype == torch.float32 else _native.RUBS_F64
-    _native.check(_native.load().rubs_b200_filter_params_rows(
-        ctypes.c_void_p(f_rows.data_ptr()), fdt, f_row0, f_rows.shape[0], W, f_rows.stride(0), H,
-        *(ctypes.c_void_p(p.data_ptr()) for p in ps), pdt, p_row0, ps[0].stride(0), dl.handle,
-        out_row0, out_rows, ctypes.c_void_p(out.data_ptr()), out.stride(0), _stream_handle()))
+    with torch.cuda.device(f_rows.device):
+        _native.check(_native.load().rubs_b200_filter_params_rows(
+            ctypes.c_void_p(f_rows.data_ptr()), fdt, f_row0, f_rows.shape[0], W, f_rows.stride(0), H,
+            *(ctypes.c_void_p(p.data_ptr()) for p in ps), pdt, p_row0, ps[0].stride(0), dl.handle,
+            out_row0, out_rows, ctypes.c_void_p(out.data_ptr()), out.stride(0), _stream_handle()))
     return out
 
 
@@ -174,20 +248,23 @@ def halo_bound_params(size, lut=None) -> tuple:
     return (m, m, m, m)
 
 
-def filter_row_band(f_own, band, H: int, size, elong, orient, lut=None, group=None):
+def row_band_plan(band, H: int, size, lut=None, group=None):
+    """The RowBandPlan of an N=4 LUT band (halo from ``halo_bound_params``)."""
+    m = halo_bound_params(size, lut)
+    return RowBandPlan(band, H, (m[2], m[3]), group, TILE, device=size.device)
+
+
+def filter_row_band(f_own, band, H: int, size, elong, orient, lut=None, group=None, plan=None):
     """One rank's share of a row-band filter: this rank holds image rows
     ``band`` (f_own) and the parameter rows of the same band; returns its
-    output rows.  Collective over the group (needs all-gather + halos)."""
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    bands = band_bounds(H, world)
-    assert tuple(band) == bands[rank], "band must match band_bounds(H, world)[rank]"
-    margins = halo_bound_params(size, lut)
-    needs = gather_needs(needed_rows(band, margins, H), group, device=f_own.device)
-    f_need = exchange_rows(f_own, band, bands, needs, rank, group)
-    return filter_rows_params(f_need, needs[rank][0], H, size, elong, orient, band[0], band[0],
-                              band[1] - band[0], lut)
+    output rows.  Collective over the group (halo exchange; the needs
+    all-gather too unless a ``plan`` from ``row_band_plan`` is given)."""
+    plan = plan or row_band_plan(band, H, size, lut, group)
+
+    def filt(f_rows, f_row0, r0, n, out):
+        filter_rows_params(f_rows, f_row0, H, size, elong, orient, band[0], r0, n, lut, out=out)
+
+    return plan.run(f_own, filt)
 
 
 # --- three directions (config 3) -------------------------------------------
@@ -207,9 +284,10 @@ def read_margins3_params(size, elong, orient):
     ps = [v.contiguous() for v in (size, elong, orient)]
     pdt = _native.RUBS_F32 if ps[0].dtype == torch.float32 else _native.RUBS_F64
     out2 = (ctypes.c_int * 2)()
-    _native.check(_native.load().rubs_b200_read_margins3_params(
-        *(ctypes.c_void_p(p.data_ptr()) for p in ps), pdt, ps[0].shape[0], ps[0].shape[1],
-        ps[0].stride(0), out2, _stream_handle()))
+    with torch.cuda.device(ps[0].device):
+        _native.check(_native.load().rubs_b200_read_margins3_params(
+            *(ctypes.c_void_p(p.data_ptr()) for p in ps), pdt, ps[0].shape[0], ps[0].shape[1],
+            ps[0].stride(0), out2, _stream_handle()))
     return tuple(out2)
 
 
@@ -235,10 +313,11 @@ def filter3_rows_params(f_rows, f_row0: int, H: int, size, elong, orient, p_row0
         out = torch.empty((out_rows, W), dtype=torch.float64, device=f_rows.device)
     pdt = _native.RUBS_F32 if ps[0].dtype == torch.float32 else _native.RUBS_F64
     fdt = _native.RUBS_F32 if f_rows.dtype == torch.float32 else _native.RUBS_F64
-    _native.check(_native.load().rubs_b200_filter3_params_rows(
-        ctypes.c_void_p(f_rows.data_ptr()), fdt, f_row0, f_rows.shape[0], W, f_rows.stride(0), H,
-        *(ctypes.c_void_p(p.data_ptr()) for p in ps), pdt, p_row0, ps[0].stride(0),
-        out_row0, out_rows, ctypes.c_void_p(out.data_ptr()), out.stride(0), _stream_handle()))
+    with torch.cuda.device(f_rows.device):
+        _native.check(_native.load().rubs_b200_filter3_params_rows(
+            ctypes.c_void_p(f_rows.data_ptr()), fdt, f_row0, f_rows.shape[0], W, f_rows.stride(0), H,
+            *(ctypes.c_void_p(p.data_ptr()) for p in ps), pdt, p_row0, ps[0].stride(0),
+            out_row0, out_rows, ctypes.c_void_p(out.data_ptr()), out.stride(0), _stream_handle()))
     return out
 
 
@@ -251,17 +330,18 @@ def reach3_bound_params(size) -> int:
     return int(math.ceil(0.5 * math.sqrt(3.0) * a)) + 2
 
 
-def filter3_row_band(f_own, band, H: int, size, elong, orient, group=None):
-    """One rank's share of an N=3 row-band filter (band = band_bounds(H,
-    world, TILE3)[rank]); collective over the group (needs all-gather +
-    halo exchange), like filter_row_band."""
-    import torch.distributed as dist
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    bands = band_bounds(H, world, TILE3)
-    assert tuple(band) == bands[rank], "band must match band_bounds(H, world, TILE3)[rank]"
+def row_band_plan3(band, H: int, size, group=None):
+    """The RowBandPlan of an N=3 band (64-row grid, reach_bound rows)."""
     reach = reach3_bound_params(size)
-    needs = gather_needs(needed_rows3(band, reach, H), group, device=f_own.device)
-    f_need = exchange_rows(f_own, band, bands, needs, rank, group)
-    return filter3_rows_params(f_need, needs[rank][0], H, size, elong, orient, band[0], band[0],
-                               band[1] - band[0])
+    return RowBandPlan(band, H, (reach - 1, reach - 1), group, TILE3, device=size.device)
+
+
+def filter3_row_band(f_own, band, H: int, size, elong, orient, group=None, plan=None):
+    """One rank's share of an N=3 row-band filter (band = band_bounds(H,
+    world, TILE3)[rank]); collective over the group, like filter_row_band."""
+    plan = plan or row_band_plan3(band, H, size, group)
+
+    def filt(f_rows, f_row0, r0, n, out):
+        filter3_rows_params(f_rows, f_row0, H, size, elong, orient, band[0], r0, n, out=out)
+
+    return plan.run(f_own, filt)

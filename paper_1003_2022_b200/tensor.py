@@ -144,7 +144,7 @@ def adaptive_smooth(f, noise_sigma: float, *, window_sigma: float = 1.5, iterati
         if not (0.0 < s_min <= s_max):
             raise ValueError("size_range must be positive and ordered")
     torch = _torch()
-    dl = device_lut(lut if lut is not None else default_lut())
+    dl = device_lut(lut if lut is not None else default_lut(), t.device)
     H, W = t.shape
     res = torch.empty((H, W), dtype=torch.float64, device=t.device)
     if H and W:

@@ -20,7 +20,7 @@ import math
 import numpy as np
 import pytest
 
-from conftest import golden
+from conftest import ROOT, golden
 from oracle import tensor_port
 import paper_1003_2022_b200 as rb
 from paper_1003_2022_b200 import tensor
@@ -228,3 +228,23 @@ def test_adaptive_smooth_large_kernels_take_the_overflow_path(cuda):
     j = tensor.structure_tensor(img, 1.5)
     exact = tensor_port.adaptive_smooth(img, 0.1, lut_tuple(), j=j, **kw)
     assert rel(got, exact) < REL_TOL
+
+
+def test_deferred_pixel_list_grows_on_demand(cuda, tmp_path):
+    # the per-pixel precision list starts small (RUBS_B200_PIX_LIST_INIT=8)
+    # and is grown to the deferred count, the deferred-tile passes rerun:
+    # outputs bitwise equal to a run whose list never overflows
+    import os
+    import subprocess
+    import sys
+    rng = np.random.default_rng(9)
+    img = tensor_port.stripe_image((160, 176), period=13.0, angle=0.9) + rng.normal(0.0, 0.1, (160, 176))
+    np.save(tmp_path / "img.npy", img)
+    ref = tensor.adaptive_smooth(img, 0.1, size_range=(0.5, 3000.0))
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1003_2022_b200 as rb; "
+            "img = np.load(%r); np.save(%r, rb.adaptive_smooth(img, 0.1, size_range=(0.5, 3000.0)))"
+            % (ROOT, str(tmp_path / "img.npy"), str(tmp_path / "out.npy")))
+    env = dict(os.environ, RUBS_B200_PIX_LIST_INIT="8")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert np.array_equal(np.load(tmp_path / "out.npy"), ref)

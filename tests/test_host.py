@@ -117,3 +117,34 @@ def test_workload_param_fields_respect_lut_domain():
     assert (th >= 0).all() and (th < math.pi).all()
     s = np.sqrt(size / 2.0)
     assert s.min() >= 2.0 - 1e-9 and s.max() <= 16.0 + 1e-9
+
+
+def test_device_lut_is_cached_per_device(monkeypatch):
+    """A LUT handle lives in one device's memory: the cache keys it by
+    (table, device), so a call on cuda:1 after cuda:0 gets its own upload
+    (mocked upload: no GPU here)."""
+    import torch
+    from paper_1003_2022_b200 import engine
+    made = []
+
+    class FakeDev:
+        def __init__(self, d):
+            self.d = d
+
+        def __enter__(self):
+            return self
+
+        def __exit__(self, *a):
+            return False
+
+    monkeypatch.setattr(engine.DeviceLut, "_create", lambda self, lut: made.append(self.device))
+    monkeypatch.setattr(torch.cuda, "device", FakeDev)
+    monkeypatch.setattr(torch.cuda, "current_device", lambda: 0)
+    monkeypatch.setattr(engine, "_LUT_CACHE", {})
+    lut = rb.default_lut()
+    a0 = engine.device_lut(lut, 0)
+    a1 = engine.device_lut(lut, "cuda:1")
+    assert a0 is not a1 and (a0.device, a1.device) == (0, 1)
+    assert engine.device_lut(lut) is a0  # current device 0
+    assert engine.device_lut(lut, torch.device("cuda", 1)) is a1
+    assert made == [0, 1]

@@ -155,3 +155,56 @@ def test_halo_bounds_cover_the_exact_margins(rng):
     rho3 = 1.0 + (np.minimum(elongation_bound3(th), 40.0) - 1.0) * rng.uniform(0.0, 0.95, n)
     a3 = np.maximum(port3.scales3_from_params(size, rho3, th), 0.05)
     assert sharding.reach3_bound_params(size) >= port3.support3(a3)[1]
+
+
+def _worker_plan(rank, world, port, f, field, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import port as cpu
+        H, W = f.shape
+        band = sharding.band_bounds(H, world)[rank]
+        fld = cpu.prepare_field(field, f.shape, 1)
+        _, _, below, above = cpu.read_margins(fld[band[0]:band[1]])
+        plan = sharding.RowBandPlan(band, H, (below, above))
+        calls = []
+
+        def filt(f_rows, f_row0, r0, n, out):
+            # the CPU port on the given rows only: rows it lacks are zero,
+            # so a wrong split or a missing halo row shows up as an error
+            calls.append((f_row0, f_rows.shape[0], r0, n))
+            out.copy_(torch.from_numpy(cpu.filter_window(f_rows.numpy(), f_row0, 0, field[r0:r0 + n], r0, 0)))
+
+        out = plan.run(torch.from_numpy(f[band[0]:band[1]].copy()), filt)
+        res = [None] * world
+        dist.all_gather_object(res, (out.numpy(), calls, plan.interior))
+        if rank == 0:
+            ret.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_band_plan_overlaps_interior_and_reproduces_whole_image():
+    """RowBandPlan: interior rows from the rank's own rows (before the halo
+    arrives), edge rows after the exchange; together == the whole image."""
+    rng = np.random.default_rng(11)
+    H, W = 320, 40
+    f = rng.random((H, W))
+    field = np.stack([np.full((H, W), 2.0), np.full((H, W), 6.0), np.full((H, W), 1.5),
+                      np.full((H, W), 4.0)], axis=-1)
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    procs = mp.start_processes(_worker_plan, args=(2, _free_port(), f, field, ret), nprocs=2,
+                               join=False, start_method="spawn")
+    res = ret.get(timeout=120)
+    procs.join()
+    import oracle
+    whole = oracle.dense(f, field)  # exact (the whole-image port has ~2e-9 of global-sum error here)
+    banded = np.concatenate([r[0] for r in res])
+    assert np.abs(banded - whole).max() < 1e-9 * np.abs(whole).max()  # the port's own sum error
+    for out, calls, interior in res:
+        assert interior is not None  # 160-row bands, ~7-row halos
+        # the interior call reads only the rank's own rows
+        assert calls[0][2] == interior[0] and calls[0][3] == interior[1] - interior[0]
+        assert interior[0] % 32 == 0 and (interior[1] % 32 == 0 or interior[1] == H)
+        assert len(calls) == 2  # interior + the one edge facing the other rank

@@ -28,3 +28,22 @@ def test_install_patches_all_bindings():
         assert rubs.engine.filter_space_variant is orig
     finally:
         sys.path.remove(REF)
+
+
+@pytest.mark.skipif(not os.path.isdir(REF), reason="reference package not present")
+def test_reference_scale_field_is_accepted():
+    # callers of the shimmed reference pass the reference's own ScaleField
+    # (reference tests/test_engine.py:84); the boundary unwraps it by duck type
+    import numpy as np
+    sys.path.insert(0, REF)
+    try:
+        import rubs
+        from paper_1003_2022_b200 import engine
+        sf = rubs.ScaleField.uniform((4, 5), [1.0, 2.0, 3.0, 4.0])
+        fld, uniform = engine._host_field(sf, (4, 5))
+        assert not uniform and fld.shape == (4, 5, 4) and np.all(fld[..., 2] == 3.0)
+        assert engine._unwrap_field(sf) is sf.scales
+        arr = np.ones((4, 5, 4))
+        assert engine._unwrap_field(arr) is arr
+    finally:
+        sys.path.remove(REF)
