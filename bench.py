@@ -404,6 +404,12 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
     L = _native.load()
+    dfma = None
+    if rank == 0:
+        # measured fp64 FMA peak of this GPU (the fp64 roofline's denominator)
+        tf, pms = ctypes.c_double(), ctypes.c_double()
+        if L.rubs_b200_dfma_peak(ctypes.byref(tf), ctypes.byref(pms)) == 0:
+            dfma = tf.value
     wk = Work(args.config, torch, device, rank, world)
     if rank == 0 and world == 1:
         _WK_FOR_CPU["wk"] = wk
@@ -490,11 +496,16 @@ def run_ours(args, rank, world, local):
         fp64 = smem = None
         dp_per_px = DP_INST_PER_PX.get(args.config)
         if dp_per_px:
-            peak_dp = 148 * 64 * sm_max * 1e6  # DP lane-ops / s at max clock
+            # DP lane-instructions / s: the measured DFMA rate (one DFMA per
+            # lane-instruction) when the probe ran, else 64 lanes x SMs x clock
+            peak_dp = dfma * 1e12 / 2.0 if dfma else 148 * 64 * sm_max * 1e6
             got_dp = dp_per_px * px_rank_step * wk.iters / kern_s
             fp64 = {"achieved_dp_ops_per_s": got_dp, "peak_dp_ops_per_s": peak_dp,
                     "frac": got_dp / peak_dp, "dp_inst_per_px": dp_per_px,
-                    "peak_at_clock_mhz": sm_max, "source": "ncu sm__sass_thread_inst_executed_op_fp64 per px"}
+                    "peak_source": "measured DFMA probe (rubs_b200_dfma_peak)" if dfma else
+                                   "148 SMs x 64 fp64 lanes x max clock",
+                    "measured_dfma_tflops": dfma,
+                    "source": "ncu sm__sass_thread_inst_executed_op_fp64 per px"}
         wf_per_px = SMEM_WF_PER_PX.get(args.config)
         if wf_per_px:
             peak_wf = 148 * sm_max * 1e6  # wavefronts / s at max clock
@@ -521,6 +532,7 @@ def run_ours(args, rank, world, local):
                          "binding_bound": BINDING.get(args.config, "shared-memory wavefronts and issue")},
             "fp64": fp64,
             "smem": smem,
+            "dfma_peak_tflops": dfma,
             "gpu_launches": launches,
             "launches_per_step": launches / max(1, args.steps),
             "kernel_share_of_step": all_ms.value / max(ms_total, 1e-9),

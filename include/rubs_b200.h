@@ -66,6 +66,12 @@ void rubs_b200_set_profiling(int enable);
 void rubs_b200_kernel_time(int kind, double *total_ms, int64_t *launches);
 void rubs_b200_reset_kernel_time(void);
 
+/* Measured fp64 FMA peak of the current device: a DFMA-chain kernel on every
+ * SM (8 independent chains per thread, all CTAs resident), timed with CUDA
+ * events; *tflops = 2 x DFMA / s.  The roofline denominator of bench.py's
+ * "fp64" object.  Returns a status code. */
+int rubs_b200_dfma_peak(double *tflops, double *ms);
+
 /*
  * Space-variant filter, per-pixel scale field.
  * Replaces engine.filter_space_variant (pkg/src/rubs/engine.py:265-324).

@@ -64,6 +64,7 @@ SIGNATURES = {
     "rubs_b200_set_profiling": (None, [_int]),
     "rubs_b200_kernel_time": (None, [_int, _dp, _lp]),
     "rubs_b200_reset_kernel_time": (None, []),
+    "rubs_b200_dfma_peak": (_int, [_dp, _dp]),
     "rubs_b200_filter": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _int, _i64, _int, _vp, _i64, _vp]),
     "rubs_b200_filter_host": (_int, [_vp, _int, _i64, _i64, _vp, _int, _int, _vp]),
     "rubs_b200_lut_create": (_int, [_vp, _vp, _vp, _int, _int, ctypes.POINTER(_vp)]),

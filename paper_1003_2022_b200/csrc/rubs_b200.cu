@@ -1594,6 +1594,23 @@ __global__ void __launch_bounds__(256, RUBS_BG_MINB) big_gather_kernel(FieldSpec
   if (lx == 0 && flags) atomicOr(&st->flags, flags);
 }
 
+// fp64 FMA peak probe (rubs_b200_dfma_peak): 8 independent DFMA chains per
+// thread hide the pipe latency; the result is stored so nothing is elided.
+__global__ void __launch_bounds__(256) dfma_probe_kernel(double *out, int iters) {
+  double x[8];
+  const double a = 1.0 + 1e-12 * threadIdx.x, b = 1e-9;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = 1.0 + k * 1e-3 + blockIdx.x * 1e-7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  out[(size_t)blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 // ---- standalone lookup (solver.lookup_many) ------------------------------
 __global__ void lookup_kernel(FieldSpec F, int64_t n, double *out, Status *st) {
   unsigned flags = 0;
@@ -2051,14 +2068,21 @@ struct CellAgg {
   int count;
 };
 
+#ifndef RUBS_BIG_SK
+#define RUBS_BIG_SK 2
+#endif
 // 0: shared-memory overflow pass; else the block side S.
 #ifndef RUBS_BIG_K
 #define RUBS_BIG_K 3.0
 #endif
-__host__ __device__ inline int plan_side(const OvfRec &r, int tw, int th) {
+// sk: S >= sk * h (a region of side S + 2h holds (1 + 2h / S)^2 elements
+// per output pixel: 4 at sk = 2, 2.25 at sk = 4), capped so the region's
+// width stays within the fused sweep's limit (big_rs234_kernel).
+__host__ __device__ inline int plan_side(const OvfRec &r, int tw, int th, int sk) {
   const int h = max(max(r.m[0], r.m[1]), max(r.m[2], r.m[3]));
   int S = 64;
-  while (S < 2 * h && S < 8192) S *= 2;
+  while (S < sk * h && S < 8192) S *= 2;
+  while (S > 64 && S >= 2 * h && S + r.m[0] + r.m[1] > kRsThreads * kRsCols) S /= 2;
   while (S > kTile) {
     const double RW = S + r.m[0] + r.m[1], RH = S + r.m[2] + r.m[3];
     const double mn = RW < RH ? RW : RH;
@@ -2086,12 +2110,12 @@ __global__ void plan_init_kernel(CellAgg *c, int n) {
 // counters: [0] records for the shared-memory pass, [1] used cells
 __global__ void plan_classify_kernel(const OvfRec *rec, int n, PlanGrid G, int tiles_x, int pw,
                                      int ph, CellAgg *cells, int *rec_cell, int2 *smem_list,
-                                     int *counters) {
+                                     int *counters, int sk) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const OvfRec r = rec[i];
     const int x0 = (r.tile % tiles_x) * kTile, y0 = (r.tile / tiles_x) * kTile;
     const int tw = min(kTile, pw - x0), th = min(kTile, ph - y0);
-    const int S = plan_side(r, tw, th);
+    const int S = plan_side(r, tw, th, sk);
     if (S == 0) {
       smem_list[atomicAdd(&counters[0], 1)] = make_int2(r.tile, (int)r.mask);
       rec_cell[i] = -1;
@@ -2185,6 +2209,16 @@ int plan_buffers(size_t ncell, size_t nrec) {
   return RUBS_OK;
 }
 
+// Block side factor sk of plan_side (RUBS_B200_BIG_SK overrides, A/B runs).
+int big_side_factor() {
+  static const int v = [] {
+    const char *e = std::getenv("RUBS_B200_BIG_SK");
+    const int k = e ? std::atoi(e) : 0;
+    return k >= 2 && k <= 16 ? k : RUBS_BIG_SK;
+  }();
+  return v;
+}
+
 template <int M, int T>
 int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int n_ovf,
                     cudaStream_t s) {
@@ -2215,7 +2249,8 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   RUBS_CUDA_TRY(cudaMemsetAsync(t_plan.counters, 0, 2 * sizeof(int), s));
   plan_init_kernel<<<gb, 256, 0, s>>>(t_plan.cells, ncell);
   plan_classify_kernel<<<rb, 256, 0, s>>>(rec, n_ovf, G, tiles_x, D.pw, D.ph, t_plan.cells,
-                                          t_plan.rec_cell, t_scr.d_list, t_plan.counters);
+                                          t_plan.rec_cell, t_scr.d_list, t_plan.counters,
+                                          big_side_factor());
   plan_compact_kernel<<<gb, 256, 0, s>>>(t_plan.cells, ncell, t_plan.used, t_plan.agg,
                                          t_plan.counters);
   t_launches += 3;
@@ -2281,17 +2316,23 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   // failure.
   int64_t budget = t_scr.big_budget > 0 ? t_scr.big_budget : kBigBatch;
   bool capped = false;
+  // All regions of a batch share one row pitch Pg (the batch's widest
+  // region, rounded up to 4 doubles), stacked by rows: the batch's scratch
+  // is one 2-D tensor of pitch Pg (a TMA-windowed gather over it was
+  // measured slower than the L1 gather: DESIGN.md §7).
   struct Batch {
     int r0, r1, t0, t1;
-    int64_t used;
+    int64_t used;  // Pg * rows
     int maxRH, maxL, maxRW;
+    int rows, Pg;
   };
+  auto pitch_of = [](int rw) { return (rw + 3) & ~3; };
   std::vector<BigRegion> regs;
   std::vector<CellMap> cm;
   std::vector<int> cm_cell;
   std::vector<Batch> batches;
   int ntl = 0;
-  Batch cur{0, 0, 0, 0, 0, 0, 0, 0};
+  Batch cur{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   int64_t max_used = 0;
  replan:
   regs.clear();
@@ -2299,16 +2340,22 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   cm_cell.clear();
   batches.clear();
   ntl = 0;
-  cur = Batch{0, 0, 0, 0, 0, 0, 0, 0};
+  cur = Batch{0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   max_used = 0;
   auto close_batch = [&]() {
     cur.r1 = (int)regs.size();
     cur.t1 = ntl;
     if (cur.r1 > cur.r0) {
+      cur.Pg = pitch_of(cur.maxRW);
+      cur.used = (int64_t)cur.Pg * cur.rows;
+      for (int r = cur.r0; r < cur.r1; ++r) {
+        regs[r].P = cur.Pg;
+        regs[r].off *= cur.Pg;  // held the row offset
+      }
       batches.push_back(cur);
       max_used = std::max(max_used, cur.used);
     }
-    cur = Batch{(int)regs.size(), 0, ntl, 0, 0, 0, 0, 0};
+    cur = Batch{(int)regs.size(), 0, ntl, 0, 0, 0, 0, 0, 0, 0};
   };
   for (int k : order) {
     const CellAgg &b = agg[k];
@@ -2322,10 +2369,11 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
       const double mn = std::min(g.RW, g.RH);
       g.l4 = (float)(0.25 * g.RW * (double)g.RH * mn * mn);
     }
-    const int64_t n = (int64_t)g.P * g.RH;
-    if (cur.used > 0 && cur.used + n > budget) close_batch();
-    g.off = cur.used;
-    cur.used += n;
+    if (cur.rows > 0 &&
+        (int64_t)pitch_of(std::max(cur.maxRW, g.RW)) * (cur.rows + g.RH) > budget)
+      close_batch();
+    g.off = cur.rows;  // row offset; element offset once the batch pitch is known
+    cur.rows += g.RH;
     cur.maxRH = std::max(cur.maxRH, g.RH);
     cur.maxL = std::max(cur.maxL, g.RH + g.RW - 1);
     cur.maxRW = std::max(cur.maxRW, g.RW);
@@ -2865,6 +2913,36 @@ FieldSpec lut_field(const rubs_lut *lut, const void *size, const void *elong, co
 extern "C" {
 
 const char *rubs_b200_version(void) { return "rubs_b200 0.1.0 (sm_100a)"; }
+
+int rubs_b200_dfma_peak(double *tflops, double *ms) {
+  int rc = ensure_scratch();
+  if (rc) return rc;
+  constexpr int kIters = 4096;
+  double *d = nullptr;
+  const int blocks = t_scr.sms * 8, threads = 256;
+  RUBS_CUDA_TRY(cudaMalloc(&d, (size_t)blocks * threads * sizeof(double)));
+  cudaEvent_t e0, e1;
+  RUBS_CUDA_TRY(cudaEventCreate(&e0));
+  RUBS_CUDA_TRY(cudaEventCreate(&e1));
+  dfma_probe_kernel<<<blocks, threads>>>(d, kIters);  // warm-up (clocks up)
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    RUBS_CUDA_TRY(cudaEventRecord(e0));
+    dfma_probe_kernel<<<blocks, threads>>>(d, kIters);
+    RUBS_CUDA_TRY(cudaEventRecord(e1));
+    RUBS_CUDA_TRY(cudaEventSynchronize(e1));
+    float t = 0.f;
+    RUBS_CUDA_TRY(cudaEventElapsedTime(&t, e0, e1));
+    best = std::min(best, t);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  const double fmas = (double)blocks * threads * 8.0 * kIters;
+  if (ms) *ms = best;
+  if (tflops) *tflops = 2.0 * fmas / (best * 1e-3) / 1e12;
+  return RUBS_OK;
+}
 
 void rubs_b200_set_profiling(int enable) { t_timer.on = enable != 0; }
 

@@ -196,21 +196,47 @@ def test_acceptance_02_impulse_response_is_sampled_kernel(cuda, rng):
         assert np.abs(out - kernel_at_offsets(a, (33, 33), (16, 16))).max() < 1e-12
 
 
-def test_acceptance_03_runtime_flat_across_kernel_sizes(cuda):
-    torch = cuda
-    f = torch.from_numpy(np.random.default_rng(1).uniform(0.0, 1.0, size=(512, 512))).cuda()
-    means = []
-    for s in (1.0, 2.0, 4.0, 8.0, 16.0):
+def _flat_cost_ms(torch, f, sizes, reps=5, calls=10):
+    """Median over `reps` of the mean device time (CUDA events) of `calls`
+    isotropic filters per size s (covariance trace; a = sqrt(3 s), N=4)."""
+    out = []
+    for s in sizes:
         a = np.full(4, math.sqrt(3.0 * s))
         rb.filter_space_invariant(f, a)
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0.record()
-        for _ in range(20):
-            rb.filter_space_invariant(f, a)
-        t1.record()
-        torch.cuda.synchronize()
-        means.append(t0.elapsed_time(t1) / 20)
-    assert max(means) / min(means) < 1.5, means
+        laps = []
+        for _ in range(reps):
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record()
+            for _ in range(calls):
+                rb.filter_space_invariant(f, a)
+            t1.record()
+            torch.cuda.synchronize()
+            laps.append(t0.elapsed_time(t1) / calls)
+        out.append(float(np.median(laps)))
+    return out
+
+
+def test_acceptance_03_runtime_flat_across_kernel_sizes(cuda):
+    # test_acceptance.py:94-108 (max/min mean time < 1.15 over s = 1..16),
+    # timed on the device at 2048^2 (at 512^2 a call is launch-bound: ~20 us)
+    torch = cuda
+    f = torch.from_numpy(np.random.default_rng(1).uniform(0.0, 1.0, size=(2048, 2048))).cuda()
+    means = _flat_cost_ms(torch, f, (1.0, 2.0, 4.0, 8.0, 16.0))
+    print("flat cost ms, s = 1..16:", [round(m, 4) for m in means])
+    assert max(means) / min(means) < 1.15, means
+
+
+@pytest.mark.xfail(strict=False, reason="large kernels (s >= 256) take the global-scratch block path: "
+                   "measured max/min ~4 over s = 1..16384 at 2048^2 (DESIGN.md §4, flat-cost table)")
+def test_acceptance_03_flat_up_to_large_kernels(cuda):
+    # the same contract extended to s = 16384 (a ~ 222, support ~540 px)
+    torch = cuda
+    f = torch.from_numpy(np.random.default_rng(1).uniform(0.0, 1.0, size=(2048, 2048))).cuda()
+    sizes = (1.0, 16.0, 256.0, 1024.0, 4096.0, 16384.0)
+    means = _flat_cost_ms(torch, f, sizes, reps=3, calls=5)
+    print("flat cost ms:", dict(zip(sizes, [round(m, 4) for m in means])),
+          "max/min", round(max(means) / min(means), 2))
+    assert max(means) / min(means) < 1.15, means
 
 
 def test_acceptance_07_gaussian_correlation_of_the_device_kernel(cuda):
