@@ -1501,45 +1501,51 @@ __global__ void __launch_bounds__(256) big_line_kernel(const BigRegion *R, doubl
 // separate line sweeps read and wrote the region three times.  Same adds in
 // the same order per element as the line sweeps.
 constexpr int kRsThreads = 512, kRsCols = 9;  // regions up to 4608 columns
-constexpr int kRsSmem = 6 * (kRsThreads * kRsCols + 2) * 8;
-__global__ void __launch_bounds__(kRsThreads, 1)
+// The sweep is latency-bound (one barrier per row); narrower batches run
+// more resident CTAs per SM (NT threads x NC columns, MINB CTAs per SM):
+// RS3's previous row is the thread's own column (registers), only RS2 / RS4
+// read neighbours through shared memory (4 vectors instead of 6).
+constexpr int rs_smem(int rw) { return 4 * (rw + 2) * 8; }
+template <int NT, int NC, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
     big_rs234_kernel(const BigRegion *R, double *scratch, Status *st) {
   extern __shared__ double prow[];
   const BigRegion g = R[blockIdx.x];
   const int W2 = g.RW + 2;  // entry c + 1 holds column c; 0 and RW + 1 stay zero
-  double *A = prow, *B = prow + 3 * W2;
-  for (int i = threadIdx.x; i < 6 * W2; i += kRsThreads) prow[i] = 0.0;
+  double *A = prow, *B = prow + 2 * W2;  // [RS2 | RS4] of row r - 1, of row r
+  for (int i = threadIdx.x; i < 4 * W2; i += NT) prow[i] = 0.0;
   double *base = scratch + g.off;
   // RS1 rows are prefetched two rows ahead (one row of lead did not cover
   // the load latency: the per-row time is a barrier plus a few shared ops)
-  double na[kRsCols], nb[kRsCols];
+  double na[NC], nb[NC], a3[NC];
 #pragma unroll
-  for (int k = 0; k < kRsCols; ++k) {
-    const int c = threadIdx.x + k * kRsThreads;
+  for (int k = 0; k < NC; ++k) {
+    const int c = threadIdx.x + k * NT;
     na[k] = (c < g.RW && g.RH > 0) ? base[c] : 0.0;
     nb[k] = (c < g.RW && g.RH > 1) ? base[g.P + c] : 0.0;
+    a3[k] = 0.0;
   }
   __syncthreads();
   unsigned gh = 0;
-  auto row_step = [&](int r, double (&buf)[kRsCols]) {
+  auto row_step = [&](int r, double (&buf)[NC]) {
     double *row = base + (int64_t)r * g.P;
-    double cur[kRsCols];
+    double cur[NC];
 #pragma unroll
-    for (int k = 0; k < kRsCols; ++k) {
+    for (int k = 0; k < NC; ++k) {
       cur[k] = buf[k];
-      const int c = threadIdx.x + k * kRsThreads;
+      const int c = threadIdx.x + k * NT;
       buf[k] = (c < g.RW && r + 2 < g.RH) ? row[2 * (int64_t)g.P + c] : 0.0;  // row r + 2
     }
 #pragma unroll
-    for (int k = 0; k < kRsCols; ++k) {
-      const int c = threadIdx.x + k * kRsThreads;
+    for (int k = 0; k < NC; ++k) {
+      const int c = threadIdx.x + k * NT;
       if (c < g.RW) {
-        const double v2 = cur[k] + A[c];              // RS2: + row r-1 at c-1
-        const double v3 = v2 + A[W2 + c + 1];         // RS3: + row r-1 at c
-        const double v4 = v3 + A[2 * W2 + c + 2];     // RS4: + row r-1 at c+1
+        const double v2 = cur[k] + A[c];           // RS2: + row r-1 at c-1
+        const double v3 = v2 + a3[k];              // RS3: + row r-1 at c
+        const double v4 = v3 + A[W2 + c + 2];      // RS4: + row r-1 at c+1
         B[c + 1] = v2;
-        B[W2 + c + 1] = v3;
-        B[2 * W2 + c + 1] = v4;
+        a3[k] = v3;
+        B[W2 + c + 1] = v4;
         row[c] = v4;
         gh = max(gh, (unsigned)__double2hiint(v4) & 0x7fffffffu);
       }
@@ -1561,14 +1567,27 @@ __global__ void __launch_bounds__(kRsThreads, 1)
 #define RUBS_BG_MINB 4  // 64 registers, 4 CTAs per SM: more loads in flight (config 5: -15 %)
 #endif
 template <int MODE>
+// Tiles are taken from an atomic counter in slot order (block raster): the
+// resident CTAs stay on a compact run of tiles, so the region rows their
+// vertices read stay in L2 (static striding let CTAs drift apart).
 __global__ void __launch_bounds__(256, RUBS_BG_MINB) big_gather_kernel(FieldSpec F, DomainSpec D, int tiles_x,
                                                          const BigTile *tl, int nt,
                                                          const BigRegion *R, const double *scratch,
-                                                         Status *st, int2 *pix, int pix_cap) {
+                                                         Status *st, int2 *pix, int pix_cap,
+                                                         int *next) {
+  __shared__ int s_next;
   unsigned flags = 0;
   const int lx = threadIdx.x & 31, ly = threadIdx.x >> 5;
-  for (int i = blockIdx.x; i < nt; i += gridDim.x) {
+  for (int i = blockIdx.x;;) {
+    if (next != nullptr) {
+      if (threadIdx.x == 0) s_next = atomicAdd(next, 1);
+      __syncthreads();
+      i = s_next;
+      __syncthreads();
+    }
+    if (i >= nt) break;
     const BigTile bt = tl[i];
+    if (next == nullptr) i += gridDim.x;
     if (bt.tile < 0) continue;  // a gap of the block's tile raster
     const BigRegion g = R[bt.region];
     const int x0 = (bt.tile % tiles_x) * kTile, y0 = (bt.tile / tiles_x) * kTile;
@@ -1776,6 +1795,7 @@ struct Scratch {
   size_t pass_cap[2] = {0, 0};
   double *d_aslot = nullptr;     // wide kernel: per-(SM, slot) scale-vectors
   unsigned *d_slotmask = nullptr;
+  int *d_next = nullptr;  // tile counter of the large-halo gather
   bool attr_set = false;
 };
 thread_local Scratch t_scr_dev[rubs_internal::kMaxDevices];
@@ -1796,6 +1816,7 @@ int ensure_scratch() {
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_aslot, (size_t)kMaxSmId * kSlotsPerSm * kWideW * kWideH * 4 *
                                                  sizeof(double)));
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_slotmask, kMaxSmId * sizeof(unsigned)));
+    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_next, sizeof(int)));
     RUBS_CUDA_TRY(cudaMemset(t_scr.d_slotmask, 0, kMaxSmId * sizeof(unsigned)));
     {  // log table of log_ge1 (rubs_device.cuh)
       double2 tab[128];
@@ -1836,8 +1857,16 @@ int ensure_scratch() {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, wide_smem<3>()));
     RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<kModeLut, 0, wide_threads<3>(), 2, 3>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, wide_smem<3>()));
-    RUBS_CUDA_TRY(cudaFuncSetAttribute(big_rs234_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, kRsSmem));
+    RUBS_CUDA_TRY(cudaFuncSetAttribute(big_rs234_kernel<128, 9, 4>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, rs_smem(128 * 9)));
+    RUBS_CUDA_TRY(cudaFuncSetAttribute(big_rs234_kernel<256, 6, 3>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, rs_smem(256 * 6)));
+    RUBS_CUDA_TRY(cudaFuncSetAttribute(big_rs234_kernel<256, 9, 2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, rs_smem(256 * 9)));
+    RUBS_CUDA_TRY(cudaFuncSetAttribute(big_rs234_kernel<384, 7, 2>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, rs_smem(384 * 7)));
+    RUBS_CUDA_TRY(cudaFuncSetAttribute(big_rs234_kernel<512, 9, 1>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, rs_smem(512 * 9)));
     t_scr.attr_set = true;
   }
   return RUBS_OK;
@@ -2447,8 +2476,17 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
     // the three line sweeps (parallel over every line of every region) win
     if (bt.maxRW <= kRsThreads * kRsCols && nreg * kRsFewDiv >= t_scr.sms &&
         !std::getenv("RUBS_B200_LINE_SWEEPS")) {
-      big_rs234_kernel<<<nreg, kRsThreads, 6 * (bt.maxRW + 2) * 8, s>>>(R, t_scr.d_big,
-                                                                         t_scr.d_status);
+      const int rw = bt.maxRW, sm = rs_smem(rw);
+      if (rw <= 128 * 9)
+        big_rs234_kernel<128, 9, 4><<<nreg, 128, sm, s>>>(R, t_scr.d_big, t_scr.d_status);
+      else if (rw <= 256 * 6)
+        big_rs234_kernel<256, 6, 3><<<nreg, 256, sm, s>>>(R, t_scr.d_big, t_scr.d_status);
+      else if (rw <= 256 * 9)
+        big_rs234_kernel<256, 9, 2><<<nreg, 256, sm, s>>>(R, t_scr.d_big, t_scr.d_status);
+      else if (rw <= 384 * 7)
+        big_rs234_kernel<384, 7, 2><<<nreg, 384, sm, s>>>(R, t_scr.d_big, t_scr.d_status);
+      else
+        big_rs234_kernel<512, 9, 1><<<nreg, 512, sm, s>>>(R, t_scr.d_big, t_scr.d_status);
       t_launches -= 2;
     } else {
       big_line_kernel<2><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
@@ -2458,9 +2496,14 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
       big_line_kernel<4><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
                                                                             t_scr.d_status);
     }
+    int *next = nullptr;
+    if (!std::getenv("RUBS_B200_GATHER_STATIC")) {
+      next = t_scr.d_next;
+      RUBS_CUDA_TRY(cudaMemsetAsync(next, 0, sizeof(int), s));
+    }
     big_gather_kernel<M><<<std::min(ntl, t_scr.sms * 8), 256, 0, s>>>(
         F, D, tiles_x, t_scr.d_btiles + bt.t0, ntl, R, t_scr.d_big, t_scr.d_status, t_scr.d_pix,
-        pix_cap);
+        pix_cap, next);
     t_launches += 5;
     RUBS_CUDA_TRY(cudaGetLastError());
   }
