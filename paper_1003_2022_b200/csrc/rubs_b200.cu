@@ -1419,18 +1419,31 @@ __global__ void __launch_bounds__(256) big_fill_rs1_kernel(ImageSpec I, const Bi
   const bool rin = ir >= 0 && ir < I.h;
   const int64_t gi = (int64_t)ir * I.ld;
   double carry = 0.0;
-  for (int c0 = 0; c0 < g.RW; c0 += 32) {
-    const int c = c0 + lane;
-    const int ic = g.rc0 + c - I.col0;
-    double v = (rin && c < g.RW && ic >= 0 && ic < I.w) ? load_px<DT>(I.f, gi + ic) : 0.0;
+  // four chunks of 32 columns per step: their loads are in flight together
+  // (one chunk at a time left the warp waiting on each load's latency)
+  for (int c0 = 0; c0 < g.RW; c0 += 128) {
+    double v[4];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const double t = __shfl_up_sync(0xffffffffu, v, o);
-      if (lane >= o) v += t;
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + 32 * u + lane;
+      const int ic = g.rc0 + c - I.col0;
+      v[u] = (rin && c < g.RW && ic >= 0 && ic < I.w) ? load_px<DT>(I.f, gi + ic) : 0.0;
     }
-    v += carry;
-    if (c < g.RW) dst[c] = v;
-    carry = __shfl_sync(0xffffffffu, v, 31);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, v[u], o);
+        if (lane >= o) v[u] += t;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + 32 * u + lane;
+      v[u] += carry;
+      if (c < g.RW) dst[c] = v[u];
+      carry = __shfl_sync(0xffffffffu, v[u], 31);
+    }
   }
 }
 
