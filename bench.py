@@ -365,11 +365,15 @@ class Work:
             houts = [torch.empty((self.H, self.W), dtype=torch.float64, pin_memory=True).numpy()
                      for _ in range(2)]
 
+            m = len(self.sets)
+            bf = [hsets[j % k][0] for j in range(m)]
+            bp = [[hsets[j % k][1][q] for j in range(m)] for q in range(3)]
+            bo = [houts[j % 2] for j in range(m)]
+
             def call():
-                for j in range(len(self.sets)):
-                    hf, hp = hsets[j % k]
-                    rb.filter_space_variant_params(hf, *hp, lut=self.lut, iterations=2, out=houts[j % 2])
-                return houts[0]
+                # the batch entry point: image j+1 uploads while j is filtered
+                # and j-1 returns (rubs_b200_filter_params_batch_host)
+                return rb.filter_space_variant_params_batch(bf, *bp, lut=self.lut, iterations=2, outs=bo)
             one = hsets[0][0].nbytes + sum(p.nbytes for p in hsets[0][1])
             return call, one * len(self.sets), self.H * self.W * 8 * len(self.sets), \
                 float(self.H * self.W) * len(self.sets)
@@ -392,6 +396,38 @@ class Work:
         hfl = pinned(s["field"], torch.float64).numpy()
         return (lambda: rb.filter_space_variant(hf, hfl, self.iters, out=hout)), hf.nbytes + hfl.nbytes, \
             hout.nbytes, float(self.H * self.W)
+
+
+def pcie_copy_seconds(torch, h2d_bytes, d2h_bytes, device, chunk=256 << 20):
+    """Seconds for bare pinned copies of h2d_bytes up and d2h_bytes down,
+    concurrently on two streams (the e2e leg's PCIe bound)."""
+    try:
+        hu = torch.empty(chunk, dtype=torch.uint8, pin_memory=True)
+        hd = torch.empty(chunk, dtype=torch.uint8, pin_memory=True)
+        du = torch.empty(chunk, dtype=torch.uint8, device=device)
+        dd = torch.empty(chunk, dtype=torch.uint8, device=device)
+        su, sd = torch.cuda.Stream(device), torch.cuda.Stream(device)
+
+        def run():
+            with torch.cuda.stream(su):
+                left = h2d_bytes
+                while left > 0:
+                    n = min(chunk, left)
+                    du[:n].copy_(hu[:n], non_blocking=True)
+                    left -= n
+            with torch.cuda.stream(sd):
+                left = d2h_bytes
+                while left > 0:
+                    n = min(chunk, left)
+                    hd[:n].copy_(dd[:n], non_blocking=True)
+                    left -= n
+            torch.cuda.synchronize(device)
+        run()
+        t0 = time.perf_counter()
+        run()
+        return time.perf_counter() - t0
+    except RuntimeError:
+        return None
 
 
 def run_ours(args, rank, world, local):
@@ -467,7 +503,13 @@ def run_ours(args, rank, world, local):
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         px_all = wk.px_per_step if (wk.row_bands or args.config == "4") else px_call * world
+        # the PCIe bound of the same bytes: bare concurrent pinned copies
+        # (H2D on one stream, D2H on another), outside the timed region
+        bound_s = pcie_copy_seconds(torch, h2d, d2h, device)
         e2e = {"value": px_all * ksteps / float(te.item()) / 1e9, "unit": UNIT,
+               "pcie_bound_value": px_all / bound_s / 1e9 if bound_s else None,
+               "pcie_bound_note": "same metric if the call took only the bare concurrent pinned copies of its "
+                                  "input and result bytes",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "steps": ksteps, "host_buffers": "pinned (inputs and result)",
                "timing": "wall clock around blocking API calls, max over ranks"

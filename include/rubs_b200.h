@@ -135,6 +135,24 @@ int rubs_b200_filter_params_host(const void *f, int f_dtype, int64_t H, int64_t 
                                  double *out);
 
 /*
+ * A batch of n same-shape images through the fused path, host buffers
+ * (BASELINE config 4: the per-image reference call engine.py:265, repeated).
+ * Image i's inputs go up while image i-1 is filtered and image i-2's result
+ * comes back (two device slots, copy and compute streams overlapped), so a
+ * batch runs at the larger of the PCIe and the compute time per image.
+ * Errors are reported for the first failing image (its index in *failed,
+ * -1 if none); pinned host buffers let the copies run asynchronously.
+ *   f[i]                       host H x W image i (f_dtype)
+ *   size[i]/elong[i]/orient[i] host H x W parameter planes (p_dtype)
+ *   out[i]                     host H x W float64 result
+ */
+int rubs_b200_filter_params_batch_host(int n, const void *const *f, int f_dtype, int64_t H,
+                                       int64_t W, const void *const *size,
+                                       const void *const *elong, const void *const *orient,
+                                       int p_dtype, const rubs_lut *lut, int iterations,
+                                       double *const *out, int *failed);
+
+/*
  * Row bands (multi-GPU sharding of one large image): one pass
  * over output rows [out_row0, out_row0 + out_rows) of an H_total x W image.
  *   f          device rows [f_row0, f_row0 + f_rows) of the image (the band

@@ -22,6 +22,7 @@ from .engine import (
     filter_space_invariant,
     filter_space_variant,
     filter_space_variant_params,
+    filter_space_variant_params_batch,
     filter_space_variant3,
     filter_space_variant3_params,
     interpolate,
@@ -72,6 +73,7 @@ __all__ = [
     "filter_space_invariant",
     "filter_space_variant",
     "filter_space_variant_params",
+    "filter_space_variant_params_batch",
     "filter_space_variant3",
     "filter_space_variant3_params",
     "scales3_many",

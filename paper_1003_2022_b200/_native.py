@@ -74,6 +74,8 @@ SIGNATURES = {
                                        _int, _vp, _i64, _vp]),
     "rubs_b200_filter_params_host": (_int, [_vp, _int, _i64, _i64, _vp, _vp, _vp, _int, _vp, _int,
                                             _vp]),
+    "rubs_b200_filter_params_batch_host": (_int, [_int, _vp, _int, _i64, _i64, _vp, _vp, _vp, _int, _vp,
+                                                  _int, _vp, ctypes.POINTER(_int)]),
     "rubs_b200_filter_rows": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _vp, _i64, _i64, _i64,
                                      _i64, _vp, _i64, _vp]),
     "rubs_b200_filter_params_rows": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _vp, _vp, _vp, _int,

@@ -3185,6 +3185,68 @@ int rubs_b200_filter_params_host(const void *f, int f_dtype, int64_t H, int64_t 
   return RUBS_OK;
 }
 
+int rubs_b200_filter_params_batch_host(int n, const void *const *f, int f_dtype, int64_t H,
+                                       int64_t W, const void *const *size,
+                                       const void *const *elong, const void *const *orient,
+                                       int p_dtype, const rubs_lut *lut, int iterations,
+                                       double *const *out, int *failed) {
+  if (failed) *failed = -1;
+  if (n < 0) return set_error(RUBS_EVALUE, "negative batch size");
+  if (f_dtype != RUBS_F32 && f_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (p_dtype != RUBS_F32 && p_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (!lut) return set_error(RUBS_EVALUE, "lut is NULL");
+  if (iterations < 1) return set_error(RUBS_EVALUE, "iterations must be >= 1");
+  if (H < 0 || W < 0) return set_error(RUBS_EVALUE, "image must be 2-D");
+  if (n == 0 || H == 0 || W == 0) return RUBS_OK;
+  int rc = stream_set(6);  // ev: [0, 2) inputs landed, [2, 4) filtered, [4, 6) returned
+  if (rc) return rc;
+  const cudaStream_t h2d = t_ss.h2d, cmp = t_ss.cmp, d2h = t_ss.d2h;
+  const size_t esz = f_dtype == RUBS_F64 ? 8 : 4, psz = p_dtype == RUBS_F64 ? 8 : 4;
+  const size_t npx = (size_t)H * W;
+  // two slots of device inputs / outputs (stage buffers 0-2 and 3-4 + pass)
+  void *df[2], *dp[2], *dout[2];
+  if ((rc = stage_buf(0, npx * esz, &df[0]))) return rc;
+  if ((rc = stage_buf(1, npx * psz * 3, &dp[0]))) return rc;
+  if ((rc = stage_buf(2, npx * 8, &dout[0]))) return rc;
+  if ((rc = stage_buf(3, npx * esz + npx * psz * 3, &df[1]))) return rc;
+  dp[1] = static_cast<char *>(df[1]) + npx * esz;
+  if ((rc = stage_buf(4, npx * 8, &dout[1]))) return rc;
+  auto upload = [&](int i) -> int {
+    const int k = i & 1;
+    char *pb = static_cast<char *>(dp[k]);
+    if (i >= 2) RUBS_CUDA_TRY(cudaStreamWaitEvent(h2d, t_ss.ev[2 + k], 0));  // slot's inputs consumed
+    RUBS_CUDA_TRY(cudaMemcpyAsync(df[k], f[i], npx * esz, cudaMemcpyHostToDevice, h2d));
+    RUBS_CUDA_TRY(cudaMemcpyAsync(pb, size[i], npx * psz, cudaMemcpyHostToDevice, h2d));
+    RUBS_CUDA_TRY(cudaMemcpyAsync(pb + npx * psz, elong[i], npx * psz, cudaMemcpyHostToDevice, h2d));
+    RUBS_CUDA_TRY(cudaMemcpyAsync(pb + 2 * npx * psz, orient[i], npx * psz, cudaMemcpyHostToDevice, h2d));
+    RUBS_CUDA_TRY(cudaEventRecord(t_ss.ev[k], h2d));
+    return RUBS_OK;
+  };
+  if ((rc = upload(0))) return rc;
+  for (int i = 0; i < n; ++i) {
+    const int k = i & 1;
+    // the next image's inputs go up while this one is filtered
+    if (i + 1 < n && (rc = upload(i + 1))) return rc;
+    RUBS_CUDA_TRY(cudaStreamWaitEvent(cmp, t_ss.ev[k], 0));
+    if (i >= 2) RUBS_CUDA_TRY(cudaStreamWaitEvent(cmp, t_ss.ev[4 + k], 0));  // slot's result returned
+    char *pb = static_cast<char *>(dp[k]);
+    rc = rubs_b200_filter_params(df[k], f_dtype, H, W, W, pb, pb + npx * psz, pb + 2 * npx * psz,
+                                 p_dtype, W, lut, iterations, static_cast<double *>(dout[k]), W, cmp);
+    if (rc) {
+      if (failed) *failed = i;
+      cudaStreamSynchronize(h2d);
+      cudaStreamSynchronize(d2h);
+      return rc;
+    }
+    RUBS_CUDA_TRY(cudaEventRecord(t_ss.ev[2 + k], cmp));
+    RUBS_CUDA_TRY(cudaStreamWaitEvent(d2h, t_ss.ev[2 + k], 0));
+    RUBS_CUDA_TRY(cudaMemcpyAsync(out[i], dout[k], npx * 8, cudaMemcpyDeviceToHost, d2h));
+    RUBS_CUDA_TRY(cudaEventRecord(t_ss.ev[4 + k], d2h));
+  }
+  RUBS_CUDA_TRY(cudaStreamSynchronize(d2h));
+  return RUBS_OK;
+}
+
 int rubs_b200_filter_rows(const void *f, int f_dtype, int64_t f_row0, int64_t f_rows, int64_t W,
                           int64_t ld_f, int64_t H_total, const double *field, int64_t field_row0,
                           int64_t ld_field, int64_t out_row0, int64_t out_rows, double *out,

@@ -438,6 +438,62 @@ def filter_space_variant_params(f, size, elongation, orientation, lut: ScaleLut 
     return out
 
 
+def filter_space_variant_params_batch(images, sizes, elongations, orientations,
+                                      lut: ScaleLut | None = None, iterations: int = 1, *, outs=None):
+    """``[filter_space_variant_params(f, s, r, t, lut, iterations) for ...]``
+    over a batch of same-shape host images (BASELINE config 4), pipelined
+    on the device: image i+1's inputs upload while image i is filtered and
+    image i-1's result comes back (rubs_b200_filter_params_batch_host).
+    ``outs``: optional list of C-contiguous float64 host arrays (pinned
+    memory lets every copy run asynchronously).  Returns the list of
+    results.  An error names the first failing image."""
+    iterations = int(iterations)
+    n = len(images)
+    if not (len(sizes) == len(elongations) == len(orientations) == n):
+        raise ValueError("batch lists must have the same length")
+    if iterations < 1:
+        raise ValueError("iterations must be >= 1")
+    if n == 0:
+        return []
+    imgs = [_host_image(f) for f in images]
+    H, W = imgs[0].shape
+    if any(im.shape != (H, W) for im in imgs) or len({im.dtype for im in imgs}) != 1:
+        raise ValueError("batch images must share one shape and dtype")
+    params = []
+    pdt = None
+    for s, r, t in zip(sizes, elongations, orientations):
+        (ps, pr, pt), shape, dt = _params_host(s, r, t)
+        if shape != (H, W):
+            ps, pr, pt = (np.ascontiguousarray(np.broadcast_to(v, (H, W))) for v in (ps, pr, pt))
+        pdt = pdt or dt
+        if dt != pdt:
+            ps, pr, pt = (np.ascontiguousarray(v, dtype=np.float64) for v in (ps, pr, pt))
+            pdt = np.float64
+        params.append((ps, pr, pt))
+    if pdt == np.float64:
+        params = [tuple(np.ascontiguousarray(v, dtype=np.float64) for v in p) for p in params]
+    outs = [_host_out(o, (H, W)) for o in (outs or [None] * n)]
+    if H == 0 or W == 0:
+        return outs
+    dl = device_lut(lut)
+    L = _native.load()
+
+    def arr(ptrs):
+        return (ctypes.c_void_p * n)(*[a.ctypes.data for a in ptrs])
+    failed = ctypes.c_int(-1)
+    rc = L.rubs_b200_filter_params_batch_host(
+        n, arr(imgs), _img_dtype_code(imgs[0].dtype), H, W, arr([p[0] for p in params]),
+        arr([p[1] for p in params]), arr([p[2] for p in params]),
+        _native.RUBS_F32 if pdt == np.float32 else _native.RUBS_F64, dl.handle, iterations, arr(outs),
+        ctypes.byref(failed))
+    if rc:
+        try:
+            _native.check(rc)
+        except Exception as e:
+            raise type(e)(f"batch image {failed.value}: {e}") from None
+    return outs
+
+
 # ---------------------------------------------------------------------------
 # Global-mode pieces kept for API parity (not on the hot path)
 

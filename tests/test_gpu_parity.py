@@ -597,3 +597,36 @@ def test_row_bands_reproduce_whole_image_bitwise(cuda):
             assert torch.equal(sharding.filter_rows_params(f[b0:b1], b0, H, *pb, band[0], band[0],
                                                            band[1] - band[0]), parts[-1])
         assert torch.equal(torch.cat(parts), whole)
+
+
+# --- batch API (BASELINE config 4: a batch of images, pipelined) -----------
+
+
+def test_batch_api_equals_per_image_calls(cuda, rng):
+    torch = cuda
+    imgs, ps = [], []
+    for i in range(5):
+        w = workloads.config4_image(i, 256, 192, param_dtype=torch.float32)
+        imgs.append(w["f"])
+        ps.append([v.numpy() for v in (w["size"], w["elong"], w["orient"])])
+    for it in (1, 2):
+        got = rb.filter_space_variant_params_batch(imgs, *[[p[q] for p in ps] for q in range(3)], iterations=it)
+        for f, p, g in zip(imgs, ps, got):
+            assert np.array_equal(g, rb.filter_space_variant_params(f, *p, iterations=it))
+    # pinned outputs, aliased across the batch (image j lands in outs[j])
+    outs = [torch.empty((256, 192), dtype=torch.float64, pin_memory=True).numpy() for _ in range(5)]
+    got = rb.filter_space_variant_params_batch(imgs, *[[p[q] for p in ps] for q in range(3)], outs=outs)
+    assert all(g is o for g, o in zip(got, outs))
+    assert rb.filter_space_variant_params_batch([], [], [], []) == []
+
+
+def test_batch_api_reports_the_failing_image(cuda, rng):
+    torch = cuda
+    w = workloads.config4_image(0, 64, 64, param_dtype=torch.float32)
+    p = [v.numpy() for v in (w["size"], w["elong"], w["orient"])]
+    bad = p[0].copy()
+    bad[3, 5] = np.nan
+    with pytest.raises(ValueError, match="batch image 2"):
+        rb.filter_space_variant_params_batch([w["f"]] * 4, [p[0], p[0], bad, p[0]], [p[1]] * 4, [p[2]] * 4)
+    with pytest.raises(ValueError):
+        rb.filter_space_variant_params_batch([w["f"], w["f"][:32]], [p[0]] * 2, [p[1]] * 2, [p[2]] * 2)
