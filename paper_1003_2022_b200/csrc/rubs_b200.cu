@@ -2928,6 +2928,79 @@ int run_streamed(const ImageSpec &I, FieldSpec F, const void *f_host,
   return status_to_code(st);
 }
 
+// Host-buffer calls on large images (H >= kBandStreamRows): the image is
+// filtered band by band COMPLETELY -- each band of output rows through the
+// whole path, deferred tiles and large-halo blocks included (run_band, the
+// row-band entry of the multi-GPU split) -- so a band's rows go back while
+// later bands are still uploading or computing.  (run_streamed defers every
+// deferred tile to the end of the call: on config 5, where almost all tiles
+// are deferred, that serialised ~110 ms of compute behind all the copies and
+// returned the result twice.)  The image goes up in chunks first, then each
+// band's parameters; band b waits for the image chunks its halo reaches
+// (the LUT bound amax * sqrt(max size of the band), as sharding.py's
+// halo_bound_params).  Band edges sit on the 32-row tile grid.
+constexpr int64_t kBandStreamRows = 8192;
+int run_streamed_bands(const ImageSpec &I, FieldSpec F, const void *f_host,
+                       const std::vector<HostPlane> &planes, double *dout, double *out_host) {
+  int rc = ensure_scratch();
+  if (rc) return rc;
+  const int H = I.h, W = I.w;
+  constexpr int kChunks = 16;
+  const int nb = 8;
+  const int per = ((H + nb - 1) / nb + kTile - 1) / kTile * kTile;  // rows per band (tile grid)
+  const int cper = (H + kChunks - 1) / kChunks;                     // rows per image chunk
+  if ((rc = stream_set((size_t)kChunks + 2 * nb))) return rc;
+  const cudaStream_t h2d = t_ss.h2d, cmp = t_ss.cmp, d2h = t_ss.d2h;
+  const size_t esz = I.dt ? 8 : 4;
+  for (int c = 0; c < kChunks; ++c) {
+    const int r0 = c * cper, r1 = std::min(H, r0 + cper);
+    if (r0 >= r1) break;
+    RUBS_CUDA_TRY(cudaMemcpyAsync(static_cast<char *>(const_cast<void *>(I.f)) + (size_t)r0 * W * esz,
+                                  static_cast<const char *>(f_host) + (size_t)r0 * W * esz,
+                                  (size_t)(r1 - r0) * W * esz, cudaMemcpyHostToDevice, h2d));
+    RUBS_CUDA_TRY(cudaEventRecord(t_ss.ev[c], h2d));
+  }
+  for (int b = 0; b < nb; ++b) {
+    const int r0 = b * per, r1 = std::min(H, r0 + per);
+    if (r0 >= r1) break;
+    for (const HostPlane &pl : planes)
+      RUBS_CUDA_TRY(cudaMemcpyAsync(static_cast<char *>(pl.dev) + r0 * pl.row_bytes,
+                                    static_cast<const char *>(pl.host) + r0 * pl.row_bytes,
+                                    (size_t)(r1 - r0) * pl.row_bytes, cudaMemcpyHostToDevice, h2d));
+    RUBS_CUDA_TRY(cudaEventRecord(t_ss.ev[kChunks + 2 * b], h2d));
+  }
+  const size_t psz = F.pdt ? 8 : 4;
+  for (int b = 0; b < nb; ++b) {
+    const int r0 = b * per, r1 = std::min(H, r0 + per);
+    if (r0 >= r1) break;
+    RUBS_CUDA_TRY(cudaStreamWaitEvent(cmp, t_ss.ev[kChunks + 2 * b], 0));
+    // the band's halo: largest size of its parameter rows (one reduction)
+    FieldSpec Fb = F;
+    Fb.ps = static_cast<const char *>(F.ps) + (size_t)r0 * F.pld * psz;
+    Fb.FH = r1 - r0;
+    Fb.FW = W;
+    RUBS_CUDA_TRY(cudaMemsetAsync(t_scr.d_status, 0, sizeof(Status), cmp));
+    size_max_kernel<<<4 * t_scr.sms, 256, 0, cmp>>>(Fb, t_scr.d_status);
+    ++t_launches;
+    Status st;
+    if ((rc = fetch_status(cmp, st))) return rc;
+    double smax = 0.0;
+    std::memcpy(&smax, &st.smax_bits, sizeof(smax));
+    const double A = std::max(F.lut_amax * std::sqrt(std::max(smax, 0.0)), 0.05);
+    const int halo = (int)std::ceil(0.5 * A + A / std::sqrt(2.0) + 1.5) + 4;
+    const int need_hi = std::min(H, r1 + halo);
+    const int last_chunk = std::min(kChunks - 1, (need_hi - 1) / cper);
+    RUBS_CUDA_TRY(cudaStreamWaitEvent(cmp, t_ss.ev[last_chunk], 0));
+    if ((rc = run_band(I, F, H, r0, r1 - r0, dout + (size_t)r0 * W, W, cmp))) return rc;
+    RUBS_CUDA_TRY(cudaEventRecord(t_ss.ev[kChunks + 2 * b + 1], cmp));
+    RUBS_CUDA_TRY(cudaStreamWaitEvent(d2h, t_ss.ev[kChunks + 2 * b + 1], 0));
+    RUBS_CUDA_TRY(cudaMemcpyAsync(out_host + (size_t)r0 * W, dout + (size_t)r0 * W,
+                                  (size_t)(r1 - r0) * W * 8, cudaMemcpyDeviceToHost, d2h));
+  }
+  RUBS_CUDA_TRY(cudaStreamSynchronize(d2h));
+  return RUBS_OK;
+}
+
 // The streamed path serves one-pass calls on the default (wide) kernel.
 bool streamable(int iterations, int64_t H, int64_t W) {
   return iterations == 1 && kernel_choice() == 2 && H >= 2 * kWideH && W > 0 &&
@@ -3171,6 +3244,8 @@ int rubs_b200_filter_params_host(const void *f, int f_dtype, int64_t H, int64_t 
     const size_t rb = (size_t)W * psz;
     std::vector<HostPlane> planes = {{size, pb, rb}, {elong, pb + npx * psz, rb},
                                      {orient, pb + 2 * npx * psz, rb}};
+    if (H >= kBandStreamRows && !std::getenv("RUBS_B200_NO_BAND_STREAM"))
+      return run_streamed_bands(I, F, f, planes, (double *)dout, out);
     return run_streamed(I, F, f, planes, (double *)dout, out);
   }
   RUBS_CUDA_TRY(cudaMemcpyAsync(df, f, npx * esz, cudaMemcpyHostToDevice, s));

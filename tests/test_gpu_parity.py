@@ -630,3 +630,22 @@ def test_batch_api_reports_the_failing_image(cuda, rng):
         rb.filter_space_variant_params_batch([w["f"]] * 4, [p[0], p[0], bad, p[0]], [p[1]] * 4, [p[2]] * 4)
     with pytest.raises(ValueError):
         rb.filter_space_variant_params_batch([w["f"], w["f"][:32]], [p[0]] * 2, [p[1]] * 2, [p[2]] * 2)
+
+
+def test_band_streamed_host_path_large_images(cuda):
+    # H >= 8192: host buffers go through the band-complete pipeline
+    # (run_streamed_bands): small kernels bitwise equal to the device path
+    # (bands on the tile grid), large kernels (block regions cut at band
+    # edges) within the precision budget of it
+    torch = cuda
+    w = workloads.config2(8192, 384, param_dtype=torch.float32)
+    p = [v.numpy() for v in (w["size"], w["elong"], w["orient"])]
+    host = rb.filter_space_variant_params(w["f"], *p)
+    dev = rb.filter_space_variant_params(torch.from_numpy(w["f"]).cuda(), *(torch.from_numpy(v).cuda() for v in p))
+    assert np.array_equal(host, dev.cpu().numpy())
+    w5 = workloads.config5(8192, 512, param_dtype=torch.float32)
+    f = w5["f"].numpy()
+    p5 = [v.numpy() for v in (w5["size"], w5["elong"], w5["orient"])]
+    host = rb.filter_space_variant_params(f, *p5)
+    dev = rb.filter_space_variant_params(torch.from_numpy(f).cuda(), *(torch.from_numpy(v).cuda() for v in p5)).cpu().numpy()
+    assert np.abs(host - dev).max() <= 1e-9 * np.abs(dev).max()
