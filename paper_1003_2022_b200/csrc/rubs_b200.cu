@@ -1809,6 +1809,8 @@ struct Scratch {
   double *d_aslot = nullptr;     // wide kernel: per-(SM, slot) scale-vectors
   unsigned *d_slotmask = nullptr;
   int *d_next = nullptr;  // tile counter of the large-halo gather
+  char *h_stage = nullptr;  // pinned staging of small transfers (small_copy)
+  size_t h_stage_cap = 0;
   bool attr_set = false;
 };
 thread_local Scratch t_scr_dev[rubs_internal::kMaxDevices];
@@ -1929,9 +1931,49 @@ int status_to_code(const Status &s) {
   return RUBS_OK;
 }
 
+// Small transfers (status words, plan records) move through SM loads and
+// stores of mapped pinned memory, not the copy engines: in a pipelined
+// host-buffer call the copy engines are busy with image bands, and a small
+// cudaMemcpyAsync queued behind them waited for whole bands (config 3n4's
+// band pipeline: ~2 ms per band of planning stall).  Sizes are multiples of
+// 4 bytes; pinned host memory is device-accessible under UVA.
+__global__ void word_copy_kernel(const unsigned *src, unsigned *dst, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+int small_copy(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) return RUBS_OK;
+  const size_t n = bytes / 4;
+  const int blocks = (int)std::min<size_t>((n + 255) / 256, 1024);
+  word_copy_kernel<<<blocks, 256, 0, s>>>(static_cast<const unsigned *>(src),
+                                          static_cast<unsigned *>(dst), n);
+  ++t_launches;
+  RUBS_CUDA_TRY(cudaGetLastError());
+  return RUBS_OK;
+}
+// Pinned staging for the small transfers of one planning round: `bytes`
+// more at *off (grown only with the stream idle: callers sync first).
+int host_stage(size_t bytes, size_t &off, char **out, cudaStream_t s) {
+  const size_t need = off + ((bytes + 15) & ~(size_t)15);
+  if (need > t_scr.h_stage_cap) {
+    RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+    if (t_scr.h_stage) cudaFreeHost(t_scr.h_stage);
+    t_scr.h_stage = nullptr;
+    t_scr.h_stage_cap = 0;
+    const size_t cap = std::max<size_t>(need * 2, 1 << 20);
+    RUBS_CUDA_TRY(cudaMallocHost(&t_scr.h_stage, cap));
+    t_scr.h_stage_cap = cap;
+    off = 0;  // earlier stagings of this round have been consumed (synced)
+  }
+  *out = t_scr.h_stage + off;
+  off += (bytes + 15) & ~(size_t)15;
+  return RUBS_OK;
+}
+
 int fetch_status(cudaStream_t s, Status &out) {
-  RUBS_CUDA_TRY(cudaMemcpyAsync(t_scr.h_status, t_scr.d_status, sizeof(Status),
-                                cudaMemcpyDeviceToHost, s));
+  int rc = small_copy(t_scr.h_status, t_scr.d_status, sizeof(Status), s);
+  if (rc) return rc;
   RUBS_CUDA_TRY(cudaStreamSynchronize(s));
   out = *t_scr.h_status;
   timer_collect();
@@ -2063,15 +2105,20 @@ void launch_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, c
 }
 
 template <class V>
-int upload(std::vector<V> &h, V *&d, size_t &cap, cudaStream_t s) {
+int upload(std::vector<V> &h, V *&d, size_t &cap, cudaStream_t s, size_t &stage_off) {
   if (h.size() > cap) {
     if (d) cudaFree(d);
     d = nullptr;
     RUBS_CUDA_TRY(cudaMalloc(&d, h.size() * sizeof(V)));
     cap = h.size();
   }
-  if (!h.empty())
-    RUBS_CUDA_TRY(cudaMemcpyAsync(d, h.data(), h.size() * sizeof(V), cudaMemcpyHostToDevice, s));
+  if (!h.empty()) {
+    char *st = nullptr;
+    int rc = host_stage(h.size() * sizeof(V), stage_off, &st, s);
+    if (rc) return rc;
+    std::memcpy(st, h.data(), h.size() * sizeof(V));
+    return small_copy(d, st, h.size() * sizeof(V), s);
+  }
   return RUBS_OK;
 }
 
@@ -2297,19 +2344,23 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
                                          t_plan.counters);
   t_launches += 3;
   RUBS_CUDA_TRY(cudaGetLastError());
-  RUBS_CUDA_TRY(cudaMemcpyAsync(t_plan.h_counters, t_plan.counters, 2 * sizeof(int),
-                                cudaMemcpyDeviceToHost, s));
+  if ((rc = small_copy(t_plan.h_counters, t_plan.counters, 2 * sizeof(int), s))) return rc;
   RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+  size_t stage_off = 0;  // pinned staging of this planning round (small_copy)
   const int n_smem = t_plan.h_counters[0], n_used = t_plan.h_counters[1];
   std::vector<int> used(n_used);
   std::vector<CellAgg> agg(n_used);
   if (n_used > 0) {
-    RUBS_CUDA_TRY(cudaMemcpyAsync(used.data(), t_plan.used, n_used * sizeof(int),
-                                  cudaMemcpyDeviceToHost, s));
-    RUBS_CUDA_TRY(cudaMemcpyAsync(agg.data(), t_plan.agg, n_used * sizeof(CellAgg),
-                                  cudaMemcpyDeviceToHost, s));
+    char *hu = nullptr, *ha = nullptr;
+    if ((rc = host_stage(n_used * sizeof(int), stage_off, &hu, s))) return rc;
+    if ((rc = host_stage(n_used * sizeof(CellAgg), stage_off, &ha, s))) return rc;
+    if ((rc = small_copy(hu, t_plan.used, n_used * sizeof(int), s))) return rc;
+    if ((rc = small_copy(ha, t_plan.agg, n_used * sizeof(CellAgg), s))) return rc;
     RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+    std::memcpy(used.data(), hu, n_used * sizeof(int));
+    std::memcpy(agg.data(), ha, n_used * sizeof(CellAgg));
   }
+  stage_off = 0;  // the stream is idle: the staging is free again
   hc.lap("device plan");
   if (hc.on) std::fprintf(stderr, "[host] %d records: %d shared-memory tiles, %d blocks\n", n_ovf, n_smem, n_used);
   // per-pixel fallback list: grown on demand (handle_overflow), starting
@@ -2329,13 +2380,13 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   if (n_smem > 0) {
     // tile order (the classify kernel appended them in arbitrary order):
     // neighbouring persistent-CTA tiles then share their region rows in L2
-    std::vector<int2> sl(n_smem);
-    RUBS_CUDA_TRY(cudaMemcpyAsync(sl.data(), t_scr.d_list, n_smem * sizeof(int2),
-                                  cudaMemcpyDeviceToHost, s));
+    char *hl = nullptr;
+    if ((rc = host_stage(n_smem * sizeof(int2), stage_off, &hl, s))) return rc;
+    if ((rc = small_copy(hl, t_scr.d_list, n_smem * sizeof(int2), s))) return rc;
     RUBS_CUDA_TRY(cudaStreamSynchronize(s));
-    std::sort(sl.begin(), sl.end(), [](const int2 &a, const int2 &b) { return a.x < b.x; });
-    RUBS_CUDA_TRY(cudaMemcpyAsync(t_scr.d_list, sl.data(), n_smem * sizeof(int2),
-                                  cudaMemcpyHostToDevice, s));
+    int2 *sl = reinterpret_cast<int2 *>(hl);
+    std::sort(sl, sl + n_smem, [](const int2 &a, const int2 &b) { return a.x < b.x; });
+    if ((rc = small_copy(t_scr.d_list, hl, n_smem * sizeof(int2), s))) return rc;
     tile_overflow_kernel<M, T><<<std::min(n_smem, t_scr.sms), kThreadsLarge,
                                  kSmemLarge, s>>>(I, F, D, tiles_x, kSmemLarge / 8, t_scr.d_list,
                                                   n_smem, t_scr.d_status,
@@ -2454,9 +2505,9 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
     t_scr.big_budget = budget;
   }
   hc.lap("scratch");
-  if ((rc = upload(regs, t_scr.d_regs, t_scr.regs_cap, s))) return rc;
-  if ((rc = upload(cm, t_plan.d_cm, t_plan.cm_cap, s))) return rc;
-  if ((rc = upload(cm_cell, t_plan.d_cm_cell, t_plan.cmc_cap, s))) return rc;
+  if ((rc = upload(regs, t_scr.d_regs, t_scr.regs_cap, s, stage_off))) return rc;
+  if ((rc = upload(cm, t_plan.d_cm, t_plan.cm_cap, s, stage_off))) return rc;
+  if ((rc = upload(cm_cell, t_plan.d_cm_cell, t_plan.cmc_cap, s, stage_off))) return rc;
   if ((size_t)ntl > t_scr.btiles_cap) {
     if (t_scr.d_btiles) cudaFree(t_scr.d_btiles);
     t_scr.d_btiles = nullptr;
@@ -2531,9 +2582,10 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
   if (rc) return rc;
   HostClock hc;
   int cnt = 0;
-  RUBS_CUDA_TRY(cudaMemcpyAsync(&cnt, &t_scr.d_status->pix_count, sizeof(int),
-                                cudaMemcpyDeviceToHost, s));
+  if ((rc = small_copy(&t_scr.h_status->pix_count, &t_scr.d_status->pix_count, sizeof(int), s)))
+    return rc;
   RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+  cnt = t_scr.h_status->pix_count;
   hc.lap("overflow kernels (sync)");
   if ((size_t)cnt > t_scr.pix_cap) {
     // more precision-deferred pixels than the list holds (rare: fields with
@@ -2546,9 +2598,10 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_pix, (size_t)cnt * sizeof(int2)));
     t_scr.pix_cap = (size_t)cnt;
     if ((rc = handle_overflow_tiles<M, T>(I, F, D, n_ovf, s))) return rc;
-    RUBS_CUDA_TRY(cudaMemcpyAsync(&cnt, &t_scr.d_status->pix_count, sizeof(int),
-                                  cudaMemcpyDeviceToHost, s));
+    if ((rc = small_copy(&t_scr.h_status->pix_count, &t_scr.d_status->pix_count, sizeof(int), s)))
+      return rc;
     RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+    cnt = t_scr.h_status->pix_count;
   }
   cnt = std::min<int64_t>(cnt, (int64_t)t_scr.pix_cap);
   if (cnt > 0) {
