@@ -1605,7 +1605,7 @@ __global__ void __launch_bounds__(256, RUBS_BG_MINB) big_gather_kernel(FieldSpec
     const BigRegion g = R[bt.region];
     const int x0 = (bt.tile % tiles_x) * kTile, y0 = (bt.tile / tiles_x) * kTile;
     const char *Sb = reinterpret_cast<const char *>(scratch + g.off);  // local coordinates
-    const int64_t P8 = (int64_t)g.P * 8;
+    const int P8 = g.P * 8;  // 32-bit offsets: a region row is < 2^31 bytes (fewer live registers)
 #pragma unroll 1
     for (int k = 0; k < 4; ++k) {
       const int x = x0 + lx, y = y0 + ly + 8 * k;
@@ -1618,7 +1618,7 @@ __global__ void __launch_bounds__(256, RUBS_BG_MINB) big_gather_kernel(FieldSpec
         // small, the block's is not -- deferred to the per-pixel pass
         if (defer_pixel(a, g.l4, x, y, pix, pix_cap, st)) continue;
         D.out[(int64_t)y * D.ld_out + x] =
-            pixel_fd_t<const char *, int64_t>(Sb, P8, n1 - g.rc0, n2 - g.rr0, a);
+            pixel_fd_t<const char *, int>(Sb, P8, n1 - g.rc0, n2 - g.rr0, a);
       }
     }
   }
