@@ -971,6 +971,12 @@ __global__ void __launch_bounds__(kThreadsLarge, 1)
 #define RUBS_DEV_SKIP_GATHER 0
 #endif
 constexpr int kWideW = 64, kWideH = 32;
+// LUT modes: tiles whose smallest size parameter is at least this are
+// planned from float32 bounds (see wide_filter_kernel, phase A)
+#ifndef RUBS_BOUND_TILE_SIZE
+#define RUBS_BOUND_TILE_SIZE 1500.0f
+#endif
+constexpr float kBoundTileSize = RUBS_BOUND_TILE_SIZE;
 // CTAs per SM of a wide-kernel launch: 2 (110 KB regions, 384 threads) by
 // default; 3 (72 KB, 256 threads) for the two-channel LUT launch of the
 // adaptive_smooth pipeline, where it measured faster (1.22 -> 0.95 ms).
@@ -1033,6 +1039,7 @@ __global__ void __launch_bounds__(NT, CT)
   __shared__ int s_unit[NCX * NCY][8];
   __shared__ int s_nu;
   __shared__ int s_slot;
+  __shared__ float s_smin;  // smallest size parameter of the tile (LUT modes)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t mbar = (uint32_t)__cvta_generic_to_shared(&s_mbar);
   // LUT modes: the exact scale-vectors of the tile are computed once (phase
@@ -1054,6 +1061,7 @@ __global__ void __launch_bounds__(NT, CT)
   }
   if (tid < 4 * NCX * NCY) (&s_cm[0][0])[tid] = 0;
   if (tid < NCX * NCY) s_cw[tid] = 0.f;
+  if (tid == 0) s_smin = INFINITY;
   __syncthreads();
   unsigned ghi = 0, flags = 0;
   uint32_t phase = 0;
@@ -1062,6 +1070,7 @@ __global__ void __launch_bounds__(NT, CT)
 
   double *const apark =
       kPark ? aslots + (size_t)s_slot * (kWideW * kWideH * 4) : nullptr;
+  bool bound_tile = false;  // planned from float32 bounds (phase A)
   // ---- A: read margins and weights of the 2048 pixels; thread = one
   //         column, rows (tid >> 6) + 4 k; 8-lane groups share an 8 x 8 cell
   {
@@ -1108,6 +1117,29 @@ __global__ void __launch_bounds__(NT, CT)
         pre[k][2] = __ldg(static_cast<const PT *>(F.pt) + i);
       }
     }
+    // LUT modes: a tile whose sizes are all large (>= kBoundTileSize) is
+    // planned from float32 bounds of its pixels' mapping (lut_bounds_f32)
+    // instead of the exact fp64 mapping: such tiles are deferred (config 5:
+    // nearly all), and the pass that computes a pixel maps it exactly itself,
+    // so the exact mapping is done once.  A unit of such a tile that does fit
+    // maps its pixels exactly in the gather (fetch below).
+    if constexpr (kPark) {
+      float smin = INFINITY;
+#pragma unroll
+      for (int k = 0; k < NK; ++k) {
+        const int ty_ = py + RS * k;
+        if (ty_ < kWideH && x0 + px < D.pw && y0 + ty_ < D.ph)
+          smin = fminf(smin, fabsf((float)pre[k][0]));
+      }
+      smin = fminf(smin, __shfl_xor_sync(0xffffffffu, smin, 16));
+      smin = fminf(smin, __shfl_xor_sync(0xffffffffu, smin, 8));
+      smin = fminf(smin, __shfl_xor_sync(0xffffffffu, smin, 4));
+      smin = fminf(smin, __shfl_xor_sync(0xffffffffu, smin, 2));
+      smin = fminf(smin, __shfl_xor_sync(0xffffffffu, smin, 1));
+      if (lane == 0) atomicMin(reinterpret_cast<int *>(&s_smin), __float_as_int(smin));
+      __syncthreads();
+    }
+    bound_tile = kPark && __int_as_float(*reinterpret_cast<volatile int *>(&s_smin)) >= kBoundTileSize;
 #pragma unroll
     for (int k = 0; k < NK; ++k) {
       const int ty_ = py + RS * k;  // tile row (warp-uniform)
@@ -1121,13 +1153,17 @@ __global__ void __launch_bounds__(NT, CT)
           int4 m;
           float w;
           if constexpr (kPark) {
-            double a[4];
-            field_from_params(F, (double)pre[k][0], (double)pre[k][1], (double)pre[k][2], a, flags);
-            m = pixel_margins_fast(a);
-            w = 1.0f / (float)(a[0] * a[1] * a[2] * a[3]);
-            double2 *dst = reinterpret_cast<double2 *>(apark + (ty_ * kWideW + px) * 4);
-            dst[0] = make_double2(a[0], a[1]);
-            dst[1] = make_double2(a[2], a[3]);
+            if (bound_tile) {
+              lut_bounds_f32(F, (double)pre[k][0], (double)pre[k][1], (double)pre[k][2], m, w, flags);
+            } else {
+              double a[4];
+              field_from_params(F, (double)pre[k][0], (double)pre[k][1], (double)pre[k][2], a, flags);
+              m = pixel_margins_fast(a);
+              w = 1.0f / (float)(a[0] * a[1] * a[2] * a[3]);
+              double2 *dst = reinterpret_cast<double2 *>(apark + (ty_ * kWideW + px) * 4);
+              dst[0] = make_double2(a[0], a[1]);
+              dst[1] = make_double2(a[2], a[3]);
+            }
           } else {
             pixel_bound<MODE>(F, D.pc_lo + x, D.pr_lo + y, m, w);
           }
@@ -1280,10 +1316,14 @@ __global__ void __launch_bounds__(NT, CT)
       x = min(x, sx + sw - 1);
       y = min(y, sy + sh - 1);
       if constexpr (kPark) {
-        const double2 *p =
-            reinterpret_cast<const double2 *>(apark + ((y - y0) * kWideW + (x - x0)) * 4);
-        const double2 lo = p[0], hi = p[1];
-        a[0] = lo.x; a[1] = lo.y; a[2] = hi.x; a[3] = hi.y;
+        if (bound_tile) {
+          field_at<MODE>(F, D.pc_lo + x, D.pr_lo + y, a, flags);  // exact mapping, once
+        } else {
+          const double2 *p =
+              reinterpret_cast<const double2 *>(apark + ((y - y0) * kWideW + (x - x0)) * 4);
+          const double2 lo = p[0], hi = p[1];
+          a[0] = lo.x; a[1] = lo.y; a[2] = hi.x; a[3] = hi.y;
+        }
       } else {
         field_at<MODE>(F, D.pc_lo + x, D.pr_lo + y, a, flags);
       }

@@ -190,6 +190,66 @@ __device__ __forceinline__ void lut_map(const FieldSpec &F, double s, double rho
   }
 }
 
+#ifndef RUBS_MARGIN_SLACK
+#define RUBS_MARGIN_SLACK 0
+#endif
+// Planning bounds of one LUT-mapped pixel in float32 (the primary kernel's
+// large-kernel tiles, which are deferred anyway: their exact mapping is
+// done by the pass that computes them).  Validation flags and the quarter
+// index exactly as lut_map; the log, blend and sqrt in float32 from the same
+// table cells (the blend is continuous across cells, so an f32 cell index
+// differing at a cell edge changes nothing).  Component error <= ~1e-6
+// relative: the margins from an extent inflated by (1 + 2e-5) + 2e-3 and
+// w x (1 + 1e-4) bound the exact ones (pixel_margins_fast, 1 / prod a).
+__device__ __forceinline__ void lut_bounds_f32(const FieldSpec &F, double s, double rho, double th,
+                                               int4 &m, float &w, unsigned &flags) {
+  const bool s_ok = (s > 0.0) && (s < INFINITY);
+  const bool r_ok = (rho >= 1.0) && (rho < INFINITY);
+  const bool t_ok = (th >= 0.0) && (th < kPi);
+  if (!(s_ok && r_ok && t_ok)) flags |= kFlagParamInvalid;
+  if (rho > F.rho_lim) flags |= kFlagOutOfGrid;
+  if (!s_ok) s = 1.0;
+  if (!r_ok) rho = 1.0;
+  if (!t_ok) th = 0.0;
+  rho = fmin(rho, F.rho_max);
+  const int q = quarter_index(th);
+  const double phi = __dsub_rn(th, __dmul_rn((double)q, kQuarter));
+  const int nr = F.n_rho, np_ = F.n_phi;
+  float u = __logf((float)rho) * (float)F.inv_log_rho_max * (float)(nr - 1);
+  float v = (float)phi * (float)F.phi_scale - 0.5f;
+  u = fminf(fmaxf(u, 0.f), (float)(nr - 1));
+  v = fminf(fmaxf(v, 0.f), (float)(np_ - 1));
+  const int i0 = min((int)u, nr - 2), j0 = min((int)v, np_ - 2);
+  const float fu = u - (float)i0, fv = v - (float)j0, gu = 1.f - fu, gv = 1.f - fv;
+  const float w00 = gu * gv, w10 = fu * gv, w01 = gu * fv, w11 = fu * fv;
+  const double2 *e00 = reinterpret_cast<const double2 *>(
+      F.lut + ((int64_t)q * nr * np_ + (int64_t)i0 * np_ + j0) * 4);
+  const double2 *e10 = e00 + (int64_t)np_ * 2;
+  const float ss = sqrtf((float)s);
+  float a[4];
+  {
+    const double2 A = __ldg(e00), B = __ldg(e10), C = __ldg(e00 + 2), Dd = __ldg(e10 + 2);
+    a[0] = ((float)A.x * w00 + (float)B.x * w10 + (float)C.x * w01 + (float)Dd.x * w11) * ss;
+    a[1] = ((float)A.y * w00 + (float)B.y * w10 + (float)C.y * w01 + (float)Dd.y * w11) * ss;
+  }
+  {
+    const double2 A = __ldg(e00 + 1), B = __ldg(e10 + 1), C = __ldg(e00 + 3), Dd = __ldg(e10 + 3);
+    a[2] = ((float)A.x * w00 + (float)B.x * w10 + (float)C.x * w01 + (float)Dd.x * w11) * ss;
+    a[3] = ((float)A.y * w00 + (float)B.y * w10 + (float)C.y * w01 + (float)Dd.y * w11) * ss;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    a[k] = fmaxf(a[k], (float)kScaleFloor);
+    if (F.scaled) a[k] = a[k] / (float)F.div;
+  }
+  const float d = (a[1] + a[3]) * 0.70710678f;
+  const float hx = 0.5f * (a[0] + d) * (1.f + 2e-5f) + 2e-3f;
+  const float hy = 0.5f * (a[2] + d) * (1.f + 2e-5f) + 2e-3f;
+  const int fx = (int)floorf(hx), fy = (int)floorf(hy), k = RUBS_MARGIN_SLACK;
+  m = make_int4(fx + 2 + k, fx + 1 + k, fy + 3 + k, fy + k);
+  w = 1.0f / (a[0] * a[1] * a[2] * a[3]) * (1.f + 1e-4f);
+}
+
 template <int MODE>
 __device__ __forceinline__ void field_raw(const FieldSpec &F, int fr, int fc, double a[4],
                                           unsigned &flags) {
