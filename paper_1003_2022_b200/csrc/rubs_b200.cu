@@ -1247,30 +1247,43 @@ __global__ void __launch_bounds__(NT, CT)
     // a cell no node fits goes to the overflow pass; the rest of the tile
     // keeps its (smaller, better-conditioned) units
     const bool in = x0 + 8 * cx < D.pw && y0 + 8 * cy < D.ph;
-    const unsigned ovf_cells = __ballot_sync(0xffffffffu, in && top < 0);
-    if (lane == 0) {
-      if (ovf_cells) {
-        // one record per 32 x 32 half with deferred cells (the overflow
-        // passes work on the 32-pixel grid), margins and w over those cells
-        for (int h = 0; h < 2; ++h) {
-          OvfRec r;
-          r.tile = ty * tiles_x32 + 2 * tx + h;
-          r.m[0] = r.m[1] = r.m[2] = r.m[3] = 0;
-          r.w = 0.f;
-          r.mask = 0;
-          for (int ccy = 0; ccy < NCY; ++ccy)
-            for (int ccx = 4 * h; ccx < 4 * h + 4; ++ccx) {
-              const int c = ccy * NCX + ccx;
-              if (!((ovf_cells >> c) & 1u)) continue;
-              r.mask |= 1u << (ccy * 4 + (ccx - 4 * h));
-              for (int j = 0; j < 4; ++j) r.m[j] = max(r.m[j], s_cm[c][j]);
-              r.w = fmaxf(r.w, s_cw[c]);
-            }
-          if (r.mask) reinterpret_cast<OvfRec *>(ovf_list)[atomicAdd(&st->ovf_count, 1)] = r;
-        }
+    const bool dfr = in && top < 0;
+    const unsigned ovf_cells = __ballot_sync(0xffffffffu, dfr);
+    if (ovf_cells) {
+      // one record per 32 x 32 half with deferred cells (the overflow passes
+      // work on the 32-pixel grid), margins and w over those cells: a max
+      // over the lanes (cells) of each half, lane 0 / lane 4 write half 0 / 1
+      // (one atomic per tile; the serial per-cell loop of lane 0 held the
+      // other warps at the barrier)
+      int rm[4];
+      float rw = 0.f;
+      for (int j = 0; j < 4; ++j) rm[j] = dfr ? s_cm[lane][j] : 0;
+      if (dfr) rw = s_cw[lane];
+#pragma unroll
+      for (int o : {1, 2, 8, 16}) {  // lanes of one half: cx bits 0-1, cy bits 3-4
+        for (int j = 0; j < 4; ++j) rm[j] = max(rm[j], __shfl_xor_sync(0xffffffffu, rm[j], o));
+        rw = fmaxf(rw, __shfl_xor_sync(0xffffffffu, rw, o));
       }
-      s_nu = __popc(wb);
+      auto half_mask = [&](int h) {
+        unsigned m = 0;
+        for (int ccy = 0; ccy < NCY; ++ccy) m |= ((ovf_cells >> (ccy * NCX + 4 * h)) & 0xFu) << (4 * ccy);
+        return m;
+      };
+      const unsigned m0 = half_mask(0), m1 = half_mask(1);
+      int base = 0;
+      if (lane == 0) base = atomicAdd(&st->ovf_count, (m0 != 0) + (m1 != 0));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if ((lane == 0 && m0) || (lane == 4 && m1)) {
+        const int h = lane >> 2;
+        OvfRec r;
+        r.tile = ty * tiles_x32 + 2 * tx + h;
+        for (int j = 0; j < 4; ++j) r.m[j] = rm[j];
+        r.w = rw;
+        r.mask = h ? m1 : m0;
+        reinterpret_cast<OvfRec *>(ovf_list)[base + (h && m0 ? 1 : 0)] = r;
+      }
     }
+    if (lane == 0) s_nu = __popc(wb);
   }
   __syncthreads();
 
@@ -3104,6 +3117,7 @@ bool streamable(int iterations, int64_t H, int64_t W) {
 
 struct rubs_lut {
   double *entries = nullptr;
+  float *entries32 = nullptr;  // the same rolled copies in float32
   int n_rho = 0, n_phi = 0;
   double rho_max = 0.0;
   double amax = 0.0;  // largest component of any entry
@@ -3120,6 +3134,7 @@ FieldSpec lut_field(const rubs_lut *lut, const void *size, const void *elong, co
   F.pdt = p_dtype;
   F.pld = ld_p;
   F.lut = lut->entries;
+  F.lut32 = lut->entries32;
   F.n_rho = lut->n_rho;
   F.n_phi = lut->n_phi;
   F.rho_max = lut->rho_max;
@@ -3269,10 +3284,16 @@ int rubs_b200_lut_create(const double *rho_grid, const double *phi_grid, const d
     for (size_t e = 0; e < (size_t)n_rho * n_phi; ++e)
       for (int k = 0; k < 4; ++k) rolled[q * per + e * 4 + k] = entries[e * 4 + ((k - q + 4) & 3)];
   size_t bytes = rolled.size() * sizeof(double);
+  // float32 copy of the rolled table: the planning bounds (lut_bounds_f32)
+  std::vector<float> rolled32(rolled.begin(), rolled.end());
   cudaError_t e = cudaMalloc(&L->entries, bytes);
   if (e == cudaSuccess) e = cudaMemcpy(L->entries, rolled.data(), bytes, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&L->entries32, rolled32.size() * sizeof(float));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(L->entries32, rolled32.data(), rolled32.size() * sizeof(float), cudaMemcpyHostToDevice);
   if (e != cudaSuccess) {
     if (L->entries) cudaFree(L->entries);
+    if (L->entries32) cudaFree(L->entries32);
     delete L;
     return set_error(RUBS_ECUDA, std::string("lut upload: ") + cudaGetErrorString(e));
   }
@@ -3283,6 +3304,7 @@ int rubs_b200_lut_create(const double *rho_grid, const double *phi_grid, const d
 void rubs_b200_lut_destroy(rubs_lut *lut) {
   if (!lut) return;
   if (lut->entries) cudaFree(lut->entries);
+  if (lut->entries32) cudaFree(lut->entries32);
   delete lut;
 }
 

@@ -63,6 +63,7 @@ struct FieldSpec {
   int pdt;  // 0 f32, 1 f64
   int64_t pld;
   const double *lut;  // (n_rho, n_phi, 4)
+  const float *lut32;  // the same in float32 (planning bounds)
   int n_rho, n_phi;
   double rho_max, log_rho_max, inv_log_rho_max;
   double phi_scale;  // n_phi / (pi / 4)
@@ -222,21 +223,15 @@ __device__ __forceinline__ void lut_bounds_f32(const FieldSpec &F, double s, dou
   const int i0 = min((int)u, nr - 2), j0 = min((int)v, np_ - 2);
   const float fu = u - (float)i0, fv = v - (float)j0, gu = 1.f - fu, gv = 1.f - fv;
   const float w00 = gu * gv, w10 = fu * gv, w01 = gu * fv, w11 = fu * fv;
-  const double2 *e00 = reinterpret_cast<const double2 *>(
-      F.lut + ((int64_t)q * nr * np_ + (int64_t)i0 * np_ + j0) * 4);
-  const double2 *e10 = e00 + (int64_t)np_ * 2;
+  const float4 *e00 = reinterpret_cast<const float4 *>(F.lut32) +
+                      ((int64_t)q * nr * np_ + (int64_t)i0 * np_ + j0);
+  const float4 *e10 = e00 + np_;
   const float ss = sqrtf((float)s);
-  float a[4];
-  {
-    const double2 A = __ldg(e00), B = __ldg(e10), C = __ldg(e00 + 2), Dd = __ldg(e10 + 2);
-    a[0] = ((float)A.x * w00 + (float)B.x * w10 + (float)C.x * w01 + (float)Dd.x * w11) * ss;
-    a[1] = ((float)A.y * w00 + (float)B.y * w10 + (float)C.y * w01 + (float)Dd.y * w11) * ss;
-  }
-  {
-    const double2 A = __ldg(e00 + 1), B = __ldg(e10 + 1), C = __ldg(e00 + 3), Dd = __ldg(e10 + 3);
-    a[2] = ((float)A.x * w00 + (float)B.x * w10 + (float)C.x * w01 + (float)Dd.x * w11) * ss;
-    a[3] = ((float)A.y * w00 + (float)B.y * w10 + (float)C.y * w01 + (float)Dd.y * w11) * ss;
-  }
+  const float4 A = __ldg(e00), B = __ldg(e10), C = __ldg(e00 + 1), Dd = __ldg(e10 + 1);
+  float a[4] = {(A.x * w00 + B.x * w10 + C.x * w01 + Dd.x * w11) * ss,
+                (A.y * w00 + B.y * w10 + C.y * w01 + Dd.y * w11) * ss,
+                (A.z * w00 + B.z * w10 + C.z * w01 + Dd.z * w11) * ss,
+                (A.w * w00 + B.w * w10 + C.w * w01 + Dd.w * w11) * ss};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     a[k] = fmaxf(a[k], (float)kScaleFloor);
