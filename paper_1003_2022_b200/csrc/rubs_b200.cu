@@ -2205,8 +2205,8 @@ struct PlanGrid {
   int gx[kPlanLevels], gy[kPlanLevels], base[kPlanLevels + 1];
 };
 struct CellAgg {
-  int x0, y0, x1, y1;
-  int m[4];
+  int x0, y0, x1, y1;  // member tiles' bounding box (domain pixels)
+  int r[4];            // region: union of the member tiles' read extents (x0, x1, y0, y1)
   int count;
 };
 
@@ -2246,7 +2246,7 @@ __host__ __device__ inline int plan_side(const OvfRec &r, int tw, int th, int sk
 
 __global__ void plan_init_kernel(CellAgg *c, int n) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    c[i] = CellAgg{INT_MAX, INT_MAX, 0, 0, {0, 0, 0, 0}, 0};
+    c[i] = CellAgg{INT_MAX, INT_MAX, 0, 0, {INT_MAX, INT_MIN, INT_MAX, INT_MIN}, 0};
 }
 
 // counters: [0] records for the shared-memory pass, [1] used cells
@@ -2271,7 +2271,13 @@ __global__ void plan_classify_kernel(const OvfRec *rec, int n, PlanGrid G, int t
     atomicMin(&c->y0, y0);
     atomicMax(&c->x1, x0 + tw);
     atomicMax(&c->y1, y0 + th);
-    for (int j = 0; j < 4; ++j) atomicMax(&c->m[j], r.m[j]);
+    // the region is the bounding box of the members' own read extents, not
+    // the member box grown by the largest margin: on smoothly varying fields
+    // the margins differ across a block (config 5: region area -x %)
+    atomicMin(&c->r[0], x0 - r.m[0]);
+    atomicMax(&c->r[1], x0 + tw + r.m[1]);
+    atomicMin(&c->r[2], y0 - r.m[2]);
+    atomicMax(&c->r[3], y0 + th + r.m[3]);
     atomicAdd(&c->count, 1);
   }
 }
@@ -2506,11 +2512,11 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   for (int k : order) {
     const CellAgg &b = agg[k];
     BigRegion g;
-    g.RW = (b.x1 - b.x0) + b.m[0] + b.m[1];
-    g.RH = (b.y1 - b.y0) + b.m[2] + b.m[3];
+    g.RW = b.r[1] - b.r[0];
+    g.RH = b.r[3] - b.r[2];
     g.P = g.RW;
-    g.rc0 = D.pc_lo + b.x0 - b.m[0];
-    g.rr0 = D.pr_lo + b.y0 - b.m[2];
+    g.rc0 = D.pc_lo + b.r[0];
+    g.rr0 = D.pr_lo + b.r[2];
     {
       const double mn = std::min(g.RW, g.RH);
       g.l4 = (float)(0.25 * g.RW * (double)g.RH * mn * mn);
