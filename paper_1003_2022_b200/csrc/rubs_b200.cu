@@ -1407,8 +1407,9 @@ constexpr int kPixSmem = 8 * kPixSlab * 8;  // 8 warps per CTA
 #endif
 constexpr int64_t kBigBatch = RUBS_BIG_BATCH;
 constexpr int64_t kBigMinBatch = 1ll << 24;  // smallest budget tried after allocation failures
-// fewer than SMs / kRsFewDiv regions in a batch: line sweeps (flat-cost table:
-// 4 regions 3.8 -> 1.6 ms; 64 regions keep the fused sweep, 1.05 vs 1.44 ms)
+// fewer than SMs / kRsFewDiv regions in a batch: segmented line sweeps
+// (flat-cost table: 4 regions 3.8 -> 1.6 -> 0.72 ms with segments; 64
+// regions keep the fused sweep; below one region per SM measured slower)
 constexpr int kRsFewDiv = 8;
 
 template <int MODE, int DT>
@@ -1501,36 +1502,61 @@ __global__ void __launch_bounds__(256) big_fill_rs1_kernel(ImageSpec I, const Bi
 }
 
 // dir 2: g[r][c] += g[r-1][c-1];  3: g[r][c] += g[r-1][c];  4: g[r][c] += g[r-1][c+1]
-template <int DIR>
-__global__ void __launch_bounds__(256) big_line_kernel(const BigRegion *R, double *scratch,
-                                                       Status *st) {
-  const BigRegion g = R[blockIdx.y];
+// Segmented line sweep for batches of few, large regions (the flat-cost
+// table's single 2048^2 image at s >= 1024: four regions of ~1600^2).  The
+// sequential sweep above walks every line with one lane, a dependent chain of
+// RH loads and stores through L2 (latency-bound: ~0.3 ms per direction at
+// RH = 1600).  Here the rows are cut into segments of kLineSeg: phase 0 sums
+// each line's part of each segment (lane = line: a warp's 32 neighbouring
+// lines touch consecutive addresses row by row), phase 1
+// turns each line's segment sums into exclusive carries, phase 2 re-walks
+// each segment from its carry.  tot holds nseg x nlines partial sums per region
+// (region r at tot + r * tot_stride).  The additions per element differ from
+// the sequential sweep only in where the running sum is restarted.
+constexpr int kLineSeg = 128;
+template <int DIR, int PHASE>
+__global__ void __launch_bounds__(256) big_line_seg_kernel(const BigRegion *R, double *scratch,
+                                                           double *tot, int64_t tot_stride,
+                                                           Status *st) {
+  const BigRegion g = R[blockIdx.z];
   const int lane = threadIdx.x & 31;
-  const int lb = (blockIdx.x * 256 + threadIdx.x) & ~31;  // first line of this warp
   const int nlines = DIR == 3 ? g.RW : g.RH + g.RW - 1;
+  const int nseg = (g.RH + kLineSeg - 1) / kLineSeg;
+  double *T = tot + blockIdx.z * tot_stride;  // [seg][line]
+  if (PHASE == 1) {
+    const int L = blockIdx.x * 256 + threadIdx.x;
+    if (blockIdx.y != 0 || L >= nlines) return;
+    double c = 0.0;
+    for (int k = 0; k < nseg; ++k) {
+      const double t = T[(int64_t)k * nlines + L];
+      T[(int64_t)k * nlines + L] = c;
+      c += t;
+    }
+    return;
+  }
+  const int seg = blockIdx.y;
+  if (seg >= nseg) return;
+  const int lb = (blockIdx.x * 256 + threadIdx.x) & ~31;  // first line of this warp
   if (lb >= nlines) return;
   double *base = scratch + g.off;
-  // line of this lane and its element in row t:
-  //   DIR 2: k = L - (RH-1), column t + k;  DIR 3: column L;  DIR 4: column L - t
   const int L = lb + lane;
-  int ta, tb, cw;  // warp's row range
+  // the warp's row range within the segment (as big_line_kernel)
+  int ta, tb;
   if (DIR == 2) {
     const int kb = lb - (g.RH - 1);
     ta = max(0, -(kb + 31));
     tb = min(g.RH - 1, g.RW - 1 - kb);
-    cw = 0;
   } else if (DIR == 3) {
     ta = 0;
     tb = g.RH - 1;
-    cw = 0;
   } else {
     ta = max(0, lb - (g.RW - 1));
     tb = min(g.RH - 1, lb + 31);
-    cw = 0;
   }
-  (void)cw;
+  ta = max(ta, seg * kLineSeg);
+  tb = min(tb, seg * kLineSeg + kLineSeg - 1);
   const int k2 = L - (g.RH - 1);
-  double s = 0.0;
+  double s = PHASE == 2 && L < nlines ? T[(int64_t)seg * nlines + L] : 0.0;
   unsigned gh = 0;
   for (int t = ta; t <= tb; t += 4) {
     double v[4];
@@ -1548,12 +1574,16 @@ __global__ void __launch_bounds__(256) big_line_kernel(const BigRegion *R, doubl
     for (int u = 0; u < 4; ++u) {
       if (ok[u]) {
         s += v[u];
-        base[idx[u]] = s;
-        if (DIR == 4) gh = max(gh, (unsigned)__double2hiint(s) & 0x7fffffffu);
+        if (PHASE == 2) {
+          base[idx[u]] = s;
+          if (DIR == 4) gh = max(gh, (unsigned)__double2hiint(s) & 0x7fffffffu);
+        }
       }
     }
   }
-  if (DIR == 4) {
+  if (PHASE == 0) {
+    if (L < nlines) T[(int64_t)seg * nlines + L] = s;
+  } else if (DIR == 4) {
     gh = __reduce_max_sync(0xffffffffu, gh);
     if (lane == 0 && gh) atomicMax(&st->guard_hi, gh);
   }
@@ -1862,6 +1892,8 @@ struct Scratch {
   double *d_aslot = nullptr;     // wide kernel: per-(SM, slot) scale-vectors
   unsigned *d_slotmask = nullptr;
   int *d_next = nullptr;  // tile counter of the large-halo gather
+  double *d_seg = nullptr;  // segment sums of the segmented line sweeps
+  size_t seg_cap = 0;
   char *h_stage = nullptr;  // pinned staging of small transfers (small_copy)
   size_t h_stage_cap = 0;
   bool attr_set = false;
@@ -2612,12 +2644,26 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
         big_rs234_kernel<512, 9, 1><<<nreg, 512, sm, s>>>(R, t_scr.d_big, t_scr.d_status);
       t_launches -= 2;
     } else {
-      big_line_kernel<2><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
-                                                                            t_scr.d_status);
-      big_line_kernel<3><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
-                                                                            t_scr.d_status);
-      big_line_kernel<4><<<dim3((bt.maxL + 255) / 256, nreg), 256, 0, s>>>(R, t_scr.d_big,
-                                                                            t_scr.d_status);
+      // few regions: segmented line sweeps (parallel along the lines too)
+      const int nseg = (bt.maxRH + kLineSeg - 1) / kLineSeg;
+      const int64_t stride = (int64_t)nseg * bt.maxL;
+      if ((size_t)(stride * nreg) > t_scr.seg_cap) {
+        if (t_scr.d_seg) cudaFree(t_scr.d_seg);
+        t_scr.d_seg = nullptr;
+        t_scr.seg_cap = 0;
+        RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_seg, (size_t)stride * nreg * sizeof(double)));
+        t_scr.seg_cap = (size_t)stride * nreg;
+      }
+      const dim3 g0((bt.maxL + 255) / 256, nseg, nreg), g1((bt.maxL + 255) / 256, 1, nreg);
+#define RUBS_SEG_SWEEP(DIRV)                                                                      \
+  big_line_seg_kernel<DIRV, 0><<<g0, 256, 0, s>>>(R, t_scr.d_big, t_scr.d_seg, stride, t_scr.d_status); \
+  big_line_seg_kernel<DIRV, 1><<<g1, 256, 0, s>>>(R, t_scr.d_big, t_scr.d_seg, stride, t_scr.d_status); \
+  big_line_seg_kernel<DIRV, 2><<<g0, 256, 0, s>>>(R, t_scr.d_big, t_scr.d_seg, stride, t_scr.d_status)
+      RUBS_SEG_SWEEP(2);
+      RUBS_SEG_SWEEP(3);
+      RUBS_SEG_SWEEP(4);
+#undef RUBS_SEG_SWEEP
+      t_launches += 6;
     }
     int *next = nullptr;
     if (!std::getenv("RUBS_B200_GATHER_STATIC")) {
