@@ -1513,7 +1513,7 @@ __global__ void __launch_bounds__(256) big_fill_rs1_kernel(ImageSpec I, const Bi
 // each segment from its carry.  tot holds nseg x nlines partial sums per region
 // (region r at tot + r * tot_stride).  The additions per element differ from
 // the sequential sweep only in where the running sum is restarted.
-constexpr int kLineSeg = 128;
+constexpr int kLineSeg = 32;
 template <int DIR, int PHASE>
 __global__ void __launch_bounds__(256) big_line_seg_kernel(const BigRegion *R, double *scratch,
                                                            double *tot, int64_t tot_stride,
@@ -1892,6 +1892,10 @@ struct Scratch {
   double *d_aslot = nullptr;     // wide kernel: per-(SM, slot) scale-vectors
   unsigned *d_slotmask = nullptr;
   int *d_next = nullptr;  // tile counter of the large-halo gather
+  // status epochs: every entry (ensure_scratch) bumps `epoch`; a clearing
+  // fetch records it, so "cleared by the previous entry, nothing in
+  // between" is clean_epoch + 1 == epoch
+  uint64_t epoch = 0, clean_epoch = ~0ull;
   double *d_seg = nullptr;  // segment sums of the segmented line sweeps
   size_t seg_cap = 0;
   char *h_stage = nullptr;  // pinned staging of small transfers (small_copy)
@@ -1908,6 +1912,7 @@ int ensure_scratch() {
   if (dev < 0 || dev >= rubs_internal::kMaxDevices)
     return set_error(RUBS_ECUDA, "device index beyond the per-device state table");
   t_dev = dev;
+  ++t_scr.epoch;
   if (t_scr.device != dev) {  // first call on this device
     t_scr.device = dev;
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_status, sizeof(Status)));
@@ -2061,6 +2066,28 @@ int fetch_status(cudaStream_t s, Status &out) {
   if (rc) return rc;
   RUBS_CUDA_TRY(cudaStreamSynchronize(s));
   out = *t_scr.h_status;
+  timer_collect();
+  return RUBS_OK;
+}
+
+// Copy the status to the host AND zero it on the device (one kernel): the
+// next one-pass call then skips its status memset (one stream operation
+// fewer between consecutive filters).
+__global__ void status_publish_kernel(unsigned *d, unsigned *h) {
+  const int i = threadIdx.x;
+  if (i < (int)(sizeof(Status) / 4)) {
+    h[i] = d[i];
+    d[i] = 0u;
+  }
+}
+int fetch_status_clear(cudaStream_t s, Status &out) {
+  status_publish_kernel<<<1, 32, 0, s>>>(reinterpret_cast<unsigned *>(t_scr.d_status),
+                                         reinterpret_cast<unsigned *>(t_scr.h_status));
+  ++t_launches;
+  RUBS_CUDA_TRY(cudaGetLastError());
+  RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+  out = *t_scr.h_status;
+  t_scr.clean_epoch = t_scr.epoch;
   timer_collect();
   return RUBS_OK;
 }
@@ -2285,32 +2312,55 @@ __global__ void plan_init_kernel(CellAgg *c, int n) {
 __global__ void plan_classify_kernel(const OvfRec *rec, int n, PlanGrid G, int tiles_x, int pw,
                                      int ph, CellAgg *cells, int *rec_cell, int2 *smem_list,
                                      int *counters, int sk) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-    const OvfRec r = rec[i];
-    const int x0 = (r.tile % tiles_x) * kTile, y0 = (r.tile / tiles_x) * kTile;
-    const int tw = min(kTile, pw - x0), th = min(kTile, ph - y0);
-    const int S = plan_side(r, tw, th, sk);
-    if (S == 0) {
-      smem_list[atomicAdd(&counters[0], 1)] = make_int2(r.tile, (int)r.mask);
-      rec_cell[i] = -1;
-      continue;
+  const int lane = threadIdx.x & 31;
+  // grid-stride loop in whole warps (the warp-aggregated atomics below need
+  // every lane; lanes past n carry no record)
+  const int n32 = (n + 31) & ~31;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n32; i += gridDim.x * blockDim.x) {
+    int cell = -1;
+    int b[8] = {INT_MAX, INT_MAX, INT_MIN, INT_MIN, INT_MAX, INT_MIN, INT_MAX, INT_MIN};
+    if (i < n) {
+      const OvfRec r = rec[i];
+      const int x0 = (r.tile % tiles_x) * kTile, y0 = (r.tile / tiles_x) * kTile;
+      const int tw = min(kTile, pw - x0), th = min(kTile, ph - y0);
+      const int S = plan_side(r, tw, th, sk);
+      if (S == 0) {
+        smem_list[atomicAdd(&counters[0], 1)] = make_int2(r.tile, (int)r.mask);
+        rec_cell[i] = -1;
+      } else {
+        const int lv = __ffs(S) - 6;  // S = 32 << lv
+        cell = G.base[lv] + (x0 / S) * G.gy[lv] + (y0 / S);
+        rec_cell[i] = cell;
+        // member box; region = bounding box of the members' own read
+        // extents (not the member box grown by the largest margin: on
+        // smoothly varying fields the margins differ across a block)
+        b[0] = x0; b[1] = y0; b[2] = x0 + tw; b[3] = y0 + th;
+        b[4] = x0 - r.m[0]; b[5] = x0 + tw + r.m[1]; b[6] = y0 - r.m[2]; b[7] = y0 + th + r.m[3];
+      }
     }
-    const int lv = __ffs(S) - 6;  // S = 32 << lv
-    const int cell = G.base[lv] + (x0 / S) * G.gy[lv] + (y0 / S);
-    rec_cell[i] = cell;
-    CellAgg *c = cells + cell;
-    atomicMin(&c->x0, x0);
-    atomicMin(&c->y0, y0);
-    atomicMax(&c->x1, x0 + tw);
-    atomicMax(&c->y1, y0 + th);
-    // the region is the bounding box of the members' own read extents, not
-    // the member box grown by the largest margin: on smoothly varying fields
-    // the margins differ across a block (config 5: region area -x %)
-    atomicMin(&c->r[0], x0 - r.m[0]);
-    atomicMax(&c->r[1], x0 + tw + r.m[1]);
-    atomicMin(&c->r[2], y0 - r.m[2]);
-    atomicMax(&c->r[3], y0 + th + r.m[3]);
-    atomicAdd(&c->count, 1);
+    // warp aggregation: neighbouring records mostly share a cell (few large
+    // blocks: thousands of records on a handful of cells serialised on the
+    // cells' atomics)
+    const unsigned peers = __match_any_sync(0xffffffffu, cell);
+    const int leader = __ffs(peers) - 1;
+    // (each group of peers reduces over its own mask; the groups are disjoint)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const bool mn = k == 0 || k == 1 || k == 4 || k == 6;
+      b[k] = mn ? __reduce_min_sync(peers, b[k]) : __reduce_max_sync(peers, b[k]);
+    }
+    if (cell >= 0 && lane == leader) {
+      CellAgg *c = cells + cell;
+      atomicMin(&c->x0, b[0]);
+      atomicMin(&c->y0, b[1]);
+      atomicMax(&c->x1, b[2]);
+      atomicMax(&c->y1, b[3]);
+      atomicMin(&c->r[0], b[4]);
+      atomicMax(&c->r[1], b[5]);
+      atomicMin(&c->r[2], b[6]);
+      atomicMax(&c->r[3], b[7]);
+      atomicAdd(&c->count, __popc(peers));
+    }
   }
 }
 
@@ -2774,17 +2824,27 @@ int launch_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cud
 // Complete a pass: status fetch (one sync), then the deferred tiles if the
 // primary launch recorded any.
 int finish_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cudaStream_t s,
-                Status &st) {
+                Status &st, bool clear = false) {
   int rc;
-  if ((rc = fetch_status(s, st))) return rc;
+  if ((rc = clear ? fetch_status_clear(s, st) : fetch_status(s, st))) return rc;
   if (st.ovf_count > 0 && !(st.flags & (kFlagFieldNonFinite | kFlagParamInvalid))) {
     {
       // the deferred-tile passes are part of the pass's filter work (kind 0)
       TimedLaunch tl(0, s);
       if ((rc = run_overflow(I, F, D, st.ovf_count, s))) return rc;
     }
-    RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s));
-    if ((rc = fetch_status(s, st))) return rc;
+    if (clear) {
+      // the status was cleared: merge the deferred passes' words into st
+      Status s2;
+      if ((rc = fetch_status_clear(s, s2))) return rc;
+      st.flags |= s2.flags;
+      st.guard_hi = std::max(st.guard_hi, s2.guard_hi);
+      st.guard_bits = std::max(st.guard_bits, s2.guard_bits);
+      st.ovf_count = 0;
+    } else {
+      RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s));
+      if ((rc = fetch_status(s, st))) return rc;
+    }
   }
   return RUBS_OK;
 }
@@ -2801,13 +2861,16 @@ int run_filter(const ImageSpec &img, FieldSpec F, int iterations, double *out, i
   F.FW = img.w;
   F.div = std::sqrt((double)iterations);
   F.scaled = iterations > 1;
-  RUBS_CUDA_TRY(cudaMemsetAsync(t_scr.d_status, 0, sizeof(Status), s));
+  // the one-pass path clears the status as it reads it: the memset is
+  // needed only when the last fetch did not clear (or a call was cut short)
+  if (!(iterations == 1 && t_scr.clean_epoch + 1 == t_scr.epoch))
+    RUBS_CUDA_TRY(cudaMemsetAsync(t_scr.d_status, 0, sizeof(Status), s));
   DomainSpec D{0, 0, img.w, img.h, out, ld_out};
   if (iterations == 1) {
     // one launch: every tile computes its own scale-vectors and margins
     if ((rc = launch_pass(img, F, D, s))) return rc;
     Status st;
-    if ((rc = finish_pass(img, F, D, s, st))) return rc;
+    if ((rc = finish_pass(img, F, D, s, st, /*clear=*/true))) return rc;
     return status_to_code(st);
   } else {
     // whole-field margins (engine.py:295) decide the pass canvases.  In LUT

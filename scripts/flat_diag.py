@@ -14,3 +14,10 @@ a = np.full(4, math.sqrt(3.0 * s))
 for _ in range(3):
     rb.filter_space_invariant(f, a)
 torch.cuda.synchronize()
+import time
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(20):
+    rb.filter_space_invariant(f, a)
+torch.cuda.synchronize()
+print(f"s={s}: {(time.perf_counter() - t0) / 20 * 1e3:.3f} ms per call (wall)")
