@@ -977,12 +977,26 @@ constexpr int kWideW = 64, kWideH = 32;
 #define RUBS_BOUND_TILE_SIZE 1500.0f
 #endif
 constexpr float kBoundTileSize = RUBS_BOUND_TILE_SIZE;
+// primary kernel stage 2: tiles whose split units would hold more than this
+// many region elements per output pixel (and that fit whole in the 224 KB
+// one-CTA-per-SM configuration) are filtered whole by a second launch
+#ifndef RUBS_W2_ELEMS
+#define RUBS_W2_ELEMS 24.0f
+#endif
+// (RUBS_B200_W2_ELEMS overrides at run time: A/B runs)
+float w2_elems() {
+  static const float v = [] {
+    const char *e = std::getenv("RUBS_B200_W2_ELEMS");
+    return e ? (float)std::atof(e) : RUBS_W2_ELEMS;
+  }();
+  return v;
+}
 // CTAs per SM of a wide-kernel launch: 2 (110 KB regions, 384 threads) by
 // default; 3 (72 KB, 256 threads) for the two-channel LUT launch of the
 // adaptive_smooth pipeline, where it measured faster (1.22 -> 0.95 ms).
 constexpr int kSlotsPerSm = 3;  // parked scale-vector slots per SM (any CT)
 template <int CT>
-__host__ __device__ constexpr int wide_smem() { return (CT == 3 ? 72 : 110) * 1024; }
+__host__ __device__ constexpr int wide_smem() { return (CT == 3 ? 72 : CT == 1 ? 224 : 110) * 1024; }
 constexpr int kSmemWide = wide_smem<2>();
 constexpr int kMaxSmId = 256;          // bound of %smid (scale-vector slots)
 #ifndef RUBS_WIDE_THREADS
@@ -990,7 +1004,7 @@ constexpr int kMaxSmId = 256;          // bound of %smid (scale-vector slots)
 #endif
 constexpr int kThreadsWide = RUBS_WIDE_THREADS;  // 2 CTAs per SM
 template <int CT>
-__host__ __device__ constexpr int wide_threads() { return CT == 3 ? 256 : kThreadsWide; }
+__host__ __device__ constexpr int wide_threads() { return CT == 3 ? 256 : CT == 1 ? 512 : kThreadsWide; }
 
 // Planning bounds of one pixel: read margins (left, right, below, above)
 // covering its taps, and an upper bound of w = 1 / (a1 a2 a3 a4).
@@ -1028,7 +1042,8 @@ __global__ void __launch_bounds__(NT, CT)
     wide_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int tiles_x32,
                        int region_cap, int *ovf_list, Status *st, double *aslots,
                        unsigned *slotmask, int tile_base, MultiChan mc,
-                       const __grid_constant__ TmaMapsN<NCH> tm) {
+                       const __grid_constant__ TmaMapsN<NCH> tm, int *w2_list, int w2_mode,
+                       float w2_elems_px) {
   constexpr int CAP = wide_cap<NCH, CT>();
   constexpr int NW = NT / 32;
   constexpr int NCX = kWideW / 8, NCY = kWideH / 8;  // 8 x 4 cells of 8 x 8
@@ -1059,13 +1074,36 @@ __global__ void __launch_bounds__(NT, CT)
       s_slot = slot;
     }
   }
+  unsigned ghi = 0, flags = 0;
+  uint32_t phase = 0;
+  // w2_mode 0: one tile per CTA (tile_base + blockIdx.x); tiles whose split
+  //   units would be costly but whose whole region fits the one-CTA-per-SM
+  //   configuration are appended to w2_list (st->w2_count) instead
+  // w2_mode 1: persistent CTAs of that configuration take the listed tiles
+  //   (st->w2_next); w2_mode 2: one tile per CTA, no list (multi-channel,
+  //   streamed bands)
+  // (the one-CTA-per-SM configuration, CT == 1, is stage 2 and loops; the
+  // others take one tile, so the loop below runs once and compiles away)
+  constexpr bool kList = CT == 1;
+  __shared__ int s_tile;
+  for (int it = 0;; ++it) {
+  if (tid == 0) {
+    int t = -1;
+    if constexpr (kList) {
+      const int k = atomicAdd(&st->w2_next, 1);
+      if (k < *(volatile int *)&st->w2_count) t = w2_list[k];
+    } else {
+      t = tile_base + blockIdx.x;
+    }
+    s_tile = t;
+  }
   if (tid < 4 * NCX * NCY) (&s_cm[0][0])[tid] = 0;
   if (tid < NCX * NCY) s_cw[tid] = 0.f;
   if (tid == 0) s_smin = INFINITY;
   __syncthreads();
-  unsigned ghi = 0, flags = 0;
-  uint32_t phase = 0;
-  const int tile = tile_base + blockIdx.x, tx = tile % tiles_x, ty = tile / tiles_x;
+  const int tile = s_tile;
+  if (tile < 0) break;
+  const int tx = tile % tiles_x, ty = tile / tiles_x;
   const int x0 = tx * kWideW, y0 = ty * kWideH;
 
   double *const apark =
@@ -1213,6 +1251,7 @@ __global__ void __launch_bounds__(NT, CT)
     };
     int u[4], d[8];
     float wm;
+    bool full2 = false;  // the whole tile fits the stage-2 configuration
     unsigned fitm = 0;  // bit L: this lane's level-L node fits
 #pragma unroll
     for (int pass = 0; pass < 2; ++pass) {
@@ -1230,6 +1269,13 @@ __global__ void __launch_bounds__(NT, CT)
         if (pass == 0) {
           int dd[8];
           if (node(L, u, wm, dd)) fitm |= 1u << L;
+          if (L == kLv - 1) {
+            // the whole tile in the one-CTA-per-SM configuration (stage 2)
+            const float mn2 = (float)min(dd[6] + 1, dd[7]);
+            const float l42 = 0.25f * (float)(dd[6] + 1) * (float)dd[7] * mn2 * mn2;
+            full2 = dd[2] > 0 && region_elems(dd[6] + 1, dd[7]) <= wide_cap<1, 1>() &&
+                    wm * l42 <= kPrecisionBudget;
+          }
         } else if (L == top) {
           node(L, u, wm, d);
         }
@@ -1237,8 +1283,32 @@ __global__ void __launch_bounds__(NT, CT)
     }
     const int top = fitm ? 31 - __clz(fitm) : -1;
     // the unit is written by its node's first lane
-    const bool writer =
+    bool writer =
         top >= 0 && cx == (cx & ~(kLw[top] - 1)) && cy == (cy & ~(kLh[top] - 1));
+    if (!kList && w2_mode == 0) {
+      // stage 2: a tile that the split units would cost more than
+      // w2_elems_px region elements per pixel (or that defers cells) but
+      // that fits whole in the 224 KB configuration goes to the list
+      const bool in_t = x0 + 8 * cx < D.pw && y0 + 8 * cy < D.ph;
+      const int re = writer ? region_elems(d[6] + 1, d[7]) : 0;
+      const int px = writer ? d[2] * d[3] : 0;
+      const int re_sum = __reduce_add_sync(0xffffffffu, re);
+      const int px_sum = __reduce_add_sync(0xffffffffu, px);
+      const bool any_ovf = __any_sync(0xffffffffu, in_t && top < 0);
+      const bool whole = __all_sync(0xffffffffu, !in_t || top == kLv - 1);
+      const bool to2 = __shfl_sync(0xffffffffu, (int)full2, 0) && !whole &&
+                       (any_ovf || (float)re_sum > w2_elems_px * (float)px_sum);
+      if (to2) {
+        if (lane == 0) {
+          w2_list[atomicAdd(&st->w2_count, 1)] = tile;
+          s_nu = 0;
+        }
+        writer = false;
+        fitm = 0;
+      }
+      if (to2) goto plan_done;
+    }
+    {
     const unsigned wb = __ballot_sync(0xffffffffu, writer);
     if (writer) {
       int *dst = s_unit[__popc(wb & ((1u << lane) - 1u))];
@@ -1284,6 +1354,8 @@ __global__ void __launch_bounds__(NT, CT)
       }
     }
     if (lane == 0) s_nu = __popc(wb);
+    }
+  plan_done:;
   }
   __syncthreads();
 
@@ -1379,6 +1451,9 @@ __global__ void __launch_bounds__(NT, CT)
     }
     __syncthreads();
   }
+  if constexpr (!kList) break;
+  __syncthreads();  // shared tile state and the region buffer free for the next tile
+  }  // tile loop
   if (kPark && tid == 0) atomicAnd(&slotmask[smid], ~(1u << (s_slot % kSlotsPerSm)));
   flush_status(st, ghi, flags);
 }
@@ -1892,6 +1967,8 @@ struct Scratch {
   double *d_aslot = nullptr;     // wide kernel: per-(SM, slot) scale-vectors
   unsigned *d_slotmask = nullptr;
   int *d_next = nullptr;  // tile counter of the large-halo gather
+  int *d_w2 = nullptr;    // primary kernel stage-2 tile list
+  size_t w2_cap = 0;
   // status epochs: every entry (ensure_scratch) bumps `epoch`; a clearing
   // fetch records it, so "cleared by the previous entry, nothing in
   // between" is clean_epoch + 1 == epoch
@@ -1956,6 +2033,18 @@ int ensure_scratch() {
     RUBS_SET_SMEM(kModeLut32, 1);
 #undef RUBS_SET_SMEM
     // multi-channel instantiations (adaptive_smooth pipeline)
+#define RUBS_SET_CT1(M, T)                                                                  \
+  RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<M, T, wide_threads<1>(), 1, 1>,      \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, wide_smem<1>()))
+    RUBS_SET_CT1(kModeField, 0);
+    RUBS_SET_CT1(kModeField, 1);
+    RUBS_SET_CT1(kModeUniform, 0);
+    RUBS_SET_CT1(kModeUniform, 1);
+    RUBS_SET_CT1(kModeLut, 0);
+    RUBS_SET_CT1(kModeLut, 1);
+    RUBS_SET_CT1(kModeLut32, 0);
+    RUBS_SET_CT1(kModeLut32, 1);
+#undef RUBS_SET_CT1
     RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<kModeUniform, 1, kThreadsWide, 3>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWide));
     RUBS_CUDA_TRY(cudaFuncSetAttribute(wide_filter_kernel<kModeLut, 1, wide_threads<3>(), 2, 3>,
@@ -2162,7 +2251,7 @@ int kernel_choice() {
 // Wide-kernel tiles of rows [wy0, wy1) of the 64 x 32 grid over domain D.
 template <int M, int T, int NCH = 1, int CT = 2>
 void launch_wide_rows(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int wy0,
-                      int wy1, cudaStream_t s, const MultiChan *mcp = nullptr) {
+                      int wy1, cudaStream_t s, const MultiChan *mcp = nullptr, int w2_mode = 2) {
   const int tiles_x = (D.pw + kTile - 1) / kTile;
   const int wx = (D.pw + kWideW - 1) / kWideW;
   if (wy1 <= wy0) return;
@@ -2179,28 +2268,57 @@ void launch_wide_rows(const ImageSpec &I, const FieldSpec &F, const DomainSpec &
     Ic.f = mc.f[ch];
     tm.m[ch] = tma_maps(Ic);
   }
+  const int grid = w2_mode == 1 ? t_scr.sms : wx * (wy1 - wy0);
   wide_filter_kernel<M, T, wide_threads<CT>(), NCH, CT>
-      <<<wx * (wy1 - wy0), wide_threads<CT>(), wide_smem<CT>(), s>>>(
+      <<<grid, wide_threads<CT>(), wide_smem<CT>(), s>>>(
       I, F, D, wx, tiles_x, wide_cap<NCH, CT>(), t_scr.d_ovf, t_scr.d_status, t_scr.d_aslot,
-      t_scr.d_slotmask, wy0 * wx, mc, tm);
+      t_scr.d_slotmask, wy0 * wx, mc, tm, t_scr.d_w2, w2_mode, w2_elems());
 }
 
 void launch_wide_rows_rt(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int wy0,
-                         int wy1, cudaStream_t s) {
+                         int wy1, cudaStream_t s, int w2_mode = 2) {
   const int m = F.mode, t = I.dt;
   if (m == kModeField) {
-    if (t) launch_wide_rows<kModeField, 1>(I, F, D, wy0, wy1, s);
-    else launch_wide_rows<kModeField, 0>(I, F, D, wy0, wy1, s);
+    if (t) launch_wide_rows<kModeField, 1>(I, F, D, wy0, wy1, s, nullptr, w2_mode);
+    else launch_wide_rows<kModeField, 0>(I, F, D, wy0, wy1, s, nullptr, w2_mode);
   } else if (m == kModeUniform) {
-    if (t) launch_wide_rows<kModeUniform, 1>(I, F, D, wy0, wy1, s);
-    else launch_wide_rows<kModeUniform, 0>(I, F, D, wy0, wy1, s);
+    if (t) launch_wide_rows<kModeUniform, 1>(I, F, D, wy0, wy1, s, nullptr, w2_mode);
+    else launch_wide_rows<kModeUniform, 0>(I, F, D, wy0, wy1, s, nullptr, w2_mode);
   } else if (m == kModeLut) {
-    if (t) launch_wide_rows<kModeLut, 1>(I, F, D, wy0, wy1, s);
-    else launch_wide_rows<kModeLut, 0>(I, F, D, wy0, wy1, s);
+    if (t) launch_wide_rows<kModeLut, 1>(I, F, D, wy0, wy1, s, nullptr, w2_mode);
+    else launch_wide_rows<kModeLut, 0>(I, F, D, wy0, wy1, s, nullptr, w2_mode);
   } else {
-    if (t) launch_wide_rows<kModeLut32, 1>(I, F, D, wy0, wy1, s);
-    else launch_wide_rows<kModeLut32, 0>(I, F, D, wy0, wy1, s);
+    if (t) launch_wide_rows<kModeLut32, 1>(I, F, D, wy0, wy1, s, nullptr, w2_mode);
+    else launch_wide_rows<kModeLut32, 0>(I, F, D, wy0, wy1, s, nullptr, w2_mode);
   }
+}
+
+// Stage 2 of the primary kernel: persistent one-CTA-per-SM launch over the
+// tiles stage 1 listed (exits at once when the list is empty).
+void launch_wide_stage2_rt(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
+                           cudaStream_t s) {
+  const int m = F.mode, t = I.dt;
+  const int wy = (D.ph + kWideH - 1) / kWideH;
+  if (m == kModeField) {
+    if (t) launch_wide_rows<kModeField, 1, 1, 1>(I, F, D, 0, wy, s, nullptr, 1);
+    else launch_wide_rows<kModeField, 0, 1, 1>(I, F, D, 0, wy, s, nullptr, 1);
+  } else if (m == kModeUniform) {
+    if (t) launch_wide_rows<kModeUniform, 1, 1, 1>(I, F, D, 0, wy, s, nullptr, 1);
+    else launch_wide_rows<kModeUniform, 0, 1, 1>(I, F, D, 0, wy, s, nullptr, 1);
+  } else if (m == kModeLut) {
+    if (t) launch_wide_rows<kModeLut, 1, 1, 1>(I, F, D, 0, wy, s, nullptr, 1);
+    else launch_wide_rows<kModeLut, 0, 1, 1>(I, F, D, 0, wy, s, nullptr, 1);
+  } else {
+    if (t) launch_wide_rows<kModeLut32, 1, 1, 1>(I, F, D, 0, wy, s, nullptr, 1);
+    else launch_wide_rows<kModeLut32, 0, 1, 1>(I, F, D, 0, wy, s, nullptr, 1);
+  }
+}
+
+
+// Stage 2 of the primary kernel on (RUBS_B200_NO_STAGE2 turns it off: A/B)
+bool use_stage2() {
+  static const bool v = std::getenv("RUBS_B200_NO_STAGE2") == nullptr;
+  return v;
 }
 
 template <int M, int T>
@@ -2209,8 +2327,13 @@ void launch_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, c
   const int ntiles = tiles_x * tiles_y;
   // ovf_count is zero here: every caller clears the status before its first
   // pass and finish_pass clears the count after the deferred tiles
-  if (kernel_choice() == 2)
-    launch_wide_rows<M, T>(I, F, D, 0, (D.ph + kWideH - 1) / kWideH, s);
+  if (kernel_choice() == 2) {
+    const int mode = use_stage2() ? 0 : 2;
+    // the stage-2 list and its take counter start empty for every pass
+    if (mode == 0) cudaMemsetAsync(&t_scr.d_status->w2_count, 0, 2 * sizeof(int), s);
+    launch_wide_rows<M, T>(I, F, D, 0, (D.ph + kWideH - 1) / kWideH, s, nullptr, mode);
+    if (mode == 0) launch_wide_stage2_rt(I, F, D, s);
+  }
   else
     tile_filter_kernel<M, T><<<ntiles, kThreadsSmall, kSmemSmall, s>>>(
         I, F, D, tiles_x, kSmemSmall / 8, t_scr.d_ovf, t_scr.d_status, tma_maps(I));
@@ -2797,6 +2920,14 @@ int ensure_ovf(const DomainSpec &D) {
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_ovf, 4 * ntiles * sizeof(OvfRec)));
     t_scr.ovf_cap = 4 * ntiles;
   }
+  // stage-2 list: at most one entry per wide tile
+  const size_t nwide = (size_t)((D.pw + kWideW - 1) / kWideW) * ((D.ph + kWideH - 1) / kWideH);
+  if (nwide > t_scr.w2_cap) {
+    if (t_scr.d_w2) cudaFree(t_scr.d_w2);
+    t_scr.d_w2 = nullptr;
+    RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_w2, nwide * sizeof(int)));
+    t_scr.w2_cap = nwide;
+  }
   return RUBS_OK;
 }
 
@@ -3120,10 +3251,16 @@ int run_streamed(const ImageSpec &I, FieldSpec F, const void *f_host,
                                     (size_t)(r1 - r0) * pl.row_bytes, cudaMemcpyHostToDevice, h2d));
     RUBS_CUDA_TRY(cudaEventRecord(t_ss.ev[2 * b], h2d));
     RUBS_CUDA_TRY(cudaStreamWaitEvent(cmp, t_ss.ev[2 * b], 0));
-    launch_wide_rows_rt(I, F, D, t0, t1, cmp);
+    launch_wide_rows_rt(I, F, D, t0, t1, cmp, use_stage2() ? 0 : 2);
     ++t_launches;
     RUBS_CUDA_TRY(cudaGetLastError());
     RUBS_CUDA_TRY(cudaEventRecord(t_ss.ev[2 * b + 1], cmp));
+  }
+  // stage 2 of the primary kernel (tiles listed by the bands) after every
+  // band; rows it writes go back with the deferred tiles' below
+  if (use_stage2()) {  // (the status, list counters included, was cleared above)
+    launch_wide_stage2_rt(I, F, D, cmp);
+    ++t_launches;
   }
   // the returns are enqueued last: a copy into pageable host memory blocks
   // the host until it has run, so every upload and launch is queued first
@@ -3138,11 +3275,15 @@ int run_streamed(const ImageSpec &I, FieldSpec F, const void *f_host,
   RUBS_CUDA_TRY(cudaStreamSynchronize(d2h));
   Status st;
   if ((rc = fetch_status(cmp, st))) return rc;
-  if (st.ovf_count > 0 && !(st.flags & (kFlagFieldNonFinite | kFlagParamInvalid))) {
-    // deferred tiles: computed now, then every row goes back once more
-    if ((rc = run_overflow(I, F, D, st.ovf_count, cmp))) return rc;
-    RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), cmp));
-    if ((rc = fetch_status(cmp, st))) return rc;
+  const bool bad = st.flags & (kFlagFieldNonFinite | kFlagParamInvalid);
+  if ((st.ovf_count > 0 || st.w2_count > 0) && !bad) {
+    // deferred tiles: computed now; rows written after their band's return
+    // (deferred and stage-2 tiles) go back once more
+    if (st.ovf_count > 0) {
+      if ((rc = run_overflow(I, F, D, st.ovf_count, cmp))) return rc;
+      RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), cmp));
+      if ((rc = fetch_status(cmp, st))) return rc;
+    }
     RUBS_CUDA_TRY(cudaMemcpyAsync(out_host, dout, (size_t)H * W * 8, cudaMemcpyDeviceToHost, cmp));
     RUBS_CUDA_TRY(cudaStreamSynchronize(cmp));
   }

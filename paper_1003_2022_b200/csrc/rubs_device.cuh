@@ -38,6 +38,8 @@ struct Status {
   int ovf_count;                  // tiles deferred to the large-smem launch
   int pix_count;                  // pixels deferred to the per-pixel pass
   unsigned long long smax_bits;   // max LUT size parameter (bits of a positive double)
+  int w2_count;                   // tiles listed for the primary kernel's stage 2
+  int w2_next;                    // stage 2's take counter
 };
 
 // A tile deferred by the primary launch (its regions exceed the primary
