@@ -1061,6 +1061,19 @@ __global__ void __launch_bounds__(NT, CT)
   // A) and parked in an L2-resident slot of this SM (two CTAs per SM: two
   // slots, claimed with an atomic bit) until the gather reads them back
   constexpr bool kPark = MODE >= kModeLut;
+  // stage 2 (CT == 1) takes its first listed tile before any set-up: with
+  // an empty list (the common case on small-kernel fields) every CTA exits
+  // at once
+  constexpr bool kList = CT == 1;
+  __shared__ int s_tile;
+  if constexpr (kList) {
+    if (tid == 0) {
+      const int k = atomicAdd(&st->w2_next, 1);
+      s_tile = k < *(volatile int *)&st->w2_count ? w2_list[k] : -1;
+    }
+    __syncthreads();
+    if (s_tile < 0) return;
+  }
   unsigned smid = 0;
   if (tid == 0) {
     mbar_init(mbar);
@@ -1084,14 +1097,16 @@ __global__ void __launch_bounds__(NT, CT)
   //   streamed bands)
   // (the one-CTA-per-SM configuration, CT == 1, is stage 2 and loops; the
   // others take one tile, so the loop below runs once and compiles away)
-  constexpr bool kList = CT == 1;
-  __shared__ int s_tile;
   for (int it = 0;; ++it) {
   if (tid == 0) {
     int t = -1;
     if constexpr (kList) {
-      const int k = atomicAdd(&st->w2_next, 1);
-      if (k < *(volatile int *)&st->w2_count) t = w2_list[k];
+      if (it == 0) {
+        t = s_tile;  // taken above
+      } else {
+        const int k = atomicAdd(&st->w2_next, 1);
+        if (k < *(volatile int *)&st->w2_count) t = w2_list[k];
+      }
     } else {
       t = tile_base + blockIdx.x;
     }
