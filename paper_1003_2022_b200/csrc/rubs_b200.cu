@@ -1037,6 +1037,17 @@ __host__ __device__ constexpr int wide_cap() {
   return (wide_smem<CT>() / 8 / NCH) & ~15;
 }
 
+// Take the next listed stage-2 tile, or -1.  A take past the end is undone,
+// so the counter never overshoots: the streamed path launches stage 2 once
+// per band, and a later launch must still find the tiles listed after an
+// earlier one ran dry.
+__device__ __forceinline__ int w2_take(Status *st, const int *w2_list) {
+  const int k = atomicAdd(&st->w2_next, 1);
+  if (k < *(volatile int *)&st->w2_count) return w2_list[k];
+  atomicSub(&st->w2_next, 1);
+  return -1;
+}
+
 template <int MODE, int DT, int NT, int NCH, int CT = 2>
 __global__ void __launch_bounds__(NT, CT)
     wide_filter_kernel(ImageSpec I, FieldSpec F, DomainSpec D, int tiles_x, int tiles_x32,
@@ -1067,10 +1078,7 @@ __global__ void __launch_bounds__(NT, CT)
   constexpr bool kList = CT == 1;
   __shared__ int s_tile;
   if constexpr (kList) {
-    if (tid == 0) {
-      const int k = atomicAdd(&st->w2_next, 1);
-      s_tile = k < *(volatile int *)&st->w2_count ? w2_list[k] : -1;
-    }
+    if (tid == 0) s_tile = w2_take(st, w2_list);
     __syncthreads();
     if (s_tile < 0) return;
   }
@@ -1104,8 +1112,7 @@ __global__ void __launch_bounds__(NT, CT)
       if (it == 0) {
         t = s_tile;  // taken above
       } else {
-        const int k = atomicAdd(&st->w2_next, 1);
-        if (k < *(volatile int *)&st->w2_count) t = w2_list[k];
+        t = w2_take(st, w2_list);
       }
     } else {
       t = tile_base + blockIdx.x;
@@ -3268,14 +3275,15 @@ int run_streamed(const ImageSpec &I, FieldSpec F, const void *f_host,
     RUBS_CUDA_TRY(cudaStreamWaitEvent(cmp, t_ss.ev[2 * b], 0));
     launch_wide_rows_rt(I, F, D, t0, t1, cmp, use_stage2() ? 0 : 2);
     ++t_launches;
+    if (use_stage2()) {
+      // stage 2 per band: the tiles listed so far are done before this
+      // band's rows go back (each listed tile is taken by exactly one
+      // stage-2 launch: the same outputs as the device path's single one)
+      launch_wide_stage2_rt(I, F, D, cmp);
+      ++t_launches;
+    }
     RUBS_CUDA_TRY(cudaGetLastError());
     RUBS_CUDA_TRY(cudaEventRecord(t_ss.ev[2 * b + 1], cmp));
-  }
-  // stage 2 of the primary kernel (tiles listed by the bands) after every
-  // band; rows it writes go back with the deferred tiles' below
-  if (use_stage2()) {  // (the status, list counters included, was cleared above)
-    launch_wide_stage2_rt(I, F, D, cmp);
-    ++t_launches;
   }
   // the returns are enqueued last: a copy into pageable host memory blocks
   // the host until it has run, so every upload and launch is queued first
@@ -3291,14 +3299,12 @@ int run_streamed(const ImageSpec &I, FieldSpec F, const void *f_host,
   Status st;
   if ((rc = fetch_status(cmp, st))) return rc;
   const bool bad = st.flags & (kFlagFieldNonFinite | kFlagParamInvalid);
-  if ((st.ovf_count > 0 || st.w2_count > 0) && !bad) {
+  if (st.ovf_count > 0 && !bad) {
     // deferred tiles: computed now; rows written after their band's return
-    // (deferred and stage-2 tiles) go back once more
-    if (st.ovf_count > 0) {
-      if ((rc = run_overflow(I, F, D, st.ovf_count, cmp))) return rc;
-      RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), cmp));
-      if ((rc = fetch_status(cmp, st))) return rc;
-    }
+    // go back once more
+    if ((rc = run_overflow(I, F, D, st.ovf_count, cmp))) return rc;
+    RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), cmp));
+    if ((rc = fetch_status(cmp, st))) return rc;
     RUBS_CUDA_TRY(cudaMemcpyAsync(out_host, dout, (size_t)H * W * 8, cudaMemcpyDeviceToHost, cmp));
     RUBS_CUDA_TRY(cudaStreamSynchronize(cmp));
   }
