@@ -610,8 +610,10 @@ SMEM_WF_PER_PX = {"2": 16.39, "3": 53.9}
 TRAFFIC_PER_PASS = {
     "2": (105.45e6, "ncu, wide_filter_kernel, profiles/ncu_r01b_summary.md"),
     "3": (1.588e9, "ncu, n3_tile_kernel, profiles/ncu_r01b_summary.md"),
-    "5": (270.3e9, "ncu launch list of one step, sum over the pass's kernels "
-                   "(profiles/ncu_r02_c5_launches.md; algorithmic 25.8 GB)"),
+    "5": (180.4e9, "ncu launch list of one step, sum over the pass's kernels "
+                   "(profiles/ncu_r02_c5_launches.csv, split in profiles/ncu_r02_summary.md; algorithmic "
+                   "25.8 GB: the rest is the large-halo regions' scratch, 4.5 elements per pixel written "
+                   "and re-read by the sweeps, then gathered)"),
 }
 
 
