@@ -227,7 +227,7 @@ def test_acceptance_03_runtime_flat_across_kernel_sizes(cuda):
 
 
 @pytest.mark.xfail(strict=False, reason="large kernels (s >= 256) take the global-scratch block path: "
-                   "measured max/min ~4 over s = 1..16384 at 2048^2 (DESIGN.md §4, flat-cost table)")
+                   "measured max/min ~2.4 over s = 1..16384 at 2048^2 (DESIGN.md §4, flat-cost table)")
 def test_acceptance_03_flat_up_to_large_kernels(cuda):
     # the same contract extended to s = 16384 (a ~ 222, support ~540 px)
     torch = cuda
