@@ -302,6 +302,37 @@ int rubs_b200_filter3_params_rows(const void *f, int f_dtype, int64_t f_row0, in
                                   int64_t p_row0, int64_t ld_p, int64_t out_row0,
                                   int64_t out_rows, double *out, int64_t ld_out, void *stream);
 
+/*
+ * N=3 lattice mode: the paper's O(1) algorithm for the off-grid directions
+ * (285, 662: "one needs to interpolate the image for
+ * implementing the associated running-sums").  The image is moved once onto
+ * the triangular lattice of spacing `spacing` (in [0.125, 1], pixels) that
+ * contains the three directions, by the adjoint of linear interpolation;
+ * the exact N=3 kernel is then applied to that resampled image in O(1) per
+ * pixel (exact int128 running sums along the lattice directions, an
+ * 8-vertex finite difference, linear interpolation on the lattice
+ * triangles).  Against the exact filter above this differs by the
+ * resampling error only; arguments and errors as
+ * rubs_b200_filter3 / _params, plus RUBS_EVALUE for non-finite image
+ * entries (integer running sums carry no NaN).
+ */
+int rubs_b200_filter3_lattice(const void *f, int f_dtype, int64_t H, int64_t W, int64_t ld_f,
+                              const double *field, int field_is_uniform, int64_t ld_field,
+                              int iterations, double spacing, double *out, int64_t ld_out,
+                              void *stream);
+int rubs_b200_filter3_lattice_params(const void *f, int f_dtype, int64_t H, int64_t W,
+                                     int64_t ld_f, const void *size, const void *elong,
+                                     const void *orient, int p_dtype, int64_t ld_p,
+                                     int iterations, double spacing, double *out,
+                                     int64_t ld_out, void *stream);
+int rubs_b200_filter3_lattice_host(const void *f, int f_dtype, int64_t H, int64_t W,
+                                   const double *field, int field_is_uniform, int iterations,
+                                   double spacing, double *out);
+int rubs_b200_filter3_lattice_params_host(const void *f, int f_dtype, int64_t H, int64_t W,
+                                          const void *size, const void *elong,
+                                          const void *orient, int p_dtype, int iterations,
+                                          double spacing, double *out);
+
 /* The N=3 mapping alone: device arrays of n parameters -> device n x 3. */
 int rubs_b200_scales3(const void *size, const void *elong, const void *orient, int p_dtype,
                       int64_t n, double *out, void *stream);

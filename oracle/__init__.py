@@ -317,3 +317,65 @@ def points3(f, field, pts, threads=None):
     with ThreadPoolExecutor(threads) as ex:
         list(ex.map(run, chunks))
     return out
+
+
+# ---------------------------------------------------------------------------
+# N=3 lattice (O(1), interpolated) mode: brute-force route (dense3_oracle.c).
+
+
+def _lib3l():
+    L = _lib3()
+    if not getattr(L, "_n3l_ready", False):
+        dp, lp = ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int64)
+        L.rubs_oracle3_splat.restype = None
+        L.rubs_oracle3_splat.argtypes = [dp, ctypes.c_int, ctypes.c_int, ctypes.c_double, lp, lp,
+                                         ctypes.c_int64, dp]
+        L.rubs_oracle3_lattice_points.restype = ctypes.c_int
+        L.rubs_oracle3_lattice_points.argtypes = [dp, ctypes.c_int, ctypes.c_int, dp, ctypes.c_int,
+                                                  ctypes.c_double, lp, ctypes.c_int64, dp]
+        L._n3l_ready = True
+    return L
+
+
+def splat3(f, h, al, ga):
+    """Lattice-mode resampling f_hex at lattice indices (al, ga)."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    al, ga = np.broadcast_arrays(np.asarray(al, np.int64), np.asarray(ga, np.int64))
+    shape = al.shape
+    al, ga = np.ascontiguousarray(al).reshape(-1), np.ascontiguousarray(ga).reshape(-1)
+    out = np.empty(al.size)
+    lp = ctypes.POINTER(ctypes.c_int64)
+    _lib3l().rubs_oracle3_splat(_dp(f), f.shape[0], f.shape[1], float(h), al.ctypes.data_as(lp),
+                                ga.ctypes.data_as(lp), al.size, _dp(out))
+    return out.reshape(shape)
+
+
+def lattice3_points(f, field, pts, h=1.0, threads=None):
+    """Lattice-mode N=3 filter (one pass) at pixels pts = (N, 2) [row, col],
+    by brute force: sum over lattice points p of f_hex[p] beta(n - p)."""
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    H, W = f.shape
+    fld, uni = _field3_arg(field, f.shape)
+    pts = np.ascontiguousarray(pts, dtype=np.int64).reshape(-1, 2)
+    out = np.empty(pts.shape[0])
+    n = pts.shape[0]
+    if n == 0:
+        return out
+    threads = threads or min(os.cpu_count() or 1, 64)
+    chunks = np.array_split(np.arange(n), min(threads * 4, n))
+    L = _lib3l()
+    lp = ctypes.POINTER(ctypes.c_int64)
+
+    def run(idx):
+        if idx.size == 0:
+            return
+        p = np.ascontiguousarray(pts[idx])
+        o = np.empty(idx.size)
+        if L.rubs_oracle3_lattice_points(_dp(f), H, W, _dp(fld), uni, float(h), p.ctypes.data_as(lp),
+                                         idx.size, _dp(o)):
+            raise RuntimeError("oracle lattice3_points failed")
+        out[idx] = o
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(run, chunks))
+    return out

@@ -170,3 +170,79 @@ int rubs_oracle3_points(const double *f, int H, int W, const double *field, int 
     }
     return 0;
 }
+
+/*
+ * Lattice (O(1)) mode of the N=3 filter, by brute force -- the independent
+ * route for this repo's interpolated three-direction algorithm (DESIGN.md
+ * §9b; off-grid running sums need interpolation).
+ *
+ * The image f = sum_m f[m] delta(x - m) is moved onto the triangular lattice
+ * p(al, ga) = h (al u1 + ga u3) = h (al - ga/2, ga sqrt3/2) (origin at pixel
+ * (0, 0)) by the adjoint of piecewise-linear interpolation -- each pixel's
+ * value is split over the three corners of its lattice triangle with its
+ * barycentric weights (mass and first moment kept):
+ *     f_hex[p] = sum_m f[m] hat((m - p) / h),
+ *     hat(d) = max(0, 1 - max(|da|, |dg|, |da - dg|)),  d = da u1 + dg u3.
+ * The lattice filter is then the EXACT N=3 kernel applied to that delta
+ * train:  out(n) = sum_p f_hex[p] beta_a(n)(n - p).
+ * Here both sums are taken literally (O(support) per pixel); the product
+ * path gets the same numbers in O(1) per pixel from running sums along the
+ * three lattice directions.
+ */
+static double splat3(const double *f, int H, int W, double h, double px, double py)
+{
+    const double gh = SIN60 * h;
+    const int c0 = (int)floor(px), r0 = (int)floor(py);
+    double acc = 0.0;
+    for (int r = r0; r <= r0 + 1; ++r)
+        for (int c = c0; c <= c0 + 1; ++c) {
+            if (r < 0 || r >= H || c < 0 || c >= W) continue;
+            const double dg = (r - py) / gh, da = (c - px) / h + 0.5 * dg;
+            double m = fabs(da);
+            if (fabs(dg) > m) m = fabs(dg);
+            if (fabs(da - dg) > m) m = fabs(da - dg);
+            if (m < 1.0) acc += f[(int64_t)r * W + c] * (1.0 - m);
+        }
+    return acc;
+}
+
+/* f_hex at lattice indices (al, ga), n of them. */
+void rubs_oracle3_splat(const double *f, int H, int W, double h, const int64_t *al,
+                        const int64_t *ga, int64_t n, double *out)
+{
+    for (int64_t i = 0; i < n; ++i)
+        out[i] = splat3(f, H, W, h, h * ((double)al[i] - 0.5 * (double)ga[i]),
+                        SIN60 * h * (double)ga[i]);
+}
+
+int rubs_oracle3_lattice_points(const double *f, int H, int W, const double *field, int uniform,
+                                double h, const int64_t *pts, int64_t npts, double *out)
+{
+    if (!(h > 0.0) || h > 1.0) return 1;
+    field3_t F;
+    F.field = field; F.uniform = uniform; F.H = H; F.W = W;
+    F.div = 1.0;
+    const double gh = SIN60 * h;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t i = 0; i < npts; ++i) {
+        const int Y = (int)pts[2 * i], X = (int)pts[2 * i + 1];
+        double a[3];
+        field3_at(&F, Y, X, a);
+        int rx, ry;
+        support3(a, &rx, &ry);
+        const int64_t g0 = (int64_t)ceil((Y - ry) / gh), g1 = (int64_t)floor((Y + ry) / gh);
+        double acc = 0.0;
+        for (int64_t g = g0; g <= g1; ++g) {
+            const double py = gh * (double)g;
+            const int64_t a0 = (int64_t)ceil((X - rx) / h + 0.5 * g);
+            const int64_t a1 = (int64_t)floor((X + rx) / h + 0.5 * g);
+            for (int64_t al = a0; al <= a1; ++al) {
+                const double px = h * ((double)al - 0.5 * (double)g);
+                const double w = rubs_oracle3_kernel(a, X - px, Y - py);
+                if (w != 0.0) acc += w * splat3(f, H, W, h, px, py);
+            }
+        }
+        out[i] = acc;
+    }
+    return 0;
+}

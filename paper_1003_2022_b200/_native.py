@@ -36,7 +36,7 @@ def build_native(verbose: bool = False, defines=(), out: str | None = None) -> s
     ``defines``/``out`` build a variant library for A/B runs."""
     os.makedirs(LIB_DIR, exist_ok=True)
     out = out or LIB_PATH
-    srcs = [os.path.join(CSRC, n) for n in ("rubs_b200.cu", "rubs_tensor.cu", "rubs_n3.cu")]
+    srcs = [os.path.join(CSRC, n) for n in ("rubs_b200.cu", "rubs_tensor.cu", "rubs_n3.cu", "rubs_n3_lattice.cu")]
     cmd = ["nvcc", *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", INCLUDE, "-o", out + ".tmp",
            *srcs]
     if verbose:
@@ -97,6 +97,13 @@ SIGNATURES = {
     "rubs_b200_filter3_host": (_int, [_vp, _int, _i64, _i64, _vp, _int, _int, _vp]),
     "rubs_b200_filter3_params": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp, _int, _i64, _int,
                                         _vp, _i64, _vp]),
+    "rubs_b200_filter3_lattice": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _int, _i64, _int, _dbl, _vp,
+                                         _i64, _vp]),
+    "rubs_b200_filter3_lattice_params": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp, _int, _i64,
+                                                _int, _dbl, _vp, _i64, _vp]),
+    "rubs_b200_filter3_lattice_host": (_int, [_vp, _int, _i64, _i64, _vp, _int, _int, _dbl, _vp]),
+    "rubs_b200_filter3_lattice_params_host": (_int, [_vp, _int, _i64, _i64, _vp, _vp, _vp, _int, _int,
+                                                     _dbl, _vp]),
     "rubs_b200_filter3_params_host": (_int, [_vp, _int, _i64, _i64, _vp, _vp, _vp, _int, _int, _vp]),
     "rubs_b200_scales3": (_int, [_vp, _vp, _vp, _int, _i64, _vp, _vp]),
     "rubs_b200_read_margins3_params": (_int, [_vp, _vp, _vp, _int, _i64, _i64, _i64,

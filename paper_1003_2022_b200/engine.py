@@ -599,12 +599,27 @@ def _torch_image(f):
     return f.contiguous()
 
 
-def filter_space_variant3(f, field, iterations: int = 1, *, out=None):
+def _n3_mode(mode, spacing) -> bool:
+    """True for the O(1) lattice mode; validates its spacing."""
+    if mode not in ("exact", "lattice"):
+        raise ValueError(f"mode must be 'exact' or 'lattice', got {mode!r}")
+    if mode == "lattice" and not (0.125 <= float(spacing) <= 1.0):
+        raise ValueError("lattice spacing must be in [0.125, 1]")
+    return mode == "lattice"
+
+
+def filter_space_variant3(f, field, iterations: int = 1, *, out=None, mode: str = "exact",
+                          spacing: float = 1.0):
     """Three-direction filter: per-pixel scales (a1, a2, a3) along 0, 60 and
     120 degrees.  ``field`` is (H, W, 3) or (3,); entries below SCALE_FLOOR
     are clamped, passes use a / sqrt(iterations) like filter_space_variant.
-    Returns float64 of f's shape (numpy, or a CUDA tensor for CUDA input)."""
+    ``mode="exact"`` computes the N=3 filter exactly (O(kernel height) per
+    pixel); ``mode="lattice"`` is the paper's O(1) algorithm on the
+    triangular lattice of the given ``spacing`` (the image resampled once,
+    DESIGN.md §9b).  Returns float64 of f's shape (numpy, or a CUDA tensor for
+    CUDA input)."""
     iterations = _check_iterations(iterations)
+    lattice = _n3_mode(mode, spacing)
     L = _native.load()
     if _is_torch(f):
         torch = _torch()
@@ -626,11 +641,16 @@ def filter_space_variant3(f, field, iterations: int = 1, *, out=None):
                 fptr = ctypes.c_void_p(dfl.data_ptr())
         if H == 0 or W == 0:
             return res
+        fdt = _native.RUBS_F32 if f.dtype == torch.float32 else _native.RUBS_F64
         with torch.cuda.device(f.device):
-            _native.check(L.rubs_b200_filter3(
-                ctypes.c_void_p(f.data_ptr()), _native.RUBS_F32 if f.dtype == torch.float32 else _native.RUBS_F64,
-                H, W, W, fptr, int(uniform), W, iterations, ctypes.c_void_p(res.data_ptr()), W,
-                _stream_handle()))
+            if lattice:
+                _native.check(L.rubs_b200_filter3_lattice(
+                    ctypes.c_void_p(f.data_ptr()), fdt, H, W, W, fptr, int(uniform), W, iterations,
+                    float(spacing), ctypes.c_void_p(res.data_ptr()), W, _stream_handle()))
+            else:
+                _native.check(L.rubs_b200_filter3(
+                    ctypes.c_void_p(f.data_ptr()), fdt, H, W, W, fptr, int(uniform), W, iterations,
+                    ctypes.c_void_p(res.data_ptr()), W, _stream_handle()))
         return res
     img = _host_image(f)
     fld, uniform = _host_field3(field, img.shape)
@@ -638,16 +658,24 @@ def filter_space_variant3(f, field, iterations: int = 1, *, out=None):
     out = _host_out(out, (H, W))
     if H == 0 or W == 0:
         return out
-    _native.check(L.rubs_b200_filter3_host(_ptr(img), _img_dtype_code(img.dtype), H, W, _ptr(fld),
-                                           int(uniform), iterations, _ptr(out)))
+    if lattice:
+        _native.check(L.rubs_b200_filter3_lattice_host(_ptr(img), _img_dtype_code(img.dtype), H, W,
+                                                       _ptr(fld), int(uniform), iterations,
+                                                       float(spacing), _ptr(out)))
+    else:
+        _native.check(L.rubs_b200_filter3_host(_ptr(img), _img_dtype_code(img.dtype), H, W, _ptr(fld),
+                                               int(uniform), iterations, _ptr(out)))
     return out
 
 
-def filter_space_variant3_params(f, size, elongation, orientation, iterations: int = 1, *, out=None):
+def filter_space_variant3_params(f, size, elongation, orientation, iterations: int = 1, *, out=None,
+                                 mode: str = "exact", spacing: float = 1.0):
     """filter_space_variant3(f, scales3_from_params(size, elongation,
-    orientation), iterations) with the (closed-form) mapping fused into the
-    filter kernel.  Raises Infeasible beyond the N=3 elongation bound."""
+    orientation), iterations, mode=mode, spacing=spacing) with the
+    (closed-form) mapping fused into the filter kernel.  Raises Infeasible
+    beyond the N=3 elongation bound."""
     iterations = _check_iterations(iterations)
+    lattice = _n3_mode(mode, spacing)
     L = _native.load()
     if _is_torch(f):
         torch = _torch()
@@ -657,10 +685,16 @@ def filter_space_variant3_params(f, size, elongation, orientation, iterations: i
                 H, W = f.shape
                 res = torch.empty((H, W), dtype=torch.float64, device=f.device)
                 if H and W:
-                    _native.check(L.rubs_b200_filter3_params(
-                        f.data_ptr(), fast[0], H, W, W, size.data_ptr(), elongation.data_ptr(),
-                        orientation.data_ptr(), fast[1], W, iterations, res.data_ptr(), W,
-                        torch.cuda.current_stream(f.device).cuda_stream))
+                    stream = torch.cuda.current_stream(f.device).cuda_stream
+                    if lattice:
+                        _native.check(L.rubs_b200_filter3_lattice_params(
+                            f.data_ptr(), fast[0], H, W, W, size.data_ptr(), elongation.data_ptr(),
+                            orientation.data_ptr(), fast[1], W, iterations, float(spacing),
+                            res.data_ptr(), W, stream))
+                    else:
+                        _native.check(L.rubs_b200_filter3_params(
+                            f.data_ptr(), fast[0], H, W, W, size.data_ptr(), elongation.data_ptr(),
+                            orientation.data_ptr(), fast[1], W, iterations, res.data_ptr(), W, stream))
                 return res
         f = _torch_image(f)
         H, W = f.shape
@@ -676,12 +710,18 @@ def filter_space_variant3_params(f, size, elongation, orientation, iterations: i
         res = torch.empty((H, W), dtype=torch.float64, device=f.device)
         if H == 0 or W == 0:
             return res
+        fdt = _native.RUBS_F32 if f.dtype == torch.float32 else _native.RUBS_F64
+        pcode = _native.RUBS_F32 if pdt == torch.float32 else _native.RUBS_F64
+        pp = [ctypes.c_void_p(p.data_ptr()) for p in ps]
         with torch.cuda.device(f.device):
-            _native.check(L.rubs_b200_filter3_params(
-                ctypes.c_void_p(f.data_ptr()), _native.RUBS_F32 if f.dtype == torch.float32 else _native.RUBS_F64,
-                H, W, W, *(ctypes.c_void_p(p.data_ptr()) for p in ps),
-                _native.RUBS_F32 if pdt == torch.float32 else _native.RUBS_F64, W, iterations,
-                ctypes.c_void_p(res.data_ptr()), W, _stream_handle()))
+            if lattice:
+                _native.check(L.rubs_b200_filter3_lattice_params(
+                    ctypes.c_void_p(f.data_ptr()), fdt, H, W, W, *pp, pcode, W, iterations, float(spacing),
+                    ctypes.c_void_p(res.data_ptr()), W, _stream_handle()))
+            else:
+                _native.check(L.rubs_b200_filter3_params(
+                    ctypes.c_void_p(f.data_ptr()), fdt, H, W, W, *pp, pcode, W, iterations,
+                    ctypes.c_void_p(res.data_ptr()), W, _stream_handle()))
         return res
     img = _host_image(f)
     H, W = img.shape
@@ -691,9 +731,15 @@ def filter_space_variant3_params(f, size, elongation, orientation, iterations: i
     out = _host_out(out, (H, W))
     if H == 0 or W == 0:
         return out
-    _native.check(L.rubs_b200_filter3_params_host(
-        _ptr(img), _img_dtype_code(img.dtype), H, W, _ptr(s), _ptr(r), _ptr(t),
-        _native.RUBS_F32 if dt == np.float32 else _native.RUBS_F64, iterations, _ptr(out)))
+    pcode = _native.RUBS_F32 if dt == np.float32 else _native.RUBS_F64
+    if lattice:
+        _native.check(L.rubs_b200_filter3_lattice_params_host(
+            _ptr(img), _img_dtype_code(img.dtype), H, W, _ptr(s), _ptr(r), _ptr(t), pcode, iterations,
+            float(spacing), _ptr(out)))
+    else:
+        _native.check(L.rubs_b200_filter3_params_host(
+            _ptr(img), _img_dtype_code(img.dtype), H, W, _ptr(s), _ptr(r), _ptr(t), pcode, iterations,
+            _ptr(out)))
     return out
 
 
