@@ -2,7 +2,7 @@
 """Benchmark of the B200 space-variant filter path (driver contract).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config 5|2|1|3|3n4|4|A]
+                    [--config 5|2|1|3|3l|3n4|4|A]
 
 Default workload: BASELINE.json config 5 -- ONE 32768^2 float32 image,
 N=4 ZP box spline, sigma up to 256 (the largest configuration that runs on
@@ -63,12 +63,12 @@ if ROOT not in sys.path:
 
 METRIC = "Gpixel/s filtered"
 UNIT = "Gpixel/s"
-CONFIGS = ["5", "2", "1", "3", "3n4", "4", "A"]
+CONFIGS = ["5", "2", "1", "3", "3l", "3n4", "4", "A"]
 BATCH4 = 64  # config 4: images per step (all ranks together)
 # Algorithmic bytes per output pixel: image + per-pixel
 # parameters + f64 output, per pass (config 4: both passes, intermediate
 # ignored; config 1: the drop-in (H,W,4) f64 field).
-BYTES_PER_PX = {"2": 28, "1": 48, "3": 24, "3n4": 24, "4": 52, "5": 24, "A": 16}
+BYTES_PER_PX = {"2": 28, "1": 48, "3": 24, "3l": 24, "3n4": 24, "4": 52, "5": 24, "A": 16}
 
 
 def parse(argv=None):
@@ -180,6 +180,10 @@ WORKLOADS = {
     "3": "config3: 8192^2 fp32 rectangles + N(0,0.05^2) noise; N=3 directions (0/60/120 deg); "
          "sigma [1,32], rho [1,6] clamped to 0.95 of the N=3 bound, smooth theta; exact N=3 path "
          "(closed-form mapping fused, f32 params)",
+    "3l": "config3: 8192^2 fp32 rectangles + N(0,0.05^2) noise; N=3 directions (0/60/120 deg); "
+          "sigma [1,32], rho [1,6] clamped to 0.95 of the N=3 bound, smooth theta; O(1) LATTICE mode: "
+          "image resampled once onto the triangular lattice (spacing 1), exact integer running sums, "
+          "8-vertex finite difference (closed-form mapping fused, f32 params)",
     "3n4": "config3 shapes with the N=4 ZP element: 8192^2 fp32 rectangles + N(0,0.05^2) noise; "
            "sigma [1,32], rho [1,6] clamped, smooth theta (LUT mapping)",
     "2": "config2: 2048^2 fp64 uniform[0,1) seed 0; N=4 ZP box spline; sigma [2,16], rho [1,4], "
@@ -192,7 +196,7 @@ WORKLOADS = {
          "noise_sigma 0.1, window 1.5; structure tensor (3 window filters), percentiles, anisotropy, "
          "LUT filter of image and flat image, gain correction",
 }
-SHAPES = {"5": (32768, 32768), "3": (8192, 8192), "3n4": (8192, 8192), "2": (2048, 2048),
+SHAPES = {"5": (32768, 32768), "3": (8192, 8192), "3l": (8192, 8192), "3n4": (8192, 8192), "2": (2048, 2048),
           "1": (256, 256), "4": (4096, 4096), "A": (2048, 2048)}
 ITERS = {"4": 2}
 
@@ -213,7 +217,7 @@ def bench_config(cfg: str, world: int) -> dict:
                              f"the band interior")
     else:
         d.update(parallelism="one image per rank per step" + (" (replicas)" if world > 1 else ""))
-    if cfg in ("5", "3", "3n4", "4"):
+    if cfg in ("5", "3", "3l", "3n4", "4"):
         d["l2"] = "inputs + output per step exceed the 126 MB L2 (no flush needed)"
     elif cfg != "1":
         d["l2"] = "4 rotating input/output sets per rank (working set > 126 MB L2)"
@@ -221,6 +225,8 @@ def bench_config(cfg: str, world: int) -> dict:
         d["l2"] = "4 rotating input sets (working set < L2: launch-bound config)"
     d["path"] = {"1": "drop-in (H,W,4) f64 field (rubs_b200_filter)",
                  "3": "fused closed-form N=3 mapping + exact N=3 filter (rubs_b200_filter3_params)",
+                 "3l": "fused closed-form N=3 mapping + O(1) lattice-mode N=3 filter "
+                       "(rubs_b200_filter3_lattice_params)",
                  "A": "rubs_b200_adaptive_smooth"}.get(
         cfg, "fused LUT mapping + filter (rubs_b200_filter_params)")
     return d
@@ -233,7 +239,7 @@ def _load_workload(cfg, torch, device, rank=0, image=None):
         return workloads.config2(device=device, param_dtype=f32)
     if cfg == "1":
         return workloads.config1()
-    if cfg == "3":
+    if cfg in ("3", "3l"):
         return workloads.config3_n3(device=device, param_dtype=f32)
     if cfg == "3n4":
         return workloads.config3(device=device, param_dtype=f32)
@@ -254,7 +260,8 @@ class Work:
         self.rank, self.world = rank, world
         self.H, self.W = SHAPES[cfg]
         self.iters = ITERS.get(cfg, 1)
-        self.n3 = cfg == "3"
+        self.n3 = cfg in ("3", "3l")
+        self.n3_mode = "lattice" if cfg == "3l" else "exact"
         self.row_bands = row_banded(cfg, world)
         self.sets = []
         self.lut = rb.default_lut()
@@ -313,7 +320,7 @@ class Work:
         if "adaptive" in s:
             return rb.adaptive_smooth(s["f"], self.w["noise_sigma"])
         if "p" in s and self.n3:
-            return rb.filter_space_variant3_params(s["f"], *s["p"], iterations=self.iters)
+            return rb.filter_space_variant3_params(s["f"], *s["p"], iterations=self.iters, mode=self.n3_mode)
         if "p" in s:
             return rb.filter_space_variant_params(s["f"], *s["p"], lut=self.lut, iterations=self.iters)
         return rb.filter_space_variant(s["f"], s["field"], self.iters)
@@ -387,7 +394,8 @@ class Work:
             hf = pinned(s["f"]).numpy()
             hp = [pinned(p).numpy() for p in s["p"]]
             if self.n3:
-                call = lambda: rb.filter_space_variant3_params(hf, *hp, iterations=self.iters, out=hout)  # noqa: E731
+                call = lambda: rb.filter_space_variant3_params(hf, *hp, iterations=self.iters, out=hout,  # noqa: E731
+                                                               mode=self.n3_mode)
             else:
                 call = lambda: rb.filter_space_variant_params(hf, *hp, lut=self.lut,  # noqa: E731
                                                               iterations=self.iters, out=hout)
@@ -593,11 +601,14 @@ KERNEL_NOTE = {
     "3n4": "the pass's filter kernels: wide_filter_kernel + the large-halo block passes",
     "4": "the filter kernels of both passes of each image",
     "3": "n3_tile_kernel",
+    "3l": "the lattice pass: lat_splat / lat_colsum / lat_diagsum / lat_gather kernels",
     "A": "the pipeline's filter launches",
 }
 BINDING = {
     "5": "on-chip: the 16-vertex gather (L1) and the block regions' scratch traffic (see traffic)",
     "3": "shared-memory wavefronts (see smem)",
+    "3l": "HBM traffic of the int128 lattice regions (16 B per lattice point, written by the splat, "
+          "swept twice, gathered)",
 }
 # From the committed ncu captures of the primary kernel (wide_filter_kernel)
 # on config 2 (profiles/ncu_r01b_summary.md, final build): fp64 instructions
@@ -621,7 +632,7 @@ TRAFFIC_PER_PASS = {
 # Parity leg (checker only, after the timed region): the GPU output at
 # sampled pixels against the exact dense oracle.
 
-PARITY_PX = {"1": 256, "2": 256, "3": 256, "3n4": 128}
+PARITY_PX = {"1": 256, "2": 256, "3": 256, "3l": 256, "3n4": 128}
 
 
 def parity_sample(cfg, wk, out):
@@ -648,7 +659,8 @@ def parity_sample(cfg, wk, out):
         par = s["field"][idx[:, 0], idx[:, 1]].double().cpu().numpy()
     else:
         par = np.stack([v[idx[:, 0], idx[:, 1]].double().cpu().numpy() for v in s["p"]], axis=1)
-    return {"pts": pts, "got": got, "par": par, "n3": wk.n3, "f": s["f"], "p": s.get("p")}
+    return {"pts": pts, "got": got, "par": par, "n3": wk.n3, "lattice": wk.n3_mode == "lattice", "f": s["f"],
+            "p": s.get("p")}
 
 
 def parity_check(cfg: str, pin) -> dict:
@@ -693,6 +705,8 @@ def parity_check(cfg: str, pin) -> dict:
         return {"max_rel_err": float(np.abs(got - ref).max() / scale), "pixels": int(len(pts)),
                 "oracle": how, "tolerance": 1e-9}
     H, W = f.shape
+    if pin.get("lattice"):
+        return _parity_lattice(f, field, pts, got)
     ref = np.empty(len(pts))
     for i, ((r, c), a) in enumerate(zip(pts, field)):
         a = np.maximum(a, 0.05)
@@ -714,6 +728,40 @@ def parity_check(cfg: str, pin) -> dict:
             "oracle": "exact dense filter per pixel (oracle/dense" + ("3" if pin["n3"] else "") +
                       "_oracle.c) on the crop its kernel reaches",
             "tolerance": 1e-9}
+
+
+def _parity_lattice(f, field, pts, got) -> dict:
+    """Lattice (O(1)) N=3 mode.  ``max_rel_err``: against the mode's own
+    definition taken literally -- the brute-force sum of the exact N=3 kernel
+    over the resampled image (oracle/dense3_oracle.c
+    rubs_oracle3_lattice_points), the 1e-9 bar.  ``mode_error_vs_exact``: the
+    mode's resampling error against the exact N=3 filter of the original
+    image (dense3_oracle.c), reported, not a pass/fail bar."""
+    import math as _m
+    import oracle
+    H, W = f.shape
+    f64 = f.double().cpu().numpy() if hasattr(f, "cpu") else np.asarray(f, np.float64)
+    ref = np.empty(len(pts))
+    exact = np.empty(len(pts))
+    for i, ((r, c), a) in enumerate(zip(pts, field)):
+        a = np.maximum(a, 0.05)
+        rx = int(_m.ceil(0.5 * a[0] + 0.25 * (a[1] + a[2]))) + 1
+        ry = int(_m.ceil(0.25 * _m.sqrt(3.0) * (a[1] + a[2]))) + 1
+        # the lattice is anchored at the image origin: the brute force takes
+        # the whole image (it only visits the pixel's support)
+        ref[i] = oracle.lattice3_points(f64, a, np.array([[r, c]]), 1.0, threads=1)[0]
+        r0, r1, c0, c1 = max(0, r - ry), min(H, r + ry + 1), max(0, c - rx), min(W, c + rx + 1)
+        exact[i] = oracle.points3(f64[r0:r1, c0:c1], a, np.array([[r - r0, c - c0]]), threads=1)[0]
+    scale = max(float(np.abs(ref).max()), 1e-300)
+    return {"max_rel_err": float(np.abs(got - ref).max() / scale), "pixels": int(len(pts)),
+            "oracle": "lattice mode by brute force: exact N=3 kernel summed over the resampled image "
+                      "(oracle/dense3_oracle.c rubs_oracle3_lattice_points)",
+            "tolerance": 1e-9,
+            "mode_error_vs_exact": {
+                "max_rel": float(np.abs(got - exact).max() / max(float(np.abs(exact).max()), 1e-300)),
+                "rms_rel": float(np.sqrt(np.mean((got - exact) ** 2)) / max(float(np.abs(exact).max()), 1e-300)),
+                "note": "the mode's resampling error against the exact N=3 filter of the original image "
+                        "(oracle/dense3_oracle.c), relative to max |output|; reported, not a bar"}}
 
 
 # ---------------------------------------------------------------------------
@@ -743,6 +791,19 @@ def _band3_worker(band):
     lo, hi = band
     port3.filter3_band(_PORT["f"], _PORT["field"], lo, hi)
     return (hi - lo) * _PORT["f"].shape[1]
+
+
+def _band3l_worker(band):
+    """One N=3 lattice-mode row band (oracle/lattice3_port.py lattice_pass on
+    the band's crop with its support rows); returns pixels produced."""
+    from oracle import lattice3_port as lp
+    f, field = _PORT["f"], _PORT["field"]
+    lo, hi = band
+    a = np.maximum(field[lo:hi], lp.SCALE_FLOOR)
+    ry = int(lp.support3(a)[1].max()) + 4
+    r0, r1 = max(0, lo - ry), min(f.shape[0], hi + ry)
+    lp.lattice_pass(f[r0:r1], r0, 0, a, lo, 0, 1.0)
+    return (hi - lo) * f.shape[1]
 
 
 def _band_worker(band):
@@ -795,17 +856,18 @@ class CpuPort:
                 field = w["field"]
             elif cfg == "2":
                 w = workloads.config2()
-            elif cfg == "3":
+            elif cfg in ("3", "3l"):
                 from oracle import port3
                 w = workloads.config3_n3(2048, 2048)
-                self.note = " (2048^2 instance of the config-3 N=3 recipe; oracle/port3.py)"
+                self.note = (" (2048^2 instance of the config-3 N=3 recipe; oracle/port3.py)" if cfg == "3" else
+                             " (2048^2 instance of the config-3 N=3 recipe; oracle/lattice3_port.py)")
             elif cfg == "3n4":
                 w = workloads.config3(2048, 2048)
                 self.note = " (2048^2 instance of the config-3 recipe)"
             else:
                 w = workloads.config4_image(0)
                 self.note = " (image 0 of the batch; two passes: each band's pass 1 covers its halo rows)"
-            if cfg == "3":
+            if cfg in ("3", "3l"):
                 field = port3.scales3_from_params(w["size"].numpy(), w["elong"].numpy(), w["orient"].numpy())
             elif cfg != "1":
                 field = port.lookup_many(lut.rho_grid, lut.phi_grid, lut.entries, w["size"].numpy(),
@@ -819,7 +881,7 @@ class CpuPort:
             self.bands = [(lo, min(self.H, lo + rows)) for lo in range(0, self.H, rows)][: self.cores]
             self.rows = rows
             self.jobs = self.bands
-            self.kind = "band3" if cfg == "3" else "band"
+            self.kind = {"3": "band3", "3l": "band3l"}.get(cfg, "band")
         self.cores = len(self.jobs)
         self.pool = mp.get_context("fork").Pool(self.cores)
 
@@ -856,7 +918,7 @@ class CpuPort:
 
     def step(self):
         worker = {"adaptive": _adaptive_worker, "window": _window_worker, "band3": _band3_worker,
-                  "band": _band_worker}[self.kind]
+                  "band3l": _band3l_worker, "band": _band_worker}[self.kind]
         t0 = time.perf_counter()
         px = sum(self.pool.map(worker, self.jobs))
         return px, time.perf_counter() - t0
@@ -875,7 +937,9 @@ class CpuPort:
                 f"({sum(h - l for l, h in self.bands)} of {self.H} rows) of {WORKLOADS[self.cfg].split(':')[0]}"
                 f"{self.note}, halo rows pre-integrated only; "
                 + ("numpy restatement of the exact N=3 row-profile algorithm (oracle/port3.py)"
-                   if self.cfg == "3" else "numpy port of the reference fast path (oracle/port.py)")
+                   if self.cfg == "3" else
+                   "numpy restatement of the N=3 lattice mode (oracle/lattice3_port.py)" if self.cfg == "3l"
+                   else "numpy port of the reference fast path (oracle/port.py)")
                 + f", {self.cores} processes x 1 thread")
 
     def close(self):

@@ -148,6 +148,37 @@ __global__ void __launch_bounds__(256) lat_margins_kernel(Field3 F, LatStatus *s
   }
 }
 
+// Parameter modes: support radii from a BOUND instead of mapping every pixel
+// (the mapping kernel above cost 1.0 ms of config 3's 7.8 ms step; this one
+// reads the size plane only).  With C = sum_k a_k^2 / 12 u_k u_k^T and trace
+// s: a1^2 = 12 (C11 - C22/3) <= 12 s and a2^2 + a3^2 = 16 C22 <= 16 s, so
+// a1 <= sqrt(12 s), a2 + a3 <= sqrt(32 s), for every elongation and
+// orientation the mapping accepts (infeasible p_k are clamped to 0, invalid
+// parameters replaced: params_to_scales3); each scale is then floored.  A
+// wider region changes no sum (exact integers), only the area swept; the
+// gather validates every pixel's parameters itself.
+template <int DT>
+__global__ void __launch_bounds__(256) lat_sizebound_kernel(Field3 F, LatStatus *st) {
+  double smax = 0.0;
+  for (int r = blockIdx.x; r < F.FH; r += gridDim.x) {
+    const int64_t row = (int64_t)(r - F.fr_off) * F.pld;
+    for (int c = threadIdx.x; c < F.FW; c += 256) {
+      const double s = load_scalar(F.ps, DT, row + c);
+      if (s > 0.0 && s < INFINITY) smax = fmax(smax, s);  // others: flagged by the gather, mapped as s = 1
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) smax = fmax(smax, __shfl_xor_sync(0xffffffffu, smax, o));
+  if ((threadIdx.x & 31) == 0) {
+    smax = fmax(smax, 1.0) * (1.0 + 1e-9);
+    const double inv = F.scaled ? 1.0 / F.div : 1.0;
+    const double a1 = (sqrt(12.0 * smax) + kScaleFloor) * inv;
+    const double a23 = (sqrt(32.0 * smax) + 2.0 * kScaleFloor) * inv;
+    atomicMax(&st->rx, (int)ceil(0.5 * a1 + 0.25 * a23) + 1);
+    atomicMax(&st->ry, (int)ceil(kQuarterSqrt3 * a23) + 1);
+  }
+}
+
 // max |f| of every canvas row (non-finite entries flagged)
 template <int DT>
 __global__ void __launch_bounds__(256) lat_rowmax_kernel(ImageSpec I, double *rowmax,
@@ -188,7 +219,13 @@ __global__ void __launch_bounds__(32) lat_scale_kernel(const double *rowmax, Ima
   for (int r = r0 + (int)threadIdx.x; r <= r1; r += 32) m = fmax(m, rowmax[r]);
 #pragma unroll
   for (int o = 16; o; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-  if (threadIdx.x == 0) S[b] = m > 0.0 ? min(max(kQBits - ilogb(m), -960), 960) : 0;
+  if (threadIdx.x == 0) {
+    // per block: {quantisation exponent, glo, alo} (the gather reads the
+    // region origin from here instead of redoing the divisions per pixel)
+    S[3 * b] = m > 0.0 ? min(max(kQBits - ilogb(m), -960), 960) : 0;
+    S[3 * b + 1] = glo;
+    S[3 * b + 2] = blk_alo(g, glo);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -208,7 +245,7 @@ __global__ void __launch_bounds__(256) lat_splat_kernel(ImageSpec I, LatGeom g, 
   const int ir0 = pr0 - I.row0;
   const bool v0 = ir0 >= 0 && ir0 < I.h, v1 = ir0 + 1 >= 0 && ir0 + 1 < I.h;
   const double dg0 = ((double)pr0 - py) * g.inv_gh, dg1 = dg0 + g.inv_gh;  // in (-1, 1]
-  const double scale = ldexp(1.0, S[b]);
+  const double scale = ldexp(1.0, S[3 * b]);
   i128 *row = G + ((int64_t)bl * g.NG + r) * g.NA;
   i128 carry = 0;
   for (int c0 = 0; c0 < g.NA; c0 += 1024) {
@@ -333,7 +370,7 @@ __global__ void __launch_bounds__(256) lat_gather_kernel(Field3 F, DomainSpec D,
     double a[3];
     scales3_at<MODE>(F, X, Y, a, flags);
     const int b = y / g.bp;
-    const int glo = blk_glo(g, b), alo = blk_alo(g, glo);
+    const int glo = __ldg(S + 3 * b + 1), alo = __ldg(S + 3 * b + 2);
     const i128 *Gb = G + (int64_t)(b - b0) * g.NG * g.NA;
     // base: the pixel shifted by -h u2, in lattice coordinates (region-local)
     const double gy = (double)Y * g.inv_gh;
@@ -344,36 +381,54 @@ __global__ void __launch_bounds__(256) lat_gather_kernel(Field3 F, DomainSpec D,
     const i128 *B = Gb + (int64_t)gi * g.NA + ai;
     const i128 B00 = ldg128(B);
     const i128 c1 = ldg128(B + 1) - B00, c2 = ldg128(B + g.NA) - B00;
-    // vertex offsets sum_k s_k a_k u_k / 2 in lattice units
-    const double h1 = 0.5 * a[0], h2 = 0.5 * a[1], h3 = 0.5 * a[2];
+    // Vertex offsets sum_k s_k a_k u_k / 2 in lattice units (al, ga):
+    // (s1 k1 + s2 k2, s2 k2 + s3 k3) with k = a / (2 h)  [u1 = (1, 0),
+    // u2 = (1, 1), u3 = (0, 1) in lattice coordinates].
+    const double k1 = 0.5 * a[0] * g.inv_h, k2 = 0.5 * a[1] * g.inv_h, k3 = 0.5 * a[2] * g.inv_h;
+    // Each vertex interpolates G linearly on its lattice triangle:
+    //   lin = G00 + w1 (Gx - G00) + w2 (G11 - Gx).
+    // G is re-based by the affine function B00 + c1 (al - ai) + c2 (ga - gi)
+    // through the pixel's base point (the finite difference annihilates it),
+    // in exact integers: the two first differences minus c1 / c2 per vertex,
+    // and the G00 terms summed over the eight vertices BEFORE any rounding
+    // (sum_v s_v (G00_v - B00 - c1 da_v - c2 dg_v): sum_v s_v = 0, one
+    // multiplication per direction for the pixel).
+    i128 sum0 = 0;
+    int sda = 0, sdg = 0;
     double acc = 0.0;
 #pragma unroll
     for (int v = 0; v < 8; ++v) {
-      const double s1 = (v & 1) ? -1.0 : 1.0, s2 = (v & 2) ? -1.0 : 1.0,
-                   s3 = (v & 4) ? -1.0 : 1.0;
-      const double ox = s1 * h1 + 0.5 * (s2 * h2 - s3 * h3);
-      const double oy = kSin60 * (s2 * h2 + s3 * h3);
-      const double og = oy * g.inv_gh;
-      const double oa = ox * g.inv_h + 0.5 * og;
+      const bool n1 = v & 1, n2 = v & 2, n3 = v & 4;
+      const bool neg = n1 ^ n2 ^ n3;
+      const double oa = (n1 ? -k1 : k1) + (n2 ? -k2 : k2);
+      const double og = (n2 ? -k2 : k2) + (n3 ? -k3 : k3);
       const double tg = gf + og, ta = af + oa;
       const double fgf = floor(tg), faf = floor(ta);
       const double wg = tg - fgf, wa = ta - faf;
       const int dg = (int)fgf, da = (int)faf;
       const i128 *T = B + (int64_t)dg * g.NA + da;
-      const bool low = wa >= wg;
-      // taps re-based by the affine function B00 + c1 (al - ai) + c2 (ga - gi)
-      const i128 base = B00 + c1 * (i128)da + c2 * (i128)dg;
-      const i128 t00 = ldg128(T) - base;
-      const i128 t11 = ldg128(T + g.NA + 1) - base - c1 - c2;
-      const i128 tx = low ? ldg128(T + 1) - base - c1 : ldg128(T + g.NA) - base - c2;
-      const double r00 = i128_to_double(t00), r11 = i128_to_double(t11),
-                   rx = i128_to_double(tx);
-      const double lin = low ? r00 + wa * (rx - r00) + wg * (r11 - rx)
-                             : r00 + wg * (rx - r00) + wa * (r11 - rx);
-      acc += (s1 * s2 * s3) * lin;
+      const bool low = wa >= wg;  // lower triangle: via (al + 1, ga); upper: via (al, ga + 1)
+      const i128 t00 = ldg128(T), t11 = ldg128(T + g.NA + 1);
+      const i128 tx = ldg128(low ? T + 1 : T + g.NA);
+      const i128 e1 = (tx - t00) - (low ? c1 : c2);
+      const i128 e2 = (t11 - tx) - (low ? c2 : c1);
+      const double w1 = low ? wa : wg, w2 = low ? wg : wa;
+      const double part = fma(w1, i128_to_double(e1), w2 * i128_to_double(e2));
+      if (neg) {
+        acc -= part;
+        sum0 -= t00;
+        sda -= da;
+        sdg -= dg;
+      } else {
+        acc += part;
+        sum0 += t00;
+        sda += da;
+        sdg += dg;
+      }
     }
+    acc += i128_to_double(sum0 - c1 * (i128)sda - c2 * (i128)sdg);
     D.out[(int64_t)y * D.ld_out + x] =
-        ldexp(acc * (g.h / (kSin60 * a[0] * a[1] * a[2])), -S[b]);
+        ldexp(acc * (g.h / (kSin60 * a[0] * a[1] * a[2])), -__ldg(S + 3 * b));
   }
   flags = __reduce_or_sync(0xffffffffu, flags);
   if ((threadIdx.x & 31) == 0 && flags) atomicOr(&st->flags, flags);
@@ -513,7 +568,7 @@ int lat_pass(const ImageSpec &I, const Field3 &F, const DomainSpec &D, int rx, i
   int rc;
   if ((rc = lat_grow(tl.G, tl.gcap, per_block * nbw))) return rc;
   if ((rc = lat_grow(tl.rowmax, tl.rcap, (size_t)std::max(I.h, 1)))) return rc;
-  if ((rc = lat_grow(tl.S, tl.scap, (size_t)g.nb))) return rc;
+  if ((rc = lat_grow(tl.S, tl.scap, (size_t)3 * g.nb))) return rc;
   void *tok = rubs_internal::timed_begin(0, s);
   const int rm_blocks = std::max(1, std::min(I.h, 148 * 8));
   if (I.dt)
@@ -567,8 +622,8 @@ int run_lattice(const ImageSpec &img, Field3 F, int iterations, double h, double
     switch (F.mode) {
       case kM3Field: lat_margins_kernel<kM3Field><<<blocks, 256, 0, s>>>(F, tl.d_st); break;
       case kM3Uniform: lat_margins_kernel<kM3Uniform><<<blocks, 256, 0, s>>>(F, tl.d_st); break;
-      case kM3Params: lat_margins_kernel<kM3Params><<<blocks, 256, 0, s>>>(F, tl.d_st); break;
-      default: lat_margins_kernel<kM3Params32><<<blocks, 256, 0, s>>>(F, tl.d_st);
+      case kM3Params: lat_sizebound_kernel<1><<<blocks, 256, 0, s>>>(F, tl.d_st); break;
+      default: lat_sizebound_kernel<0><<<blocks, 256, 0, s>>>(F, tl.d_st);
     }
     rubs_internal::count_launches(1);
     LAT_CUDA_TRY(cudaGetLastError());
