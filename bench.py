@@ -621,6 +621,10 @@ SMEM_WF_PER_PX = {"2": 16.39, "3": 53.9}
 TRAFFIC_PER_PASS = {
     "2": (105.45e6, "ncu, wide_filter_kernel, profiles/ncu_r01b_summary.md"),
     "3": (1.588e9, "ncu, n3_tile_kernel, profiles/ncu_r01b_summary.md"),
+    "3l": (11.57e9, "ncu launch list of one pass, sum over the lat_* kernels "
+                    "(profiles/ncu_r02_c3l_launches.csv; algorithmic 1.61 GB: the rest is the int128 lattice "
+                    "region, 16 B per lattice point, written by the splat, read and written by the two line "
+                    "sums, read by the gather)"),
     "5": (180.4e9, "ncu launch list of one step, sum over the pass's kernels "
                    "(profiles/ncu_r02_c5_launches.csv, split in profiles/ncu_r02_summary.md; algorithmic "
                    "25.8 GB: the rest is the large-halo regions' scratch, 4.5 elements per pixel written "

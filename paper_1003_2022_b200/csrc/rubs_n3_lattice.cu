@@ -304,6 +304,14 @@ __global__ void __launch_bounds__(256) lat_splat_kernel(ImageSpec I, LatGeom g, 
   }
 }
 
+// Loads in flight per thread in the two line sums below: the grids are small
+// (one thread per column / diagonal of a few blocks, ~8 warps per SM on
+// config 3), so the memory-level parallelism has to come from each thread.
+#ifndef RUBS_LAT_UNROLL
+#define RUBS_LAT_UNROLL 32
+#endif
+constexpr int kLineUnroll = RUBS_LAT_UNROLL;
+
 // K2: running sum along ga (thread per column).
 __global__ void __launch_bounds__(128) lat_colsum_kernel(LatGeom g, i128 *G) {
   const int i = blockIdx.x * 128 + threadIdx.x;
@@ -312,12 +320,12 @@ __global__ void __launch_bounds__(128) lat_colsum_kernel(LatGeom g, i128 *G) {
   const int64_t ld = g.NA;
   i128 acc = 0;
   int r = 0;
-  for (; r + 8 <= g.NG; r += 8) {
-    i128 v[8];
+  for (; r + kLineUnroll <= g.NG; r += kLineUnroll) {
+    i128 v[kLineUnroll];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = ld128(p + (r + j) * ld);
+    for (int j = 0; j < kLineUnroll; ++j) v[j] = ld128(p + (r + j) * ld);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < kLineUnroll; ++j) {
       acc += v[j];
       st128(p + (r + j) * ld, acc);
     }
@@ -339,12 +347,12 @@ __global__ void __launch_bounds__(128) lat_diagsum_kernel(LatGeom g, i128 *G) {
   const int n = r1 - r0 + 1;
   i128 acc = 0;
   int r = 0;
-  for (; r + 8 <= n; r += 8) {
-    i128 v[8];
+  for (; r + kLineUnroll <= n; r += kLineUnroll) {
+    i128 v[kLineUnroll];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = ld128(p + (r + j) * st);
+    for (int j = 0; j < kLineUnroll; ++j) v[j] = ld128(p + (r + j) * st);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < kLineUnroll; ++j) {
       acc += v[j];
       st128(p + (r + j) * st, acc);
     }
