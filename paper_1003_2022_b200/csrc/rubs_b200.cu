@@ -1623,11 +1623,20 @@ __global__ void __launch_bounds__(256) big_line_seg_kernel(const BigRegion *R, d
   if (PHASE == 1) {
     const int L = blockIdx.x * 256 + threadIdx.x;
     if (blockIdx.y != 0 || L >= nlines) return;
+    // eight segment sums loaded before the carries are stored back (a load
+    // cannot move above a store through the same pointer: one at a time was
+    // a chain of nseg L2 round trips, ~30 us per direction at 50 segments)
     double c = 0.0;
-    for (int k = 0; k < nseg; ++k) {
-      const double t = T[(int64_t)k * nlines + L];
-      T[(int64_t)k * nlines + L] = c;
-      c += t;
+    double *Tl = T + L;
+    for (int k = 0; k < nseg; k += 8) {
+      double t[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) t[u] = k + u < nseg ? Tl[(int64_t)(k + u) * nlines] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (k + u < nseg) Tl[(int64_t)(k + u) * nlines] = c;
+        c += t[u];
+      }
     }
     return;
   }
@@ -2631,13 +2640,27 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
   t_launches += 3;
   RUBS_CUDA_TRY(cudaGetLastError());
   if ((rc = small_copy(t_plan.h_counters, t_plan.counters, 2 * sizeof(int), s))) return rc;
-  RUBS_CUDA_TRY(cudaStreamSynchronize(s));
   size_t stage_off = 0;  // pinned staging of this planning round (small_copy)
+  // The first kPlanSpec used cells travel with the counters (speculatively:
+  // their number is not known yet); a call with few blocks -- one image at a
+  // large uniform scale: four -- then needs no second round trip.
+  constexpr int kPlanSpec = 128;
+  const int n_spec = std::min(ncell, kPlanSpec);
+  char *hu0 = nullptr, *ha0 = nullptr;
+  if ((rc = host_stage(n_spec * sizeof(int), stage_off, &hu0, s))) return rc;
+  if ((rc = host_stage(n_spec * sizeof(CellAgg), stage_off, &ha0, s))) return rc;
+  if ((rc = small_copy(hu0, t_plan.used, n_spec * sizeof(int), s))) return rc;
+  if ((rc = small_copy(ha0, t_plan.agg, n_spec * sizeof(CellAgg), s))) return rc;
+  RUBS_CUDA_TRY(cudaStreamSynchronize(s));
   const int n_smem = t_plan.h_counters[0], n_used = t_plan.h_counters[1];
   std::vector<int> used(n_used);
   std::vector<CellAgg> agg(n_used);
-  if (n_used > 0) {
+  if (n_used > 0 && n_used <= n_spec) {
+    std::memcpy(used.data(), hu0, n_used * sizeof(int));
+    std::memcpy(agg.data(), ha0, n_used * sizeof(CellAgg));
+  } else if (n_used > 0) {
     char *hu = nullptr, *ha = nullptr;
+    stage_off = 0;
     if ((rc = host_stage(n_used * sizeof(int), stage_off, &hu, s))) return rc;
     if ((rc = host_stage(n_used * sizeof(CellAgg), stage_off, &ha, s))) return rc;
     if ((rc = small_copy(hu, t_plan.used, n_used * sizeof(int), s))) return rc;
@@ -2875,17 +2898,34 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
 }
 
 // The deferred tiles, then the pixels they deferred in turn (per-pixel pass).
+// `merged` (the one-pass path, whose status reads clear the device words):
+// the read of the deferred-pixel count is a clearing read of the whole
+// status, so a call that defers no pixels -- the usual case -- has its final
+// status here and the caller needs no further round trip; every later read
+// is merged in.
 template <int M, int T>
 int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int n_ovf,
-                    cudaStream_t s) {
+                    cudaStream_t s, Status *merged) {
   int rc = handle_overflow_tiles<M, T>(I, F, D, n_ovf, s);
   if (rc) return rc;
   HostClock hc;
   int cnt = 0;
-  if ((rc = small_copy(&t_scr.h_status->pix_count, &t_scr.d_status->pix_count, sizeof(int), s)))
-    return rc;
-  RUBS_CUDA_TRY(cudaStreamSynchronize(s));
-  cnt = t_scr.h_status->pix_count;
+  auto merge = [&](const Status &s2) {
+    merged->flags |= s2.flags;
+    merged->guard_hi = std::max(merged->guard_hi, s2.guard_hi);
+    merged->guard_bits = std::max(merged->guard_bits, s2.guard_bits);
+  };
+  if (merged) {
+    Status s2;
+    if ((rc = fetch_status_clear(s, s2))) return rc;
+    merge(s2);
+    cnt = s2.pix_count;
+  } else {
+    if ((rc = small_copy(&t_scr.h_status->pix_count, &t_scr.d_status->pix_count, sizeof(int), s)))
+      return rc;
+    RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+    cnt = t_scr.h_status->pix_count;
+  }
   hc.lap("overflow kernels (sync)");
   if ((size_t)cnt > t_scr.pix_cap) {
     // more precision-deferred pixels than the list holds (rare: fields with
@@ -2898,10 +2938,17 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
     RUBS_CUDA_TRY(cudaMalloc(&t_scr.d_pix, (size_t)cnt * sizeof(int2)));
     t_scr.pix_cap = (size_t)cnt;
     if ((rc = handle_overflow_tiles<M, T>(I, F, D, n_ovf, s))) return rc;
-    if ((rc = small_copy(&t_scr.h_status->pix_count, &t_scr.d_status->pix_count, sizeof(int), s)))
-      return rc;
-    RUBS_CUDA_TRY(cudaStreamSynchronize(s));
-    cnt = t_scr.h_status->pix_count;
+    if (merged) {
+      Status s2;
+      if ((rc = fetch_status_clear(s, s2))) return rc;
+      merge(s2);
+      cnt = s2.pix_count;
+    } else {
+      if ((rc = small_copy(&t_scr.h_status->pix_count, &t_scr.d_status->pix_count, sizeof(int), s)))
+        return rc;
+      RUBS_CUDA_TRY(cudaStreamSynchronize(s));
+      cnt = t_scr.h_status->pix_count;
+    }
   }
   cnt = std::min<int64_t>(cnt, (int64_t)t_scr.pix_cap);
   if (cnt > 0) {
@@ -2909,27 +2956,32 @@ int handle_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D,
         I, F, D, t_scr.d_pix, cnt, t_scr.d_status);
     ++t_launches;
     RUBS_CUDA_TRY(cudaGetLastError());
+    if (merged) {
+      Status s2;
+      if ((rc = fetch_status_clear(s, s2))) return rc;
+      merge(s2);
+    }
   }
   return RUBS_OK;
 }
 
 template <int M, int T>
 int overflow_dispatch(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int n,
-                      cudaStream_t s) {
-  return handle_overflow<M, T>(I, F, D, n, s);
+                      cudaStream_t s, Status *merged) {
+  return handle_overflow<M, T>(I, F, D, n, s, merged);
 }
 
 int run_overflow(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, int n,
-                 cudaStream_t s) {
+                 cudaStream_t s, Status *merged = nullptr) {
   const int m = F.mode, t = I.dt;
-  if (m == kModeField) return t ? overflow_dispatch<kModeField, 1>(I, F, D, n, s)
-                                : overflow_dispatch<kModeField, 0>(I, F, D, n, s);
-  if (m == kModeUniform) return t ? overflow_dispatch<kModeUniform, 1>(I, F, D, n, s)
-                                  : overflow_dispatch<kModeUniform, 0>(I, F, D, n, s);
-  if (m == kModeLut) return t ? overflow_dispatch<kModeLut, 1>(I, F, D, n, s)
-                              : overflow_dispatch<kModeLut, 0>(I, F, D, n, s);
-  return t ? overflow_dispatch<kModeLut32, 1>(I, F, D, n, s)
-           : overflow_dispatch<kModeLut32, 0>(I, F, D, n, s);
+  if (m == kModeField) return t ? overflow_dispatch<kModeField, 1>(I, F, D, n, s, merged)
+                                : overflow_dispatch<kModeField, 0>(I, F, D, n, s, merged);
+  if (m == kModeUniform) return t ? overflow_dispatch<kModeUniform, 1>(I, F, D, n, s, merged)
+                                  : overflow_dispatch<kModeUniform, 0>(I, F, D, n, s, merged);
+  if (m == kModeLut) return t ? overflow_dispatch<kModeLut, 1>(I, F, D, n, s, merged)
+                              : overflow_dispatch<kModeLut, 0>(I, F, D, n, s, merged);
+  return t ? overflow_dispatch<kModeLut32, 1>(I, F, D, n, s, merged)
+           : overflow_dispatch<kModeLut32, 0>(I, F, D, n, s, merged);
 }
 
 // Overflow-record capacity for a pass over D: at most one record per tile
@@ -2984,15 +3036,11 @@ int finish_pass(const ImageSpec &I, const FieldSpec &F, const DomainSpec &D, cud
     {
       // the deferred-tile passes are part of the pass's filter work (kind 0)
       TimedLaunch tl(0, s);
-      if ((rc = run_overflow(I, F, D, st.ovf_count, s))) return rc;
+      if ((rc = run_overflow(I, F, D, st.ovf_count, s, clear ? &st : nullptr))) return rc;
     }
     if (clear) {
-      // the status was cleared: merge the deferred passes' words into st
-      Status s2;
-      if ((rc = fetch_status_clear(s, s2))) return rc;
-      st.flags |= s2.flags;
-      st.guard_hi = std::max(st.guard_hi, s2.guard_hi);
-      st.guard_bits = std::max(st.guard_bits, s2.guard_bits);
+      // the status was cleared by the first read; the deferred passes' words
+      // were merged into st by their own (clearing) reads
       st.ovf_count = 0;
     } else {
       RUBS_CUDA_TRY(cudaMemsetAsync(&t_scr.d_status->ovf_count, 0, sizeof(int), s));
