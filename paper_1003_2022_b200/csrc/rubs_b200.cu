@@ -2728,7 +2728,13 @@ int handle_overflow_tiles(const ImageSpec &I, const FieldSpec &F, const DomainSp
     int maxRH, maxL, maxRW;
     int rows, Pg;
   };
-  auto pitch_of = [](int rw) { return (rw + 3) & ~3; };
+  static const int pitch_align = [] {
+    const char *e = std::getenv("RUBS_B200_BIG_PITCH");
+    const int k = e ? std::atoi(e) : 0;
+    return k >= 1 && k <= 64 ? k : 16;
+  }();
+  const int pitch_mask = pitch_align - 1;
+  auto pitch_of = [pitch_mask](int rw) { return (rw + pitch_mask) & ~pitch_mask; };
   std::vector<BigRegion> regs;
   std::vector<CellMap> cm;
   std::vector<int> cm_cell;
