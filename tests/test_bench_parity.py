@@ -51,3 +51,29 @@ def test_parity_check_three_directions(rng):
     par = np.stack([size, rho, th], axis=1)
     res = bench.parity_check("3", {"pts": pts, "got": exact, "par": par, "n3": True, "f": f})
     assert res["max_rel_err"] < 1e-13
+
+
+def test_parity_check_lattice_mode(rng):
+    """Config 3l: the parity figure is against the lattice mode's brute-force
+    definition (here fed with the numpy restatement's output), the mode's own
+    resampling error against the exact filter is reported beside it."""
+    from oracle import lattice3_port as lp
+    H, W = 44, 40
+    f = rng.random((H, W)).astype(np.float32)
+    pts = _pts(rng, H, W, 24)
+    size = rng.uniform(4.0, 80.0, (H, W))
+    th = rng.uniform(0.0, math.pi, (H, W))
+    rho = np.minimum(rng.uniform(1.0, 4.0, (H, W)), 2.9)
+    field = port3.scales3_from_params(size, rho, th)
+    got = lp.lattice3(f.astype(np.float64), field)[pts[:, 0], pts[:, 1]]
+    par = np.stack([v[pts[:, 0], pts[:, 1]] for v in (size, rho, th)], axis=1)
+    res = bench.parity_check("3l", {"pts": pts, "got": got, "par": par, "n3": True, "lattice": True, "f": f})
+    assert res["max_rel_err"] < 1e-11
+    mode = res["mode_error_vs_exact"]
+    assert 0.0 < mode["rms_rel"] <= mode["max_rel"] < 0.2
+
+
+def test_lattice_config_is_listed_with_the_same_config_object_in_both_arms():
+    assert "3l" in bench.CONFIGS and bench.SHAPES["3l"] == bench.SHAPES["3"]
+    assert bench.bench_config("3l", 1)["path"].startswith("fused closed-form N=3 mapping + O(1) lattice")
+    assert not bench.row_banded("3l", 8)  # the lattice mode has no row-band entry: replicas
