@@ -45,8 +45,10 @@
 #include <algorithm>
 #include <climits>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
+#include <vector>
 
 #include "../../include/rubs_b200.h"
 #include "rubs_device.cuh"
@@ -182,9 +184,9 @@ __global__ void __launch_bounds__(256) lat_sizebound_kernel(Field3 F, LatStatus 
 // max |f| of every canvas row (non-finite entries flagged)
 template <int DT>
 __global__ void __launch_bounds__(256) lat_rowmax_kernel(ImageSpec I, double *rowmax,
-                                                         LatStatus *st) {
+                                                         LatStatus *st, int r_lo, int r_hi) {
   __shared__ double wm[8];
-  for (int r = blockIdx.x; r < I.h; r += gridDim.x) {
+  for (int r = r_lo + blockIdx.x; r < r_hi; r += gridDim.x) {
     double m = 0.0;
     bool bad = false;
     for (int c = threadIdx.x; c < I.w; c += blockDim.x) {
@@ -210,8 +212,8 @@ __global__ void __launch_bounds__(256) lat_rowmax_kernel(ImageSpec I, double *ro
 // quantisation exponent S of each block: 2^S max|f over the block's region
 // rows| < 2^(kQBits + 1)
 __global__ void __launch_bounds__(32) lat_scale_kernel(const double *rowmax, ImageSpec I,
-                                                       LatGeom g, int *S) {
-  const int b = blockIdx.x;
+                                                       LatGeom g, int *S, int b_first) {
+  const int b = b_first + blockIdx.x;
   const int glo = blk_glo(g, b);
   const int r0 = max((int)floor(glo * g.gh) - 1 - I.row0, 0);
   const int r1 = min((int)ceil((glo + g.NG - 1) * g.gh) + 1 - I.row0, I.h - 1);
@@ -458,6 +460,7 @@ struct LatScratch {
   size_t pcap[2] = {0, 0};
   void *stage[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   size_t stcap[5] = {0, 0, 0, 0, 0};
+  cudaStream_t up = nullptr, cmp = nullptr, down = nullptr;  // host-buffer pipeline
 };
 thread_local LatScratch tl_dev[rubs_internal::kMaxDevices];
 thread_local int tl_cur = 0;
@@ -514,7 +517,7 @@ int lat_code(const LatStatus &st) {
 
 // Block geometry of one pass: bp minimises region entries per output row,
 // (NG x NA) / bp, over multiples of 32.
-LatGeom lat_geometry(const DomainSpec &D, int rx, int ry, double h) {
+LatGeom lat_geometry(const DomainSpec &D, int rx, int ry, double h, int bp_cap = INT_MAX) {
   LatGeom g{};
   g.h = h;
   g.gh = h * kSin60;
@@ -531,7 +534,7 @@ LatGeom lat_geometry(const DomainSpec &D, int rx, int ry, double h) {
   };
   int best = 32;
   double best_cost = 1e300;
-  const int top = std::max(32, ((D.ph + 31) / 32) * 32);
+  const int top = std::max(32, std::min(((D.ph + 31) / 32) * 32, bp_cap / 32 * 32));
   for (int bp = 32; bp <= top; bp += 32) {
     int NG, NA;
     dims(bp, NG, NA);
@@ -562,6 +565,25 @@ void lat_launch_gather(const Field3 &F, const DomainSpec &D, const LatGeom &g, i
   lat_gather_kernel<M><<<grid, dim3(32, 8), 0, s>>>(F, D, g, b0, ylo, yhi, tl.S, tl.G, tl.d_st);
 }
 
+// Blocks [b0, b0 + n) of a pass, their regions in tl.G: splat + three
+// running sums + gather.
+void lat_block_kernels(const ImageSpec &I, const Field3 &F, const DomainSpec &D, const LatGeom &g,
+                       int b0, int n, cudaStream_t s) {
+  if (I.dt)
+    lat_splat_kernel<1><<<dim3(g.NG, n), 256, 0, s>>>(I, g, b0, tl.S, tl.G);
+  else
+    lat_splat_kernel<0><<<dim3(g.NG, n), 256, 0, s>>>(I, g, b0, tl.S, tl.G);
+  lat_colsum_kernel<<<dim3((g.NA + 127) / 128, n), 128, 0, s>>>(g, tl.G);
+  lat_diagsum_kernel<<<dim3((g.NA + g.NG - 1 + 127) / 128, n), 128, 0, s>>>(g, tl.G);
+  const int ylo = b0 * g.bp, yhi = std::min(D.ph, (b0 + n) * g.bp);
+  switch (F.mode) {
+    case kM3Field: lat_launch_gather<kM3Field>(F, D, g, b0, ylo, yhi, s); break;
+    case kM3Uniform: lat_launch_gather<kM3Uniform>(F, D, g, b0, ylo, yhi, s); break;
+    case kM3Params: lat_launch_gather<kM3Params>(F, D, g, b0, ylo, yhi, s); break;
+    default: lat_launch_gather<kM3Params32>(F, D, g, b0, ylo, yhi, s);
+  }
+}
+
 int lat_pass(const ImageSpec &I, const Field3 &F, const DomainSpec &D, int rx, int ry, double h,
              cudaStream_t s) {
   LatGeom g = lat_geometry(D, rx, ry, h);
@@ -580,26 +602,13 @@ int lat_pass(const ImageSpec &I, const Field3 &F, const DomainSpec &D, int rx, i
   void *tok = rubs_internal::timed_begin(0, s);
   const int rm_blocks = std::max(1, std::min(I.h, 148 * 8));
   if (I.dt)
-    lat_rowmax_kernel<1><<<rm_blocks, 256, 0, s>>>(I, tl.rowmax, tl.d_st);
+    lat_rowmax_kernel<1><<<rm_blocks, 256, 0, s>>>(I, tl.rowmax, tl.d_st, 0, I.h);
   else
-    lat_rowmax_kernel<0><<<rm_blocks, 256, 0, s>>>(I, tl.rowmax, tl.d_st);
-  lat_scale_kernel<<<g.nb, 32, 0, s>>>(tl.rowmax, I, g, tl.S);
+    lat_rowmax_kernel<0><<<rm_blocks, 256, 0, s>>>(I, tl.rowmax, tl.d_st, 0, I.h);
+  lat_scale_kernel<<<g.nb, 32, 0, s>>>(tl.rowmax, I, g, tl.S, 0);
   int launches = 2;
   for (int b0 = 0; b0 < g.nb; b0 += nbw) {
-    const int n = std::min(nbw, g.nb - b0);
-    if (I.dt)
-      lat_splat_kernel<1><<<dim3(g.NG, n), 256, 0, s>>>(I, g, b0, tl.S, tl.G);
-    else
-      lat_splat_kernel<0><<<dim3(g.NG, n), 256, 0, s>>>(I, g, b0, tl.S, tl.G);
-    lat_colsum_kernel<<<dim3((g.NA + 127) / 128, n), 128, 0, s>>>(g, tl.G);
-    lat_diagsum_kernel<<<dim3((g.NA + g.NG - 1 + 127) / 128, n), 128, 0, s>>>(g, tl.G);
-    const int ylo = b0 * g.bp, yhi = std::min(D.ph, (b0 + n) * g.bp);
-    switch (F.mode) {
-      case kM3Field: lat_launch_gather<kM3Field>(F, D, g, b0, ylo, yhi, s); break;
-      case kM3Uniform: lat_launch_gather<kM3Uniform>(F, D, g, b0, ylo, yhi, s); break;
-      case kM3Params: lat_launch_gather<kM3Params>(F, D, g, b0, ylo, yhi, s); break;
-      default: lat_launch_gather<kM3Params32>(F, D, g, b0, ylo, yhi, s);
-    }
+    lat_block_kernels(I, F, D, g, b0, std::min(nbw, g.nb - b0), s);
     launches += 4;
   }
   rubs_internal::timed_end(tok);
@@ -711,6 +720,133 @@ int lat_stage(int k, size_t bytes, void **out) {
   return RUBS_OK;
 }
 
+// Host-buffer call, one pass, parameter modes, on three streams (uploads,
+// kernels, downloads): the size plane goes up first (the support bound needs
+// it: one small round trip while the image follows), then the image in row
+// chunks, then each block's elongation / orientation rows; block b's
+// kernels start when its image rows and parameters have landed, and its
+// output rows travel back while block b + 1 is filtered.  The blocks are
+// capped at 1/8 of the rows (the last block's kernels and download are the
+// part that does not overlap).  Results equal the device-pointer entry's up
+// to the quantisation exponents of the (smaller) blocks.
+constexpr int kLatStreamRows = 2048;  // images with at least this many rows
+constexpr int kLatChunkRows = 512;
+
+int lat_stream_params_host(const void *f, int f_dtype, int64_t H, int64_t W, const void *size,
+                           const void *elong, const void *orient, int p_dtype, double h,
+                           double *out, void *df, void *dout, void *const dp[3]) {
+  int rc;
+  if (!tl.up) {
+    LAT_CUDA_TRY(cudaStreamCreateWithFlags(&tl.up, cudaStreamNonBlocking));
+    LAT_CUDA_TRY(cudaStreamCreateWithFlags(&tl.cmp, cudaStreamNonBlocking));
+    LAT_CUDA_TRY(cudaStreamCreateWithFlags(&tl.down, cudaStreamNonBlocking));
+  }
+  const cudaStream_t up = tl.up, cmp = tl.cmp, down = tl.down;
+  const size_t esz = f_dtype == RUBS_F64 ? 8 : 4, psz = p_dtype == RUBS_F64 ? 8 : 4;
+  std::vector<cudaEvent_t> evs;
+  auto fail = [&](int code) {
+    cudaStreamSynchronize(up);
+    cudaStreamSynchronize(cmp);
+    cudaStreamSynchronize(down);
+    for (cudaEvent_t e : evs) cudaEventDestroy(e);
+    return code;
+  };
+  auto mark = [&](cudaStream_t st, cudaEvent_t &e) -> cudaError_t {
+    cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    if (err != cudaSuccess) return err;
+    evs.push_back(e);
+    return cudaEventRecord(e, st);
+  };
+#define LAT_PIPE_TRY(expr)                                                                  \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess)                                                                  \
+      return fail(set_error(RUBS_ECUDA, std::string(#expr ": ") + cudaGetErrorString(_e))); \
+  } while (0)
+  // uploads that need no geometry: the size plane, then the image in chunks
+  cudaEvent_t e_size;
+  LAT_PIPE_TRY(cudaMemcpyAsync(dp[0], size, (size_t)H * W * psz, cudaMemcpyHostToDevice, up));
+  LAT_PIPE_TRY(mark(up, e_size));
+  const int nchunk = (int)((H + kLatChunkRows - 1) / kLatChunkRows);
+  std::vector<cudaEvent_t> e_img(nchunk);
+  for (int c = 0; c < nchunk; ++c) {
+    const int64_t r0 = (int64_t)c * kLatChunkRows, r1 = std::min<int64_t>(H, r0 + kLatChunkRows);
+    LAT_PIPE_TRY(cudaMemcpyAsync(static_cast<char *>(df) + r0 * W * esz,
+                                 static_cast<const char *>(f) + r0 * W * esz,
+                                 (size_t)(r1 - r0) * W * esz, cudaMemcpyHostToDevice, up));
+    LAT_PIPE_TRY(mark(up, e_img[c]));
+  }
+  // the support bound (one round trip on the kernel stream)
+  Field3 F = lat_params_of(dp[0], dp[1], dp[2], p_dtype, W);
+  F.FH = (int)H;
+  F.FW = (int)W;
+  F.div = 1.0;
+  F.scaled = 0;
+  LAT_PIPE_TRY(cudaStreamWaitEvent(cmp, e_size, 0));
+  LAT_PIPE_TRY(cudaMemsetAsync(tl.d_st, 0, sizeof(LatStatus), cmp));
+  if (p_dtype == RUBS_F64)
+    lat_sizebound_kernel<1><<<4 * 148, 256, 0, cmp>>>(F, tl.d_st);
+  else
+    lat_sizebound_kernel<0><<<4 * 148, 256, 0, cmp>>>(F, tl.d_st);
+  LatStatus st;
+  if ((rc = lat_fetch(cmp, st))) return fail(rc);
+  DomainSpec D{0, 0, (int)W, (int)H, static_cast<double *>(dout), W};
+  const LatGeom g = lat_geometry(D, st.rx, st.ry, h, std::max(64, (int)(H / 8)));
+  const size_t per_block = (size_t)g.NG * g.NA;
+  if ((double)g.NG * g.NA * std::min(g.NG, g.NA) > 4.0e18 || g.NA > (1 << 30))
+    return fail(set_error(RUBS_EUNSUPPORTED, "lattice region beyond the exact int128 range"));
+  if ((rc = lat_grow(tl.G, tl.gcap, per_block)) || (rc = lat_grow(tl.rowmax, tl.rcap, (size_t)H)) ||
+      (rc = lat_grow(tl.S, tl.scap, (size_t)3 * g.nb)))
+    return fail(rc);
+  // each block's elongation / orientation rows, in block order
+  std::vector<cudaEvent_t> e_par(g.nb), e_done(g.nb);
+  for (int b = 0; b < g.nb; ++b) {
+    const int64_t r0 = (int64_t)b * g.bp, r1 = std::min<int64_t>(H, r0 + g.bp);
+    const void *src[2] = {elong, orient};
+    for (int k = 0; k < 2; ++k)
+      LAT_PIPE_TRY(cudaMemcpyAsync(static_cast<char *>(dp[1 + k]) + r0 * W * psz,
+                                   static_cast<const char *>(src[k]) + r0 * W * psz,
+                                   (size_t)(r1 - r0) * W * psz, cudaMemcpyHostToDevice, up));
+    LAT_PIPE_TRY(mark(up, e_par[b]));
+  }
+  const ImageSpec I{df, f_dtype, W, (int)H, (int)W, 0, 0};
+  int rm_done = 0, img_waited = -1, launches = 1;
+  for (int b = 0; b < g.nb; ++b) {
+    // image rows the block's region reaches
+    const int glo = blk_glo(g, b);
+    const int need = (int)std::min<int64_t>(H, (int64_t)std::ceil((glo + g.NG - 1) * g.gh) + 2);
+    const int chunk = std::max(0, (need - 1) / kLatChunkRows);
+    for (int c = img_waited + 1; c <= chunk; ++c) LAT_PIPE_TRY(cudaStreamWaitEvent(cmp, e_img[c], 0));
+    img_waited = std::max(img_waited, chunk);
+    LAT_PIPE_TRY(cudaStreamWaitEvent(cmp, e_par[b], 0));
+    if (need > rm_done) {
+      const int blocks = std::max(1, std::min(need - rm_done, 148 * 8));
+      if (I.dt)
+        lat_rowmax_kernel<1><<<blocks, 256, 0, cmp>>>(I, tl.rowmax, tl.d_st, rm_done, need);
+      else
+        lat_rowmax_kernel<0><<<blocks, 256, 0, cmp>>>(I, tl.rowmax, tl.d_st, rm_done, need);
+      rm_done = need;
+      ++launches;
+    }
+    lat_scale_kernel<<<1, 32, 0, cmp>>>(tl.rowmax, I, g, tl.S, b);
+    lat_block_kernels(I, F, D, g, b, 1, cmp);
+    launches += 5;
+    LAT_PIPE_TRY(cudaGetLastError());
+    LAT_PIPE_TRY(mark(cmp, e_done[b]));
+    LAT_PIPE_TRY(cudaStreamWaitEvent(down, e_done[b], 0));
+    const int64_t r0 = (int64_t)b * g.bp, r1 = std::min<int64_t>(H, r0 + g.bp);
+    LAT_PIPE_TRY(cudaMemcpyAsync(out + r0 * W, static_cast<double *>(dout) + r0 * W,
+                                 (size_t)(r1 - r0) * W * 8, cudaMemcpyDeviceToHost, down));
+  }
+  rubs_internal::count_launches(launches);
+  LAT_PIPE_TRY(cudaStreamSynchronize(down));
+  LAT_PIPE_TRY(cudaStreamSynchronize(up));
+  if ((rc = lat_fetch(cmp, st))) return fail(rc);
+  for (cudaEvent_t e : evs) cudaEventDestroy(e);
+#undef LAT_PIPE_TRY
+  return lat_code(st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -783,6 +919,9 @@ int rubs_b200_filter3_lattice_params_host(const void *f, int f_dtype, int64_t H,
   if ((rc = lat_stage(0, n * esz, &df)) || (rc = lat_stage(1, n * 8, &dout))) return rc;
   for (int k = 0; k < 3; ++k)
     if ((rc = lat_stage(2 + k, n * psz, &dp[k]))) return rc;
+  if (iterations == 1 && H >= kLatStreamRows && !std::getenv("RUBS_B200_NO_STREAM"))
+    return lat_stream_params_host(f, f_dtype, H, W, size, elong, orient, p_dtype, spacing, out, df,
+                                  dout, dp);
   const cudaStream_t s = 0;
   const void *src[3] = {size, elong, orient};
   LAT_CUDA_TRY(cudaMemcpyAsync(df, f, n * esz, cudaMemcpyHostToDevice, s));

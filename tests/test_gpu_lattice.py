@@ -200,3 +200,41 @@ def test_config3_full_size_sampled(cuda, rng):
         ref[i] = oracle.lattice3_points(f64, a, p[None, :], 1.0, threads=1)[0]
     got = out[pts[:, 0], pts[:, 1]].cpu().numpy()
     assert np.abs(got - ref).max() < REL_TOL * np.abs(ref).max()
+
+
+def test_host_pipeline_equals_device_entry(cuda, rng):
+    """Host buffers, one pass, >= 2048 rows: the three-stream block pipeline
+    (size plane, image chunks, per-block parameters up; rows back per block)
+    against the device-pointer entry.  The blocks differ (capped at 1/8 of
+    the rows), so the quantisation exponents do: equal far below the bar,
+    not bitwise."""
+    torch = cuda
+    H, W = 2304, 200
+    f = rng.random((H, W)).astype(np.float32)
+    s = smooth_random_field(rng, (H, W), 2.0, 300.0).astype(np.float32)
+    th = np.minimum(smooth_random_field(rng, (H, W), 0.0, math.pi - 1e-6).astype(np.float32),
+                    np.nextafter(np.float32(math.pi), np.float32(0)))
+    rho = np.minimum(smooth_random_field(rng, (H, W), 1.0, 6.0),
+                     0.95 * rb.elongation_bound3(th.astype(np.float64))).astype(np.float32)
+    host = rb.filter_space_variant3_params(f, s, rho, th, mode="lattice")
+    dev = rb.filter_space_variant3_params(*(torch.from_numpy(v).cuda() for v in (f, s, rho, th)),
+                                          mode="lattice").cpu().numpy()
+    assert rel_err(host, dev) < 1e-12
+    pts = np.stack([rng.integers(0, H, 48), rng.integers(0, W, 48)], axis=1)
+    pts = np.vstack([pts, [[0, 0], [H - 1, W - 1], [287, 5], [288, 5], [2303, 0]]])  # block edges too
+    field = port3.scales3_from_params(*(v[pts[:, 0], pts[:, 1]].astype(float) for v in (s, rho, th)))
+    f64 = f.astype(np.float64)
+    ref = np.array([oracle.lattice3_points(f64, a, p[None, :], 1.0, threads=1)[0]
+                    for p, a in zip(pts, field)])
+    assert np.abs(host[pts[:, 0], pts[:, 1]] - ref).max() < REL_TOL * np.abs(ref).max()
+    # errors surface from the pipeline as from the plain path
+    bad = s.copy()
+    bad[1500, 7] = -1.0
+    with pytest.raises(ValueError):
+        rb.filter_space_variant3_params(f, bad, rho, th, mode="lattice")
+    with pytest.raises(rb.Infeasible):
+        rb.filter_space_variant3_params(f, s, np.full_like(rho, 50.0), np.full_like(th, 0.6), mode="lattice")
+    fbad = f.copy()
+    fbad[2000, 3] = np.inf
+    with pytest.raises(ValueError):
+        rb.filter_space_variant3_params(fbad, s, rho, th, mode="lattice")
