@@ -202,7 +202,7 @@ ITERS = {"4": 2}
 
 
 def row_banded(cfg: str, world: int) -> bool:
-    return cfg in ("5", "3") and world > 1
+    return cfg in ("5", "3", "3l") and world > 1
 
 
 def bench_config(cfg: str, world: int) -> dict:
@@ -290,14 +290,19 @@ class Work:
         else:
             self.sets = [{"f": torch.as_tensor(w["f"]).to(device), "p": [w["size"], w["elong"], w["orient"]]}]
         if self.row_bands:
-            align = sharding.TILE3 if self.n3 else sharding.TILE
+            align = (sharding.TILE3L if self.n3_mode == "lattice" else sharding.TILE3) if self.n3 \
+                else sharding.TILE
             self.band = sharding.band_bounds(self.H, world, align)[rank]
             s0 = self.sets[0]
             b0, b1 = self.band
             self.own = s0["f"][b0:b1].contiguous()
             self.pb = [p[b0:b1].contiguous() for p in s0["p"]]
-            self.plan = (sharding.row_band_plan3(self.band, self.H, self.pb[0]) if self.n3 else
-                         sharding.row_band_plan(self.band, self.H, self.pb[0], self.lut))
+            if self.n3_mode == "lattice":
+                self.plan = sharding.row_band_plan3_lattice(self.band, self.H, self.pb[0])
+            elif self.n3:
+                self.plan = sharding.row_band_plan3(self.band, self.H, self.pb[0])
+            else:
+                self.plan = sharding.row_band_plan(self.band, self.H, self.pb[0], self.lut)
             self.sets = []
             torch.cuda.empty_cache()
             self.px_per_step = float(self.H * self.W)  # the ranks share one image
@@ -306,6 +311,8 @@ class Work:
 
     def step(self, i):
         rb, sharding = self.rb, __import__("paper_1003_2022_b200.sharding", fromlist=["x"])
+        if self.row_bands and self.n3_mode == "lattice":
+            return sharding.filter3_lattice_row_band(self.own, self.band, self.H, *self.pb, plan=self.plan)
         if self.row_bands and self.n3:
             return sharding.filter3_row_band(self.own, self.band, self.H, *self.pb, plan=self.plan)
         if self.row_bands:
@@ -354,7 +361,9 @@ class Work:
             def call():
                 f_rows = hf.to(dev, non_blocking=True)
                 ps = [p.to(dev, non_blocking=True) for p in hp]
-                if self.n3:
+                if self.n3_mode == "lattice":
+                    out = sharding.filter3_lattice_rows_params(f_rows, n0, self.H, *ps, b0, b0, b1 - b0)
+                elif self.n3:
                     out = sharding.filter3_rows_params(f_rows, n0, self.H, *ps, b0, b0, b1 - b0)
                 else:
                     out = sharding.filter_rows_params(f_rows, n0, self.H, *ps, b0, b0, b1 - b0, self.lut)

@@ -325,6 +325,20 @@ int rubs_b200_filter3_lattice_params(const void *f, int f_dtype, int64_t H, int6
                                      const void *orient, int p_dtype, int64_t ld_p,
                                      int iterations, double spacing, double *out,
                                      int64_t ld_out, void *stream);
+/* Row-band entry of the lattice mode (one pass, fused mapping): output rows
+ * [out_row0, out_row0 + out_rows) of an H_total-row image whose rows
+ * [f_row0, f_row0 + f_rows) are given (rows outside count as zero, so the
+ * caller supplies the band's halo: its kernels' vertical reach + 1); the
+ * parameter arrays hold global rows from p_row0 on.  Mirrors
+ * rubs_b200_filter3_params_rows.  Bands reproduce the whole-image call up to
+ * the blocks' quantisation exponents (~1e-17 relative), not bit for bit. */
+int rubs_b200_filter3_lattice_params_rows(const void *f, int f_dtype, int64_t f_row0,
+                                          int64_t f_rows, int64_t W, int64_t ld_f,
+                                          int64_t H_total, const void *size, const void *elong,
+                                          const void *orient, int p_dtype, int64_t p_row0,
+                                          int64_t ld_p, int64_t out_row0, int64_t out_rows,
+                                          double spacing, double *out, int64_t ld_out,
+                                          void *stream);
 int rubs_b200_filter3_lattice_host(const void *f, int f_dtype, int64_t H, int64_t W,
                                    const double *field, int field_is_uniform, int iterations,
                                    double spacing, double *out);

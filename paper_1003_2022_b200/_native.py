@@ -101,6 +101,9 @@ SIGNATURES = {
                                          _i64, _vp]),
     "rubs_b200_filter3_lattice_params": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _vp, _vp, _int, _i64,
                                                 _int, _dbl, _vp, _i64, _vp]),
+    "rubs_b200_filter3_lattice_params_rows": (_int, [_vp, _int, _i64, _i64, _i64, _i64, _i64, _vp, _vp,
+                                                     _vp, _int, _i64, _i64, _i64, _i64, _dbl, _vp, _i64,
+                                                     _vp]),
     "rubs_b200_filter3_lattice_host": (_int, [_vp, _int, _i64, _i64, _vp, _int, _int, _dbl, _vp]),
     "rubs_b200_filter3_lattice_params_host": (_int, [_vp, _int, _i64, _i64, _vp, _vp, _vp, _int, _int,
                                                      _dbl, _vp]),

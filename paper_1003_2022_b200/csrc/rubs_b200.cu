@@ -103,7 +103,14 @@ struct TimedLaunch {
 
 // Called after the stream was synchronised.
 void timer_collect() {
+  // a bracket whose end event has not completed yet (one still open around
+  // the read that triggered this collection closes later) stays pending
+  size_t keep = 0;
   for (auto &p : t_timer.pending) {
+    if (cudaEventQuery(p.second.second) == cudaErrorNotReady) {
+      t_timer.pending[keep++] = p;
+      continue;
+    }
     float ms = 0.f;
     if (cudaEventElapsedTime(&ms, p.second.first, p.second.second) == cudaSuccess) {
       t_timer.ms[p.first] += ms;
@@ -112,7 +119,8 @@ void timer_collect() {
     t_timer.pool.push_back(p.second.first);
     t_timer.pool.push_back(p.second.second);
   }
-  t_timer.pending.clear();
+  t_timer.pending.resize(keep);
+  (void)cudaGetLastError();  // cudaErrorNotReady is not sticky, but leave no trace
 }
 
 int set_error(int code, const std::string &msg) {
@@ -3515,6 +3523,7 @@ int rubs_b200_dfma_peak(double *tflops, double *ms) {
 void rubs_b200_set_profiling(int enable) { t_timer.on = enable != 0; }
 
 void rubs_b200_kernel_time(int kind, double *total_ms, int64_t *launches) {
+  timer_collect();  // brackets closed after the call's last status read
   double ms = 0.0;
   int64_t n = 0;
   for (int k = 0; k < 2; ++k)

@@ -160,9 +160,10 @@ __global__ void __launch_bounds__(256) lat_margins_kernel(Field3 F, LatStatus *s
 // wider region changes no sum (exact integers), only the area swept; the
 // gather validates every pixel's parameters itself.
 template <int DT>
-__global__ void __launch_bounds__(256) lat_sizebound_kernel(Field3 F, LatStatus *st) {
+__global__ void __launch_bounds__(256) lat_sizebound_kernel(Field3 F, LatStatus *st, int r_lo,
+                                                            int r_hi) {
   double smax = 0.0;
-  for (int r = blockIdx.x; r < F.FH; r += gridDim.x) {
+  for (int r = r_lo + blockIdx.x; r < r_hi; r += gridDim.x) {
     const int64_t row = (int64_t)(r - F.fr_off) * F.pld;
     for (int c = threadIdx.x; c < F.FW; c += 256) {
       const double s = load_scalar(F.ps, DT, row + c);
@@ -639,8 +640,8 @@ int run_lattice(const ImageSpec &img, Field3 F, int iterations, double h, double
     switch (F.mode) {
       case kM3Field: lat_margins_kernel<kM3Field><<<blocks, 256, 0, s>>>(F, tl.d_st); break;
       case kM3Uniform: lat_margins_kernel<kM3Uniform><<<blocks, 256, 0, s>>>(F, tl.d_st); break;
-      case kM3Params: lat_sizebound_kernel<1><<<blocks, 256, 0, s>>>(F, tl.d_st); break;
-      default: lat_sizebound_kernel<0><<<blocks, 256, 0, s>>>(F, tl.d_st);
+      case kM3Params: lat_sizebound_kernel<1><<<blocks, 256, 0, s>>>(F, tl.d_st, 0, F.FH); break;
+      default: lat_sizebound_kernel<0><<<blocks, 256, 0, s>>>(F, tl.d_st, 0, F.FH);
     }
     rubs_internal::count_launches(1);
     LAT_CUDA_TRY(cudaGetLastError());
@@ -785,9 +786,9 @@ int lat_stream_params_host(const void *f, int f_dtype, int64_t H, int64_t W, con
   LAT_PIPE_TRY(cudaStreamWaitEvent(cmp, e_size, 0));
   LAT_PIPE_TRY(cudaMemsetAsync(tl.d_st, 0, sizeof(LatStatus), cmp));
   if (p_dtype == RUBS_F64)
-    lat_sizebound_kernel<1><<<4 * 148, 256, 0, cmp>>>(F, tl.d_st);
+    lat_sizebound_kernel<1><<<4 * 148, 256, 0, cmp>>>(F, tl.d_st, 0, F.FH);
   else
-    lat_sizebound_kernel<0><<<4 * 148, 256, 0, cmp>>>(F, tl.d_st);
+    lat_sizebound_kernel<0><<<4 * 148, 256, 0, cmp>>>(F, tl.d_st, 0, F.FH);
   LatStatus st;
   if ((rc = lat_fetch(cmp, st))) return fail(rc);
   DomainSpec D{0, 0, (int)W, (int)H, static_cast<double *>(dout), W};
@@ -874,6 +875,49 @@ int rubs_b200_filter3_lattice_params(const void *f, int f_dtype, int64_t H, int6
   ImageSpec I{f, f_dtype, ld_f, (int)H, (int)W, 0, 0};
   return run_lattice(I, lat_params_of(size, elong, orient, p_dtype, ld_p), iterations, spacing,
                      out, ld_out, static_cast<cudaStream_t>(stream));
+}
+
+int rubs_b200_filter3_lattice_params_rows(const void *f, int f_dtype, int64_t f_row0,
+                                          int64_t f_rows, int64_t W, int64_t ld_f,
+                                          int64_t H_total, const void *size, const void *elong,
+                                          const void *orient, int p_dtype, int64_t p_row0,
+                                          int64_t ld_p, int64_t out_row0, int64_t out_rows,
+                                          double spacing, double *out, int64_t ld_out,
+                                          void *stream) {
+  int rc;
+  if ((rc = lat_check_image(f_dtype, H_total, W))) return rc;
+  if (p_dtype != RUBS_F32 && p_dtype != RUBS_F64) return set_error(RUBS_EVALUE, "bad dtype");
+  if (!(spacing >= 0.125 && spacing <= 1.0))
+    return set_error(RUBS_EVALUE, "lattice spacing must be in [0.125, 1]");
+  if (out_row0 < 0 || out_rows < 0 || out_row0 + out_rows > H_total || p_row0 > out_row0 ||
+      f_row0 < 0 || f_rows < 0 || f_row0 + f_rows > H_total)
+    return set_error(RUBS_EVALUE, "row ranges out of the image");
+  if ((rc = lat_ensure())) return rc;
+  if (out_rows == 0 || W == 0) return RUBS_OK;
+  const cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const ImageSpec I{f, f_dtype, ld_f, (int)f_rows, (int)W, 0, (int)f_row0};
+  Field3 F = lat_params_of(size, elong, orient, p_dtype, ld_p);
+  F.FH = (int)H_total;
+  F.FW = (int)W;
+  F.fr_off = (int)p_row0;
+  F.div = 1.0;
+  F.scaled = 0;
+  LAT_CUDA_TRY(cudaMemsetAsync(tl.d_st, 0, sizeof(LatStatus), s));
+  // the support bound from the band's own size rows (the rows it filters)
+  if (p_dtype == RUBS_F64)
+    lat_sizebound_kernel<1><<<4 * 148, 256, 0, s>>>(F, tl.d_st, (int)out_row0,
+                                                    (int)(out_row0 + out_rows));
+  else
+    lat_sizebound_kernel<0><<<4 * 148, 256, 0, s>>>(F, tl.d_st, (int)out_row0,
+                                                    (int)(out_row0 + out_rows));
+  rubs_internal::count_launches(1);
+  LAT_CUDA_TRY(cudaGetLastError());
+  LatStatus st;
+  if ((rc = lat_fetch(s, st))) return rc;
+  const DomainSpec D{0, (int)out_row0, (int)W, (int)out_rows, out, ld_out};
+  if ((rc = lat_pass(I, F, D, st.rx, st.ry, spacing, s))) return rc;
+  if ((rc = lat_fetch(s, st))) return rc;
+  return lat_code(st);
 }
 
 int rubs_b200_filter3_lattice_host(const void *f, int f_dtype, int64_t H, int64_t W,

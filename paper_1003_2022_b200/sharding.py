@@ -345,3 +345,68 @@ def filter3_row_band(f_own, band, H: int, size, elong, orient, group=None, plan=
         filter3_rows_params(f_rows, f_row0, H, size, elong, orient, band[0], r0, n, out=out)
 
     return plan.run(f_own, filt)
+
+
+# --- three directions, lattice mode (O(1) per pixel) ------------------------
+# The lattice pass is exact after the resampling, and a pixel's output only
+# depends on the resampled image inside its kernel support, so a band needs
+# its kernels' vertical reach plus the resampling footprint (one pixel row)
+# of halo; rows beyond that may be missing (they count as zero).  There is no
+# tile grid: band edges sit on a 32-row grid for even sizes only.  Bands
+# reproduce the whole-image call up to the blocks' quantisation exponents
+# (~1e-17 relative), not bit for bit.
+
+TILE3L = 32
+
+
+def filter3_lattice_rows_params(f_rows, f_row0: int, H: int, size, elong, orient, p_row0: int,
+                                out_row0: int, out_rows: int, out=None, spacing: float = 1.0):
+    """Lattice-mode N=3 output rows [out_row0, out_row0 + out_rows) of the
+    H-row image whose rows [f_row0, f_row0 + len(f_rows)) are given
+    (rubs_b200_filter3_lattice_params_rows)."""
+    import torch
+    from . import _native
+    from .engine import _stream_handle
+    f_rows = f_rows.contiguous()
+    ps = [v.contiguous() for v in (size, elong, orient)]
+    W = f_rows.shape[1]
+    if out is None:
+        out = torch.empty((out_rows, W), dtype=torch.float64, device=f_rows.device)
+    pdt = _native.RUBS_F32 if ps[0].dtype == torch.float32 else _native.RUBS_F64
+    fdt = _native.RUBS_F32 if f_rows.dtype == torch.float32 else _native.RUBS_F64
+    with torch.cuda.device(f_rows.device):
+        _native.check(_native.load().rubs_b200_filter3_lattice_params_rows(
+            ctypes.c_void_p(f_rows.data_ptr()), fdt, f_row0, f_rows.shape[0], W, f_rows.stride(0), H,
+            *(ctypes.c_void_p(p.data_ptr()) for p in ps), pdt, p_row0, ps[0].stride(0),
+            out_row0, out_rows, float(spacing), ctypes.c_void_p(out.data_ptr()), out.stride(0),
+            _stream_handle()))
+    return out
+
+
+def reach3_lattice_bound(size) -> int:
+    """Halo rows of a lattice-mode band with sizes up to size.max(): the
+    kernels' vertical reach ceil((a2 + a3) sqrt3 / 4) + 1 with a2 + a3 <=
+    sqrt(32 size) (a2^2 + a3^2 = 16 C22 <= 16 size), plus the resampling
+    footprint (each lattice point draws on pixels within one row)."""
+    smax = float(size.max().item()) if hasattr(size, "max") else float(np.max(size))
+    a23 = math.sqrt(32.0 * max(smax, 1.0)) * (1.0 + 1e-9) + 0.1
+    return int(math.ceil(0.25 * math.sqrt(3.0) * a23)) + 3
+
+
+def row_band_plan3_lattice(band, H: int, size, group=None):
+    """The RowBandPlan of a lattice-mode N=3 band."""
+    reach = reach3_lattice_bound(size)
+    return RowBandPlan(band, H, (reach - 1, reach - 1), group, TILE3L, device=size.device)
+
+
+def filter3_lattice_row_band(f_own, band, H: int, size, elong, orient, group=None, plan=None,
+                             spacing: float = 1.0):
+    """One rank's share of a lattice-mode N=3 row-band filter (band =
+    band_bounds(H, world, TILE3L)[rank]); collective over the group."""
+    plan = plan or row_band_plan3_lattice(band, H, size, group)
+
+    def filt(f_rows, f_row0, r0, n, out):
+        filter3_lattice_rows_params(f_rows, f_row0, H, size, elong, orient, band[0], r0, n, out=out,
+                                    spacing=spacing)
+
+    return plan.run(f_own, filt)

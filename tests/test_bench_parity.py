@@ -76,4 +76,4 @@ def test_parity_check_lattice_mode(rng):
 def test_lattice_config_is_listed_with_the_same_config_object_in_both_arms():
     assert "3l" in bench.CONFIGS and bench.SHAPES["3l"] == bench.SHAPES["3"]
     assert bench.bench_config("3l", 1)["path"].startswith("fused closed-form N=3 mapping + O(1) lattice")
-    assert not bench.row_banded("3l", 8)  # the lattice mode has no row-band entry: replicas
+    assert bench.row_banded("3l", 8) and not bench.row_banded("3l", 1)  # one image: row bands at N > 1

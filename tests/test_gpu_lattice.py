@@ -238,3 +238,26 @@ def test_host_pipeline_equals_device_entry(cuda, rng):
     fbad[2000, 3] = np.inf
     with pytest.raises(ValueError):
         rb.filter_space_variant3_params(fbad, s, rho, th, mode="lattice")
+
+
+def test_row_bands_reproduce_whole_image(cuda, rng):
+    """Lattice-mode row bands (2, 3, 8 bands, each from the image rows its
+    halo bound needs): equal to the whole-image call far below the bar (the
+    blocks' quantisation exponents differ, so not bitwise)."""
+    torch = cuda
+    from paper_1003_2022_b200 import sharding
+    H, W = 1000, 320
+    w = workloads.config3_n3(H, W, device="cuda", param_dtype=torch.float32)
+    f = torch.from_numpy(w["f"]).cuda()
+    params = (w["size"], w["elong"], w["orient"])
+    whole = rb.filter_space_variant3_params(f, *params, mode="lattice")
+    scale = float(whole.abs().max())
+    for world in (2, 3, 8):
+        parts = []
+        for band in sharding.band_bounds(H, world, sharding.TILE3L):
+            pb = [p[band[0]:band[1]] for p in params]
+            reach = sharding.reach3_lattice_bound(pb[0])
+            n0, n1 = sharding.needed_rows3(band, reach, H)
+            parts.append(sharding.filter3_lattice_rows_params(f[n0:n1], n0, H, *pb, band[0], band[0],
+                                                              band[1] - band[0]))
+        assert float((torch.cat(parts) - whole).abs().max()) < 1e-12 * scale

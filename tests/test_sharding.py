@@ -208,3 +208,70 @@ def test_row_band_plan_overlaps_interior_and_reproduces_whole_image():
         assert calls[0][2] == interior[0] and calls[0][3] == interior[1] - interior[0]
         assert interior[0] % 32 == 0 and (interior[1] % 32 == 0 or interior[1] == H)
         assert len(calls) == 2  # interior + the one edge facing the other rank
+
+
+def _worker_lattice(rank, world, port, f, field, size, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import lattice3_port as lp
+        H, W = f.shape
+        band = sharding.band_bounds(H, world, sharding.TILE3L)[rank]
+        plan = sharding.row_band_plan3_lattice(band, H, torch.from_numpy(size[band[0]:band[1]]))
+        calls = []
+
+        def filt(f_rows, f_row0, r0, n, out):
+            # the numpy restatement of the lattice pass on the given rows only
+            # (rows it lacks are zero: a missing halo row shows up as an error)
+            calls.append((f_row0, f_rows.shape[0], r0, n))
+            a = np.maximum(field[r0:r0 + n], lp.SCALE_FLOOR)
+            out.copy_(torch.from_numpy(lp.lattice_pass(f_rows.numpy(), f_row0, 0, a, r0, 0, 1.0)))
+
+        out = plan.run(torch.from_numpy(f[band[0]:band[1]].copy()), filt)
+        res = [None] * world
+        dist.all_gather_object(res, (out.numpy(), calls, plan.interior))
+        if rank == 0:
+            ret.put(res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_lattice_mode_row_bands_reproduce_whole_image():
+    """N=3 lattice mode in row bands at world size 2: the halo is the
+    kernels' reach bound plus the resampling footprint; interior rows are
+    filtered from the rank's own rows while the exchange is in flight."""
+    from oracle import lattice3_port as lp, port3
+    rng = np.random.default_rng(13)
+    H, W = 256, 36
+    f = rng.random((H, W))
+    size = np.linspace(2.0, 40.0, H)[:, None] * np.ones((1, W))
+    th = rng.uniform(0.0, np.pi, (H, W))
+    rho = np.full((H, W), 1.5)
+    field = port3.scales3_from_params(size, rho, th)
+    ctx = mp.get_context("spawn")
+    ret = ctx.Queue()
+    procs = mp.start_processes(_worker_lattice, args=(2, _free_port(), f, field, size, ret), nprocs=2,
+                               join=False, start_method="spawn")
+    res = ret.get(timeout=120)
+    procs.join()
+    whole = lp.lattice3(f, field)
+    banded = np.concatenate([r[0] for r in res])
+    assert np.abs(banded - whole).max() < 1e-10 * np.abs(whole).max()
+    for out, calls, interior in res:
+        assert interior is not None and len(calls) == 2
+
+
+def test_lattice_halo_bound_covers_the_support(rng):
+    import math
+    from oracle import port3
+    from paper_1003_2022_b200 import elongation_bound3
+    n = 4000
+    size = rng.uniform(0.1, 2.0e5, n)
+    th = rng.uniform(0.0, math.pi, n)
+    rho3 = 1.0 + (np.minimum(elongation_bound3(th), 40.0) - 1.0) * rng.uniform(0.0, 0.999, n)
+    a3 = np.maximum(port3.scales3_from_params(size, rho3, th), 0.05)
+    ry = int(np.max(port3.support3(a3)[1]))
+    assert sharding.reach3_lattice_bound(size) >= ry + 1  # + the resampling footprint
+    # the device's own bound (csrc lat_sizebound_kernel) in numpy: a1 <= sqrt(12 s), a2 + a3 <= sqrt(32 s)
+    assert np.all(a3[:, 0] <= np.sqrt(12.0 * size) * (1 + 1e-12) + 0.05)
+    assert np.all(a3[:, 1] + a3[:, 2] <= np.sqrt(32.0 * size) * (1 + 1e-12) + 0.1)
