@@ -634,7 +634,7 @@ TRAFFIC_PER_PASS = {
                     "(profiles/ncu_r02_c3l_launches.csv; algorithmic 1.61 GB: the rest is the int128 lattice "
                     "region, 16 B per lattice point, written by the splat, read and written by the two line "
                     "sums, read by the gather)"),
-    "5": (180.4e9, "ncu launch list of one step, sum over the pass's kernels "
+    "5": (180.2e9, "ncu launch list of one step, sum over the pass's kernels "
                    "(profiles/ncu_r02_c5_launches.csv, split in profiles/ncu_r02_summary.md; algorithmic "
                    "25.8 GB: the rest is the large-halo regions' scratch, 4.5 elements per pixel written "
                    "and re-read by the sweeps, then gathered)"),
