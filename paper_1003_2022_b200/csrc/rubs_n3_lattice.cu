@@ -137,8 +137,8 @@ __global__ void __launch_bounds__(256) lat_margins_kernel(Field3 F, LatStatus *s
        i += (int64_t)gridDim.x * blockDim.x) {
     double a[3];
     scales3_at<MODE>(F, (int)(i % F.FW), (int)(i / F.FW) + F.fr_off, a, flags);
-    rx = max(rx, (int)ceil(0.5 * a[0] + 0.25 * (a[1] + a[2])) + 1);
-    ry = max(ry, (int)ceil(kQuarterSqrt3 * (a[1] + a[2])) + 1);
+    rx = max(rx, (int)fmin(ceil(0.5 * a[0] + 0.25 * (a[1] + a[2])) + 1.0, 1.0e8));
+    ry = max(ry, (int)fmin(ceil(kQuarterSqrt3 * (a[1] + a[2])) + 1.0, 1.0e8));
   }
   rx = __reduce_max_sync(0xffffffffu, rx);
   ry = __reduce_max_sync(0xffffffffu, ry);
@@ -177,8 +177,10 @@ __global__ void __launch_bounds__(256) lat_sizebound_kernel(Field3 F, LatStatus 
     const double inv = F.scaled ? 1.0 / F.div : 1.0;
     const double a1 = (sqrt(12.0 * smax) + kScaleFloor) * inv;
     const double a23 = (sqrt(32.0 * smax) + 2.0 * kScaleFloor) * inv;
-    atomicMax(&st->rx, (int)ceil(0.5 * a1 + 0.25 * a23) + 1);
-    atomicMax(&st->ry, (int)ceil(kQuarterSqrt3 * a23) + 1);
+    // (sizes beyond any image are refused by the region check: keep the
+    // conversion to int defined)
+    atomicMax(&st->rx, (int)fmin(ceil(0.5 * a1 + 0.25 * a23) + 1.0, 1.0e8));
+    atomicMax(&st->ry, (int)fmin(ceil(kQuarterSqrt3 * a23) + 1.0, 1.0e8));
   }
 }
 
@@ -502,6 +504,8 @@ int lat_fetch(cudaStream_t s, LatStatus &out) {
 }
 
 int lat_code(const LatStatus &st) {
+  if (st.rx > (1 << 24) || st.ry > (1 << 24))
+    return set_error(RUBS_EUNSUPPORTED, "kernel support beyond the lattice mode's range");
   if (st.flags & kFlagFieldNonFinite)
     return set_error(RUBS_EVALUE, "scale field entries must be finite");
   if (st.flags & kFlagParamInvalid)
@@ -791,6 +795,7 @@ int lat_stream_params_host(const void *f, int f_dtype, int64_t H, int64_t W, con
     lat_sizebound_kernel<0><<<4 * 148, 256, 0, cmp>>>(F, tl.d_st, 0, F.FH);
   LatStatus st;
   if ((rc = lat_fetch(cmp, st))) return fail(rc);
+  if (st.rx > (1 << 24) || st.ry > (1 << 24)) return fail(lat_code(st));
   DomainSpec D{0, 0, (int)W, (int)H, static_cast<double *>(dout), W};
   const LatGeom g = lat_geometry(D, st.rx, st.ry, h, std::max(64, (int)(H / 8)));
   const size_t per_block = (size_t)g.NG * g.NA;
@@ -914,6 +919,7 @@ int rubs_b200_filter3_lattice_params_rows(const void *f, int f_dtype, int64_t f_
   LAT_CUDA_TRY(cudaGetLastError());
   LatStatus st;
   if ((rc = lat_fetch(s, st))) return rc;
+  if (st.rx > (1 << 24) || st.ry > (1 << 24)) return lat_code(st);
   const DomainSpec D{0, (int)out_row0, (int)W, (int)out_rows, out, ld_out};
   if ((rc = lat_pass(I, F, D, st.rx, st.ry, spacing, s))) return rc;
   if ((rc = lat_fetch(s, st))) return rc;

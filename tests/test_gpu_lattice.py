@@ -261,3 +261,15 @@ def test_row_bands_reproduce_whole_image(cuda, rng):
             parts.append(sharding.filter3_lattice_rows_params(f[n0:n1], n0, H, *pb, band[0], band[0],
                                                               band[1] - band[0]))
         assert float((torch.cat(parts) - whole).abs().max()) < 1e-12 * scale
+
+
+def test_absurd_kernel_sizes_are_refused(cuda, rng):
+    """Supports beyond any image (size 1e30) fail with an error, through the
+    size bound of the parameter entries and the exact margins of the field
+    entries alike."""
+    f = rng.random((40, 40))
+    ones = np.ones((40, 40))
+    with pytest.raises(RuntimeError):
+        rb.filter_space_variant3_params(f, ones * 1e30, ones, ones * 0.3, mode="lattice")
+    with pytest.raises(RuntimeError):
+        rb.filter_space_variant3(f, np.array([1e20, 3.0, 3.0]), mode="lattice")
