@@ -273,3 +273,20 @@ def test_absurd_kernel_sizes_are_refused(cuda, rng):
         rb.filter_space_variant3_params(f, ones * 1e30, ones, ones * 0.3, mode="lattice")
     with pytest.raises(RuntimeError):
         rb.filter_space_variant3(f, np.array([1e20, 3.0, 3.0]), mode="lattice")
+
+
+def test_two_passes_fused_params_match_port(cuda, rng):
+    """Iterated passes through the fused-parameter entry: its canvases come
+    from the size-plane bound (larger than the exact supports), which changes
+    nothing but rounding against the restatement's exact canvases."""
+    H, W = 72, 64
+    f = rng.random((H, W))
+    s = smooth_random_field(rng, (H, W), 4.0, 90.0)
+    th = smooth_random_field(rng, (H, W), 0.0, math.pi - 1e-9)
+    rho = np.minimum(smooth_random_field(rng, (H, W), 1.0, 5.0), 0.95 * rb.elongation_bound3(th))
+    field = port3.scales3_from_params(s, rho, th)
+    got = rb.filter_space_variant3_params(f, s, rho, th, 2, mode="lattice")
+    assert rel_err(got, lp.lattice3(f, field, 1.0, iterations=2)) < REL_TOL
+    got_t = rb.filter_space_variant3_params(*(cuda.from_numpy(v).cuda() for v in (f, s, rho, th)), 2,
+                                            mode="lattice").cpu().numpy()
+    assert np.array_equal(got, got_t)
