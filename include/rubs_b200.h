@@ -73,6 +73,16 @@ void rubs_b200_reset_kernel_time(void);
 int rubs_b200_dfma_peak(double *tflops, double *ms);
 
 /*
+ * 1 if a four-direction filter call on this thread since the last query met
+ * pixels whose OWN minimal region exceeds the float64 precision budget
+ * ("needle" kernels: three widths at the 0.05 floor next to one of tens of
+ * pixels) -- their results may be accurate to ~1e-8 relative
+ * instead of 1e-9.  Not an error (the reference's fast path is at ~1e-6 on
+ * such inputs); reading clears it.  No reference counterpart.
+ */
+int rubs_b200_precision_limited(void);
+
+/*
  * Space-variant filter, per-pixel scale field.
  * Replaces engine.filter_space_variant (pkg/src/rubs/engine.py:265-324).
  *   f        device image, H x W, dtype RUBS_F32 | RUBS_F64, row stride ld_f

@@ -43,6 +43,7 @@ from .geometry import (
     scales3_from_params,
     sigma_to_size,
 )
+from ._native import PrecisionWarning
 from .solver import Infeasible, OutOfGrid, ScaleLut, build_lut, default_lut, optimize_scale_vector
 from .tensor import AnisotropyMaps, adaptive_smooth, anisotropy_from_tensor, structure_tensor
 
@@ -61,6 +62,7 @@ __all__ = [
     "ScaleLut",
     "Infeasible",
     "OutOfGrid",
+    "PrecisionWarning",
     "MIN_ELONGATION_BOUND",
     "as_scale_vector",
     "build_lut",

@@ -65,6 +65,7 @@ SIGNATURES = {
     "rubs_b200_kernel_time": (None, [_int, _dp, _lp]),
     "rubs_b200_reset_kernel_time": (None, []),
     "rubs_b200_dfma_peak": (_int, [_dp, _dp]),
+    "rubs_b200_precision_limited": (_int, []),
     "rubs_b200_filter": (_int, [_vp, _int, _i64, _i64, _i64, _vp, _int, _i64, _int, _vp, _i64, _vp]),
     "rubs_b200_filter_host": (_int, [_vp, _int, _i64, _i64, _vp, _int, _int, _vp]),
     "rubs_b200_lut_create": (_int, [_vp, _vp, _vp, _int, _int, ctypes.POINTER(_vp)]),
@@ -136,9 +137,18 @@ def load(path: str | None = None):
     return L
 
 
+class PrecisionWarning(RuntimeWarning):
+    """A filter call met needle kernels (rubs_b200_precision_limited)."""
+
+
 def check(rc: int) -> None:
     """Map a C status to the reference's exception classes."""
     if rc == RUBS_OK:
+        if _lib is not None and _lib.rubs_b200_precision_limited():
+            import warnings
+            warnings.warn("some kernels are too anisotropic for the float64 running sums (three widths at "
+                          "the 0.05 floor next to a long one): their pixels may be accurate to ~1e-8 "
+                          "relative instead of 1e-9", PrecisionWarning, stacklevel=3)
         return
     msg = load().rubs_b200_last_error().decode(errors="replace")
     if rc == RUBS_EVALUE:

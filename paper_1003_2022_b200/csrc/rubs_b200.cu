@@ -58,6 +58,7 @@ constexpr int kSmemSmall = 112 * 1024;  // dynamic shared memory, primary CTA
 constexpr int kSmemLarge = 225 * 1024;  // overflow CTA (+ static <= 227 KiB)
 
 thread_local std::string t_last_error;
+thread_local int t_precision_limited = 0;  // since the last rubs_b200_precision_limited()
 thread_local int64_t t_launches = 0;
 
 // optional per-kernel event timing (bench.py roofline)
@@ -686,6 +687,9 @@ __device__ __forceinline__ void pixel_fd_n(uint32_t Sb, int P8, int n1, int n2, 
 #define RUBS_PREC_BUDGET 5e5f
 #endif
 constexpr float kPrecisionBudget = RUBS_PREC_BUDGET;  // w * L4 (see above)
+// w * L4 from which a pixel that cannot get a smaller region is reported as
+// precision-limited: 0.5 * 2^-53 * 2e7 ~ 1e-9
+constexpr float kPrecisionWarn = 2.0e7f;
 
 // Per-pixel precision fallback.  The overflow passes share one region among
 // many pixels; a pixel whose weight w = 1/(a1 a2 a3 a4) is large (a small,
@@ -711,7 +715,15 @@ __device__ __forceinline__ bool defer_pixel(const double a[4], float l4, int x, 
   // only if the pixel's own region fits a warp's slab (large w goes with a
   // small kernel; a pixel that is neither stays in the shared region)
   const int4 m = pixel_margins_fast(a);
-  if (region_pitch(1 + m.x + m.y) * (1 + m.z + m.w) > kPixSlab) return false;
+  if (region_pitch(1 + m.x + m.y) * (1 + m.z + m.w) > kPixSlab) {
+    // neither: the pixel stays in the shared region.  If even its OWN
+    // minimal region predicts an error near 1e-9 (kappa eps w L4 with the
+    // worst kappa met, 0.5) it is a needle kernel, limited in any region:
+    // the call reports it (rubs_b200_precision_limited)
+    const float rw = (float)(1 + m.x + m.y), rh = (float)(1 + m.z + m.w), mn = fminf(rw, rh);
+    if (w * 0.25f * rw * rh * mn * mn > kPrecisionWarn) atomicOr(&st->flags, kFlagPrecisionLimited);
+    return false;
+  }
   // beyond the list's capacity the pixel is only counted: the host grows
   // the list to the count and runs the deferred-tile passes again
   const int i = atomicAdd(&st->pix_count, 1);
@@ -1536,6 +1548,11 @@ __global__ void __launch_bounds__(256) pixel_kernel(ImageSpec I, FieldSpec F, Do
       if (lane == 0) atomicOr(&st->flags, kFlagRegionTooLarge);
       continue;
     }
+    {
+      const float mn = (float)min(RW, RH);
+      const float l4own = 0.25f * (float)RW * (float)RH * mn * mn;
+      if (l4own / (float)(a[0] * a[1] * a[2] * a[3]) > kPrecisionWarn) flags |= kFlagPrecisionLimited;
+    }
     const int rc0 = n1 - m.x, rr0 = n2 - m.z;
     // region load (zero outside the image), then the four running sums
     for (int e = lane; e < RW * RH; e += 32) {
@@ -2116,6 +2133,7 @@ int ensure_pass(int k, size_t n) {
 }
 
 int status_to_code(const Status &s) {
+  if (s.flags & kFlagPrecisionLimited) t_precision_limited = 1;
   if (s.flags & kFlagFieldNonFinite)
     return set_error(RUBS_EVALUE, "scale field entries must be finite");
   if (s.flags & kFlagParamInvalid)
@@ -3542,6 +3560,12 @@ void rubs_b200_reset_kernel_time(void) {
 const char *rubs_b200_last_error(void) { return t_last_error.c_str(); }
 int64_t rubs_b200_launch_count(void) { return t_launches; }
 void rubs_b200_reset_launch_count(void) { t_launches = 0; }
+
+int rubs_b200_precision_limited(void) {
+  const int v = t_precision_limited;
+  t_precision_limited = 0;
+  return v;
+}
 
 int rubs_b200_filter(const void *f, int f_dtype, int64_t H, int64_t W, int64_t ld_f,
                      const double *field, int field_is_uniform, int64_t ld_field, int iterations,

@@ -29,6 +29,11 @@ constexpr unsigned kFlagFieldNonFinite = 1u;  // engine.py:214-215 -> ValueError
 constexpr unsigned kFlagParamInvalid = 2u;    // solver.py:298-303 -> ValueError
 constexpr unsigned kFlagOutOfGrid = 4u;       // solver.py:304-307 -> OutOfGrid
 constexpr unsigned kFlagRegionTooLarge = 8u;  // halo beyond the on-chip region capacity
+// Not an error: some pixel's OWN minimal region already exceeds the float64
+// precision budget w L4 (a "needle" kernel: three floored widths next to a
+// long one), so its result may be accurate to ~1e-8 only.
+// Reported through rubs_b200_precision_limited().
+constexpr unsigned kFlagPrecisionLimited = 64u;
 
 struct Status {
   unsigned int flags;
