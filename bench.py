@@ -457,6 +457,12 @@ def run_ours(args, rank, world, local):
     if world > 1:
         dist.init_process_group("nccl", device_id=device)
     L = _native.load()
+    # PrecisionWarning = the filter met needle kernels; the
+    # line reports how many calls of this run raised it (0 on every config)
+    import warnings
+    _rec = warnings.catch_warnings(record=True)
+    wlist = _rec.__enter__()
+    warnings.simplefilter("always", _native.PrecisionWarning)
     dfma = None
     if rank == 0:
         # measured fp64 FMA peak of this GPU (the fp64 roofline's denominator)
@@ -596,9 +602,11 @@ def run_ours(args, rank, world, local):
             "launches_per_step": launches / max(1, args.steps),
             "kernel_share_of_step": all_ms.value / max(ms_total, 1e-9),
             "clocks": clk,
+            "precision_warnings": sum(1 for w_ in wlist if issubclass(w_.category, _native.PrecisionWarning)),
         }
         if pin is not None:
             result["_parity_in"] = pin
+    _rec.__exit__(None, None, None)
     if world > 1:
         dist.destroy_process_group()
     return result
