@@ -537,19 +537,24 @@ LatGeom lat_geometry(const DomainSpec &D, int rx, int ry, double h, int bp_cap =
     NG = (int)std::ceil((double)(bp - 1 + 2 * g.RY) / g.gh) + 6;
     NA = (int)std::ceil((double)(D.pw - 1 + 2 * RX) / h + 0.5 * NG) + 6;
   };
-  int best = 32;
-  double best_cost = 1e300;
+  // bp: region points per pass, NG x NA x blocks, is flat near its minimum;
+  // among the sizes within 4 % of it the SMALLEST wins (more blocks = more
+  // columns and diagonals for the line sums, which draw their parallelism
+  // from them: config 3, 1024 against 2048 rows per block: -2 %)
   const int top = std::max(32, std::min(((D.ph + 31) / 32) * 32, bp_cap / 32 * 32));
-  for (int bp = 32; bp <= top; bp += 32) {
+  auto cost_of = [&](int bp) {
     int NG, NA;
     dims(bp, NG, NA);
-    const int nb = (D.ph + bp - 1) / bp;
-    const double cost = (double)NG * NA * nb;
-    if (cost < best_cost * 0.999) {
-      best_cost = cost;
+    return (double)NG * NA * ((D.ph + bp - 1) / bp);
+  };
+  double best_cost = 1e300;
+  for (int bp = 32; bp <= top; bp += 32) best_cost = std::min(best_cost, cost_of(bp));
+  int best = top;
+  for (int bp = 32; bp <= top; bp += 32)
+    if (cost_of(bp) <= 1.04 * best_cost) {
       best = bp;
+      break;
     }
-  }
   g.bp = best;
   g.nb = (D.ph + best - 1) / best;
   dims(best, g.NG, g.NA);
@@ -591,7 +596,12 @@ void lat_block_kernels(const ImageSpec &I, const Field3 &F, const DomainSpec &D,
 
 int lat_pass(const ImageSpec &I, const Field3 &F, const DomainSpec &D, int rx, int ry, double h,
              cudaStream_t s) {
-  LatGeom g = lat_geometry(D, rx, ry, h);
+  static const int bp_cap = [] {
+    const char *e = std::getenv("RUBS_B200_LAT_BP");
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 32 ? v : INT_MAX;
+  }();
+  LatGeom g = lat_geometry(D, rx, ry, h, bp_cap);
   const size_t per_block = (size_t)g.NG * g.NA;
   if ((double)g.NG * g.NA * std::min(g.NG, g.NA) > 4.0e18 || g.NA > (1 << 30))
     return set_error(RUBS_EUNSUPPORTED, "lattice region beyond the exact int128 range");
